@@ -1,0 +1,970 @@
+// api.cpp — host side of libfl1cuda.so: the C-ABI declared in include/fl1cuda.h.
+//
+// Owns device memory for dictionaries (HBM-resident, immutable, shareable),
+// per-solve workspaces (cached per context), the launch loop around the
+// persistent engine kernel, and the marshalling of SolveResult
+// (fastl1.hpp:61-71). There is no CPU compute path: every product with a
+// dictionary runs on the GPU; the host only validates arguments (with the
+// reference's messages) and moves bytes.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <limits>
+#include <memory>
+#include <mutex>
+#include <random>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "engine.cuh"
+
+namespace fl1 {
+size_t engine_smem_bytes(int64_t ld, int64_t sukro_m);
+cudaError_t engine_configure(int64_t ld, int64_t sukro_m, int device, int* grid_out);
+cudaError_t engine_launch(const EngineParams& p, int64_t sukro_m, cudaStream_t stream);
+cudaError_t screen_kernel_launch(int64_t n, const double* dots, const double* eps, const double* en,
+                                 const double* an, double cn, double r, int8_t* keep, int8_t* look,
+                                 cudaStream_t stream);
+}  // namespace fl1
+
+using fl1::DevLevel;
+using fl1::EngineParams;
+using fl1::EngineState;
+
+namespace {
+
+thread_local std::string g_err;
+
+struct CudaError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw CudaError(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+template <class F>
+int guard(F&& f) {
+  try {
+    f();
+    return FL1_OK;
+  } catch (const std::invalid_argument& e) {
+    g_err = e.what();
+    return FL1_EINVAL;
+  } catch (const CudaError& e) {
+    g_err = e.what();
+    return FL1_ECUDA;
+  } catch (const std::bad_alloc&) {
+    g_err = "out of memory";
+    return FL1_ENOMEM;
+  } catch (const std::logic_error& e) {
+    g_err = e.what();
+    return FL1_EUNSUPPORTED;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return FL1_ERUNTIME;
+  }
+}
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  DevBuf() = default;
+  explicit DevBuf(size_t b) : bytes(b) {
+    if (b) ck(cudaMalloc(&p, b), "cudaMalloc");
+  }
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+  template <class T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+};
+
+int64_t even_ld(int64_t n) { return (n + 1) / 2 * 2; }
+
+}  // namespace
+
+// ---------------------------------------------------------------- handles
+struct Workspace {
+  int64_t n = 0, k = 0, ld = 0;
+  int64_t sk_elems = 0;  // SuKro scratch capacity (nterms * m * q)
+  int64_t sk_m = 0;
+  int grid = 0;
+  int64_t units = 1;
+  int64_t trace_cap = 0;
+  std::unique_ptr<DevBuf> mem;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  EngineParams base{};  // pointers filled
+  ~Workspace() {
+    if (ev0) cudaEventDestroy(ev0);
+    if (ev1) cudaEventDestroy(ev1);
+    if (stream) cudaStreamDestroy(stream);
+  }
+};
+
+struct fl1_ctx {
+  int device = 0;
+  int sms = 0;
+  int64_t l2 = 0, hbm = 0;
+  std::mutex mu;
+  std::vector<std::unique_ptr<Workspace>> pool;
+  std::unique_ptr<DevBuf> gauss;  // cold-start vector (solver.cpp:80-82)
+  int64_t gauss_len = 0;
+
+  void bind() const { ck(cudaSetDevice(device), "cudaSetDevice"); }
+
+  // first `len` draws of mt19937_64(0x11b5c417) / normal_distribution, resident in HBM
+  const double* gauss0(int64_t len) {
+    std::lock_guard<std::mutex> g(mu);
+    if (gauss_len < len) {
+      std::mt19937_64 rng(0x11b5c417ULL);
+      std::normal_distribution<double> nd(0.0, 1.0);
+      std::vector<double> h(static_cast<size_t>(len));
+      for (auto& e : h) e = nd(rng);
+      auto buf = std::make_unique<DevBuf>(h.size() * sizeof(double));
+      ck(cudaMemcpy(buf->p, h.data(), h.size() * sizeof(double), cudaMemcpyHostToDevice), "upload gauss0");
+      gauss = std::move(buf);
+      gauss_len = len;
+    }
+    return gauss->as<double>();
+  }
+
+  std::unique_ptr<Workspace> acquire(int64_t n, int64_t k, int64_t trace_cap, int64_t sk_elems, int64_t sk_m);
+  void release(std::unique_ptr<Workspace> w) {
+    std::lock_guard<std::mutex> g(mu);
+    if (pool.size() < 4) pool.push_back(std::move(w));
+  }
+};
+
+struct DictImpl {
+  fl1_ctx* ctx = nullptr;
+  int kind = fl1::kDense;
+  int64_t n = 0, k = 0, ld = 0;
+  int64_t m = 0, q = 0;
+  int nterms = 0;
+  std::unique_ptr<DevBuf> a, left, right, col_scale;
+  std::vector<double> h_left, h_right, h_scale;  // SuKro factors (small) kept for column()
+  std::vector<double> norms;                     // atom_norms2
+  uint64_t matvec_flops() const {
+    if (kind == fl1::kDense) return static_cast<uint64_t>(n) * static_cast<uint64_t>(k);
+    return static_cast<uint64_t>(nterms) * (static_cast<uint64_t>(m) * static_cast<uint64_t>(k) +
+                                            static_cast<uint64_t>(q) * static_cast<uint64_t>(n));
+  }
+};
+struct fl1_dict {
+  std::shared_ptr<DictImpl> d;
+};
+
+struct ApproxImpl {
+  std::shared_ptr<DictImpl> dict;
+  std::vector<double> eps, an, en;
+  double op_err = 0.0, rc = 1.0;
+  std::unique_ptr<DevBuf> d_eps, d_an, d_en;
+  bool is_exact() const { return op_err == 0.0; }
+};
+struct fl1_approx {
+  std::shared_ptr<ApproxImpl> a;
+};
+
+struct fl1_seq {
+  std::vector<std::shared_ptr<ApproxImpl>> lv;
+  void validate() const {  // ApproxSequence::validate (dictionary.cpp:227-251)
+    if (lv.empty()) throw std::invalid_argument("empty approximation sequence");
+    const int64_t k = lv.front()->dict->k;
+    for (size_t i = 0; i < lv.size(); ++i) {
+      const ApproxImpl& d = *lv[i];
+      if (d.dict->k != k) throw std::invalid_argument("sequence has mismatched atom counts");
+      bool bad = static_cast<int64_t>(d.eps.size()) != k;
+      if (!bad)
+        for (double e : d.eps) bad = bad || e < 0;
+      if (bad) throw std::invalid_argument("invalid atom error bounds");
+      if (d.rc <= 0.0 || d.rc > 1.0) throw std::invalid_argument("relative complexity out of (0, 1]");
+      if (i > 0) {
+        const ApproxImpl& p = *lv[i - 1];
+        if (d.rc <= p.rc) throw std::invalid_argument("relative complexity must strictly increase");
+        for (int64_t j = 0; j < k; ++j)
+          if (d.eps[static_cast<size_t>(j)] > p.eps[static_cast<size_t>(j)] + 1e-15)
+            throw std::invalid_argument("error bounds must be non-increasing along the sequence");
+      }
+    }
+    if (!lv.back()->is_exact() || lv.back()->rc != 1.0)
+      throw std::invalid_argument("sequence must end with the exact dictionary");
+  }
+};
+
+struct fl1_result {
+  int64_t k = 0;
+  std::vector<double> x;
+  bool converged = false;
+  double final_gap = std::numeric_limits<double>::quiet_NaN();
+  uint64_t iterations = 0;
+  uint64_t total_flops = 0;
+  std::vector<fl1_trace_row> trace;
+  std::vector<fl1_switch_event> switches;
+  std::vector<int32_t> final_active;
+  bool gap_warning = false;
+  double device_ms = 0.0, setup_ms = 0.0;
+  int64_t launches = 0, power_steps = 0;
+  double prof[6] = {0, 0, 0, 0, 0, 0};
+};
+
+// ---------------------------------------------------------------- workspace
+namespace {
+
+struct Carver {
+  char* base;
+  size_t off = 0;
+  template <class T>
+  T* take(int64_t count) {
+    off = (off + 255) / 256 * 256;
+    T* r = reinterpret_cast<T*>(base + off);
+    off += static_cast<size_t>(count) * sizeof(T);
+    return r;
+  }
+};
+
+size_t carve(EngineParams& p, char* base, int64_t n, int64_t k, int64_t ld, int grid, int64_t units,
+             int64_t trace_cap, int64_t sk_elems) {
+  (void)n;
+  Carver c{base};
+  const int64_t kk = std::max<int64_t>(k, 1);
+  const int64_t vec = std::max(ld, kk);
+  p.y = c.take<double>(ld);
+  p.x_init = c.take<double>(vec);
+  p.U = c.take<double>(ld);
+  p.V = c.take<double>(ld);
+  p.rho = c.take<double>(ld);
+  p.up = c.take<double>(static_cast<int64_t>(grid) * ld);
+  p.dvp = c.take<double>(static_cast<int64_t>(grid) * ld);
+  p.pup = c.take<double>(static_cast<int64_t>(grid) * ld);
+  p.vec_out = c.take<double>(vec);
+  p.corr = c.take<double>(kk);
+  p.corr_y = c.take<double>(kk);
+  p.part = c.take<double>(kk * units);
+  p.cnt = c.take<int32_t>(kk);
+  p.pv = c.take<double>(kk);
+  p.pw = c.take<double>(kk);
+  p.PU = c.take<double>(ld);
+  p.sk_scat = nullptr;
+  p.sk_t = sk_elems > 0 ? c.take<double>(2 * sk_elems) : nullptr;
+  p.sk_x = sk_elems > 0 ? c.take<double>(2 * kk) : nullptr;
+  p.sk_ks = 8;
+  p.bred = c.take<double>(static_cast<int64_t>(grid) * fl1::kBred);
+  for (int b = 0; b < 2; ++b) {
+    fl1::Bank& bk = p.bank[b];
+    bk.idx = c.take<int32_t>(kk);
+    bk.x = c.take<double>(kk);
+    bk.xp = c.take<double>(kk);
+    bk.eps = c.take<double>(kk);
+    bk.en = c.take<double>(kk);
+    bk.an = c.take<double>(kk);
+    bk.aty = c.take<double>(kk);
+    bk.atye = c.take<double>(kk);
+    bk.lead = c.take<double>(kk);
+    bk.keep = c.take<int8_t>(kk);
+  }
+  p.trace = c.take<fl1_trace_row>(std::max<int64_t>(trace_cap, 1));
+  p.sw = c.take<fl1_switch_event>(fl1::kMaxLevels);
+  p.st = c.take<EngineState>(1);
+  return c.off + 256;
+}
+
+}  // namespace
+
+std::unique_ptr<Workspace> fl1_ctx::acquire(int64_t n, int64_t k, int64_t trace_cap, int64_t sk_elems,
+                                            int64_t sk_m) {
+  const int64_t ld = even_ld(n);
+  {
+    std::lock_guard<std::mutex> g(mu);
+    for (size_t i = 0; i < pool.size(); ++i) {
+      Workspace& w = *pool[i];
+      if (w.n == n && w.k == k && w.trace_cap >= trace_cap && w.sk_elems >= sk_elems && w.sk_m >= sk_m) {
+        auto r = std::move(pool[i]);
+        pool.erase(pool.begin() + static_cast<long>(i));
+        return r;
+      }
+    }
+  }
+  auto w = std::make_unique<Workspace>();
+  w->n = n;
+  w->k = k;
+  w->ld = ld;
+  w->units = (n + fl1::kUnit - 1) / fl1::kUnit;
+  w->trace_cap = trace_cap;
+  w->sk_elems = sk_elems;
+  w->sk_m = sk_m;
+  {
+    const cudaError_t e = fl1::engine_configure(ld, sk_m, device, &w->grid);
+    if (e == cudaErrorInvalidConfiguration)
+      throw std::logic_error("signal length too large for the shared-memory resident residual");
+    ck(e, "engine_configure");
+  }
+  EngineParams p{};
+  const size_t bytes = carve(p, nullptr, n, k, ld, w->grid, w->units, trace_cap, sk_elems);
+  w->mem = std::make_unique<DevBuf>(bytes);
+  ck(cudaMemset(w->mem->p, 0, bytes), "workspace memset");
+  carve(p, w->mem->as<char>(), n, k, ld, w->grid, w->units, trace_cap, sk_elems);
+  p.grid = w->grid;
+  p.n = n;
+  p.k = k;
+  p.ld = ld;
+  p.trace_cap = trace_cap;
+  w->base = p;
+  ck(cudaStreamCreateWithFlags(&w->stream, cudaStreamNonBlocking), "stream");
+  ck(cudaEventCreate(&w->ev0), "event");
+  ck(cudaEventCreate(&w->ev1), "event");
+  return w;
+}
+
+namespace {
+
+struct WsLease {
+  fl1_ctx* ctx;
+  std::unique_ptr<Workspace> w;
+  WsLease(fl1_ctx* c, int64_t n, int64_t k, int64_t cap, int64_t sk_elems, int64_t sk_m)
+      : ctx(c), w(c->acquire(n, k, cap, sk_elems, sk_m)) {}
+  ~WsLease() {
+    if (w) ctx->release(std::move(w));
+  }
+};
+
+DevLevel make_level(const ApproxImpl* a) {
+  DevLevel lv{};
+  const DictImpl& d = *a->dict;
+  lv.kind = d.kind;
+  lv.nterms = d.nterms;
+  lv.m = d.m;
+  lv.q = d.q;
+  lv.a = d.a ? d.a->as<double>() : nullptr;
+  lv.left = d.left ? d.left->as<double>() : nullptr;
+  lv.right = d.right ? d.right->as<double>() : nullptr;
+  lv.col_scale = d.col_scale ? d.col_scale->as<double>() : nullptr;
+  lv.eps = a->d_eps->as<double>();
+  lv.an = a->d_an->as<double>();
+  lv.en = a->d_en->as<double>();
+  lv.op_err = a->op_err;
+  lv.rc = a->rc;
+  lv.matvec_flops = d.matvec_flops();
+  return lv;
+}
+
+// A level over a bare dictionary (utility modes): eps = 0 metadata not needed.
+DevLevel make_dict_level(const DictImpl& d) {
+  DevLevel lv{};
+  lv.kind = d.kind;
+  lv.nterms = d.nterms;
+  lv.m = d.m;
+  lv.q = d.q;
+  lv.a = d.a ? d.a->as<double>() : nullptr;
+  lv.left = d.left ? d.left->as<double>() : nullptr;
+  lv.right = d.right ? d.right->as<double>() : nullptr;
+  lv.col_scale = d.col_scale ? d.col_scale->as<double>() : nullptr;
+  lv.matvec_flops = d.matvec_flops();
+  return lv;
+}
+
+int64_t sk_elems_of(const DictImpl& d) {
+  return d.kind == fl1::kSukro ? static_cast<int64_t>(d.nterms) * d.m * d.q : 0;
+}
+
+EngineState run_utility(DictImpl& d, int mode, const double* in_host, double* out_host, size_t out_len) {
+  d.ctx->bind();
+  WsLease lease(d.ctx, d.n, d.k, 1, sk_elems_of(d), d.kind == fl1::kSukro ? d.m : 0);
+  Workspace& w = *lease.w;
+  EngineParams p = w.base;
+  p.mode = mode;
+  p.n_levels = 1;
+  p.lv[0] = make_dict_level(d);
+  p.mode_level = 0;
+  p.gauss0 = d.ctx->gauss0(d.k);
+  EngineState st{};
+  ck(cudaMemcpyAsync(p.st, &st, sizeof(st), cudaMemcpyHostToDevice, w.stream), "state upload");
+  // identity bank
+  std::vector<int32_t> ident(static_cast<size_t>(d.k));
+  for (int64_t j = 0; j < d.k; ++j) ident[static_cast<size_t>(j)] = static_cast<int32_t>(j);
+  ck(cudaMemcpyAsync(p.bank[0].idx, ident.data(), ident.size() * sizeof(int32_t), cudaMemcpyHostToDevice,
+                     w.stream),
+     "ident upload");
+  if (in_host) {
+    const int64_t len = mode == fl1::kModeAdjoint ? d.n : d.k;
+    double* dst = const_cast<double*>(p.x_init);
+    if (mode == fl1::kModeAdjoint) ck(cudaMemsetAsync(dst, 0, static_cast<size_t>(w.ld) * sizeof(double), w.stream), "memset");
+    ck(cudaMemcpyAsync(dst, in_host, static_cast<size_t>(len) * sizeof(double), cudaMemcpyHostToDevice, w.stream),
+       "input upload");
+  }
+  ck(fl1::engine_launch(p, w.sk_m, w.stream), "engine launch");
+  if (out_host)
+    ck(cudaMemcpyAsync(out_host, p.vec_out, out_len * sizeof(double), cudaMemcpyDeviceToHost, w.stream),
+       "output download");
+  ck(cudaMemcpyAsync(&st, p.st, sizeof(st), cudaMemcpyDeviceToHost, w.stream), "state download");
+  ck(cudaStreamSynchronize(w.stream), "sync");
+  return st;
+}
+
+std::shared_ptr<DictImpl> new_dense(fl1_ctx* ctx, const double* a, int64_t n, int64_t k, bool device_src) {
+  if (!ctx) throw std::invalid_argument("null context");
+  if (n < 1 || k < 1) throw std::invalid_argument("dictionary must have at least one row and one column");
+  if (k > std::numeric_limits<int32_t>::max()) throw std::invalid_argument("too many atoms");
+  ctx->bind();
+  auto d = std::make_shared<DictImpl>();
+  d->ctx = ctx;
+  d->kind = fl1::kDense;
+  d->n = n;
+  d->k = k;
+  d->ld = even_ld(n);
+  d->a = std::make_unique<DevBuf>(static_cast<size_t>(d->ld) * static_cast<size_t>(k) * sizeof(double));
+  std::vector<double> host;
+  const double* src = a;
+  if (device_src) {
+    host.resize(static_cast<size_t>(n) * static_cast<size_t>(k));
+    ck(cudaMemcpy(host.data(), a, host.size() * sizeof(double), cudaMemcpyDeviceToHost), "download");
+    src = host.data();
+  }
+  if (d->ld == n) {
+    ck(cudaMemcpy(d->a->p, src, static_cast<size_t>(n) * static_cast<size_t>(k) * sizeof(double),
+                  cudaMemcpyHostToDevice),
+       "dictionary upload");
+  } else {
+    ck(cudaMemset(d->a->p, 0, d->a->bytes), "memset");
+    ck(cudaMemcpy2D(d->a->p, static_cast<size_t>(d->ld) * sizeof(double), src, static_cast<size_t>(n) * sizeof(double),
+                    static_cast<size_t>(n) * sizeof(double), static_cast<size_t>(k), cudaMemcpyHostToDevice),
+       "dictionary upload");
+  }
+  // atom norms (DenseDictionary ctor, dictionary.cpp:63)
+  d->norms.resize(static_cast<size_t>(k));
+  for (int64_t j = 0; j < k; ++j) {
+    double s = 0.0;
+    const double* c = src + j * n;
+    for (int64_t i = 0; i < n; ++i) s += c[i] * c[i];
+    d->norms[static_cast<size_t>(j)] = std::sqrt(s);
+  }
+  return d;
+}
+
+std::unique_ptr<DevBuf> upload(const std::vector<double>& v) {
+  auto b = std::make_unique<DevBuf>(std::max<size_t>(v.size(), 1) * sizeof(double));
+  if (!v.empty()) ck(cudaMemcpy(b->p, v.data(), v.size() * sizeof(double), cudaMemcpyHostToDevice), "upload");
+  return b;
+}
+
+// ---------------------------------------------------------------- solve
+void do_solve(fl1_seq* s, const double* y, bool y_device, double lambda, const fl1_switch_config* cfg,
+              const fl1_run_options* opts, fl1_result** out) {
+  if (!s || !cfg || !opts || !out) throw std::invalid_argument("null argument");
+  s->validate();  // run_lasso (fastl1.cpp:755)
+  const ApproxImpl& exact = *s->lv.back();
+  const DictImpl& ed = *exact.dict;
+  fl1_ctx* ctx = ed.ctx;
+  const int64_t n = ed.n, k = ed.k;
+  for (const auto& l : s->lv) {
+    if (l->dict->ctx != ctx) throw std::invalid_argument("levels live on different contexts");
+    if (l->dict->n != n) throw std::invalid_argument("sequence has mismatched signal lengths");
+  }
+  int64_t sk_elems = 0, sk_m = 0;
+  for (const auto& l : s->lv) {
+    sk_elems = std::max(sk_elems, sk_elems_of(*l->dict));
+    if (l->dict->kind == fl1::kSukro) sk_m = std::max(sk_m, l->dict->m);
+  }
+  if (s->lv.size() > static_cast<size_t>(fl1::kMaxLevels)) throw std::invalid_argument("too many levels");
+  // Engine ctor validation (fastl1.cpp:268-273)
+  if (lambda <= 0) throw std::invalid_argument("lambda must be positive");
+  if (cfg->gamma_threshold <= 0.0 || cfg->gamma_threshold >= 1.0)
+    throw std::invalid_argument("gamma threshold must lie in (0, 1)");
+  if (cfg->screening_interval < 1) throw std::invalid_argument("screening interval must be >= 1");
+  if (opts->solver != FL1_ISTA && opts->solver != FL1_FISTA) throw std::invalid_argument("unknown solver");
+  if (opts->rule != FL1_RULE_GAP && opts->rule != FL1_RULE_DYNAMIC) throw std::invalid_argument("unknown rule");
+  if (opts->variant < FL1_PLAIN || opts->variant > FL1_MULTI_DICT) throw std::invalid_argument("unknown variant");
+  const int levels = static_cast<int>(s->lv.size());
+  const int start_level = opts->variant == FL1_MULTI_DICT ? 0 : levels - 1;
+  if (opts->full_lipschitz && opts->n_full_lipschitz < levels)
+    throw std::invalid_argument("full_lipschitz must list one value per level");
+
+  ctx->bind();
+  const uint64_t want_rows = opts->collect_trace ? cfg->max_iterations : 1;
+  const int64_t cap = static_cast<int64_t>(std::min<uint64_t>(std::max<uint64_t>(want_rows, 1), 1u << 20));
+  WsLease lease(ctx, n, k, cap, sk_elems, sk_m);
+  Workspace& w = *lease.w;
+  EngineParams p = w.base;
+  p.mode = fl1::kModeSolve;
+  p.n_levels = levels;
+  for (int i = 0; i < levels; ++i) p.lv[i] = make_level(s->lv[static_cast<size_t>(i)].get());
+  p.lambda = lambda;
+  p.gamma_threshold = cfg->gamma_threshold;
+  p.interval = cfg->screening_interval;
+  p.precompute_aty = cfg->precompute_aty;
+  p.tol = cfg->tolerance;
+  p.rel_tol = cfg->rel_tolerance;
+  p.max_it = cfg->max_iterations;
+  p.solver = opts->solver;
+  p.rule = opts->rule;
+  p.variant = opts->variant;
+  p.has_full_l = opts->full_lipschitz != nullptr;
+  for (int i = 0; i < levels && p.has_full_l; ++i) p.full_l[i] = opts->full_lipschitz[i];
+  p.collect_trace = opts->collect_trace ? 1 : 0;
+  p.observe = opts->observer ? 1 : 0;
+  p.has_x_init = opts->x_init ? 1 : 0;
+  p.gauss0 = ctx->gauss0(k);
+  p.trace_cap = w.trace_cap;
+
+  auto res = std::make_unique<fl1_result>();
+  res->k = k;
+  EngineState st{};
+  st.dict_index = start_level;
+  st.t_k = 1.0;
+
+  ck(cudaEventRecord(w.ev0, w.stream), "event");
+  ck(cudaMemcpyAsync(p.st, &st, sizeof(st), cudaMemcpyHostToDevice, w.stream), "state upload");
+  ck(cudaMemsetAsync(const_cast<double*>(p.y), 0, static_cast<size_t>(w.ld) * sizeof(double), w.stream), "memset");
+  ck(cudaMemcpyAsync(const_cast<double*>(p.y), y, static_cast<size_t>(n) * sizeof(double),
+                     y_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, w.stream),
+     "y upload");
+  if (opts->x_init)
+    ck(cudaMemcpyAsync(const_cast<double*>(p.x_init), opts->x_init, static_cast<size_t>(k) * sizeof(double),
+                       cudaMemcpyHostToDevice, w.stream),
+       "x_init upload");
+  std::vector<fl1_trace_row> host_rows;
+  int64_t launches = 0;
+  std::vector<int32_t> h_idx;
+  std::vector<int8_t> h_keep;
+  std::vector<double> h_rho, h_y;
+  while (true) {
+    ck(fl1::engine_launch(p, w.sk_m, w.stream), "engine launch");
+    ++launches;
+    ck(cudaMemcpyAsync(&st, p.st, sizeof(st), cudaMemcpyDeviceToHost, w.stream), "state download");
+    ck(cudaStreamSynchronize(w.stream), "engine sync");
+    if (st.event == fl1::kEvTraceFull || st.event == fl1::kEvDone) {
+      if (p.collect_trace && st.n_trace > 0) {
+        const size_t old = host_rows.size();
+        host_rows.resize(old + static_cast<size_t>(st.n_trace));
+        ck(cudaMemcpy(host_rows.data() + old, p.trace, static_cast<size_t>(st.n_trace) * sizeof(fl1_trace_row),
+                      cudaMemcpyDeviceToHost),
+           "trace download");
+        st.trace_base += static_cast<uint64_t>(st.n_trace);
+        st.n_trace = 0;
+      }
+    }
+    if (st.event == fl1::kEvObserve) {
+      // ScreeningEvent (fastl1.cpp:704-734) from the device snapshot
+      const int64_t S0 = st.obs_S;
+      const fl1::Bank& ob = p.bank[st.obs_bank];
+      h_idx.resize(static_cast<size_t>(S0));
+      h_keep.resize(static_cast<size_t>(S0));
+      h_rho.resize(static_cast<size_t>(w.ld));
+      if (S0 > 0) {
+        ck(cudaMemcpy(h_idx.data(), ob.idx, static_cast<size_t>(S0) * sizeof(int32_t), cudaMemcpyDeviceToHost), "obs");
+        ck(cudaMemcpy(h_keep.data(), ob.keep, static_cast<size_t>(S0), cudaMemcpyDeviceToHost), "obs");
+      }
+      ck(cudaMemcpy(h_rho.data(), p.rho, static_cast<size_t>(w.ld) * sizeof(double), cudaMemcpyDeviceToHost), "obs");
+      if (h_y.empty()) {
+        h_y.resize(static_cast<size_t>(n));
+        ck(cudaMemcpy(h_y.data(), p.y, static_cast<size_t>(n) * sizeof(double), cudaMemcpyDeviceToHost), "obs");
+      }
+      const std::vector<double>& ray = st.obs_ray_is_y ? h_y : h_rho;
+      std::vector<double> tp(static_cast<size_t>(n)), tt(static_cast<size_t>(n)), center(static_cast<size_t>(n));
+      for (int64_t i = 0; i < n; ++i) {
+        tp[static_cast<size_t>(i)] = st.obs_scale_prime * ray[static_cast<size_t>(i)];
+        tt[static_cast<size_t>(i)] = st.obs_scale_tilde * ray[static_cast<size_t>(i)];
+        center[static_cast<size_t>(i)] =
+            opts->rule == FL1_RULE_GAP ? tp[static_cast<size_t>(i)] : h_y[static_cast<size_t>(i)] / lambda;
+      }
+      std::vector<int32_t> kept;
+      for (int64_t q = 0; q < S0; ++q)
+        if (h_keep[static_cast<size_t>(q)]) kept.push_back(h_idx[static_cast<size_t>(q)]);
+      fl1_screen_event ev{};
+      ev.iter = st.obs_iter;
+      ev.dict_index = st.obs_dict;
+      ev.n = n;
+      ev.center = center.data();
+      ev.radius = st.obs_radius;
+      ev.theta_prime = tp.data();
+      ev.theta_tilde = tt.data();
+      ev.scale_prime = st.obs_scale_prime;
+      ev.scale_tilde = st.obs_scale_tilde;
+      ev.n_active_before = S0;
+      ev.active_before = h_idx.data();
+      ev.n_kept = static_cast<int64_t>(kept.size());
+      ev.kept = kept.data();
+      opts->observer(&ev, opts->observer_user);
+      st.obs_pending = 0;
+    }
+    if (st.done) break;
+    // resume: push the edited state back
+    st.event = fl1::kEvNone;
+    p.mode = fl1::kModeResume;
+    ck(cudaMemcpyAsync(p.st, &st, sizeof(st), cudaMemcpyHostToDevice, w.stream), "state upload");
+  }
+  // finish (fastl1.cpp:741-748)
+  const fl1::Bank& fb = p.bank[st.cur];
+  std::vector<int32_t> idx(static_cast<size_t>(st.S));
+  std::vector<double> xs(static_cast<size_t>(st.S));
+  if (st.S > 0) {
+    ck(cudaMemcpyAsync(idx.data(), fb.idx, idx.size() * sizeof(int32_t), cudaMemcpyDeviceToHost, w.stream), "x");
+    ck(cudaMemcpyAsync(xs.data(), fb.x, xs.size() * sizeof(double), cudaMemcpyDeviceToHost, w.stream), "x");
+  }
+  std::vector<fl1_switch_event> sws(static_cast<size_t>(st.n_switches));
+  if (st.n_switches > 0)
+    ck(cudaMemcpyAsync(sws.data(), p.sw, sws.size() * sizeof(fl1_switch_event), cudaMemcpyDeviceToHost, w.stream),
+       "switches");
+  ck(cudaEventRecord(w.ev1, w.stream), "event");
+  ck(cudaStreamSynchronize(w.stream), "finish sync");
+  float ms = 0.f;
+  ck(cudaEventElapsedTime(&ms, w.ev0, w.ev1), "elapsed");
+  res->x.assign(static_cast<size_t>(k), 0.0);
+  for (size_t q = 0; q < idx.size(); ++q) res->x[static_cast<size_t>(idx[q])] = xs[q];
+  res->final_active = std::move(idx);
+  res->converged = st.converged != 0;
+  res->iterations = st.converged ? st.t : cfg->max_iterations;
+  res->final_gap = st.converged ? st.final_gap : std::numeric_limits<double>::quiet_NaN();
+  res->total_flops = st.ledger;
+  res->gap_warning = st.warning != 0;
+  res->trace = std::move(host_rows);
+  res->switches = std::move(sws);
+  res->device_ms = ms;
+  res->setup_ms = (st.t0_ns - st.start_ns) * 1e-6;
+  res->launches = launches;
+  res->power_steps = st.power_steps;
+  for (int i = 0; i < 5; ++i) res->prof[i] = st.prof_ns[i];
+  res->prof[5] = st.prof_bytes;
+  *out = res.release();
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* fl1_last_error(void) { return g_err.c_str(); }
+const char* fl1_version(void) { return "fl1cuda 0.1 (sm_100a persistent engine)"; }
+
+int fl1_ctx_create(int device, fl1_ctx** out) {
+  return guard([&] {
+    if (!out) throw std::invalid_argument("null out");
+    int count = 0;
+    ck(cudaGetDeviceCount(&count), "cudaGetDeviceCount");
+    if (device < 0 || device >= count) throw std::invalid_argument("no such CUDA device");
+    auto c = std::make_unique<fl1_ctx>();
+    c->device = device;
+    c->bind();
+    ck(cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, device), "attr");
+    int l2 = 0;
+    ck(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, device), "attr");
+    c->l2 = l2;
+    size_t fr = 0, tot = 0;
+    ck(cudaMemGetInfo(&fr, &tot), "meminfo");
+    c->hbm = static_cast<int64_t>(tot);
+    *out = c.release();
+  });
+}
+int fl1_ctx_destroy(fl1_ctx* ctx) {
+  return guard([&] {
+    if (!ctx) return;
+    ctx->bind();
+    delete ctx;
+  });
+}
+int fl1_ctx_info(fl1_ctx* ctx, int32_t* sm_count, int64_t* l2_bytes, int64_t* hbm_bytes) {
+  return guard([&] {
+    if (sm_count) *sm_count = ctx->sms;
+    if (l2_bytes) *l2_bytes = ctx->l2;
+    if (hbm_bytes) *hbm_bytes = ctx->hbm;
+  });
+}
+
+int fl1_dict_dense(fl1_ctx* ctx, const double* a, int64_t n, int64_t k, fl1_dict** out) {
+  return guard([&] { *out = new fl1_dict{new_dense(ctx, a, n, k, false)}; });
+}
+int fl1_dict_dense_device(fl1_ctx* ctx, const double* a, int64_t n, int64_t k, fl1_dict** out) {
+  return guard([&] { *out = new fl1_dict{new_dense(ctx, a, n, k, true)}; });
+}
+int fl1_dict_sukro(fl1_ctx* ctx, int32_t n_terms, int64_t m, int64_t q, const double* const* left,
+                   const double* const* right, const double* col_scale, fl1_dict** out) {
+  return guard([&] {
+    if (!ctx) throw std::invalid_argument("null context");
+    if (n_terms < 1) throw std::invalid_argument("SuKro needs at least one term");
+    if (m < 1 || q < 1) throw std::invalid_argument("empty SuKro factor");
+    if (m > fl1::kSukroMaxM || q > fl1::kSukroMaxQ)
+      throw std::logic_error("SuKro factors larger than 128 x 256 are not supported by this build");
+    if (q * q > std::numeric_limits<int32_t>::max()) throw std::invalid_argument("too many atoms");
+    ctx->bind();
+    auto d = std::make_shared<DictImpl>();
+    d->ctx = ctx;
+    d->kind = fl1::kSukro;
+    d->m = m;
+    d->q = q;
+    d->n = m * m;
+    d->k = q * q;
+    d->ld = even_ld(d->n);
+    d->nterms = n_terms;
+    const size_t blk = static_cast<size_t>(m * q);
+    d->h_left.resize(blk * static_cast<size_t>(n_terms));
+    d->h_right.resize(blk * static_cast<size_t>(n_terms));
+    for (int t = 0; t < n_terms; ++t) {
+      std::copy(left[t], left[t] + blk, d->h_left.begin() + static_cast<long>(blk) * t);
+      std::copy(right[t], right[t] + blk, d->h_right.begin() + static_cast<long>(blk) * t);
+    }
+    if (col_scale) d->h_scale.assign(col_scale, col_scale + d->k);
+    d->left = upload(d->h_left);
+    d->right = upload(d->h_right);
+    if (col_scale) d->col_scale = upload(d->h_scale);
+    // atom norms from the explicit columns (host, setup only)
+    d->norms.resize(static_cast<size_t>(d->k));
+    for (int64_t j = 0; j < d->k; ++j) {
+      const int64_t jb = j / q, jc = j % q;
+      double s2 = 0.0;
+      for (int64_t rb = 0; rb < m; ++rb)
+        for (int64_t rc = 0; rc < m; ++rc) {
+          double v = 0.0;
+          for (int t = 0; t < n_terms; ++t)
+            v += d->h_left[blk * static_cast<size_t>(t) + static_cast<size_t>(jb * m + rb)] *
+                 d->h_right[blk * static_cast<size_t>(t) + static_cast<size_t>(jc * m + rc)];
+          if (col_scale) v *= d->h_scale[static_cast<size_t>(j)];
+          s2 += v * v;
+        }
+      d->norms[static_cast<size_t>(j)] = std::sqrt(s2);
+    }
+    *out = new fl1_dict{d};
+  });
+}
+int fl1_dict_destroy(fl1_dict* d) {
+  return guard([&] { delete d; });
+}
+int fl1_dict_shape(const fl1_dict* d, int64_t* rows, int64_t* cols) {
+  return guard([&] {
+    *rows = d->d->n;
+    *cols = d->d->k;
+  });
+}
+int fl1_dict_is_dense(const fl1_dict* d) { return d->d->kind == fl1::kDense ? 1 : 0; }
+uint64_t fl1_dict_matvec_flops(const fl1_dict* d) { return d->d->matvec_flops(); }
+int fl1_dict_atom_norms(const fl1_dict* d, double* out) {
+  return guard([&] { std::copy(d->d->norms.begin(), d->d->norms.end(), out); });
+}
+int fl1_dict_apply(fl1_dict* d, const double* x, double* out) {
+  return guard([&] { run_utility(*d->d, fl1::kModeApply, x, out, static_cast<size_t>(d->d->n)); });
+}
+int fl1_dict_apply_adjoint(fl1_dict* d, const double* r, double* out) {
+  return guard([&] { run_utility(*d->d, fl1::kModeAdjoint, r, out, static_cast<size_t>(d->d->k)); });
+}
+int fl1_dict_column(fl1_dict* dh, int64_t j, double* out) {
+  return guard([&] {
+    const DictImpl& d = *dh->d;
+    if (j < 0 || j >= d.k) throw std::invalid_argument("column index out of range");
+    d.ctx->bind();
+    if (d.kind == fl1::kDense) {
+      ck(cudaMemcpy(out, d.a->as<double>() + j * d.ld, static_cast<size_t>(d.n) * sizeof(double),
+                    cudaMemcpyDeviceToHost),
+         "column download");
+      return;
+    }
+    const size_t blk = static_cast<size_t>(d.m * d.q);
+    const int64_t jb = j / d.q, jc = j % d.q;
+    std::fill(out, out + d.n, 0.0);
+    for (int t = 0; t < d.nterms; ++t)
+      for (int64_t rb = 0; rb < d.m; ++rb) {
+        const double bv = d.h_left[blk * static_cast<size_t>(t) + static_cast<size_t>(jb * d.m + rb)];
+        for (int64_t rc = 0; rc < d.m; ++rc)
+          out[rb * d.m + rc] += bv * d.h_right[blk * static_cast<size_t>(t) + static_cast<size_t>(jc * d.m + rc)];
+      }
+    if (!d.h_scale.empty())
+      for (int64_t i = 0; i < d.n; ++i) out[i] *= d.h_scale[static_cast<size_t>(j)];
+  });
+}
+
+int fl1_approx_create(fl1_dict* d, const double* eps, double op_err, double rc, const double* an,
+                      const double* en, fl1_approx** out) {
+  return guard([&] {
+    if (!d || !eps || !an || !en) throw std::invalid_argument("null argument");
+    auto a = std::make_shared<ApproxImpl>();
+    const int64_t k = d->d->k;
+    a->dict = d->d;
+    a->eps.assign(eps, eps + k);
+    a->an.assign(an, an + k);
+    a->en.assign(en, en + k);
+    a->op_err = op_err;
+    a->rc = rc;
+    d->d->ctx->bind();
+    a->d_eps = upload(a->eps);
+    a->d_an = upload(a->an);
+    a->d_en = upload(a->en);
+    *out = new fl1_approx{a};
+  });
+}
+int fl1_approx_exact(fl1_dict* d, fl1_approx** out) {  // make_exact_approx (dictionary.cpp:216-225)
+  return guard([&] {
+    if (!d) throw std::invalid_argument("null argument");
+    if (d->d->kind != fl1::kDense) throw std::invalid_argument("make_exact_approx needs a dense dictionary");
+    auto a = std::make_shared<ApproxImpl>();
+    a->dict = d->d;
+    a->eps.assign(static_cast<size_t>(d->d->k), 0.0);
+    a->an = d->d->norms;
+    a->en = d->d->norms;
+    a->op_err = 0.0;
+    a->rc = 1.0;
+    d->d->ctx->bind();
+    a->d_eps = upload(a->eps);
+    a->d_an = upload(a->an);
+    a->d_en = upload(a->en);
+    *out = new fl1_approx{a};
+  });
+}
+int fl1_approx_destroy(fl1_approx* a) {
+  return guard([&] { delete a; });
+}
+int fl1_seq_create(fl1_approx* const* levels, int32_t n_levels, fl1_seq** out) {
+  return guard([&] {
+    auto s = std::make_unique<fl1_seq>();
+    for (int i = 0; i < n_levels; ++i) {
+      if (!levels[i]) throw std::invalid_argument("null level");
+      s->lv.push_back(levels[i]->a);
+    }
+    s->validate();
+    *out = s.release();
+  });
+}
+int fl1_seq_destroy(fl1_seq* s) {
+  return guard([&] { delete s; });
+}
+
+int fl1_solve(fl1_seq* s, const double* y, double lambda, const fl1_switch_config* cfg,
+              const fl1_run_options* opts, fl1_result** out) {
+  return guard([&] { do_solve(s, y, false, lambda, cfg, opts, out); });
+}
+int fl1_solve_device(fl1_seq* s, const double* y, double lambda, const fl1_switch_config* cfg,
+                     const fl1_run_options* opts, fl1_result** out) {
+  return guard([&] { do_solve(s, y, true, lambda, cfg, opts, out); });
+}
+int fl1_result_info_get(const fl1_result* r, fl1_result_info* o) {
+  return guard([&] {
+    *o = fl1_result_info{};
+    o->k = r->k;
+    o->converged = r->converged;
+    o->gap_warning = r->gap_warning;
+    o->final_gap = r->final_gap;
+    o->iterations = r->iterations;
+    o->total_flops = r->total_flops;
+    o->n_trace = static_cast<int64_t>(r->trace.size());
+    o->n_switches = static_cast<int64_t>(r->switches.size());
+    o->n_final_active = static_cast<int64_t>(r->final_active.size());
+    o->device_ms = r->device_ms;
+    o->setup_ms = r->setup_ms;
+    o->kernel_launches = r->launches;
+    o->power_iterations = r->power_steps;
+  });
+}
+int fl1_result_x(const fl1_result* r, double* out) {
+  return guard([&] { std::copy(r->x.begin(), r->x.end(), out); });
+}
+int fl1_result_trace(const fl1_result* r, fl1_trace_row* out) {
+  return guard([&] { std::copy(r->trace.begin(), r->trace.end(), out); });
+}
+int fl1_result_switches(const fl1_result* r, fl1_switch_event* out) {
+  return guard([&] { std::copy(r->switches.begin(), r->switches.end(), out); });
+}
+int fl1_result_final_active(const fl1_result* r, int32_t* out) {
+  return guard([&] { std::copy(r->final_active.begin(), r->final_active.end(), out); });
+}
+int fl1_result_profile(const fl1_result* r, double* out) {
+  return guard([&] { std::copy(r->prof, r->prof + 6, out); });
+}
+void fl1_result_free(fl1_result* r) { delete r; }
+
+int fl1_lambda_max(fl1_dict* d, const double* y, double* out) {  // screening.cpp:9-11
+  return guard([&] {
+    std::vector<double> c(static_cast<size_t>(d->d->k));
+    run_utility(*d->d, fl1::kModeAdjoint, y, c.data(), c.size());
+    double m = 0.0;
+    for (double e : c) m = std::max(m, std::abs(e));
+    *out = m;
+  });
+}
+int fl1_lipschitz_bound(fl1_dict* d, double* out) {  // solver.cpp:108-114
+  return guard([&] {
+    const EngineState st = run_utility(*d->d, fl1::kModePower, nullptr, nullptr, 0);
+    *out = st.power_est * 1.05;
+  });
+}
+int fl1_screen_precomputed(fl1_ctx* ctx, int64_t n, const double* dots, const double* eps, const double* en,
+                           const double* an, double cn, double r, int32_t* kept, int64_t* n_kept,
+                           int64_t* lookahead) {
+  return guard([&] {
+    ctx->bind();
+    const size_t b = static_cast<size_t>(std::max<int64_t>(n, 1)) * sizeof(double);
+    DevBuf dd(b), de(b), den(b), dan(b), keep(b), look(b);
+    if (n > 0) {
+      ck(cudaMemcpy(dd.p, dots, static_cast<size_t>(n) * 8, cudaMemcpyHostToDevice), "up");
+      ck(cudaMemcpy(de.p, eps, static_cast<size_t>(n) * 8, cudaMemcpyHostToDevice), "up");
+      ck(cudaMemcpy(den.p, en, static_cast<size_t>(n) * 8, cudaMemcpyHostToDevice), "up");
+      ck(cudaMemcpy(dan.p, an, static_cast<size_t>(n) * 8, cudaMemcpyHostToDevice), "up");
+      ck(fl1::screen_kernel_launch(n, dd.as<double>(), de.as<double>(), den.as<double>(), dan.as<double>(), cn, r,
+                                   keep.as<int8_t>(), look.as<int8_t>(), nullptr),
+         "screen kernel");
+    }
+    std::vector<int8_t> hk(static_cast<size_t>(n)), hl(static_cast<size_t>(n));
+    if (n > 0) {
+      ck(cudaMemcpy(hk.data(), keep.p, static_cast<size_t>(n), cudaMemcpyDeviceToHost), "down");
+      ck(cudaMemcpy(hl.data(), look.p, static_cast<size_t>(n), cudaMemcpyDeviceToHost), "down");
+    }
+    int64_t w = 0, la = 0;
+    for (int64_t j = 0; j < n; ++j) {
+      if (hk[static_cast<size_t>(j)]) kept[w++] = static_cast<int32_t>(j);
+      la += hl[static_cast<size_t>(j)];
+    }
+    *n_kept = w;
+    *lookahead = la;
+  });
+}
+
+// ---- scalar formulas (host)
+double fl1_soft_threshold(double z, double u) {
+  const double mag = std::abs(z) - u;
+  if (mag <= 0.0) return 0.0;
+  return z > 0.0 ? mag : -mag;
+}
+double fl1_gap_ratio(double gt, double gp) {
+  if (gp <= 1e-15) return 0.0;
+  return std::min(std::max(gt / gp, 0.0), 1.0);
+}
+int fl1_switch_dictionary(int i, int last, double gamma, double gthr, int64_t la, double rc, int64_t ta) {
+  if (i >= last) return last;
+  if (static_cast<double>(la) <= rc * static_cast<double>(ta)) return last;
+  if (gamma <= gthr) return i + 1;
+  return i;
+}
+uint64_t fl1_flops_plain(uint64_t k, uint64_t n, uint64_t z) { return (k + z) * n + 4 * k + n; }
+uint64_t fl1_flops_screened(uint64_t a, uint64_t n, uint64_t z) { return (a + z) * n + 6 * a + 5 * n; }
+uint64_t fl1_flops_stable(uint64_t mv, uint64_t n, uint64_t a, uint64_t z) { return mv + z * n + 8 * a + 7 * n; }
+uint64_t fl1_recompute_flops(const fl1_trace_row* trace, int64_t n_rows, const fl1_seq* s, int32_t variant,
+                             int64_t n, int64_t k, int32_t* rows_match) {
+  const auto un = static_cast<uint64_t>(n), uk = static_cast<uint64_t>(k);
+  const int last = static_cast<int>(s->lv.size()) - 1;
+  uint64_t total = 0;
+  bool all = true;
+  for (int64_t r = 0; r < n_rows; ++r) {
+    const fl1_trace_row& row = trace[r];
+    const auto a = static_cast<uint64_t>(row.active_size), z = static_cast<uint64_t>(row.x_nnz);
+    if (variant == FL1_PLAIN) total += fl1_flops_plain(uk, un, z);
+    else if (variant == FL1_SCREENED) total += fl1_flops_screened(a, un, z);
+    else if (row.dict_index < last)
+      total += fl1_flops_stable(s->lv[static_cast<size_t>(row.dict_index)]->dict->matvec_flops(), un, a, z);
+    else total += fl1_flops_screened(a, un, z);
+    all = all && total == row.flops_cum;
+  }
+  if (rows_match) *rows_match = all ? 1 : 0;
+  return total;
+}
+double fl1_stable_gap_delta(double rn, double e, double x1) { return rn * e * x1 + 0.5 * e * e * x1 * x1; }
+double fl1_sphere_test(double d, double an, double r) { return d + r * an; }
+double fl1_stable_zone_test(double d, double eps, double cn, double en, double r) { return d + eps * cn + r * en; }
+double fl1_stable_ball_test(double d, double eps, double cn, double an, double r) {
+  return d + eps * cn + r * an + r * eps;
+}
+
+}  // extern "C"

@@ -1,0 +1,1468 @@
+// engine.cu — the FastL1 iteration loop as ONE persistent cooperative kernel.
+//
+// Reference path replaced: Engine::run and everything it calls per iteration
+// (fastl1.cpp:459-645): compute_products (359-394), dual_scalars/dual_of
+// (406-457), the GAP / Dynamic sphere tests (494-566, screening.cpp:103-106,
+// 136-150), the switching rule (26-38, 556-565), the prox / FISTA update
+// (572-591, solver.cpp:9-13), apply_restriction + ActiveOp compaction
+// (667-702, 115-129, 176-201), ActiveOp::apply / apply_adjoint for dense and
+// SuKro operators (131-161, dictionary.cpp:150-164), the restricted power
+// iteration (326-333, solver.cpp:72-104) and the ledger / trace (611-623).
+//
+// Layout: one CTA of 512 threads per SM, launched cooperatively. One
+// iteration is four grid-wide phases separated by grid.sync():
+//   A  rho_g = y - ((1+m)u - m v) built redundantly in every CTA's shared
+//      memory; A_S^T rho_g streams every preserved column ONCE: each CTA owns
+//      a contiguous column range, each warp a contiguous range of 4 KiB units
+//      inside it, loads are 128-bit and software-pipelined one unit ahead, the
+//      dot is a warp-shuffle reduction, and columns split between warps are
+//      merged in shared memory in warp order. The pass also emits the per-CTA
+//      maxima of |corr_j| and |corr_j| + eps_j ||rho_g|| (dual scaling).
+//   B  every CTA reduces the per-CTA partials in the same fixed order, so all
+//      CTAs hold bit-identical scales, gaps, stop / screen / switch decisions;
+//      per-atom sphere test, soft-threshold and FISTA update on a CTA slice.
+//   D  stream compaction of the preserved set into the other bank; the
+//      sparse apply u = A_S x as (row tile x position chunk) partials plus the
+//      v-history fix for dropped atoms; ledger + trace row.
+//   E  partials combined by row slices into u (and v <- u_old - fix).
+// Restricted power iterations (halvings) and dictionary switches run in the
+// same kernel. No reduction uses floating-point atomics: every sum has a
+// fixed order, so a solve is bit-reproducible on a given device.
+#include <cooperative_groups.h>
+#include <cuda_runtime.h>
+#include <math_constants.h>
+
+#include <algorithm>
+#include <cfloat>
+#include <cmath>
+#include <cstdint>
+
+#include "engine.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace fl1 {
+namespace {
+
+constexpr unsigned kFull = 0xffffffffu;
+constexpr int64_t kRedundantCombine = 8192;  // doubles of partials each CTA may re-sum instead of a sync
+
+// per-CTA partial slots (bred[cta * kBred + slot])
+enum Slot {
+  kSlMaxPlain = 0,
+  kSlMaxStable = 1,
+  kSlL1 = 2,
+  kSlKept = 3,
+  kSlLook = 4,
+  kSlNnz = 5,
+  kSlMaxEps = 6,
+  kSlPw2 = 7,
+  kSlPvw = 8,
+  kSlSum = 9,
+  kSlMaxPlainY = 10,
+  kSlMaxStableY = 11,
+  kSlLead2 = 12,
+};
+
+struct Frag {
+  int64_t pos;
+  double sum;
+};
+
+struct Sh {
+  EngineState s;
+  double red[kWarps * 4];
+  double res[kBred];
+  // per-iteration scalars (identical in every CTA)
+  double t_next;
+  double rho_sq, rho_dot_y, rho_x_sq, rho_norm;
+  double scale_prime, scale_tilde, ray_sq, ray_dot_y;
+  double gap_prime, gap_tilde, primal, x_l1;
+  double radius, center_norm, gamma;
+  int ray_is_y, stop_now, screen_now, stable_test, next_dict, speed;
+  int64_t S_new, look, nnz;
+  int64_t scan_base;
+  int32_t wscan[kWarps];
+  int32_t wcount[2][kWarps];
+  Frag frag[kWarps][2];
+  int32_t nfrag[kWarps];
+};
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(kFull, v, o);
+  return v;  // valid in lane 0
+}
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_down_sync(kFull, v, o));
+  return v;
+}
+
+// Deterministic block reduction of up to 4 values (sum or max per value).
+template <int NV>
+__device__ void block_reduce(double (&v)[NV], const bool (&is_max)[NV], Sh& sh) {
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+#pragma unroll
+  for (int q = 0; q < NV; ++q) v[q] = is_max[q] ? warp_max(v[q]) : warp_sum(v[q]);
+  __syncthreads();
+  if (l == 0) {
+#pragma unroll
+    for (int q = 0; q < NV; ++q) sh.red[q * kWarps + w] = v[q];
+  }
+  __syncthreads();
+  if (w == 0) {
+#pragma unroll
+    for (int q = 0; q < NV; ++q) {
+      double r = l < kWarps ? sh.red[q * kWarps + l] : (is_max[q] ? -DBL_MAX : 0.0);
+      r = is_max[q] ? warp_max(r) : warp_sum(r);
+      if (l == 0) sh.red[q * kWarps] = r;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < NV; ++q) v[q] = sh.red[q * kWarps];
+  __syncthreads();
+}
+
+// Reduce per-CTA partial slots in a fixed order; warp `slot` handles one slot.
+__device__ void grid_reduce(const EngineParams& p, Sh& sh, unsigned mask_sum, unsigned mask_max) {
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  for (int slot = w; slot < kBred; slot += kWarps) {
+    if (!(((mask_sum | mask_max) >> slot) & 1u)) continue;
+    const bool mx = (mask_max >> slot) & 1u;
+    double acc = mx ? -DBL_MAX : 0.0;
+    for (int b = l; b < p.grid; b += 32) {
+      const double e = __ldcg(p.bred + static_cast<int64_t>(b) * kBred + slot);
+      acc = mx ? fmax(acc, e) : acc + e;
+    }
+    acc = mx ? warp_max(acc) : warp_sum(acc);
+    if (l == 0) sh.res[slot] = acc;
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ void put_slot(const EngineParams& p, int slot, double v) {
+  __stcg(p.bred + static_cast<int64_t>(blockIdx.x) * kBred + slot, v);
+}
+
+__device__ __forceinline__ double2 ldg_stream2(const double2* ptr) {
+  double2 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];" : "=d"(r.x), "=d"(r.y) : "l"(ptr));
+  return r;
+}
+
+__device__ __forceinline__ double soft_threshold(double z, double u) {  // solver.cpp:9-13
+  const double mag = fabs(z) - u;
+  if (mag <= 0.0) return 0.0;
+  return z > 0.0 ? mag : -mag;
+}
+
+// CTA slice [lo, hi) of n items (balanced, contiguous).
+__device__ __forceinline__ void slice(int64_t n, int64_t& lo, int64_t& hi) {
+  lo = n * blockIdx.x / gridDim.x;
+  hi = n * (blockIdx.x + 1) / gridDim.x;
+}
+
+__device__ __forceinline__ double globaltimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return static_cast<double>(t);
+}
+
+// What an adjoint pass emits besides out[pos].
+struct PassOut {
+  double* out;
+  int track;             // per-CTA maxima of |out| and |out| + eps*eps_scale
+  double eps_scale;
+  bool div_lambda;       // maxima of |out|/lambda (exact-fit branch, fastl1.cpp:440-446)
+  int slot_plain, slot_stable;
+  const double* vdot;    // non-null: per-CTA sums of out^2 and vdot*out (power iteration)
+};
+
+struct PassAcc {
+  double mp = 0.0, ms = 0.0, w2 = 0.0, vw = 0.0;
+  __device__ __forceinline__ void add(const EngineParams& p, const PassOut& po, const double* eps, int64_t pos,
+                                      double total, bool store = false) {
+    if (store) __stcg(po.out + pos, total);
+    if (po.track) {
+      const double ac = po.div_lambda ? fabs(total) / p.lambda : fabs(total);
+      mp = fmax(mp, ac);
+      ms = fmax(ms, ac + eps[pos] * po.eps_scale);
+    }
+    if (po.vdot) {
+      w2 = fma(total, total, w2);
+      vw = fma(po.vdot[pos], total, vw);
+    }
+  }
+};
+
+__device__ void finish_pass(const EngineParams& p, Sh& sh, const PassOut& po, PassAcc& acc) {
+  if (po.track) {
+    double v[2] = {acc.mp, acc.ms};
+    const bool mx[2] = {true, true};
+    block_reduce<2>(v, mx, sh);
+    if (threadIdx.x == 0) {
+      put_slot(p, po.slot_plain, v[0]);
+      put_slot(p, po.slot_stable, v[1]);
+    }
+  }
+  if (po.vdot) {
+    double v[2] = {acc.w2, acc.vw};
+    const bool mx[2] = {false, false};
+    block_reduce<2>(v, mx, sh);
+    if (threadIdx.x == 0) {
+      put_slot(p, kSlPw2, v[0]);
+      put_slot(p, kSlPvw, v[1]);
+    }
+  }
+}
+
+// ----------------------------------------------------------------------------
+// Dense adjoint over the preserved columns: out[pos] = a_{idx[pos]} . r, with
+// r (length ld, zero padded) in shared memory (ActiveOp::apply_adjoint 148-161).
+// ----------------------------------------------------------------------------
+__device__ __noinline__ void dense_adjoint(const EngineParams& p, Sh& sh, const DevLevel& lv,
+                                           const int32_t* __restrict__ idx, const double* __restrict__ eps, int64_t S,
+                                           const double* __restrict__ r, const PassOut& po) {
+  const int64_t n = p.n;
+  const int U = static_cast<int>((n + kUnit - 1) / kUnit);
+  const int last_nd2 = static_cast<int>(((n - static_cast<int64_t>(U - 1) * kUnit) + 1) >> 1);
+  const int64_t ld2 = p.ld >> 1;
+  int64_t c0, c1;
+  slice(S, c0, c1);
+  const int Ub = static_cast<int>((c1 - c0) * U);  // units of this CTA (< 2^31 by construction)
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  const int u_lo = static_cast<int>(static_cast<int64_t>(Ub) * w / kWarps);
+  const int u_hi = static_cast<int>(static_cast<int64_t>(Ub) * (w + 1) / kWarps);
+  const double2* __restrict__ A2 = reinterpret_cast<const double2*>(lv.a) + l;
+  const double2* __restrict__ r2 = reinterpret_cast<const double2*>(r) + l;
+  double* __restrict__ out = po.out;
+  PassAcc acc;
+  int nf = 0;
+  // Units are visited in order; three register buffers form a ring so two
+  // units' 128-bit loads are in flight while the current unit is reduced.
+  constexpr int kV = kUnit / 64;  // double2 loads per lane per unit
+  auto issue = [&](double2 (&b)[kV], int u) {
+    const int cl = u / U, h = u - cl * U;
+    const double2* src = A2 + static_cast<int64_t>(__ldg(idx + c0 + cl)) * ld2 + h * (kUnit / 2);
+    if (h != U - 1 || last_nd2 == kUnit / 2) {
+#pragma unroll
+      for (int q = 0; q < kV; ++q) b[q] = ldg_stream2(src + 32 * q);
+    } else {
+#pragma unroll
+      for (int q = 0; q < kV; ++q) b[q] = (l + 32 * q < last_nd2) ? ldg_stream2(src + 32 * q) : make_double2(0.0, 0.0);
+    }
+  };
+  double s = 0.0;
+  bool began_here = (u_lo % U) == 0;
+  auto consume = [&](const double2 (&b)[kV], int u) {
+    const int cl = u / U, h = u - cl * U;
+    const double2* rr = r2 + h * (kUnit / 2);
+#pragma unroll
+    for (int q = 0; q < kV; ++q) {
+      const double2 rv = rr[32 * q];
+      s = fma(b[q].x, rv.x, s);
+      s = fma(b[q].y, rv.y, s);
+    }
+    const bool col_end = h == U - 1;
+    if (col_end || u + 1 == u_hi) {
+      const double t = warp_sum(s);
+      const bool whole = col_end && began_here;
+      if (l == 0) {
+        if (whole) {
+          out[c0 + cl] = t;
+        } else {
+          sh.frag[w][nf].pos = c0 + cl;
+          sh.frag[w][nf].sum = t;
+        }
+      }
+      if (!whole) ++nf;
+      s = 0.0;
+      began_here = true;
+    }
+  };
+  if (u_lo < u_hi) {
+    double2 b0[kV], b1[kV], b2[kV];
+    issue(b0, u_lo);
+    if (u_lo + 1 < u_hi) issue(b1, u_lo + 1);
+    int u = u_lo;
+    while (true) {
+      if (u + 2 < u_hi) issue(b2, u + 2);
+      consume(b0, u);
+      if (++u >= u_hi) break;
+      if (u + 2 < u_hi) issue(b0, u + 2);
+      consume(b1, u);
+      if (++u >= u_hi) break;
+      if (u + 2 < u_hi) issue(b1, u + 2);
+      consume(b2, u);
+      if (++u >= u_hi) break;
+    }
+  }
+  if (l == 0) sh.nfrag[w] = nf;
+  __syncthreads();
+  // merge columns split between warps, in warp (= unit) order
+  if (threadIdx.x == 0) {
+    int64_t cp = -1;
+    double cs = 0.0;
+    for (int ww = 0; ww < kWarps; ++ww)
+      for (int f = 0; f < sh.nfrag[ww]; ++f) {
+        const Frag fr = sh.frag[ww][f];
+        if (fr.pos != cp) {
+          if (cp >= 0) out[cp] = cs;
+          cp = fr.pos;
+          cs = fr.sum;
+        } else {
+          cs += fr.sum;
+        }
+      }
+    if (cp >= 0) out[cp] = cs;
+  }
+  __syncthreads();
+  // per-CTA statistics over this CTA's columns (fixed thread -> position map)
+  if (po.track || po.vdot) {
+    for (int64_t pos = c0 + threadIdx.x; pos < c1; pos += kThreads) acc.add(p, po, eps, pos, out[pos]);
+  }
+  finish_pass(p, sh, po, acc);
+  __syncthreads();  // sh.frag is reused by the next pass
+}
+
+// ----------------------------------------------------------------------------
+// SuKro adjoint (SukroDictionary::apply_adjoint, dictionary.cpp:158-164, then the
+// ActiveOp gather 157-160): out[pos] = d_j * [sum_t C_t^T R B_t](s, jj) for
+// j = idx[pos] = jj*q + s. Stage 1 (all CTAs): T_t(s, rb) = sum_rc C_t(rc,s) R(rc,rb);
+// grid sync; stage 2: one warp per preserved atom. r is in shared memory.
+// ----------------------------------------------------------------------------
+__device__ __noinline__ void sukro_adjoint(const EngineParams& p, Sh& sh, const DevLevel& lv, const int32_t* __restrict__ idx,
+                              const double* __restrict__ eps, int64_t S, const double* __restrict__ r,
+                              double* __restrict__ rt, const PassOut& po) {
+  cg::grid_group grid = cg::this_grid();
+  const int64_t m = lv.m, q = lv.q;
+  const int nt = lv.nterms;
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  // R^T with a padded row stride (bank-conflict free): rt[rb*(m+1) + rc] = R(rc, rb)
+  for (int64_t e = threadIdx.x; e < m * m; e += kThreads) {
+    const int64_t rb = e / m, rc = e - rb * m;
+    rt[rb * (m + 1) + rc] = r[e];
+  }
+  __syncthreads();
+  // stage 1: warp task (t, s): lanes over rb
+  const int64_t tasks = static_cast<int64_t>(nt) * q;
+  const int64_t gw = static_cast<int64_t>(blockIdx.x) * kWarps + w, nw = static_cast<int64_t>(gridDim.x) * kWarps;
+  for (int64_t task = gw; task < tasks; task += nw) {
+    const int64_t t = task / q, s = task - t * q;
+    const double* __restrict__ ccol = lv.right + t * m * q + s * m;
+    double cv[kSukroMaxM / 32];
+#pragma unroll
+    for (int e = 0; e < kSukroMaxM / 32; ++e) cv[e] = (l + 32 * e < m) ? ccol[l + 32 * e] : 0.0;
+    double a[kSukroMaxM / 32];
+#pragma unroll
+    for (int e = 0; e < kSukroMaxM / 32; ++e) a[e] = 0.0;
+    for (int64_t rc = 0; rc < m; ++rc) {
+      double cb = 0.0;
+#pragma unroll
+      for (int e = 0; e < kSukroMaxM / 32; ++e)
+        if ((rc >> 5) == e) cb = __shfl_sync(kFull, cv[e], static_cast<int>(rc & 31));
+#pragma unroll
+      for (int e = 0; e < kSukroMaxM / 32; ++e) {
+        const int64_t rb = l + 32 * e;
+        if (rb < m) a[e] = fma(cb, rt[rb * (m + 1) + rc], a[e]);
+      }
+    }
+    double* __restrict__ dst = p.sk_t + (t * q + s) * m;
+#pragma unroll
+    for (int e = 0; e < kSukroMaxM / 32; ++e)
+      if (l + 32 * e < m) __stcg(dst + l + 32 * e, a[e]);
+  }
+  grid.sync();
+  // stage 2: warp per preserved atom, lanes over rb
+  int64_t lo, hi;
+  slice(S, lo, hi);
+  PassAcc acc;
+  for (int64_t pos = lo + w; pos < hi; pos += kWarps) {
+    const int64_t j = idx[pos];
+    const int64_t jj = j / q, s = j - jj * q;
+    double a = 0.0;
+    for (int t = 0; t < nt; ++t) {
+      const double* __restrict__ trow = p.sk_t + (static_cast<int64_t>(t) * q + s) * m;
+      const double* __restrict__ bcol = lv.left + static_cast<int64_t>(t) * m * q + jj * m;
+      for (int64_t rb = l; rb < m; rb += 32) a = fma(__ldcg(trow + rb), bcol[rb], a);
+    }
+    a = warp_sum(a);
+    if (l == 0) {
+      const double total = lv.col_scale ? lv.col_scale[j] * a : a;
+      acc.add(p, po, eps, pos, total, true);
+    }
+  }
+  finish_pass(p, sh, po, acc);
+}
+
+__device__ void op_adjoint(const EngineParams& p, Sh& sh, const DevLevel& lv, const int32_t* idx, const double* eps,
+                           int64_t S, const double* r, double* scratch, const PassOut& po) {
+  if (lv.kind == kDense)
+    dense_adjoint(p, sh, lv, idx, eps, S, r, po);
+  else
+    sukro_adjoint(p, sh, lv, idx, eps, S, r, scratch, po);
+}
+
+// ----------------------------------------------------------------------------
+// Apply: partial sums of u = sum_pos coef(pos) a_{idx[pos]}.
+// ----------------------------------------------------------------------------
+struct ApplySrc {
+  const int32_t* idx;
+  const double* coef;      // values (x or power vector)
+  const double* coef_div;  // if non-null: coef = coef_div[pos] / div
+  double div;
+  const int8_t* keep;      // nullable: only keep != 0 contribute
+  const double* xp;        // nullable: keep == 0 && xp != 0 feed the v fix (apply_restriction 673-684)
+  __device__ __forceinline__ double c(int64_t pos) const { return coef_div ? coef_div[pos] / div : coef[pos]; }
+  __device__ __forceinline__ bool kept(int64_t pos) const { return keep == nullptr || keep[pos] != 0; }
+};
+
+// Row tiling of the dense apply: a work item covers kThreads/G double2 rows with
+// G column groups (so short signals still use every thread).
+struct ApplyTiling {
+  int tr2;  // double2 rows per tile
+  int G;    // column groups per work item
+  int64_t R;  // row tiles
+};
+__device__ __forceinline__ ApplyTiling apply_tiling(const EngineParams& p) {
+  ApplyTiling t;
+  const int64_t rows2 = p.ld >> 1;
+  int tr2 = kThreads;
+  while (tr2 > 32 && tr2 / 2 >= rows2) tr2 /= 2;
+  t.tr2 = tr2;
+  t.G = kThreads / tr2;
+  t.R = (rows2 + tr2 - 1) / tr2;
+  return t;
+}
+
+__device__ __forceinline__ int dense_apply_chunks(const EngineParams& p, int64_t work) {
+  const int64_t R = apply_tiling(p).R;
+  int64_t cmax = p.grid / R;
+  if (cmax < 1) cmax = 1;
+  int64_t c = (work + 3) / 4;
+  if (c < 1) c = 1;
+  if (c > cmax) c = cmax;
+  return static_cast<int>(c);
+}
+
+// Dense: work item b -> (row tile b % R, position chunk b / R); the nonzero
+// coefficients of each chunk are stream-compacted (order preserved) into shared
+// memory; thread (g, i2) owns rows 2*i2, 2*i2+1 of the tile and streams columns
+// g, g+G, ... of the list with 8 independent 128-bit loads in flight; the G
+// group sums are added in group order. out[c*ld + i] holds chunk c's sum.
+__device__ __noinline__ void dense_apply_partials(const EngineParams& p, Sh& sh, const DevLevel& lv,
+                                                  const ApplySrc& src, int64_t S, int C, double* __restrict__ out,
+                                                  double* __restrict__ fix_out, int32_t* s_list, double* s_coef,
+                                                  double* s_fixc) {
+  const int64_t ld = p.ld;
+  const ApplyTiling tl = apply_tiling(p);
+  const int64_t b = blockIdx.x;
+  if (b >= tl.R * C) return;
+  const int64_t r = b % tl.R, c = b / tl.R;
+  const int64_t plo = S * c / C, phi = S * (c + 1) / C;
+  const int g = threadIdx.x / tl.tr2;
+  const int64_t i2 = r * tl.tr2 + (threadIdx.x - g * tl.tr2);  // double2 row index
+  const bool row_ok = 2 * i2 < ld;
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  double2 acc = make_double2(0.0, 0.0), facc = make_double2(0.0, 0.0);
+  const bool want_fix = fix_out != nullptr;
+  const double2* __restrict__ A2 = reinterpret_cast<const double2*>(lv.a) + i2;
+  const int64_t ld2 = ld / 2;
+  for (int64_t base = plo; base < phi; base += kApplyCap) {
+    const int64_t end = min(phi, base + static_cast<int64_t>(kApplyCap));
+    const int64_t nb = end - base;
+    const int per = static_cast<int>((nb + kThreads - 1) / kThreads);
+    const int64_t my_lo = base + static_cast<int64_t>(threadIdx.x) * per;
+    int mine = 0, mine_fix = 0;
+    for (int q = 0; q < per; ++q) {
+      const int64_t pos = my_lo + q;
+      if (pos < end) {
+        const bool kp = src.kept(pos);
+        if (kp && src.c(pos) != 0.0) ++mine;
+        if (!kp && want_fix && src.xp[pos] != 0.0) ++mine_fix;
+      }
+    }
+    int incl = mine, incl2 = mine_fix;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t1 = __shfl_up_sync(kFull, incl, o);
+      const int t2 = __shfl_up_sync(kFull, incl2, o);
+      if (l >= o) {
+        incl += t1;
+        incl2 += t2;
+      }
+    }
+    if (l == 31) {
+      sh.wcount[0][w] = incl;
+      sh.wcount[1][w] = incl2;
+    }
+    __syncthreads();
+    int woff = 0, woff2 = 0, tot = 0, tot2 = 0;
+    for (int q = 0; q < kWarps; ++q) {
+      if (q < w) {
+        woff += sh.wcount[0][q];
+        woff2 += sh.wcount[1][q];
+      }
+      tot += sh.wcount[0][q];
+      tot2 += sh.wcount[1][q];
+    }
+    int o1 = woff + incl - mine;
+    int o2 = woff2 + incl2 - mine_fix;
+    for (int q = 0; q < per; ++q) {
+      const int64_t pos = my_lo + q;
+      if (pos < end) {
+        const bool kp = src.kept(pos);
+        const double cf = src.c(pos);
+        if (kp && cf != 0.0) {
+          s_list[o1] = src.idx[pos];
+          s_coef[o1] = cf;
+          ++o1;
+        }
+        if (!kp && want_fix && src.xp[pos] != 0.0) {
+          s_list[kApplyCap + o2] = src.idx[pos];
+          s_fixc[o2] = src.xp[pos];
+          ++o2;
+        }
+      }
+    }
+    __syncthreads();
+    if (row_ok) {
+      const int G = tl.G;
+      int e = g;
+      for (; e + 7 * G < tot; e += 8 * G) {
+        double2 a[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) a[q] = ldg_stream2(A2 + static_cast<int64_t>(s_list[e + q * G]) * ld2);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const double cf = s_coef[e + q * G];
+          acc.x = fma(cf, a[q].x, acc.x);
+          acc.y = fma(cf, a[q].y, acc.y);
+        }
+      }
+      for (; e < tot; e += G) {
+        const double2 a = ldg_stream2(A2 + static_cast<int64_t>(s_list[e]) * ld2);
+        const double cf = s_coef[e];
+        acc.x = fma(cf, a.x, acc.x);
+        acc.y = fma(cf, a.y, acc.y);
+      }
+      for (int f = g; f < tot2; f += G) {
+        const double2 a = ldg_stream2(A2 + static_cast<int64_t>(s_list[kApplyCap + f]) * ld2);
+        const double cf = s_fixc[f];
+        facc.x = fma(cf, a.x, facc.x);
+        facc.y = fma(cf, a.y, facc.y);
+      }
+    }
+    __syncthreads();
+  }
+  // combine the G column groups in group order (shared memory reuses the list area)
+  double2* red = reinterpret_cast<double2*>(s_coef);  // >= 2*kThreads double2 of scratch (coef + fixc)
+  if (tl.G > 1) {
+    red[threadIdx.x] = acc;
+    if (want_fix) red[kThreads + threadIdx.x] = facc;
+    __syncthreads();
+    if (g == 0) {
+      for (int gg = 1; gg < tl.G; ++gg) {
+        const double2 o = red[gg * tl.tr2 + threadIdx.x];
+        acc.x += o.x;
+        acc.y += o.y;
+        if (want_fix) {
+          const double2 of = red[kThreads + gg * tl.tr2 + threadIdx.x];
+          facc.x += of.x;
+          facc.y += of.y;
+        }
+      }
+    }
+    __syncthreads();
+  }
+  if (row_ok && g == 0) {
+    __stcg(reinterpret_cast<double2*>(out + c * ld) + i2, acc);
+    if (want_fix) __stcg(reinterpret_cast<double2*>(fix_out + c * ld) + i2, facc);
+  }
+}
+
+// SuKro apply (SukroDictionary::apply, dictionary.cpp:150-156, on the ActiveOp
+// zero-padded iterate 141-145): u = vec(sum_t C_t X B_t^T), X = reshape(d o x, q, q).
+// Scatter (own slice) -> sync -> W_t = X B_t^T -> sync -> split-K partials of
+// sum_t C_t W_t into out[ks*ld + i]; the scatter is undone in the last stage so
+// the padded operands stay zero between calls. A second source carries the v fix.
+__device__ __noinline__ int sukro_apply_partials(const EngineParams& p, const DevLevel& lv, const ApplySrc& src, int64_t S,
+                                    double* __restrict__ out, double* __restrict__ fix_out) {
+  cg::grid_group grid = cg::this_grid();
+  const int64_t m = lv.m, q = lv.q, K = p.k, ld = p.ld;
+  const int nt = lv.nterms;
+  const int nsrc = fix_out ? 2 : 1;
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  int64_t lo, hi;
+  slice(S, lo, hi);
+  for (int64_t pos = lo + threadIdx.x; pos < hi; pos += kThreads) {
+    const int64_t j = src.idx[pos];
+    const double d = lv.col_scale ? lv.col_scale[j] : 1.0;
+    if (src.kept(pos)) {
+      const double cf = src.c(pos);
+      if (cf != 0.0) p.sk_x[j] = d * cf;
+    } else if (nsrc == 2 && src.xp[pos] != 0.0) {
+      p.sk_x[K + j] = d * src.xp[pos];
+    }
+  }
+  grid.sync();
+  // stage 1: W_t(s, rb) = sum_jj X(s, jj) B_t(rb, jj); warp task (src, t, rb), lanes over s
+  const int64_t gw = static_cast<int64_t>(blockIdx.x) * kWarps + w, nw = static_cast<int64_t>(gridDim.x) * kWarps;
+  const int64_t tasks1 = static_cast<int64_t>(nsrc) * nt * m;
+  for (int64_t task = gw; task < tasks1; task += nw) {
+    const int64_t sr = task / (nt * m);
+    const int64_t rem = task - sr * nt * m;
+    const int64_t t = rem / m, rb = rem - t * m;
+    const double* __restrict__ X = p.sk_x + sr * K;
+    const double* __restrict__ B = lv.left + t * m * q;
+    double a[kSukroMaxQ / 32];
+#pragma unroll
+    for (int e = 0; e < kSukroMaxQ / 32; ++e) a[e] = 0.0;
+    for (int64_t j0 = 0; j0 < q; j0 += 32) {
+      const double bl = (j0 + l < q) ? B[(j0 + l) * m + rb] : 0.0;  // B_t(rb, jj) for jj = j0 + lane
+      const int jn = static_cast<int>(min(static_cast<int64_t>(32), q - j0));
+      for (int jq = 0; jq < jn; ++jq) {
+        const double bv = __shfl_sync(kFull, bl, jq);
+        const double* __restrict__ xcol = X + (j0 + jq) * q;
+#pragma unroll
+        for (int e = 0; e < kSukroMaxQ / 32; ++e) {
+          const int64_t s = l + 32 * e;
+          if (s < q) a[e] = fma(__ldcg(xcol + s), bv, a[e]);
+        }
+      }
+    }
+    double* __restrict__ dst = p.sk_t + (sr * nt + t) * m * q + rb * q;
+#pragma unroll
+    for (int e = 0; e < kSukroMaxQ / 32; ++e)
+      if (l + 32 * e < q) __stcg(dst + l + 32 * e, a[e]);
+  }
+  grid.sync();
+  // stage 2: out(rc, rb) = sum_t sum_s C_t(rc, s) W_t(s, rb), split over s into KS chunks
+  const int KS = p.sk_ks;
+  const int64_t tasks2 = static_cast<int64_t>(nsrc) * KS * m;
+  for (int64_t task = gw; task < tasks2; task += nw) {
+    const int64_t sr = task / (KS * m);
+    const int64_t rem = task - sr * KS * m;
+    const int64_t ks = rem / m, rb = rem - ks * m;
+    const int64_t s_lo = q * ks / KS, s_hi = q * (ks + 1) / KS;
+    double a[kSukroMaxM / 32];
+#pragma unroll
+    for (int e = 0; e < kSukroMaxM / 32; ++e) a[e] = 0.0;
+    for (int t = 0; t < nt; ++t) {
+      const double* __restrict__ Wr = p.sk_t + (sr * nt + t) * m * q + rb * q;
+      const double* __restrict__ Ct = lv.right + static_cast<int64_t>(t) * m * q;
+      for (int64_t s0 = s_lo; s0 < s_hi; s0 += 32) {
+        const double wl = (s0 + l < s_hi) ? __ldcg(Wr + s0 + l) : 0.0;
+        const int sn = static_cast<int>(min(static_cast<int64_t>(32), s_hi - s0));
+        for (int sq = 0; sq < sn; ++sq) {
+          const double wv = __shfl_sync(kFull, wl, sq);
+          const double* __restrict__ ccol = Ct + (s0 + sq) * m;
+#pragma unroll
+          for (int e = 0; e < kSukroMaxM / 32; ++e) {
+            const int64_t rc = l + 32 * e;
+            if (rc < m) a[e] = fma(ccol[rc], wv, a[e]);
+          }
+        }
+      }
+    }
+    double* __restrict__ dst = (sr == 0 ? out : fix_out) + ks * ld + rb * m;
+#pragma unroll
+    for (int e = 0; e < kSukroMaxM / 32; ++e)
+      if (l + 32 * e < m) __stcg(dst + l + 32 * e, a[e]);
+  }
+  // undo the scatter (own slice, same predicate as above)
+  for (int64_t pos = lo + threadIdx.x; pos < hi; pos += kThreads) {
+    const int64_t j = src.idx[pos];
+    if (src.kept(pos)) {
+      if (src.c(pos) != 0.0) p.sk_x[j] = 0.0;
+    } else if (nsrc == 2 && src.xp[pos] != 0.0) {
+      p.sk_x[K + j] = 0.0;
+    }
+  }
+  return KS;
+}
+
+// Returns the number of partial chunks written to out (and fix_out).
+__device__ int op_apply_partials(const EngineParams& p, Sh& sh, const DevLevel& lv, const ApplySrc& src, int64_t S,
+                                 int64_t work, double* out, double* fix_out, int32_t* s_list, double* s_coef,
+                                 double* s_fixc) {
+  if (lv.kind == kDense) {
+    const int C = dense_apply_chunks(p, work);
+    dense_apply_partials(p, sh, lv, src, S, C, out, fix_out, s_list, s_coef, s_fixc);
+    return C;
+  }
+  return sukro_apply_partials(p, lv, src, S, out, fix_out);
+}
+
+// ----------------------------------------------------------------------------
+// Restricted power iteration (detail::power_iteration_sq_norm, solver.cpp:72-104)
+// over the current bank. Returns the Rayleigh estimate and leaves the final
+// normalised vector in bank.lead. Three grid syncs per step.
+// ----------------------------------------------------------------------------
+struct Scratch {
+  double* vec;     // ld doubles (shared memory)
+  double* rt;      // SuKro R^T (shared memory)
+  int32_t* list;   // 2 * kApplyCap
+  double* coef;    // kApplyCap
+  double* fixc;    // kApplyCap
+};
+
+__device__ __noinline__ double power_iteration(const EngineParams& p, Sh& sh, const DevLevel& lv, const Bank& bk, int64_t S,
+                                  bool try_warm, const Scratch& sc) {
+  cg::grid_group grid = cg::this_grid();
+  int64_t lo, hi;
+  slice(S, lo, hi);
+  {
+    double a_lead = 0.0, a_g = 0.0;
+    for (int64_t q = lo + threadIdx.x; q < hi; q += kThreads) {
+      if (try_warm) a_lead = fma(bk.lead[q], bk.lead[q], a_lead);
+      a_g = fma(p.gauss0[q], p.gauss0[q], a_g);
+    }
+    double v[2] = {a_lead, a_g};
+    const bool mx[2] = {false, false};
+    block_reduce<2>(v, mx, sh);
+    if (threadIdx.x == 0) {
+      put_slot(p, kSlLead2, v[0]);
+      put_slot(p, kSlSum, v[1]);
+    }
+  }
+  grid.sync();
+  grid_reduce(p, sh, (1u << kSlLead2) | (1u << kSlSum), 0u);
+  const bool warm = try_warm && sh.res[kSlLead2] > 0.0;
+  const double* cur_src = warm ? bk.lead : p.gauss0;
+  double cur_div = sqrt(warm ? sh.res[kSlLead2] : sh.res[kSlSum]);
+  double estimate = 0.0;
+  const int max_iter = warm ? 12 : 200;
+  const double rel_tol = warm ? 1e-5 : 1e-9;
+  const int min_iter = warm ? 2 : 4;
+  bool have_w = false;  // pw holds the last w (v = pw / cur_div)
+  for (int it = 0; it < max_iter; ++it) {
+    if (threadIdx.x == 0) sh.s.power_steps += 1;
+    // v for this step: materialise on this CTA's slice (Rayleigh quotient reads it)
+    for (int64_t q = lo + threadIdx.x; q < hi; q += kThreads) p.pv[q] = cur_src[q] / cur_div;
+    ApplySrc as{bk.idx, nullptr, cur_src, cur_div, nullptr, nullptr};
+    const int C = op_apply_partials(p, sh, lv, as, S, S, p.pup, nullptr, sc.list, sc.coef, sc.fixc);
+    grid.sync();
+    if (static_cast<int64_t>(C) * p.ld <= kRedundantCombine) {
+      // few partials: every CTA sums them itself (same order) instead of a combine phase
+      for (int64_t i = threadIdx.x; i < p.ld; i += kThreads) {
+        double acc = 0.0;
+        for (int c = 0; c < C; ++c) acc += __ldcg(p.pup + static_cast<int64_t>(c) * p.ld + i);
+        sc.vec[i] = acc;
+      }
+    } else {
+      int64_t ilo, ihi;
+      slice(p.ld, ilo, ihi);
+      for (int64_t i = ilo + threadIdx.x; i < ihi; i += kThreads) {
+        double acc = 0.0;
+        for (int c = 0; c < C; ++c) acc += __ldcg(p.pup + static_cast<int64_t>(c) * p.ld + i);
+        __stcg(p.PU + i, acc);
+      }
+      grid.sync();
+      for (int64_t i = threadIdx.x; i < p.ld; i += kThreads) sc.vec[i] = __ldcg(p.PU + i);
+    }
+    __syncthreads();
+    PassOut po{p.pw, 0, 0.0, false, 0, 0, p.pv};
+    op_adjoint(p, sh, lv, bk.idx, bk.eps, S, sc.vec, sc.rt, po);
+    grid.sync();
+    grid_reduce(p, sh, (1u << kSlPw2) | (1u << kSlPvw), 0u);
+    const double nrm = sqrt(sh.res[kSlPw2]);
+    if (nrm == 0.0) {
+      estimate = 0.0;
+      break;
+    }
+    const double prev = estimate;
+    estimate = sh.res[kSlPvw];
+    cur_src = p.pw;
+    cur_div = nrm;
+    have_w = true;
+    if (it > min_iter && fabs(estimate - prev) <= rel_tol * estimate) break;
+  }
+  // leading vector (v after the last update)
+  for (int64_t q = lo + threadIdx.x; q < hi; q += kThreads) bk.lead[q] = have_w ? p.pw[q] / cur_div : p.pv[q];
+  grid.sync();
+  return estimate;
+}
+
+// ActiveOp::gather_metadata (189-201) for the CTA slice; per-CTA max eps to a slot.
+__device__ void gather_metadata(const EngineParams& p, Sh& sh, const DevLevel& lv, const Bank& bk, int64_t S) {
+  int64_t lo, hi;
+  slice(S, lo, hi);
+  double me = -DBL_MAX;
+  for (int64_t q = lo + threadIdx.x; q < hi; q += kThreads) {
+    const int64_t g = bk.idx[q];
+    const double e = lv.eps[g];
+    bk.eps[q] = e;
+    bk.en[q] = lv.en[g];
+    bk.an[q] = lv.an[g];
+    me = fmax(me, e);
+  }
+  double v[1] = {me};
+  const bool mx[1] = {true};
+  block_reduce<1>(v, mx, sh);
+  if (threadIdx.x == 0) put_slot(p, kSlMaxEps, v[0]);
+}
+
+__device__ __forceinline__ void load_vec_smem(const EngineParams& p, const double* src, double* dst) {
+  for (int64_t i = threadIdx.x; i < p.ld; i += kThreads) dst[i] = src[i];
+  __syncthreads();
+}
+
+// Combine apply partials into U by row slices. shift: v <- u_old - fix (FISTA).
+__device__ void combine_u(const EngineParams& p, int C, bool shift, bool fix) {
+  int64_t lo, hi;
+  slice(p.ld, lo, hi);
+  for (int64_t i = lo + threadIdx.x; i < hi; i += kThreads) {
+    double u = 0.0;
+    for (int c = 0; c < C; ++c) u += __ldcg(p.up + static_cast<int64_t>(c) * p.ld + i);
+    if (shift) {
+      double v = __ldcg(p.U + i);
+      if (fix) {
+        double f = 0.0;
+        for (int c = 0; c < C; ++c) f += __ldcg(p.dvp + static_cast<int64_t>(c) * p.ld + i);
+        v -= f;
+      }
+      __stcg(p.V + i, v);
+    }
+    __stcg(p.U + i, u);
+  }
+}
+
+// setup_dictionary (fastl1.cpp:283-324). first: constructor call.
+__device__ __noinline__ void setup_dictionary(const EngineParams& p, Sh& sh, bool first, const Scratch& sc) {
+  cg::grid_group grid = cg::this_grid();
+  EngineState& s = sh.s;
+  const DevLevel& lv = p.lv[s.dict_index];
+  Bank bk = p.bank[s.cur];
+  if (!first) {  // ActiveOp::rebase (105-112)
+    gather_metadata(p, sh, lv, bk, s.S);
+    grid.sync();
+    grid_reduce(p, sh, 0u, 1u << kSlMaxEps);
+    if (threadIdx.x == 0) s.max_eps = s.S > 0 ? sh.res[kSlMaxEps] : 0.0;
+    __syncthreads();
+  }
+  if (p.rule == FL1_RULE_DYNAMIC) {
+    load_vec_smem(p, p.y, sc.vec);
+    PassOut po{bk.aty, 0, 0.0, false, 0, 0, nullptr};
+    op_adjoint(p, sh, lv, bk.idx, bk.eps, s.S, sc.vec, sc.rt, po);
+    if (p.precompute_aty && !s.atye_valid) {
+      grid.sync();
+      PassOut pe{bk.atye, 0, 0.0, false, 0, 0, nullptr};
+      op_adjoint(p, sh, p.lv[p.n_levels - 1], bk.idx, bk.eps, s.S, sc.vec, sc.rt, pe);
+      if (threadIdx.x == 0) s.atye_valid = 1;
+    }
+    grid.sync();
+  }
+  if (p.has_full_l && s.S == p.k) {
+    if (threadIdx.x == 0) s.lipschitz = p.full_l[s.dict_index];
+  } else {
+    const double sq = power_iteration(p, sh, lv, bk, s.S, s.lead_valid != 0, sc);
+    if (threadIdx.x == 0) {
+      s.lead_valid = 1;
+      s.lipschitz = fmax(sq, 1e-300) * 1.05;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    s.inv_l = 1.0 / s.lipschitz;
+    s.active_at_last_l = s.S;
+  }
+  // u = op.apply(x)
+  ApplySrc as{bk.idx, bk.x, nullptr, 1.0, nullptr, nullptr};
+  const int C = op_apply_partials(p, sh, lv, as, s.S, s.S, p.up, nullptr, sc.list, sc.coef, sc.fixc);
+  grid.sync();
+  combine_u(p, C, false, false);
+  if (threadIdx.x == 0) {
+    s.momentum_ready = 0;
+    s.t_k = 1.0;
+  }
+  grid.sync();
+}
+
+__device__ uint64_t row_flops(const EngineParams& p, int dict, int64_t active, int64_t nnz) {  // 647-665
+  const uint64_t un = static_cast<uint64_t>(p.n), uk = static_cast<uint64_t>(p.k);
+  const uint64_t ua = static_cast<uint64_t>(active), uz = static_cast<uint64_t>(nnz);
+  const int last = p.n_levels - 1;
+  if (p.variant == FL1_PLAIN) return (uk + uz) * un + 4 * uk + un;
+  if (p.variant == FL1_MULTI_DICT && dict < last) return p.lv[dict].matvec_flops + uz * un + 8 * ua + 7 * un;
+  return (ua + uz) * un + 6 * ua + 5 * un;
+}
+
+}  // namespace
+
+// ============================================================================
+__global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_constant__ EngineParams p) {
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ __align__(16) double dyn[];
+  __shared__ Sh sh;
+  EngineState& s = sh.s;
+  Scratch sc;
+  sc.vec = dyn;
+  sc.rt = dyn + p.ld;  // SuKro R^T; aliases the apply scratch (never live together)
+  sc.list = reinterpret_cast<int32_t*>(dyn + p.ld);
+  sc.coef = dyn + p.ld + kApplyCap;
+  sc.fixc = dyn + p.ld + 2 * kApplyCap;
+
+  if (threadIdx.x == 0) s = *p.st;
+  __syncthreads();
+  if (threadIdx.x == 0) s.launches += 1;
+
+  const int64_t n = p.n, k = p.k, ld = p.ld;
+
+  // --------------------------------------------------------------- utility modes
+  if (p.mode == kModeAdjoint || p.mode == kModeApply || p.mode == kModePower) {
+    const DevLevel& lv = p.lv[p.mode_level];
+    Bank bk = p.bank[0];  // identity bank prepared by the host
+    if (p.mode == kModeAdjoint) {
+      load_vec_smem(p, p.x_init, sc.vec);
+      PassOut po{p.vec_out, 0, 0.0, false, 0, 0, nullptr};
+      op_adjoint(p, sh, lv, bk.idx, bk.eps, k, sc.vec, sc.rt, po);
+    } else if (p.mode == kModeApply) {
+      ApplySrc as{bk.idx, p.x_init, nullptr, 1.0, nullptr, nullptr};
+      const int C = op_apply_partials(p, sh, lv, as, k, k, p.up, nullptr, sc.list, sc.coef, sc.fixc);
+      grid.sync();
+      int64_t lo, hi;
+      slice(ld, lo, hi);
+      for (int64_t i = lo + threadIdx.x; i < hi; i += kThreads) {
+        double acc = 0.0;
+        for (int c = 0; c < C; ++c) acc += __ldcg(p.up + static_cast<int64_t>(c) * ld + i);
+        p.vec_out[i] = acc;
+      }
+    } else {
+      const double sq = power_iteration(p, sh, lv, bk, k, false, sc);
+      if (blockIdx.x == 0 && threadIdx.x == 0) {
+        s.power_est = sq;
+        *p.st = s;
+      }
+    }
+    return;
+  }
+
+  // --------------------------------------------------------------- Engine ctor
+  if (p.mode == kModeSolve) {
+    if (threadIdx.x == 0) s.start_ns = globaltimer_ns();
+    {
+      double acc = 0.0;
+      for (int64_t i = threadIdx.x; i < n; i += kThreads) acc = fma(p.y[i], p.y[i], acc);
+      double v[1] = {acc};
+      const bool mx[1] = {false};
+      block_reduce<1>(v, mx, sh);
+      if (threadIdx.x == 0) {
+        s.y_sq = v[0];
+        s.y_norm = sqrt(v[0]);
+      }
+    }
+    Bank bk = p.bank[0];
+    int64_t lo, hi;
+    slice(k, lo, hi);
+    for (int64_t q = lo + threadIdx.x; q < hi; q += kThreads) {
+      bk.idx[q] = static_cast<int32_t>(q);
+      bk.x[q] = p.has_x_init ? p.x_init[q] : 0.0;
+      bk.xp[q] = 0.0;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      s.S = k;
+      s.cur = 0;
+    }
+    __syncthreads();
+    gather_metadata(p, sh, p.lv[s.dict_index], bk, k);
+    grid.sync();
+    grid_reduce(p, sh, 0u, 1u << kSlMaxEps);
+    if (threadIdx.x == 0) s.max_eps = sh.res[kSlMaxEps];
+    __syncthreads();
+    setup_dictionary(p, sh, true, sc);
+    if (threadIdx.x == 0) s.t0_ns = globaltimer_ns();
+    __syncthreads();
+  }
+
+  // --------------------------------------------------------------- Engine::run
+  const int last = p.n_levels - 1;
+  const double lambda = p.lambda;
+  while (true) {
+    if (s.t >= p.max_it) {
+      if (threadIdx.x == 0) {
+        s.converged = 0;
+        s.done = 1;
+        s.event = kEvDone;
+      }
+      break;
+    }
+    if (p.collect_trace && s.n_trace >= p.trace_cap) {
+      if (threadIdx.x == 0) s.event = kEvTraceFull;
+      break;
+    }
+    const DevLevel& lv = p.lv[s.dict_index];
+    const Bank bk = p.bank[s.cur];
+    const int64_t S = s.S;
+    int64_t lo, hi;
+    slice(S, lo, hi);
+    double tp0 = 0.0;
+    if (threadIdx.x == 0) tp0 = globaltimer_ns();
+
+    // ---------------------------------------------------------- phase A
+    double momentum = 0.0, t_next = s.t_k;  // 465-470
+    if (p.solver == FL1_FISTA && s.momentum_ready) {
+      t_next = 0.5 * (1.0 + sqrt(1.0 + 4.0 * s.t_k * s.t_k));
+      momentum = (s.t_k - 1.0) / t_next;
+    }
+    {  // compute_products (359-369): rho_g in shared memory
+      double arr = 0.0, ary = 0.0, aee = 0.0;
+      for (int64_t i = threadIdx.x; i < ld; i += kThreads) {
+        const double u = __ldcg(p.U + i);
+        const double uw = momentum != 0.0 ? (1.0 + momentum) * u - momentum * __ldcg(p.V + i) : u;
+        const double yi = i < n ? p.y[i] : 0.0;
+        const double r = i < n ? yi - uw : 0.0;
+        sc.vec[i] = r;
+        if (p.observe && blockIdx.x == 0) p.rho[i] = r;
+        arr = fma(r, r, arr);
+        ary = fma(yi, r, ary);
+        if (momentum != 0.0 && i < n) {
+          const double e = yi - u;
+          aee = fma(e, e, aee);
+        }
+      }
+      double v[3] = {arr, ary, aee};
+      const bool mx[3] = {false, false, false};
+      block_reduce<3>(v, mx, sh);
+      if (threadIdx.x == 0) {
+        sh.t_next = t_next;
+        sh.rho_sq = v[0];
+        sh.rho_dot_y = v[1];
+        sh.rho_x_sq = momentum != 0.0 ? v[2] : v[0];
+        sh.rho_norm = sqrt(v[0]);
+      }
+    }
+    {  // ||x||_1 partial on this CTA's slice (473)
+      double acc = 0.0;
+      for (int64_t q = lo + threadIdx.x; q < hi; q += kThreads) acc += fabs(bk.x[q]);
+      double v[1] = {acc};
+      const bool mx[1] = {false};
+      block_reduce<1>(v, mx, sh);
+      if (threadIdx.x == 0) put_slot(p, kSlL1, v[0]);
+    }
+    const bool exact_fit = !(sh.rho_sq > 0.0);
+    if (!exact_fit) {
+      // corr = A_S^T rho_g fused with the dual-scaling maxima (414-418)
+      PassOut po{p.corr, 1, sh.rho_norm, false, kSlMaxPlain, kSlMaxStable, nullptr};
+      op_adjoint(p, sh, lv, bk.idx, bk.eps, S, sc.vec, sc.rt, po);
+    } else {
+      // exact fit (428-449): corr = A^T 0 = 0, dual point along y
+      for (int64_t q = lo + threadIdx.x; q < hi; q += kThreads) p.corr[q] = 0.0;
+      if (p.rule == FL1_RULE_DYNAMIC) {
+        double mp = 0.0, ms = 0.0;
+        for (int64_t q = lo + threadIdx.x; q < hi; q += kThreads) {
+          const double cy = bk.aty[q];
+          p.corr_y[q] = cy;
+          const double ac = fabs(cy) / lambda;
+          mp = fmax(mp, ac);
+          ms = fmax(ms, ac + bk.eps[q] * s.y_norm / lambda);
+        }
+        double v[2] = {mp, ms};
+        const bool mx[2] = {true, true};
+        block_reduce<2>(v, mx, sh);
+        if (threadIdx.x == 0) {
+          put_slot(p, kSlMaxPlainY, v[0]);
+          put_slot(p, kSlMaxStableY, v[1]);
+        }
+      } else {
+        load_vec_smem(p, p.y, sc.vec);
+        PassOut po{p.corr_y, 1, s.y_norm / lambda, true, kSlMaxPlainY, kSlMaxStableY, nullptr};
+        op_adjoint(p, sh, lv, bk.idx, bk.eps, S, sc.vec, sc.rt, po);
+      }
+    }
+    grid.sync();  // ------------------------------------------------ sync 1
+    double tp1 = 0.0;
+    if (threadIdx.x == 0) {
+      tp1 = globaltimer_ns();
+      s.prof_ns[0] += tp1 - tp0;
+      if (lv.kind == kDense) s.prof_bytes += 8.0 * static_cast<double>(p.n) * static_cast<double>(S);
+    }
+
+    // ---------------------------------------------------------- phase B
+    grid_reduce(p, sh, 1u << kSlL1,
+                exact_fit ? ((1u << kSlMaxPlainY) | (1u << kSlMaxStableY))
+                          : ((1u << kSlMaxPlain) | (1u << kSlMaxStable)));
+    if (threadIdx.x == 0) {
+      const double x_l1 = sh.res[kSlL1];
+      const double primal = 0.5 * sh.rho_x_sq + lambda * x_l1;
+      double sp, st, ray_sq, ray_dot_y;  // dual_scalars (406-450)
+      if (!exact_fit) {
+        ray_sq = sh.rho_sq;
+        ray_dot_y = sh.rho_dot_y;
+        const double dp = S > 0 ? sh.res[kSlMaxPlain] : 0.0;
+        const double ds = S > 0 ? sh.res[kSlMaxStable] : 0.0;
+        const double projection = sh.rho_dot_y / (lambda * sh.rho_sq);
+        const double ap = ds > 0 ? 1.0 / ds : CUDART_INF;
+        const double at = dp > 0 ? 1.0 / dp : CUDART_INF;
+        sp = fmin(fmax(projection, -ap), ap);
+        st = fmin(fmax(projection, -at), at);
+      } else {
+        ray_sq = s.y_sq;
+        ray_dot_y = s.y_sq;
+        const double dp = S > 0 ? sh.res[kSlMaxPlainY] : 0.0;
+        const double ds = S > 0 ? sh.res[kSlMaxStableY] : 0.0;
+        sp = 1.0 / (lambda * fmax(1.0, ds));
+        st = 1.0 / (lambda * fmax(1.0, dp));
+      }
+      auto dual_of = [&](double scale) {  // 453-457
+        const double dist_sq =
+            scale * scale * ray_sq - 2.0 * scale * ray_dot_y / lambda + s.y_sq / (lambda * lambda);
+        return 0.5 * s.y_sq - 0.5 * lambda * lambda * dist_sq;
+      };
+      double gp = primal - dual_of(sp);
+      double gt = primal - dual_of(st);
+      if (gp < -1e-10 || gt < -1e-10) s.warning = 1;
+      gp = fmax(gp, 0.0);
+      gt = fmax(gt, 0.0);
+      const bool exact_phase = s.dict_index == last;
+      const double stop_tol = p.rel_tol > 0 ? p.rel_tol * primal : p.tol;
+      const bool stop_now = exact_phase && gt <= stop_tol;
+      const bool screen_now = !stop_now && p.variant != FL1_PLAIN && (s.t % static_cast<uint64_t>(p.interval) == 0);
+      double radius = 0.0, center_norm = 0.0;
+      int stable_test = 1;
+      if (screen_now) {
+        if (p.rule == FL1_RULE_GAP) {
+          double delta = 0.0;
+          if (!exact_phase) {  // stable_gap_delta (screening.cpp:103-106)
+            const double rn = sqrt(sh.rho_x_sq), e = s.max_eps;
+            delta = rn * e * x_l1 + 0.5 * e * e * x_l1 * x_l1;
+          }
+          radius = sqrt(2.0 * gp + 2.0 * delta) / lambda;
+          center_norm = fabs(sp) * sqrt(ray_sq);
+        } else {
+          const double dist_sq = sp * sp * ray_sq - 2.0 * sp * ray_dot_y / lambda + s.y_sq / (lambda * lambda);
+          radius = sqrt(fmax(dist_sq, 0.0));
+          center_norm = s.y_norm / lambda;
+          if (p.precompute_aty && s.atye_valid) stable_test = 0;
+        }
+      }
+      sh.x_l1 = x_l1;
+      sh.primal = primal;
+      sh.scale_prime = sp;
+      sh.scale_tilde = st;
+      sh.ray_sq = ray_sq;
+      sh.ray_dot_y = ray_dot_y;
+      sh.ray_is_y = exact_fit ? 1 : 0;
+      sh.gap_prime = gp;
+      sh.gap_tilde = gt;
+      sh.stop_now = stop_now ? 1 : 0;
+      sh.screen_now = screen_now ? 1 : 0;
+      sh.radius = radius;
+      sh.center_norm = center_norm;
+      sh.stable_test = stable_test;
+    }
+    __syncthreads();
+    {
+      const bool stop_now = sh.stop_now, screen_now = sh.screen_now;
+      const double sp = sh.scale_prime, cn = sh.center_norm, R = sh.radius;
+      const double inv_l = s.inv_l, thresh = lambda * s.inv_l;
+      const bool fista = p.solver == FL1_FISTA;
+      const bool use_atye = p.precompute_aty && s.atye_valid;
+      double kept = 0.0, look = 0.0, nnz = 0.0;
+      for (int64_t q = lo + threadIdx.x; q < hi; q += kThreads) {
+        const double c = p.corr[q];
+        const double xo = bk.x[q];
+        int keep = 1;
+        if (screen_now) {
+          double d;
+          if (p.rule == FL1_RULE_GAP)
+            d = fabs(sp * (sh.ray_is_y ? p.corr_y[q] : c));
+          else
+            d = use_atye ? fabs(bk.atye[q] / lambda) : fabs(bk.aty[q] / lambda);
+          if (sh.stable_test) {
+            keep = (d + bk.eps[q] * cn + R * bk.en[q]) >= 1.0;  // stable_zone_test
+            look += (d + R * bk.an[q]) >= 1.0 ? 1.0 : 0.0;      // sphere_test, approx norms
+          } else {
+            keep = (d + R * bk.en[q]) >= 1.0;
+            look += keep ? 1.0 : 0.0;
+          }
+        }
+        if (stop_now) {
+          nnz += xo != 0.0 ? 1.0 : 0.0;
+        } else {
+          const double g = momentum != 0.0 ? (1.0 + momentum) * xo - momentum * bk.xp[q] : xo;
+          const double xn = soft_threshold(g + inv_l * c, thresh);
+          if (fista) bk.xp[q] = xo;
+          bk.x[q] = xn;
+          bk.keep[q] = static_cast<int8_t>(keep);
+          if (keep) {
+            kept += 1.0;
+            nnz += xn != 0.0 ? 1.0 : 0.0;
+          }
+        }
+      }
+      double v[3] = {kept, look, nnz};
+      const bool mx[3] = {false, false, false};
+      block_reduce<3>(v, mx, sh);
+      if (threadIdx.x == 0) {
+        put_slot(p, kSlKept, v[0]);
+        put_slot(p, kSlLook, v[1]);
+        put_slot(p, kSlNnz, v[2]);
+      }
+    }
+    grid.sync();  // ------------------------------------------------ sync 2
+    double tp2 = 0.0;
+    if (threadIdx.x == 0) {
+      tp2 = globaltimer_ns();
+      s.prof_ns[1] += tp2 - tp1;
+    }
+
+    // ---------------------------------------------------------- phase D
+    grid_reduce(p, sh, (1u << kSlKept) | (1u << kSlLook) | (1u << kSlNnz), 0u);
+    if (threadIdx.x == 0) {
+      sh.S_new = sh.stop_now ? S : static_cast<int64_t>(sh.res[kSlKept]);
+      sh.look = static_cast<int64_t>(sh.res[kSlLook]);
+      sh.nnz = static_cast<int64_t>(sh.res[kSlNnz]);
+      sh.gamma = -1.0;
+      sh.next_dict = s.dict_index;
+      sh.speed = 0;
+      if (sh.screen_now && s.dict_index != last) {
+        const double gp = sh.gap_prime, gt = sh.gap_tilde;  // gap_ratio (26-30)
+        double gamma = 0.0;
+        if (!(gp <= 1e-15)) gamma = fmin(fmax(gt / gp, 0.0), 1.0);
+        sh.gamma = gamma;
+        if (p.variant == FL1_MULTI_DICT) {  // switch_dictionary (32-38)
+          const double rc = p.lv[s.dict_index].rc;
+          const double la = static_cast<double>(sh.look);
+          const bool speed = la <= rc * static_cast<double>(k);
+          int nd = s.dict_index;
+          if (speed)
+            nd = last;
+          else if (gamma <= p.gamma_threshold)
+            nd = s.dict_index + 1;
+          sh.next_dict = nd;
+          sh.speed = speed ? 1 : 0;
+        }
+      }
+      if (p.observe && sh.screen_now) {
+        s.obs_pending = 1;
+        s.obs_iter = s.t;
+        s.obs_S = S;
+        s.obs_radius = sh.radius;
+        s.obs_scale_prime = sh.scale_prime;
+        s.obs_scale_tilde = sh.scale_tilde;
+        s.obs_center_scale = sh.scale_prime;
+        s.obs_dict = s.dict_index;
+        s.obs_bank = s.cur;
+        s.obs_ray_is_y = sh.ray_is_y;
+      }
+    }
+    __syncthreads();
+    const bool stop_now = sh.stop_now;
+    const int64_t S_new = sh.S_new;
+    const bool shrink = !stop_now && S_new < S;
+    const bool fista = p.solver == FL1_FISTA;
+    int C_apply = 0;
+    if (!stop_now) {
+      if (shrink) {  // apply_restriction: stream compaction into the other bank (686-701)
+        const Bank nb = p.bank[s.cur ^ 1];
+        if (threadIdx.x < 32) {
+          double acc = 0.0;
+          for (int b = threadIdx.x; b < static_cast<int>(blockIdx.x); b += 32)
+            acc += __ldcg(p.bred + static_cast<int64_t>(b) * kBred + kSlKept);
+          acc = warp_sum(acc);
+          if (threadIdx.x == 0) sh.scan_base = static_cast<int64_t>(acc);
+        }
+        __syncthreads();
+        const bool lead_ok = s.lead_valid != 0;
+        const bool dyn = p.rule == FL1_RULE_DYNAMIC;
+        const bool atye = s.atye_valid != 0;
+        int64_t out_base = sh.scan_base;
+        double me = -DBL_MAX;
+        const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+        for (int64_t q0 = lo; q0 < hi; q0 += kThreads) {
+          const int64_t q = q0 + threadIdx.x;
+          const int kp = q < hi ? bk.keep[q] : 0;
+          const unsigned bal = __ballot_sync(kFull, kp);
+          if (l == 0) sh.wscan[w] = __popc(bal);
+          __syncthreads();
+          int64_t off = out_base;
+          int tot = 0;
+          for (int ww = 0; ww < kWarps; ++ww) {
+            if (ww < w) off += sh.wscan[ww];
+            tot += sh.wscan[ww];
+          }
+          off += __popc(bal & ((1u << l) - 1u));
+          if (kp) {
+            nb.idx[off] = bk.idx[q];
+            nb.x[off] = bk.x[q];
+            if (fista) nb.xp[off] = bk.xp[q];
+            nb.eps[off] = bk.eps[q];
+            nb.en[off] = bk.en[q];
+            nb.an[off] = bk.an[q];
+            if (dyn) nb.aty[off] = bk.aty[q];
+            if (atye) nb.atye[off] = bk.atye[q];
+            if (lead_ok) nb.lead[off] = bk.lead[q];
+            me = fmax(me, bk.eps[q]);
+          }
+          out_base += tot;
+          __syncthreads();
+        }
+        double v[1] = {me};
+        const bool mx[1] = {true};
+        block_reduce<1>(v, mx, sh);
+        if (threadIdx.x == 0) put_slot(p, kSlMaxEps, v[0]);
+      }
+      // u = A_S x_next over the kept nonzeros (131-146); v fix for dropped atoms
+      const bool need_fix = shrink && fista;
+      ApplySrc as{bk.idx, bk.x, nullptr, 1.0, bk.keep, need_fix ? bk.xp : nullptr};
+      C_apply = op_apply_partials(p, sh, lv, as, S, sh.nnz + (need_fix ? 8 : 0), p.up, need_fix ? p.dvp : nullptr,
+                                  sc.list, sc.coef, sc.fixc);
+    }
+    if (threadIdx.x == 0) {  // ledger + trace (611-623)
+      s.ledger += row_flops(p, s.dict_index, S, sh.nnz);
+      if (p.collect_trace && blockIdx.x == 0) {
+        fl1_trace_row row;
+        row.iter = s.t;
+        row.dict_index = s.dict_index;
+        row.active_size = static_cast<int32_t>(S);
+        row.gap = s.dict_index == last ? sh.gap_tilde : -1.0;
+        row.gamma = sh.gamma;
+        row.flops_cum = s.ledger;
+        row.wall_ms = (globaltimer_ns() - s.t0_ns) * 1e-6;
+        row.x_nnz = static_cast<int32_t>(sh.nnz);
+        row.pad_ = 0;
+        p.trace[s.n_trace] = row;
+      }
+      if (p.collect_trace) s.n_trace += 1;
+    }
+    if (stop_now) {
+      if (threadIdx.x == 0) {
+        s.converged = 1;
+        s.final_gap = sh.gap_tilde;
+        s.t += 1;
+        s.done = 1;
+        s.event = kEvDone;
+        s.prof_ns[2] += globaltimer_ns() - tp2;
+      }
+      __syncthreads();
+      break;
+    }
+    grid.sync();  // ------------------------------------------------ sync 3
+    // ---------------------------------------------------------- phase E
+    combine_u(p, C_apply, fista, shrink && fista);
+    if (threadIdx.x == 0) {
+      if (fista) {  // 581-590
+        if (s.momentum_ready) s.t_k = sh.t_next;
+        s.momentum_ready = 1;
+      }
+      if (shrink) {
+        s.cur ^= 1;
+        s.S = S_new;
+      }
+    }
+    __syncthreads();
+    if (shrink) {
+      grid_reduce(p, sh, 0u, 1u << kSlMaxEps);  // slot written before sync 3
+      if (threadIdx.x == 0) s.max_eps = S_new > 0 ? sh.res[kSlMaxEps] : 0.0;
+    }
+    grid.sync();  // ------------------------------------------------ sync 4
+    double tp3 = 0.0;
+    if (threadIdx.x == 0) {
+      tp3 = globaltimer_ns();
+      s.prof_ns[2] += tp3 - tp2;
+    }
+    // Lipschitz refresh after a halving (603-608)
+    if (s.S * 2 <= s.active_at_last_l && s.S > 0 && sh.next_dict == s.dict_index) {
+      const double sq = power_iteration(p, sh, lv, p.bank[s.cur], s.S, s.lead_valid != 0, sc);
+      if (threadIdx.x == 0) {
+        s.lead_valid = 1;
+        s.lipschitz = fmax(sq, 1e-300) * 1.05;
+        s.inv_l = 1.0 / s.lipschitz;
+        s.active_at_last_l = s.S;
+        s.prof_ns[3] += globaltimer_ns() - tp3;
+      }
+      __syncthreads();
+    }
+    const int next_dict = sh.next_dict;
+    const int sw_speed = sh.speed;
+    if (threadIdx.x == 0) s.t += 1;
+    __syncthreads();
+    if (next_dict != s.dict_index) {  // switch (633-637)
+      if (threadIdx.x == 0) {
+        if (blockIdx.x == 0) {
+          fl1_switch_event ev;
+          ev.iter = s.t - 1;
+          ev.from = s.dict_index;
+          ev.to = next_dict;
+          ev.speed = sw_speed;
+          ev.pad_ = 0;
+          p.sw[s.n_switches] = ev;
+        }
+        s.n_switches += 1;
+        s.dict_index = next_dict;
+      }
+      __syncthreads();
+      double tsw = 0.0;
+      if (threadIdx.x == 0) tsw = globaltimer_ns();
+      setup_dictionary(p, sh, false, sc);
+      if (threadIdx.x == 0) s.prof_ns[4] += globaltimer_ns() - tsw;
+    }
+    if (s.obs_pending) {
+      if (threadIdx.x == 0) s.event = kEvObserve;
+      __syncthreads();
+      break;
+    }
+  }
+  __syncthreads();
+  if (blockIdx.x == 0 && threadIdx.x == 0) *p.st = s;
+}
+
+// screen_precomputed (screening.cpp:136-150) as a standalone device kernel.
+__global__ void screen_kernel(int64_t n, const double* __restrict__ dots, const double* __restrict__ eps,
+                              const double* __restrict__ en, const double* __restrict__ an, double cn, double r,
+                              int8_t* keep, int8_t* look) {
+  for (int64_t j = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; j < n;
+       j += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const double d = dots[j];
+    keep[j] = (d + eps[j] * cn + r * en[j]) >= 1.0 ? 1 : 0;
+    look[j] = (d + r * an[j]) >= 1.0 ? 1 : 0;
+  }
+}
+
+// ---------------------------------------------------------------- host helpers
+cudaError_t screen_kernel_launch(int64_t n, const double* dots, const double* eps, const double* en,
+                                 const double* an, double cn, double r, int8_t* keep, int8_t* look,
+                                 cudaStream_t stream) {
+  const int64_t blocks = std::min<int64_t>((n + 255) / 256, 4096);
+  screen_kernel<<<static_cast<unsigned>(std::max<int64_t>(blocks, 1)), 256, 0, stream>>>(n, dots, eps, en, an, cn, r,
+                                                                                         keep, look);
+  return cudaGetLastError();
+}
+
+size_t engine_smem_bytes(int64_t ld, int64_t sukro_m) {
+  const int64_t scratch = std::max<int64_t>(3 * kApplyCap, sukro_m * (sukro_m + 1));
+  return static_cast<size_t>(ld + scratch) * sizeof(double);
+}
+
+cudaError_t engine_configure(int64_t ld, int64_t sukro_m, int device, int* grid_out) {
+  const size_t smem = engine_smem_bytes(ld, sukro_m);
+  int optin = 0;
+  cudaError_t e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+  if (e != cudaSuccess) return e;
+  if (smem + sizeof(Sh) + 1024 > static_cast<size_t>(optin)) return cudaErrorInvalidConfiguration;
+  e = cudaFuncSetAttribute(engine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           optin - static_cast<int>(sizeof(Sh)) - 1024);
+  if (e != cudaSuccess) return e;
+  int per_sm = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, engine_kernel, kThreads, smem);
+  if (e != cudaSuccess) return e;
+  int sms = 0;
+  e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  if (e != cudaSuccess) return e;
+  if (per_sm < 1) return cudaErrorInvalidConfiguration;
+  *grid_out = sms;  // one persistent CTA per SM
+  return cudaSuccess;
+}
+
+cudaError_t engine_launch(const EngineParams& p, int64_t sukro_m, cudaStream_t stream) {
+  EngineParams local = p;
+  void* args[] = {&local};
+  return cudaLaunchCooperativeKernel(reinterpret_cast<void*>(engine_kernel), dim3(p.grid), dim3(kThreads), args,
+                                     engine_smem_bytes(p.ld, sukro_m), stream);
+}
+
+}  // namespace fl1

@@ -1,0 +1,171 @@
+// engine.cuh — data layout shared by the host side (api.cpp) and the persistent
+// engine kernel (engine.cu). Everything here lives in HBM; the kernel keeps a
+// per-CTA copy of the scalar state (EngineState) in shared memory, and every
+// CTA evolves it identically from identical, fixed-order reductions, so no
+// scalar ever needs a host round trip.
+#pragma once
+
+#include <cstdint>
+
+#include "../../include/fl1cuda.h"
+
+namespace fl1 {
+
+constexpr int kMaxLevels = 8;
+#ifndef FL1_THREADS
+#define FL1_THREADS 512
+#endif
+#ifndef FL1_UNIT
+#define FL1_UNIT 256
+#endif
+constexpr int kThreads = FL1_THREADS;  // one persistent CTA per SM
+constexpr int kWarps = kThreads / 32;
+constexpr int kUnit = FL1_UNIT;  // doubles per A^T r work unit (one column segment)
+
+enum OpKind : int32_t { kDense = 0, kSukro = 1 };
+
+// One level of the ApproxSequence as the device sees it (dictionary.hpp:111-120).
+struct DevLevel {
+  int32_t kind;
+  int32_t nterms;
+  int64_t m, q;             // SuKro side lengths (N = m^2, K = q^2)
+  const double* a;          // dense: column-major, leading dimension ld
+  const double* left;       // SuKro: nterms blocks of m x q (B_t), column-major
+  const double* right;      // SuKro: nterms blocks of m x q (C_t)
+  const double* col_scale;  // SuKro column scale (extension), nullable
+  const double* eps;        // K: atom_error_bounds
+  const double* an;         // K: approx_atom_norms2
+  const double* en;         // K: exact_atom_norms2
+  double op_err;
+  double rc;
+  uint64_t matvec_flops;
+};
+
+// Per-atom arrays over the preserved set, in position order (ActiveOp state,
+// fastl1.cpp:203-210, plus the Engine's compact vectors, 226-247). Two banks:
+// a shrinking screening pass compacts bank[cur] into bank[cur^1].
+struct Bank {
+  int32_t* idx;   // global column index
+  double* x;      // iterate
+  double* xp;     // FISTA history
+  double* eps;    // gathered atom_error_bounds
+  double* en;     // gathered exact norms
+  double* an;     // gathered approx norms
+  double* aty;    // Atilde^T y (dynamic rule)
+  double* atye;   // A^T y (precompute_aty variant)
+  double* lead;   // power-iteration leading vector
+  int8_t* keep;   // screening decision of the last pass
+};
+
+enum Mode : int32_t { kModeSolve = 0, kModeResume = 1, kModePower = 2, kModeApply = 3, kModeAdjoint = 4 };
+enum Event : int32_t { kEvNone = 0, kEvDone = 1, kEvTraceFull = 2, kEvObserve = 3 };
+
+// Scalar engine state (Engine members, fastl1.cpp:213-252), persisted in HBM
+// between launches (trace flush / observer) and mirrored in every CTA.
+struct EngineState {
+  uint64_t t;
+  uint64_t ledger;
+  uint64_t trace_base;   // iteration index of trace row 0 in the device buffer
+  int64_t S;             // preserved-set size
+  int64_t active_at_last_l;
+  int64_t n_trace;       // rows in the device trace buffer
+  int64_t power_steps;
+  int64_t launches;
+  double t_k;
+  double lipschitz;
+  double inv_l;
+  double max_eps;
+  double y_sq;
+  double y_norm;
+  double final_gap;
+  double t0_ns;          // %globaltimer at run() start
+  double start_ns;       // %globaltimer at kernel start (solve mode)
+  int32_t dict_index;
+  int32_t cur;           // current bank
+  int32_t momentum_ready;
+  int32_t warning;
+  int32_t u_chunks;      // partial chunks holding u = A x
+  int32_t fix_pending;   // dvp holds a v correction to apply
+  int32_t lead_valid;    // bank lead holds S entries
+  int32_t atye_valid;
+  int32_t n_switches;
+  int32_t converged;
+  int32_t event;
+  int32_t done;
+  // observer snapshot of the last screening instant
+  uint64_t obs_iter;
+  int64_t obs_S;
+  double obs_radius;
+  double obs_scale_prime;
+  double obs_scale_tilde;
+  double obs_center_scale;  // center = obs_center_scale * ray (ray = rho or y)
+  int32_t obs_dict;
+  int32_t obs_bank;
+  int32_t obs_ray_is_y;
+  int32_t obs_pending;
+  // mode results
+  double power_est;
+  // device-side phase profile (block 0, %globaltimer ns): A+sync1, B+sync2,
+  // D+sync3, power iteration, switch setup; bytes of A^T r streamed
+  double prof_ns[6];
+  double prof_bytes;
+};
+
+struct EngineParams {
+  int32_t mode;
+  int32_t grid;
+  int64_t n, k, ld;
+  int32_t n_levels;
+  DevLevel lv[kMaxLevels];
+  double lambda;
+  // SwitchConfig
+  double gamma_threshold;
+  int32_t interval;
+  int32_t precompute_aty;
+  double tol;
+  double rel_tol;
+  uint64_t max_it;
+  // RunOptions
+  int32_t solver, rule, variant;
+  int32_t has_full_l;
+  double full_l[kMaxLevels];
+  int32_t collect_trace;
+  int32_t observe;
+  int32_t has_x_init;
+  int32_t mode_level;  // level used by Power / Apply / Adjoint modes
+  // vectors (length ld, zero padded)
+  const double* y;
+  const double* x_init;  // length K (solve) or K (apply mode input)
+  double* U;    // u = A x (combined)
+  double* V;    // v = A x_prev (before a pending fix)
+  double* rho;  // residual snapshot (observer)
+  double* up;   // apply partials: chunk-major, ld each
+  double* dvp;  // v-fix partials
+  double* pup;  // power-iteration apply partials
+  double* vec_out;  // Apply/Adjoint mode output (length ld or K)
+  double* corr;     // K
+  double* corr_y;   // K (exact-fit fallback)
+  double* part;     // K * units-per-column
+  int32_t* cnt;     // K column-completion counters
+  double* pv;       // K
+  double* pw;       // K
+  double* PU;       // ld: power-iteration A v (combined)
+  int32_t* sk_scat; // SuKro: per-CTA count of scattered entries (unscatter bookkeeping)
+  const double* gauss0;  // K: mt19937_64(0x11b5c417) normals (solver.cpp:80-82)
+  double* sk_t;     // SuKro scratch: 2 * nterms * q * m (T_t / W_t for two sources)
+  double* sk_x;     // SuKro scratch: 2 * K zero-padded operands (iterate, v-fix)
+  int32_t sk_ks;    // SuKro apply split-K chunks
+  double* bred;     // per-CTA partials: grid * kBred doubles
+  Bank bank[2];
+  fl1_trace_row* trace;
+  int64_t trace_cap;
+  fl1_switch_event* sw;
+  EngineState* st;
+};
+
+constexpr int kBred = 16;  // doubles of per-CTA partials
+constexpr int kApplyCap = 1024;  // positions compacted per apply sub-chunk
+constexpr int kSukroMaxM = 128;
+constexpr int kSukroMaxQ = 256;
+
+}  // namespace fl1

@@ -1,0 +1,16 @@
+"""One solve of a BASELINE config on the CUDA library; prints a one-line summary."""
+import os, sys
+sys.path.insert(0, os.path.join(os.path.dirname(__file__), '..'))
+import numpy as np
+from paper_1812_06635_b200 import fastl1 as F, synthetic as syn
+name = sys.argv[1] if len(sys.argv) > 1 else 'c2'
+inst = syn.dense_instance(name)
+d = F.DenseDictionary(inst.a)
+L = F.lipschitz_bound(d)
+seq = F.ApproxSequence([F.make_exact_approx(d)])
+cfg = F.SwitchConfig(screening_interval=10, max_iterations=5000, rel_tolerance=1e-6)
+out = F.run_lasso(seq, inst.y, inst.lam, cfg, F.RunOptions(variant=F.VARIANT_SCREENED, full_lipschitz=[L]))
+pr = out.profile
+print(f"lib={os.path.basename(os.environ.get('FL1_LIB','default'))} {name} it={out.iterations} dev_ms={out.device_ms:.3f} "
+      f"A={pr[0]/1e6:.3f} B={pr[1]/1e6:.3f} D={pr[2]/1e6:.3f} power={pr[3]/1e6:.3f} ({out.power_iterations} steps) "
+      f"A_GBps={pr[5]/max(pr[0],1):.0f} gap={out.final_gap:.6e}")
