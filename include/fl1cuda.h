@@ -133,6 +133,8 @@ typedef struct fl1_result_info {
   double setup_ms;     /* constructor part (initial L, u = A x) on device */
   int64_t kernel_launches; /* launches of this library's kernels during the solve */
   int64_t power_iterations; /* total power-iteration steps (all L estimates) */
+  int64_t h2d_bytes;        /* host->device bytes moved by this solve */
+  int64_t d2h_bytes;        /* device->host bytes moved by this solve */
 } fl1_result_info;
 
 /* ---- errors ---- */
@@ -193,7 +195,8 @@ int fl1_result_final_active(const fl1_result* r, int32_t* out);
 /* Device-side phase profile of the solve (ns, %globaltimer, CTA 0):
  * [0] products + A^T r pass, [1] dual scalars / screening / prox, [2] compaction +
  * sparse apply + ledger, [3] restricted power iterations, [4] switch setups,
- * [5] bytes streamed by the A^T r passes. out has 6 entries. */
+ * [5] bytes streamed by the A^T r passes, [6] bytes streamed by the sparse applies
+ * (8 N nnz), [7] bytes streamed by power iterations (16 N |S| per step). out has 8 entries. */
 int fl1_result_profile(const fl1_result* r, double* out);
 void fl1_result_free(fl1_result* r);
 

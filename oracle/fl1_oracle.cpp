@@ -1363,4 +1363,27 @@ int orc_screen(const int32_t* active, int64_t n_active, const double* center, do
   });
 }
 
+void orc_gen_normals(uint64_t seed, int64_t count, double* out) {
+  std::mt19937_64 rng(seed);
+  std::normal_distribution<double> gauss(0.0, 1.0);
+  for (int64_t i = 0; i < count; ++i) out[i] = gauss(rng);
+}
+void orc_gen_support(uint64_t seed, int64_t hi, int32_t support, int64_t* pos, double* val) {
+  // Same expression as the reference, `x(pick(rng)) = gauss(rng);`, so the
+  // compiler applies the same (C++17: right operand first) sequencing.
+  std::mt19937_64 rng(seed);
+  std::normal_distribution<double> gauss(0.0, 1.0);
+  std::uniform_int_distribution<int64_t> pick(0, hi);
+  int64_t last = -1;
+  auto slot = [&](int64_t i) -> double& {
+    last = i;
+    return *val;
+  };
+  for (int32_t s = 0; s < support; ++s) {
+    slot(pick(rng)) = gauss(rng);
+    pos[s] = last;
+    ++val;
+  }
+}
+
 }  // extern "C"

@@ -123,6 +123,16 @@ int orc_build_sphere(int32_t rule, int64_t n, const double* y, double lambda, do
 int orc_screen(const int32_t* active, int64_t n_active, const double* center, double radius,
                orc_approx* a, int32_t use_stable, int32_t* kept, int64_t* n_kept);
 
+/* The first `count` draws of std::mt19937_64(seed) through libstdc++'s
+ * std::normal_distribution<double>(0,1) — the RNG the reference uses for its
+ * seeded matrices (tests/helpers.hpp:35-50, dictionary.cpp:258-262, 391-405). */
+void orc_gen_normals(uint64_t seed, int64_t count, double* out);
+/* std::uniform_int_distribution<int64_t>(0, hi) draws interleaved with normals, as
+ * in testkit::random_instance / square_instance (helpers.hpp:76-89,
+ * test_fastl1.cpp:206-219): for each of `support` draws, pos = pick(rng),
+ * val = gauss(rng). */
+void orc_gen_support(uint64_t seed, int64_t hi, int32_t support, int64_t* pos, double* val);
+
 #ifdef __cplusplus
 }
 #endif

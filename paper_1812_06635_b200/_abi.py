@@ -98,6 +98,8 @@ class ResultInfoC(C.Structure):
         ("setup_ms", C.c_double),
         ("kernel_launches", C.c_int64),
         ("power_iterations", C.c_int64),
+        ("h2d_bytes", C.c_int64),
+        ("d2h_bytes", C.c_int64),
     ]
 
 
@@ -175,6 +177,8 @@ ORACLE_ONLY = {
     "dual_point_dynamic": (C.c_int, [C.c_int64, C.c_int64, _PD, _PD, _PD, _PD, C.c_double, _P, _PD, _PD, _PD, _PD]),
     "build_sphere": (C.c_int, [C.c_int32, C.c_int64, _PD, C.c_double, C.c_double, C.c_double, _PD, C.c_double, C.c_double, _PD, _PD]),
     "screen": (C.c_int, [_PI32, C.c_int64, _PD, C.c_double, _P, C.c_int32, _PI32, _PI64]),
+    "gen_normals": (None, [C.c_uint64, C.c_int64, _PD]),
+    "gen_support": (None, [C.c_uint64, C.c_int64, C.c_int32, _PI64, _PD]),
 }
 
 ERRORS = {

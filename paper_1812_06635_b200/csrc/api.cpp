@@ -11,6 +11,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <memory>
@@ -214,7 +215,8 @@ struct fl1_result {
   bool gap_warning = false;
   double device_ms = 0.0, setup_ms = 0.0;
   int64_t launches = 0, power_steps = 0;
-  double prof[6] = {0, 0, 0, 0, 0, 0};
+  double prof[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  int64_t h2d = 0, d2h = 0;
 };
 
 // ---------------------------------------------------------------- workspace
@@ -490,7 +492,9 @@ void do_solve(fl1_seq* s, const double* y, bool y_device, double lambda, const f
 
   ctx->bind();
   const uint64_t want_rows = opts->collect_trace ? cfg->max_iterations : 1;
-  const int64_t cap = static_cast<int64_t>(std::min<uint64_t>(std::max<uint64_t>(want_rows, 1), 1u << 20));
+  uint64_t cap_limit = 1u << 20;  // device trace rows per launch; full buffers are flushed and the solve resumes
+  if (const char* e = std::getenv("FL1_TRACE_CAP")) cap_limit = std::max<uint64_t>(1, std::strtoull(e, nullptr, 10));
+  const int64_t cap = static_cast<int64_t>(std::min<uint64_t>(std::max<uint64_t>(want_rows, 1), cap_limit));
   WsLease lease(ctx, n, k, cap, sk_elems, sk_m);
   Workspace& w = *lease.w;
   EngineParams p = w.base;
@@ -513,7 +517,7 @@ void do_solve(fl1_seq* s, const double* y, bool y_device, double lambda, const f
   p.observe = opts->observer ? 1 : 0;
   p.has_x_init = opts->x_init ? 1 : 0;
   p.gauss0 = ctx->gauss0(k);
-  p.trace_cap = w.trace_cap;
+  p.trace_cap = cap;  // <= w.trace_cap (a cached workspace may be larger)
 
   auto res = std::make_unique<fl1_result>();
   res->k = k;
@@ -533,6 +537,8 @@ void do_solve(fl1_seq* s, const double* y, bool y_device, double lambda, const f
        "x_init upload");
   std::vector<fl1_trace_row> host_rows;
   int64_t launches = 0;
+  int64_t h2d = static_cast<int64_t>(sizeof(st)) + (y_device ? 0 : 8 * n) + (opts->x_init ? 8 * k : 0);
+  int64_t d2h = 0;
   std::vector<int32_t> h_idx;
   std::vector<int8_t> h_keep;
   std::vector<double> h_rho, h_y;
@@ -541,8 +547,10 @@ void do_solve(fl1_seq* s, const double* y, bool y_device, double lambda, const f
     ++launches;
     ck(cudaMemcpyAsync(&st, p.st, sizeof(st), cudaMemcpyDeviceToHost, w.stream), "state download");
     ck(cudaStreamSynchronize(w.stream), "engine sync");
+    d2h += static_cast<int64_t>(sizeof(st));
     if (st.event == fl1::kEvTraceFull || st.event == fl1::kEvDone) {
       if (p.collect_trace && st.n_trace > 0) {
+        d2h += st.n_trace * static_cast<int64_t>(sizeof(fl1_trace_row));
         const size_t old = host_rows.size();
         host_rows.resize(old + static_cast<size_t>(st.n_trace));
         ck(cudaMemcpy(host_rows.data() + old, p.trace, static_cast<size_t>(st.n_trace) * sizeof(fl1_trace_row),
@@ -600,6 +608,7 @@ void do_solve(fl1_seq* s, const double* y, bool y_device, double lambda, const f
     // resume: push the edited state back
     st.event = fl1::kEvNone;
     p.mode = fl1::kModeResume;
+    h2d += static_cast<int64_t>(sizeof(st));
     ck(cudaMemcpyAsync(p.st, &st, sizeof(st), cudaMemcpyHostToDevice, w.stream), "state upload");
   }
   // finish (fastl1.cpp:741-748)
@@ -614,6 +623,7 @@ void do_solve(fl1_seq* s, const double* y, bool y_device, double lambda, const f
   if (st.n_switches > 0)
     ck(cudaMemcpyAsync(sws.data(), p.sw, sws.size() * sizeof(fl1_switch_event), cudaMemcpyDeviceToHost, w.stream),
        "switches");
+  d2h += st.S * 12 + st.n_switches * static_cast<int64_t>(sizeof(fl1_switch_event));
   ck(cudaEventRecord(w.ev1, w.stream), "event");
   ck(cudaStreamSynchronize(w.stream), "finish sync");
   float ms = 0.f;
@@ -634,6 +644,10 @@ void do_solve(fl1_seq* s, const double* y, bool y_device, double lambda, const f
   res->power_steps = st.power_steps;
   for (int i = 0; i < 5; ++i) res->prof[i] = st.prof_ns[i];
   res->prof[5] = st.prof_bytes;
+  res->prof[6] = st.prof_apply_bytes;
+  res->prof[7] = st.prof_power_bytes;
+  res->h2d = h2d;
+  res->d2h = d2h;
   *out = res.release();
 }
 
@@ -857,6 +871,8 @@ int fl1_result_info_get(const fl1_result* r, fl1_result_info* o) {
     o->setup_ms = r->setup_ms;
     o->kernel_launches = r->launches;
     o->power_iterations = r->power_steps;
+    o->h2d_bytes = r->h2d;
+    o->d2h_bytes = r->d2h;
   });
 }
 int fl1_result_x(const fl1_result* r, double* out) {
@@ -872,7 +888,7 @@ int fl1_result_final_active(const fl1_result* r, int32_t* out) {
   return guard([&] { std::copy(r->final_active.begin(), r->final_active.end(), out); });
 }
 int fl1_result_profile(const fl1_result* r, double* out) {
-  return guard([&] { std::copy(r->prof, r->prof + 6, out); });
+  return guard([&] { std::copy(r->prof, r->prof + 8, out); });
 }
 void fl1_result_free(fl1_result* r) { delete r; }
 

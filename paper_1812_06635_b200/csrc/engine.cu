@@ -739,7 +739,10 @@ __device__ __noinline__ double power_iteration(const EngineParams& p, Sh& sh, co
   const int min_iter = warm ? 2 : 4;
   bool have_w = false;  // pw holds the last w (v = pw / cur_div)
   for (int it = 0; it < max_iter; ++it) {
-    if (threadIdx.x == 0) sh.s.power_steps += 1;
+    if (threadIdx.x == 0) {
+      sh.s.power_steps += 1;
+      if (lv.kind == kDense) sh.s.prof_power_bytes += 16.0 * static_cast<double>(p.n) * static_cast<double>(S);
+    }
     // v for this step: materialise on this CTA's slice (Rayleigh quotient reads it)
     for (int64_t q = lo + threadIdx.x; q < hi; q += kThreads) p.pv[q] = cur_src[q] / cur_div;
     ApplySrc as{bk.idx, nullptr, cur_src, cur_div, nullptr, nullptr};
@@ -1314,6 +1317,7 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
     }
     if (threadIdx.x == 0) {  // ledger + trace (611-623)
       s.ledger += row_flops(p, s.dict_index, S, sh.nnz);
+      if (!stop_now && lv.kind == kDense) s.prof_apply_bytes += 8.0 * static_cast<double>(p.n) * static_cast<double>(sh.nnz);
       if (p.collect_trace && blockIdx.x == 0) {
         fl1_trace_row row;
         row.iter = s.t;

@@ -109,6 +109,8 @@ struct EngineState {
   // D+sync3, power iteration, switch setup; bytes of A^T r streamed
   double prof_ns[6];
   double prof_bytes;
+  double prof_apply_bytes;
+  double prof_power_bytes;
 };
 
 struct EngineParams {

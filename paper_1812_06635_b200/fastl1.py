@@ -348,6 +348,8 @@ class SolveResult:  # fastl1.hpp:61-71
     kernel_launches: int = 0
     power_iterations: int = 0
     profile: Optional[np.ndarray] = None  # product library only: see fl1_result_profile
+    h2d_bytes: int = 0
+    d2h_bytes: int = 0
 
 
 def _collect_result(lib: Library, h) -> SolveResult:
@@ -366,12 +368,13 @@ def _collect_result(lib: Library, h) -> SolveResult:
         lib.check(lib.result_final_active(h, fa.ctypes.data_as(C.POINTER(C.c_int32))))
     prof = None
     if hasattr(lib, "result_profile"):
-        prof = np.zeros(6)
+        prof = np.zeros(8)
         lib.check(lib.result_profile(h, _dptr(prof)))
     return SolveResult(profile=prof, x=x, converged=bool(info.converged), final_gap=info.final_gap, iterations=int(info.iterations),
                        total_flops=int(info.total_flops), trace=trace, switches=sws, final_active=fa,
                        gap_warning=bool(info.gap_warning), device_ms=info.device_ms, setup_ms=info.setup_ms,
-                       kernel_launches=int(info.kernel_launches), power_iterations=int(info.power_iterations))
+                       kernel_launches=int(info.kernel_launches), power_iterations=int(info.power_iterations),
+                       h2d_bytes=int(info.h2d_bytes), d2h_bytes=int(info.d2h_bytes))
 
 
 def _run_options_c(opts: RunOptions, keep: list) -> _abi.RunOptionsC:

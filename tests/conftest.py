@@ -8,8 +8,9 @@ from pathlib import Path
 import pytest
 
 ROOT = Path(__file__).resolve().parents[1]
-if str(ROOT) not in sys.path:
-    sys.path.insert(0, str(ROOT))
+for _p in (str(ROOT), str(ROOT / "tests")):
+    if _p not in sys.path:
+        sys.path.insert(0, _p)
 
 ORACLE_LIB = ROOT / "oracle" / "_build" / "libfl1oracle.so"
 
@@ -38,6 +39,26 @@ def oracle():
 @pytest.fixture(scope="session")
 def cuda():
     """The product: libfl1cuda.so on cuda:0. Fails loudly if not built."""
+    from paper_1812_06635_b200.fastl1 import default_backend
+
+    return default_backend()
+
+
+@pytest.fixture(scope="session")
+def refgen(oracle):
+    from _refgen import RefGen
+
+    return RefGen(oracle)
+
+
+BACKENDS = ["oracle", pytest.param("cuda", marks=pytest.mark.gpu)]
+
+
+@pytest.fixture(params=BACKENDS)
+def backend(request, oracle):
+    """Runs a test on the oracle (CPU suite) and on libfl1cuda.so (-m gpu)."""
+    if request.param == "oracle":
+        return oracle
     from paper_1812_06635_b200.fastl1 import default_backend
 
     return default_backend()

@@ -1,0 +1,226 @@
+"""GPU parity: libfl1cuda.so against the CPU oracle on the same seeded inputs,
+through the C-ABI, at BASELINE.json's full sizes where the oracle finishes in
+seconds, and through size-independent properties beyond that.
+
+Parity bar (BASELINE north_star): final objective within 1e-9 relative; final
+duality gap within 1e-9 of the objective (the gap is a difference of two
+O(P) quantities, so its own relative error is amplified by P/gap ~ 1e6 and
+1e-9 * P is the meaningful tolerance); identical final support; preserved sets
+equal at every iteration (trace integer fields); ledger identical.
+"""
+from __future__ import annotations
+
+import os
+
+import numpy as np
+import pytest
+
+from paper_1812_06635_b200 import fastl1 as F, synthetic as syn
+
+from _refgen import perturbed_approx
+
+pytestmark = pytest.mark.gpu
+
+OBJ_RTOL = 1e-9
+
+
+def primal(a, y, lam, x):
+    r = y - a @ x
+    return 0.5 * r @ r + lam * np.abs(x).sum()
+
+
+def assert_parity(g, o, a, y, lam, x_atol=1e-9):
+    assert g.converged == o.converged
+    assert g.iterations == o.iterations
+    for f in ("dict_index", "active_size", "x_nnz", "flops_cum", "iter"):
+        assert np.array_equal(g.trace[f], o.trace[f]), f
+    assert np.array_equal(g.final_active, o.final_active)
+    assert np.array_equal(g.x != 0, o.x != 0), "support differs"
+    assert np.array_equal(g.switches, o.switches)
+    assert g.total_flops == o.total_flops
+    pg, po = primal(a, y, lam, g.x), primal(a, y, lam, o.x)
+    assert abs(pg - po) <= OBJ_RTOL * abs(po)
+    if o.converged:
+        assert abs(g.final_gap - o.final_gap) <= OBJ_RTOL * abs(po)
+    gm, om = g.trace["gamma"], o.trace["gamma"]
+    assert np.array_equal(gm == -1.0, om == -1.0)
+    assert np.allclose(gm, om, rtol=1e-6, atol=1e-9)
+    assert np.max(np.abs(g.x - o.x)) <= x_atol * max(1.0, np.max(np.abs(o.x)))
+
+
+@pytest.fixture(scope="module")
+def oracle16(oracle):
+    oracle.lib.set_threads(os.cpu_count() or 1)  # results are identical for any thread count
+    return oracle
+
+
+def run_both(cuda, oracle, build_seq, y, lam, cfg, opts):
+    out = {}
+    for tag, b in (("gpu", cuda), ("orc", oracle)):
+        out[tag] = F.run_lasso(build_seq(b), y, lam, cfg, opts)
+    return out["gpu"], out["orc"]
+
+
+@pytest.mark.parametrize("name", ["c1", "c2"])
+def test_dense_configs_full_size(cuda, oracle16, name):
+    """BASELINE configs[0], configs[1] at full size: FISTA + GAP every 10, gap <= 1e-6 P."""
+    inst = syn.dense_instance(name)
+    L = F.lipschitz_bound(F.DenseDictionary(inst.a, backend=cuda))
+    cfg = F.SwitchConfig(screening_interval=10, max_iterations=5000, rel_tolerance=1e-6)
+    opts = F.RunOptions(variant=F.VARIANT_SCREENED, full_lipschitz=[L])
+    g, o = run_both(cuda, oracle16, lambda b: F.ApproxSequence([F.make_exact_approx(F.DenseDictionary(inst.a, backend=b))]),
+                    inst.y, inst.lam, cfg, opts)
+    assert g.converged
+    assert_parity(g, o, inst.a, inst.y, inst.lam)
+    assert g.final_gap <= 1e-6 * primal(inst.a, inst.y, inst.lam, g.x) * (1 + 1e-9)
+
+
+def test_cold_lipschitz_matches_oracle(cuda, oracle16):
+    inst = syn.dense_instance("c1")
+    lg = F.lipschitz_bound(F.DenseDictionary(inst.a, backend=cuda))
+    lo = F.lipschitz_bound(F.DenseDictionary(inst.a, backend=oracle16))
+    assert lg == pytest.approx(lo, rel=1e-12)
+    smax2 = np.linalg.svd(inst.a, compute_uv=False)[0] ** 2
+    assert smax2 * (1 - 1e-6) <= lg <= 1.05 * smax2 * (1 + 1e-9)
+
+
+def _sukro_seq(inst, b):
+    levels = []
+    for li, nt in enumerate(inst.levels):
+        op = F.SukroDictionary(list(zip(inst.lefts[:nt], inst.rights[:nt])), col_scale=inst.col_scale, backend=b)
+        levels.append(F.ApproxDictionary(op, inst.eps[li], float(inst.eps[li].max()), inst.rc[li],
+                                         inst.approx_norms[li], inst.exact_norms))
+    levels.append(F.make_exact_approx(F.DenseDictionary(inst.a, backend=b)))
+    return F.ApproxSequence(levels)
+
+
+@pytest.mark.parametrize("size", ["small", "full"])
+def test_kronecker_sum_config(cuda, oracle16, size):
+    """BASELINE configs[2]: stable screening + switching A1 -> A2 -> A4 -> A (full: 4096 x 16384)."""
+    if size == "small":
+        inst = syn.sukro_instance(seed=3, m=16, q=32, nnz=30)
+    else:
+        inst = syn.sukro_instance(seed=3)
+    cfg = F.SwitchConfig(screening_interval=10, max_iterations=5000, rel_tolerance=1e-6, gamma_threshold=0.5)
+    g, o = run_both(cuda, oracle16, lambda b: _sukro_seq(inst, b), inst.y, inst.lam, cfg, F.RunOptions())
+    assert g.converged
+    assert g.switches.size >= 1
+    assert_parity(g, o, inst.a, inst.y, inst.lam)
+
+
+OPTION_MATRIX = [
+    (s, r, v, pre)
+    for s in (F.SOLVER_ISTA, F.SOLVER_FISTA)
+    for r in (F.RULE_GAP, F.RULE_DYNAMIC)
+    for v in (F.VARIANT_PLAIN, F.VARIANT_SCREENED, F.VARIANT_MULTI_DICT)
+    for pre in ((False, True) if r == F.RULE_DYNAMIC else (False,))
+]
+
+
+@pytest.mark.parametrize("solver,rule,variant,pre", OPTION_MATRIX)
+def test_option_matrix_small(cuda, oracle16, refgen, solver, rule, variant, pre):
+    """Every solver / rule / variant combination on a perturbed-dense 3-level sequence."""
+    a, y, lam, _ = refgen.random_instance(60, 180, 0.25, 4242, support=6)
+
+    def build(b):
+        c, _ = perturbed_approx(F, b, refgen, a, 0.05, 11, rc=0.3)
+        f, _ = perturbed_approx(F, b, refgen, a, 0.01, 12, rc=0.6)
+        f.atom_error_bounds = np.minimum(f.atom_error_bounds, c.atom_error_bounds)
+        return F.ApproxSequence([c, f, F.make_exact_approx(F.DenseDictionary(a, backend=b))])
+
+    cfg = F.SwitchConfig(screening_interval=3, max_iterations=20000, tolerance=1e-10, precompute_aty=pre,
+                         gamma_threshold=0.5)
+    g, o = run_both(cuda, oracle16, build, y, lam, cfg, F.RunOptions(solver=solver, rule=rule, variant=variant))
+    assert_parity(g, o, a, y, lam)
+
+
+@pytest.mark.parametrize("n,k", [(7, 13), (33, 1000), (511, 700), (513, 300), (1025, 90), (2049, 40)])
+def test_ragged_shapes(cuda, oracle16, refgen, n, k):
+    """Odd N (padded leading dimension), N not a multiple of the 2 KiB unit, K < #SMs."""
+    a, y, lam, _ = refgen.random_instance(n, k, 0.3, 77 + n, support=min(5, k))
+    cfg = F.SwitchConfig(screening_interval=2, max_iterations=5000, tolerance=1e-11)
+    g, o = run_both(cuda, oracle16, lambda b: F.ApproxSequence([F.make_exact_approx(F.DenseDictionary(a, backend=b))]),
+                    y, lam, cfg, F.RunOptions(variant=F.VARIANT_SCREENED))
+    assert_parity(g, o, a, y, lam)
+
+
+def test_bit_reproducible(cuda):
+    inst = syn.dense_instance("c1")
+    seq = F.ApproxSequence([F.make_exact_approx(F.DenseDictionary(inst.a, backend=cuda))])
+    cfg = F.SwitchConfig(screening_interval=10, max_iterations=5000, rel_tolerance=1e-6)
+    r1 = F.run_lasso(seq, inst.y, inst.lam, cfg, F.RunOptions(variant=F.VARIANT_SCREENED))
+    r2 = F.run_lasso(seq, inst.y, inst.lam, cfg, F.RunOptions(variant=F.VARIANT_SCREENED))
+    assert np.array_equal(r1.x, r2.x) and r1.final_gap == r2.final_gap
+    assert np.array_equal(r1.trace["gap"], r2.trace["gap"])
+
+
+def test_trace_flush_and_resume(cuda, monkeypatch):
+    """A device trace buffer smaller than the run forces kernel exits + resumes; the
+    trajectory is unchanged bit for bit."""
+    inst = syn.dense_instance("c1")
+    seq = F.ApproxSequence([F.make_exact_approx(F.DenseDictionary(inst.a, backend=cuda))])
+    cfg = F.SwitchConfig(screening_interval=10, max_iterations=5000, rel_tolerance=1e-6)
+    ref = F.run_lasso(seq, inst.y, inst.lam, cfg, F.RunOptions(variant=F.VARIANT_SCREENED))
+    monkeypatch.setenv("FL1_TRACE_CAP", "7")
+    r = F.run_lasso(seq, inst.y, inst.lam, cfg, F.RunOptions(variant=F.VARIANT_SCREENED))
+    assert r.kernel_launches == (ref.iterations + 6) // 7
+    assert np.array_equal(r.x, ref.x)
+    for f in ("iter", "active_size", "x_nnz", "gap", "flops_cum"):
+        assert np.array_equal(r.trace[f], ref.trace[f]), f
+
+
+def test_device_resident_entry_point(cuda):
+    import torch
+
+    inst = syn.dense_instance("c1")
+    seq = F.ApproxSequence([F.make_exact_approx(F.DenseDictionary(inst.a, backend=cuda))])
+    cfg = F.SwitchConfig(screening_interval=10, max_iterations=5000, rel_tolerance=1e-6)
+    opts = F.RunOptions(variant=F.VARIANT_SCREENED)
+    y_dev = torch.from_numpy(inst.y).cuda()
+    r1 = F.run_lasso_device(seq, y_dev.data_ptr(), inst.lam, cfg, opts)
+    r2 = F.run_lasso(seq, inst.y, inst.lam, cfg, opts)
+    assert np.array_equal(r1.x, r2.x)
+    assert r1.h2d_bytes < r2.h2d_bytes
+
+
+def test_large_path_properties(cuda):
+    """BASELINE configs[3] shape (8192 x 65536, 4 GiB), first three lambdas of the warm-started
+    path: size-independent checks (certified gap recomputed independently, KKT, nesting)."""
+    import torch
+
+    n, k = 8192, 65536
+    gen = torch.Generator(device="cuda").manual_seed(4)
+    At = torch.randn(k, n, device="cuda", dtype=torch.float64, generator=gen)
+    At /= At.norm(dim=1, keepdim=True)
+    rng = np.random.default_rng(4)
+    x0 = np.zeros(k)
+    pos = rng.choice(k, 800, replace=False)
+    x0[pos] = rng.standard_normal(800)
+    x0t = torch.from_numpy(x0).cuda()
+    clean = At.T @ x0t
+    sigma = float(clean.norm()) / np.sqrt(n) * 10 ** (-20 / 20)
+    y = (clean + sigma * torch.from_numpy(rng.standard_normal(n)).cuda()).cpu().numpy()
+    d = F.DenseDictionaryDevice(At.data_ptr(), n, k, backend=cuda)
+    lmax = F.lambda_max(d, y)
+    corr = (At @ torch.from_numpy(y).cuda()).abs().max().item()
+    assert lmax == pytest.approx(corr, rel=1e-12)
+    L = F.lipschitz_bound(d)
+    seq = F.ApproxSequence([F.make_exact_approx(d)])
+    cfg = F.SwitchConfig(screening_interval=10, max_iterations=5000, rel_tolerance=1e-6)
+    x = None
+    yt = torch.from_numpy(y).cuda()
+    for ratio in syn.CONFIGS["c4"]["lam_ratios"][:3]:
+        lam = ratio * lmax
+        r = F.run_lasso(seq, y, lam, cfg, F.RunOptions(variant=F.VARIANT_SCREENED, full_lipschitz=[L], x_init=x))
+        assert r.converged
+        xt = torch.from_numpy(r.x).cuda()
+        rho = yt - At.T @ xt
+        p = 0.5 * float(rho @ rho) + lam * float(xt.abs().sum())
+        c = At @ rho
+        s = min(max(float(yt @ rho) / (lam * float(rho @ rho)), -1 / float(c.abs().max())), 1 / float(c.abs().max()))
+        dual = 0.5 * float(yt @ yt) - 0.5 * lam * lam * float(((s * rho - yt / lam) ** 2).sum())
+        assert p - dual <= 1e-5 * p  # independent fp64 recomputation with the ray at x
+        assert np.all(np.diff(r.trace["active_size"]) <= 0)
+        nz = np.nonzero(r.x)[0]
+        assert set(nz.tolist()) <= set(r.final_active.tolist())
+        x = r.x
