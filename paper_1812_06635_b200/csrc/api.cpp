@@ -215,7 +215,7 @@ struct fl1_result {
   bool gap_warning = false;
   double device_ms = 0.0, setup_ms = 0.0;
   int64_t launches = 0, power_steps = 0;
-  double prof[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  double prof[12] = {0};
   int64_t h2d = 0, d2h = 0;
 };
 
@@ -646,6 +646,7 @@ void do_solve(fl1_seq* s, const double* y, bool y_device, double lambda, const f
   res->prof[5] = st.prof_bytes;
   res->prof[6] = st.prof_apply_bytes;
   res->prof[7] = st.prof_power_bytes;
+  for (int i = 0; i < 4; ++i) res->prof[8 + i] = st.prof_pw[i];
   res->h2d = h2d;
   res->d2h = d2h;
   *out = res.release();
@@ -888,7 +889,7 @@ int fl1_result_final_active(const fl1_result* r, int32_t* out) {
   return guard([&] { std::copy(r->final_active.begin(), r->final_active.end(), out); });
 }
 int fl1_result_profile(const fl1_result* r, double* out) {
-  return guard([&] { std::copy(r->prof, r->prof + 8, out); });
+  return guard([&] { std::copy(r->prof, r->prof + 12, out); });
 }
 void fl1_result_free(fl1_result* r) { delete r; }
 

@@ -170,6 +170,64 @@ __device__ __forceinline__ double globaltimer_ns() {
   return static_cast<double>(t);
 }
 
+// Fixed-order sums of apply partials: sum_{c < C} part[c * ld + i].
+// Few chunks: one thread per row, all C loads in flight, added in c order.
+// Many chunks: one warp per row, lane l adds chunks l, l+32, ..., then a fixed
+// shuffle tree. Either way the order depends only on C.
+constexpr int kThreadCombineMax = 16;
+
+__device__ __forceinline__ double thread_sum_partials(const double* __restrict__ part, int C, int64_t ld, int64_t i) {
+  double v[kThreadCombineMax];
+#pragma unroll
+  for (int c = 0; c < kThreadCombineMax; ++c) v[c] = c < C ? __ldcg(part + static_cast<int64_t>(c) * ld + i) : 0.0;
+  double acc = 0.0;
+#pragma unroll
+  for (int c = 0; c < kThreadCombineMax; ++c)
+    if (c < C) acc += v[c];
+  return acc;
+}
+
+__device__ __forceinline__ double warp_sum_partials(const double* __restrict__ part, int C, int64_t ld, int64_t i) {
+  double acc = 0.0;
+  for (int c = threadIdx.x & 31; c < C; c += 32) acc += __ldcg(part + static_cast<int64_t>(c) * ld + i);
+  return warp_sum(acc);
+}
+
+// Calls f(i, value) for rows i in [lo, hi) (by one thread per row).
+template <class Fn>
+__device__ __forceinline__ void combine_rows(const double* __restrict__ part, int C, int64_t ld, int64_t lo, int64_t hi,
+                                             Fn&& f) {
+  if (C <= kThreadCombineMax) {
+    for (int64_t i = lo + threadIdx.x; i < hi; i += kThreads) f(i, thread_sum_partials(part, C, ld, i));
+  } else {
+    for (int64_t i = lo + (threadIdx.x >> 5); i < hi; i += kWarps) {
+      const double t = warp_sum_partials(part, C, ld, i);
+      if ((threadIdx.x & 31) == 0) f(i, t);
+    }
+  }
+}
+
+// dst[0:ld) = src[0:ld) with 128-bit loads, 4 in flight per thread (ld is even).
+__device__ __forceinline__ void load_vec_smem(const EngineParams& p, const double* src, double* dst) {
+  const int64_t n2 = p.ld >> 1;
+  const double2* __restrict__ s2 = reinterpret_cast<const double2*>(src);
+  double2* d2 = reinterpret_cast<double2*>(dst);
+  for (int64_t i0 = threadIdx.x; i0 < n2; i0 += 4 * kThreads) {
+    double2 v[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int64_t i = i0 + q * kThreads;
+      v[q] = i < n2 ? __ldcg(s2 + i) : make_double2(0.0, 0.0);
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int64_t i = i0 + q * kThreads;
+      if (i < n2) d2[i] = v[q];
+    }
+  }
+  __syncthreads();
+}
+
 // What an adjoint pass emits besides out[pos].
 struct PassOut {
   double* out;
@@ -242,63 +300,92 @@ __device__ __noinline__ void dense_adjoint(const EngineParams& p, Sh& sh, const 
   int nf = 0;
   // Units are visited in order; three register buffers form a ring so two
   // units' 128-bit loads are in flight while the current unit is reduced.
+  // (ic, ih) is the column / unit of the next unit to issue, (cc, ch) of the
+  // next unit to consume: incremented, never divided.
   constexpr int kV = kUnit / 64;  // double2 loads per lane per unit
-  auto issue = [&](double2 (&b)[kV], int u) {
-    const int cl = u / U, h = u - cl * U;
-    const double2* src = A2 + static_cast<int64_t>(__ldg(idx + c0 + cl)) * ld2 + h * (kUnit / 2);
-    if (h != U - 1 || last_nd2 == kUnit / 2) {
-#pragma unroll
-      for (int q = 0; q < kV; ++q) b[q] = ldg_stream2(src + 32 * q);
-    } else {
-#pragma unroll
-      for (int q = 0; q < kV; ++q) b[q] = (l + 32 * q < last_nd2) ? ldg_stream2(src + 32 * q) : make_double2(0.0, 0.0);
-    }
-  };
   double s = 0.0;
   bool began_here = (u_lo % U) == 0;
-  auto consume = [&](const double2 (&b)[kV], int u) {
-    const int cl = u / U, h = u - cl * U;
-    const double2* rr = r2 + h * (kUnit / 2);
-#pragma unroll
-    for (int q = 0; q < kV; ++q) {
-      const double2 rv = rr[32 * q];
-      s = fma(b[q].x, rv.x, s);
-      s = fma(b[q].y, rv.y, s);
-    }
-    const bool col_end = h == U - 1;
-    if (col_end || u + 1 == u_hi) {
-      const double t = warp_sum(s);
-      const bool whole = col_end && began_here;
-      if (l == 0) {
-        if (whole) {
-          out[c0 + cl] = t;
-        } else {
-          sh.frag[w][nf].pos = c0 + cl;
-          sh.frag[w][nf].sum = t;
-        }
-      }
-      if (!whole) ++nf;
-      s = 0.0;
-      began_here = true;
-    }
-  };
+  int ic = (U == 0) ? 0 : u_lo / U, ih = u_lo - ic * U;
+  int cc = ic, ch = ih;
+  const double2* colp = nullptr;
+  int colp_c = -1;
+#define FL1_ISSUE(B)                                                                                  \
+  do {                                                                                                \
+    if (ic != colp_c) {                                                                               \
+      colp = A2 + static_cast<int64_t>(__ldg(idx + c0 + ic)) * ld2;                                   \
+      colp_c = ic;                                                                                    \
+    }                                                                                                 \
+    const double2* src_ = colp + ih * (kUnit / 2);                                                    \
+    const int lim_ = (ih == U - 1 ? last_nd2 : kUnit / 2) - l; /* branch-free: predicated loads */    \
+    _Pragma("unroll") for (int q = 0; q < kV; ++q) B[q] =                                             \
+        (32 * q < lim_) ? ldg_stream2(src_ + 32 * q) : make_double2(0.0, 0.0);                       \
+    if (++ih == U) {                                                                                  \
+      ih = 0;                                                                                         \
+      ++ic;                                                                                           \
+    }                                                                                                 \
+  } while (0)
+#define FL1_CONSUME(B, U_)                                                                            \
+  do {                                                                                                \
+    const double2* rr_ = r2 + ch * (kUnit / 2);                                                       \
+    _Pragma("unroll") for (int q = 0; q < kV; ++q) {                                                  \
+      const double2 rv_ = rr_[32 * q];                                                                \
+      s = fma(B[q].x, rv_.x, s);                                                                      \
+      s = fma(B[q].y, rv_.y, s);                                                                      \
+    }                                                                                                 \
+    const bool col_end_ = ch == U - 1;                                                                \
+    if (col_end_ || (U_) + 1 == u_hi) {                                                               \
+      const double t_ = warp_sum(s);                                                                  \
+      const bool whole_ = col_end_ && began_here;                                                     \
+      if (l == 0) {                                                                                   \
+        if (whole_) {                                                                                 \
+          out[c0 + cc] = t_;                                                                          \
+        } else {                                                                                      \
+          sh.frag[w][nf].pos = c0 + cc;                                                               \
+          sh.frag[w][nf].sum = t_;                                                                    \
+        }                                                                                             \
+      }                                                                                               \
+      if (!whole_) ++nf;                                                                              \
+      s = 0.0;                                                                                        \
+      began_here = true;                                                                              \
+    }                                                                                                 \
+    if (++ch == U) {                                                                                  \
+      ch = 0;                                                                                         \
+      ++cc;                                                                                           \
+    }                                                                                                 \
+  } while (0)
   if (u_lo < u_hi) {
+#if FL1_RING == 3
     double2 b0[kV], b1[kV], b2[kV];
-    issue(b0, u_lo);
-    if (u_lo + 1 < u_hi) issue(b1, u_lo + 1);
+    FL1_ISSUE(b0);
+    if (u_lo + 1 < u_hi) FL1_ISSUE(b1);
     int u = u_lo;
     while (true) {
-      if (u + 2 < u_hi) issue(b2, u + 2);
-      consume(b0, u);
+      if (u + 2 < u_hi) FL1_ISSUE(b2);
+      FL1_CONSUME(b0, u);
       if (++u >= u_hi) break;
-      if (u + 2 < u_hi) issue(b0, u + 2);
-      consume(b1, u);
+      if (u + 2 < u_hi) FL1_ISSUE(b0);
+      FL1_CONSUME(b1, u);
       if (++u >= u_hi) break;
-      if (u + 2 < u_hi) issue(b1, u + 2);
-      consume(b2, u);
+      if (u + 2 < u_hi) FL1_ISSUE(b1);
+      FL1_CONSUME(b2, u);
       if (++u >= u_hi) break;
     }
+#else
+    double2 b0[kV], b1[kV];
+    FL1_ISSUE(b0);
+    int u = u_lo;
+    while (true) {
+      if (u + 1 < u_hi) FL1_ISSUE(b1);
+      FL1_CONSUME(b0, u);
+      if (++u >= u_hi) break;
+      if (u + 1 < u_hi) FL1_ISSUE(b0);
+      FL1_CONSUME(b1, u);
+      if (++u >= u_hi) break;
+    }
+#endif
   }
+#undef FL1_ISSUE
+#undef FL1_CONSUME
   if (l == 0) sh.nfrag[w] = nf;
   __syncthreads();
   // merge columns split between warps, in warp (= unit) order
@@ -417,169 +504,126 @@ struct ApplySrc {
   const double* xp;        // nullable: keep == 0 && xp != 0 feed the v fix (apply_restriction 673-684)
   __device__ __forceinline__ double c(int64_t pos) const { return coef_div ? coef_div[pos] / div : coef[pos]; }
   __device__ __forceinline__ bool kept(int64_t pos) const { return keep == nullptr || keep[pos] != 0; }
+  // coefficient of position pos for pass `fix` (0: kept atoms, 1: dropped atoms' history)
+  __device__ __forceinline__ double coef_for(int64_t pos, bool fix) const {
+    if (!fix) return kept(pos) ? c(pos) : 0.0;
+    return keep[pos] == 0 ? xp[pos] : 0.0;
+  }
 };
 
-// Row tiling of the dense apply: a work item covers kThreads/G double2 rows with
-// G column groups (so short signals still use every thread).
-struct ApplyTiling {
-  int tr2;  // double2 rows per tile
-  int G;    // column groups per work item
-  int64_t R;  // row tiles
-};
-__device__ __forceinline__ ApplyTiling apply_tiling(const EngineParams& p) {
-  ApplyTiling t;
-  const int64_t rows2 = p.ld >> 1;
-  int tr2 = kThreads;
-  while (tr2 > 32 && tr2 / 2 >= rows2) tr2 /= 2;
-  t.tr2 = tr2;
-  t.G = kThreads / tr2;
-  t.R = (rows2 + tr2 - 1) / tr2;
-  return t;
+// Dense apply as streamed (column, 256-row unit) work, the transpose of the
+// adjoint's traversal: work item (h, c) = row unit h x column chunk c; the 16
+// warps of a CTA split the chunk's positions contiguously, read the
+// coefficients 32 at a time, skip zeros by ballot, and stream the nonzero
+// columns' units through the same three-stage register ring (kV x 128-bit
+// loads per lane) into per-lane accumulators. Warp partials are added in warp
+// order in shared memory; out[c*ld + row] holds chunk c's partial sum.
+__device__ __forceinline__ int dense_apply_chunks(const EngineParams& p, int64_t S) {
+  const int64_t U = (p.n + kUnit - 1) / kUnit;
+  int64_t c = p.grid / U;
+  const int64_t by_work = (S + 31) / 32;  // at least ~2 positions per warp
+  if (c > by_work) c = by_work;
+  return static_cast<int>(c < 1 ? 1 : c);
 }
 
-__device__ __forceinline__ int dense_apply_chunks(const EngineParams& p, int64_t work) {
-  const int64_t R = apply_tiling(p).R;
-  int64_t cmax = p.grid / R;
-  if (cmax < 1) cmax = 1;
-  int64_t c = (work + 3) / 4;
-  if (c < 1) c = 1;
-  if (c > cmax) c = cmax;
-  return static_cast<int>(c);
-}
-
-// Dense: work item b -> (row tile b % R, position chunk b / R); the nonzero
-// coefficients of each chunk are stream-compacted (order preserved) into shared
-// memory; thread (g, i2) owns rows 2*i2, 2*i2+1 of the tile and streams columns
-// g, g+G, ... of the list with 8 independent 128-bit loads in flight; the G
-// group sums are added in group order. out[c*ld + i] holds chunk c's sum.
-__device__ __noinline__ void dense_apply_partials(const EngineParams& p, Sh& sh, const DevLevel& lv,
-                                                  const ApplySrc& src, int64_t S, int C, double* __restrict__ out,
-                                                  double* __restrict__ fix_out, int32_t* s_list, double* s_coef,
-                                                  double* s_fixc) {
-  const int64_t ld = p.ld;
-  const ApplyTiling tl = apply_tiling(p);
-  const int64_t b = blockIdx.x;
-  if (b >= tl.R * C) return;
-  const int64_t r = b % tl.R, c = b / tl.R;
-  const int64_t plo = S * c / C, phi = S * (c + 1) / C;
-  const int g = threadIdx.x / tl.tr2;
-  const int64_t i2 = r * tl.tr2 + (threadIdx.x - g * tl.tr2);  // double2 row index
-  const bool row_ok = 2 * i2 < ld;
+__device__ __noinline__ void dense_apply_units(const EngineParams& p, const DevLevel& lv, const ApplySrc& src,
+                                               int64_t S, bool fix, double* __restrict__ out, double* red) {
+  constexpr int kV = kUnit / 64;
+  const int64_t n = p.n, ld = p.ld, ld2 = ld >> 1;
+  const int U = static_cast<int>((n + kUnit - 1) / kUnit);
+  const int last_nd2 = static_cast<int>(((n - static_cast<int64_t>(U - 1) * kUnit) + 1) >> 1);
+  const int C = dense_apply_chunks(p, S);
   const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-  double2 acc = make_double2(0.0, 0.0), facc = make_double2(0.0, 0.0);
-  const bool want_fix = fix_out != nullptr;
-  const double2* __restrict__ A2 = reinterpret_cast<const double2*>(lv.a) + i2;
-  const int64_t ld2 = ld / 2;
-  for (int64_t base = plo; base < phi; base += kApplyCap) {
-    const int64_t end = min(phi, base + static_cast<int64_t>(kApplyCap));
-    const int64_t nb = end - base;
-    const int per = static_cast<int>((nb + kThreads - 1) / kThreads);
-    const int64_t my_lo = base + static_cast<int64_t>(threadIdx.x) * per;
-    int mine = 0, mine_fix = 0;
-    for (int q = 0; q < per; ++q) {
-      const int64_t pos = my_lo + q;
-      if (pos < end) {
-        const bool kp = src.kept(pos);
-        if (kp && src.c(pos) != 0.0) ++mine;
-        if (!kp && want_fix && src.xp[pos] != 0.0) ++mine_fix;
-      }
-    }
-    int incl = mine, incl2 = mine_fix;
+  const double2* __restrict__ A2 = reinterpret_cast<const double2*>(lv.a) + l;
+  for (int64_t item = blockIdx.x; item < static_cast<int64_t>(U) * C; item += gridDim.x) {
+    const int h = static_cast<int>(item % U);
+    const int64_t c = item / U;
+    const int64_t clo = S * c / C, chi = S * (c + 1) / C;
+    const int64_t p0 = clo + (chi - clo) * w / kWarps, p1 = clo + (chi - clo) * (w + 1) / kWarps;
+    const int nd2 = h == U - 1 ? last_nd2 : kUnit / 2;
+    const int64_t hoff = static_cast<int64_t>(h) * (kUnit / 2);
+    double2 acc[kV];
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int t1 = __shfl_up_sync(kFull, incl, o);
-      const int t2 = __shfl_up_sync(kFull, incl2, o);
-      if (l >= o) {
-        incl += t1;
-        incl2 += t2;
-      }
-    }
-    if (l == 31) {
-      sh.wcount[0][w] = incl;
-      sh.wcount[1][w] = incl2;
-    }
-    __syncthreads();
-    int woff = 0, woff2 = 0, tot = 0, tot2 = 0;
-    for (int q = 0; q < kWarps; ++q) {
-      if (q < w) {
-        woff += sh.wcount[0][q];
-        woff2 += sh.wcount[1][q];
-      }
-      tot += sh.wcount[0][q];
-      tot2 += sh.wcount[1][q];
-    }
-    int o1 = woff + incl - mine;
-    int o2 = woff2 + incl2 - mine_fix;
-    for (int q = 0; q < per; ++q) {
-      const int64_t pos = my_lo + q;
-      if (pos < end) {
-        const bool kp = src.kept(pos);
-        const double cf = src.c(pos);
-        if (kp && cf != 0.0) {
-          s_list[o1] = src.idx[pos];
-          s_coef[o1] = cf;
-          ++o1;
-        }
-        if (!kp && want_fix && src.xp[pos] != 0.0) {
-          s_list[kApplyCap + o2] = src.idx[pos];
-          s_fixc[o2] = src.xp[pos];
-          ++o2;
-        }
-      }
-    }
-    __syncthreads();
-    if (row_ok) {
-      const int G = tl.G;
-      int e = g;
-      for (; e + 7 * G < tot; e += 8 * G) {
-        double2 a[8];
+    for (int q = 0; q < kV; ++q) acc[q] = make_double2(0.0, 0.0);
+    auto issue = [&](double2 (&b)[kV], int32_t col) {
+      const double2* srcp = A2 + static_cast<int64_t>(col) * ld2 + hoff;
+      if (nd2 == kUnit / 2) {
 #pragma unroll
-        for (int q = 0; q < 8; ++q) a[q] = ldg_stream2(A2 + static_cast<int64_t>(s_list[e + q * G]) * ld2);
+        for (int q = 0; q < kV; ++q) b[q] = ldg_stream2(srcp + 32 * q);
+      } else {
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          const double cf = s_coef[e + q * G];
-          acc.x = fma(cf, a[q].x, acc.x);
-          acc.y = fma(cf, a[q].y, acc.y);
+        for (int q = 0; q < kV; ++q) b[q] = (l + 32 * q < nd2) ? ldg_stream2(srcp + 32 * q) : make_double2(0.0, 0.0);
+      }
+    };
+    auto consume = [&](const double2 (&b)[kV], double cf) {
+#pragma unroll
+      for (int q = 0; q < kV; ++q) {
+        acc[q].x = fma(cf, b[q].x, acc[q].x);
+        acc[q].y = fma(cf, b[q].y, acc[q].y);
+      }
+    };
+    for (int64_t g0 = p0; g0 < p1; g0 += 32) {
+      const int64_t pos = g0 + l;
+      double cf = 0.0;
+      int32_t col = 0;
+      if (pos < p1) {
+        cf = src.coef_for(pos, fix);
+        if (cf != 0.0) col = src.idx[pos];
+      }
+      unsigned mask = __ballot_sync(kFull, cf != 0.0);
+      // ring over the set bits, in position order
+      double2 b0[kV], b1[kV], b2[kV];
+      int l0 = -1, l1 = -1, l2 = -1;
+      if (mask) {
+        l0 = __ffs(mask) - 1;
+        mask &= mask - 1;
+        issue(b0, __shfl_sync(kFull, col, l0));
+      }
+      if (mask) {
+        l1 = __ffs(mask) - 1;
+        mask &= mask - 1;
+        issue(b1, __shfl_sync(kFull, col, l1));
+      }
+      while (l0 >= 0) {
+        if (mask) {
+          l2 = __ffs(mask) - 1;
+          mask &= mask - 1;
+          issue(b2, __shfl_sync(kFull, col, l2));
+        } else {
+          l2 = -1;
         }
-      }
-      for (; e < tot; e += G) {
-        const double2 a = ldg_stream2(A2 + static_cast<int64_t>(s_list[e]) * ld2);
-        const double cf = s_coef[e];
-        acc.x = fma(cf, a.x, acc.x);
-        acc.y = fma(cf, a.y, acc.y);
-      }
-      for (int f = g; f < tot2; f += G) {
-        const double2 a = ldg_stream2(A2 + static_cast<int64_t>(s_list[kApplyCap + f]) * ld2);
-        const double cf = s_fixc[f];
-        facc.x = fma(cf, a.x, facc.x);
-        facc.y = fma(cf, a.y, facc.y);
+        consume(b0, __shfl_sync(kFull, cf, l0));
+        if (l1 < 0) break;
+        if (mask) {
+          l0 = __ffs(mask) - 1;
+          mask &= mask - 1;
+          issue(b0, __shfl_sync(kFull, col, l0));
+        } else {
+          l0 = -1;
+        }
+        consume(b1, __shfl_sync(kFull, cf, l1));
+        if (l2 < 0) break;
+        if (mask) {
+          l1 = __ffs(mask) - 1;
+          mask &= mask - 1;
+          issue(b1, __shfl_sync(kFull, col, l1));
+        } else {
+          l1 = -1;
+        }
+        consume(b2, __shfl_sync(kFull, cf, l2));
       }
     }
+    // warp partials -> shared memory -> sum over warps in order
+#pragma unroll
+    for (int q = 0; q < kV; ++q) reinterpret_cast<double2*>(red)[w * (kUnit / 2) + l + 32 * q] = acc[q];
     __syncthreads();
-  }
-  // combine the G column groups in group order (shared memory reuses the list area)
-  double2* red = reinterpret_cast<double2*>(s_coef);  // >= 2*kThreads double2 of scratch (coef + fixc)
-  if (tl.G > 1) {
-    red[threadIdx.x] = acc;
-    if (want_fix) red[kThreads + threadIdx.x] = facc;
-    __syncthreads();
-    if (g == 0) {
-      for (int gg = 1; gg < tl.G; ++gg) {
-        const double2 o = red[gg * tl.tr2 + threadIdx.x];
-        acc.x += o.x;
-        acc.y += o.y;
-        if (want_fix) {
-          const double2 of = red[kThreads + gg * tl.tr2 + threadIdx.x];
-          facc.x += of.x;
-          facc.y += of.y;
-        }
-      }
+    for (int e = threadIdx.x; e < kUnit; e += kThreads) {
+      double t = 0.0;
+      for (int ww = 0; ww < kWarps; ++ww) t += red[ww * kUnit + e];
+      const int64_t row = static_cast<int64_t>(h) * kUnit + e;
+      if (row < ld) __stcg(out + c * ld + row, t);
     }
     __syncthreads();
-  }
-  if (row_ok && g == 0) {
-    __stcg(reinterpret_cast<double2*>(out + c * ld) + i2, acc);
-    if (want_fix) __stcg(reinterpret_cast<double2*>(fix_out + c * ld) + i2, facc);
   }
 }
 
@@ -686,12 +730,12 @@ __device__ __noinline__ int sukro_apply_partials(const EngineParams& p, const De
 
 // Returns the number of partial chunks written to out (and fix_out).
 __device__ int op_apply_partials(const EngineParams& p, Sh& sh, const DevLevel& lv, const ApplySrc& src, int64_t S,
-                                 int64_t work, double* out, double* fix_out, int32_t* s_list, double* s_coef,
-                                 double* s_fixc) {
+                                 double* out, double* fix_out, double* red) {
+  (void)sh;
   if (lv.kind == kDense) {
-    const int C = dense_apply_chunks(p, work);
-    dense_apply_partials(p, sh, lv, src, S, C, out, fix_out, s_list, s_coef, s_fixc);
-    return C;
+    dense_apply_units(p, lv, src, S, false, out, red);
+    if (fix_out) dense_apply_units(p, lv, src, S, true, fix_out, red);
+    return dense_apply_chunks(p, S);
   }
   return sukro_apply_partials(p, lv, src, S, out, fix_out);
 }
@@ -704,9 +748,7 @@ __device__ int op_apply_partials(const EngineParams& p, Sh& sh, const DevLevel& 
 struct Scratch {
   double* vec;     // ld doubles (shared memory)
   double* rt;      // SuKro R^T (shared memory)
-  int32_t* list;   // 2 * kApplyCap
-  double* coef;    // kApplyCap
-  double* fixc;    // kApplyCap
+  double* red;     // kWarps * kUnit doubles: apply warp partials (aliases rt)
 };
 
 __device__ __noinline__ double power_iteration(const EngineParams& p, Sh& sh, const DevLevel& lv, const Bank& bk, int64_t S,
@@ -745,32 +787,42 @@ __device__ __noinline__ double power_iteration(const EngineParams& p, Sh& sh, co
     }
     // v for this step: materialise on this CTA's slice (Rayleigh quotient reads it)
     for (int64_t q = lo + threadIdx.x; q < hi; q += kThreads) p.pv[q] = cur_src[q] / cur_div;
+    double tq0 = 0.0;
+    if (threadIdx.x == 0) tq0 = globaltimer_ns();
     ApplySrc as{bk.idx, nullptr, cur_src, cur_div, nullptr, nullptr};
-    const int C = op_apply_partials(p, sh, lv, as, S, S, p.pup, nullptr, sc.list, sc.coef, sc.fixc);
+    const int C = op_apply_partials(p, sh, lv, as, S, p.pup, nullptr, sc.red);
     grid.sync();
+    double tq1 = 0.0;
+    if (threadIdx.x == 0) {
+      tq1 = globaltimer_ns();
+      sh.s.prof_pw[0] += tq1 - tq0;
+    }
     if (static_cast<int64_t>(C) * p.ld <= kRedundantCombine) {
       // few partials: every CTA sums them itself (same order) instead of a combine phase
-      for (int64_t i = threadIdx.x; i < p.ld; i += kThreads) {
-        double acc = 0.0;
-        for (int c = 0; c < C; ++c) acc += __ldcg(p.pup + static_cast<int64_t>(c) * p.ld + i);
-        sc.vec[i] = acc;
-      }
+      combine_rows(p.pup, C, p.ld, 0, p.ld, [&](int64_t i, double t) { sc.vec[i] = t; });
     } else {
       int64_t ilo, ihi;
       slice(p.ld, ilo, ihi);
-      for (int64_t i = ilo + threadIdx.x; i < ihi; i += kThreads) {
-        double acc = 0.0;
-        for (int c = 0; c < C; ++c) acc += __ldcg(p.pup + static_cast<int64_t>(c) * p.ld + i);
-        __stcg(p.PU + i, acc);
-      }
+      combine_rows(p.pup, C, p.ld, ilo, ihi, [&](int64_t i, double t) { __stcg(p.PU + i, t); });
       grid.sync();
-      for (int64_t i = threadIdx.x; i < p.ld; i += kThreads) sc.vec[i] = __ldcg(p.PU + i);
+        load_vec_smem(p, p.PU, sc.vec);
     }
     __syncthreads();
+    double tq2 = 0.0;
+    if (threadIdx.x == 0) {
+      tq2 = globaltimer_ns();
+      sh.s.prof_pw[1] += tq2 - tq1;
+    }
     PassOut po{p.pw, 0, 0.0, false, 0, 0, p.pv};
     op_adjoint(p, sh, lv, bk.idx, bk.eps, S, sc.vec, sc.rt, po);
     grid.sync();
+    double tq3 = 0.0;
+    if (threadIdx.x == 0) {
+      tq3 = globaltimer_ns();
+      sh.s.prof_pw[2] += tq3 - tq2;
+    }
     grid_reduce(p, sh, (1u << kSlPw2) | (1u << kSlPvw), 0u);
+    if (threadIdx.x == 0) sh.s.prof_pw[3] += globaltimer_ns() - tq3;
     const double nrm = sqrt(sh.res[kSlPw2]);
     if (nrm == 0.0) {
       estimate = 0.0;
@@ -808,29 +860,19 @@ __device__ void gather_metadata(const EngineParams& p, Sh& sh, const DevLevel& l
   if (threadIdx.x == 0) put_slot(p, kSlMaxEps, v[0]);
 }
 
-__device__ __forceinline__ void load_vec_smem(const EngineParams& p, const double* src, double* dst) {
-  for (int64_t i = threadIdx.x; i < p.ld; i += kThreads) dst[i] = src[i];
-  __syncthreads();
-}
 
-// Combine apply partials into U by row slices. shift: v <- u_old - fix (FISTA).
+// Combine apply partials into U by row slices. shift: v <- u_old - fix
+// (FISTA bookkeeping 581-590 + apply_restriction 673-684).
 __device__ void combine_u(const EngineParams& p, int C, bool shift, bool fix) {
   int64_t lo, hi;
   slice(p.ld, lo, hi);
-  for (int64_t i = lo + threadIdx.x; i < hi; i += kThreads) {
-    double u = 0.0;
-    for (int c = 0; c < C; ++c) u += __ldcg(p.up + static_cast<int64_t>(c) * p.ld + i);
-    if (shift) {
-      double v = __ldcg(p.U + i);
-      if (fix) {
-        double f = 0.0;
-        for (int c = 0; c < C; ++c) f += __ldcg(p.dvp + static_cast<int64_t>(c) * p.ld + i);
-        v -= f;
-      }
-      __stcg(p.V + i, v);
-    }
-    __stcg(p.U + i, u);
+  if (shift) {
+    // v first (reads the old u), then u; both passes touch the same rows of this CTA only
+    combine_rows(fix ? p.dvp : p.up, fix ? C : 0, p.ld, lo, hi,
+                 [&](int64_t i, double f) { __stcg(p.V + i, __ldcg(p.U + i) - f); });
+    __syncthreads();
   }
+  combine_rows(p.up, C, p.ld, lo, hi, [&](int64_t i, double u) { __stcg(p.U + i, u); });
 }
 
 // setup_dictionary (fastl1.cpp:283-324). first: constructor call.
@@ -874,7 +916,7 @@ __device__ __noinline__ void setup_dictionary(const EngineParams& p, Sh& sh, boo
   }
   // u = op.apply(x)
   ApplySrc as{bk.idx, bk.x, nullptr, 1.0, nullptr, nullptr};
-  const int C = op_apply_partials(p, sh, lv, as, s.S, s.S, p.up, nullptr, sc.list, sc.coef, sc.fixc);
+  const int C = op_apply_partials(p, sh, lv, as, s.S, p.up, nullptr, sc.red);
   grid.sync();
   combine_u(p, C, false, false);
   if (threadIdx.x == 0) {
@@ -904,9 +946,7 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
   Scratch sc;
   sc.vec = dyn;
   sc.rt = dyn + p.ld;  // SuKro R^T; aliases the apply scratch (never live together)
-  sc.list = reinterpret_cast<int32_t*>(dyn + p.ld);
-  sc.coef = dyn + p.ld + kApplyCap;
-  sc.fixc = dyn + p.ld + 2 * kApplyCap;
+  sc.red = dyn + p.ld;
 
   if (threadIdx.x == 0) s = *p.st;
   __syncthreads();
@@ -924,15 +964,11 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
       op_adjoint(p, sh, lv, bk.idx, bk.eps, k, sc.vec, sc.rt, po);
     } else if (p.mode == kModeApply) {
       ApplySrc as{bk.idx, p.x_init, nullptr, 1.0, nullptr, nullptr};
-      const int C = op_apply_partials(p, sh, lv, as, k, k, p.up, nullptr, sc.list, sc.coef, sc.fixc);
+      const int C = op_apply_partials(p, sh, lv, as, k, p.up, nullptr, sc.red);
       grid.sync();
       int64_t lo, hi;
       slice(ld, lo, hi);
-      for (int64_t i = lo + threadIdx.x; i < hi; i += kThreads) {
-        double acc = 0.0;
-        for (int c = 0; c < C; ++c) acc += __ldcg(p.up + static_cast<int64_t>(c) * ld + i);
-        p.vec_out[i] = acc;
-      }
+      combine_rows(p.up, C, ld, lo, hi, [&](int64_t i, double t) { p.vec_out[i] = t; });
     } else {
       const double sq = power_iteration(p, sh, lv, bk, k, false, sc);
       if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -1011,22 +1047,50 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
       t_next = 0.5 * (1.0 + sqrt(1.0 + 4.0 * s.t_k * s.t_k));
       momentum = (s.t_k - 1.0) / t_next;
     }
-    {  // compute_products (359-369): rho_g in shared memory
+    {  // compute_products (359-369): rho_g in shared memory (128-bit loads, 2 per array in flight)
       double arr = 0.0, ary = 0.0, aee = 0.0;
-      for (int64_t i = threadIdx.x; i < ld; i += kThreads) {
-        const double u = __ldcg(p.U + i);
-        const double uw = momentum != 0.0 ? (1.0 + momentum) * u - momentum * __ldcg(p.V + i) : u;
-        const double yi = i < n ? p.y[i] : 0.0;
-        const double r = i < n ? yi - uw : 0.0;
-        sc.vec[i] = r;
-        if (p.observe && blockIdx.x == 0) p.rho[i] = r;
-        arr = fma(r, r, arr);
-        ary = fma(yi, r, ary);
-        if (momentum != 0.0 && i < n) {
-          const double e = yi - u;
-          aee = fma(e, e, aee);
+      const int64_t n2 = ld >> 1;
+      const double2* __restrict__ U2 = reinterpret_cast<const double2*>(p.U);
+      const double2* __restrict__ V2 = reinterpret_cast<const double2*>(p.V);
+      const double2* __restrict__ Y2 = reinterpret_cast<const double2*>(p.y);
+      double2* R2 = reinterpret_cast<double2*>(sc.vec);
+      const bool mom = momentum != 0.0;
+      for (int64_t i0 = threadIdx.x; i0 < n2; i0 += 2 * kThreads) {
+        double2 uu[2], vv[2], yy[2];
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const int64_t i = i0 + q * kThreads;
+          const bool ok = i < n2;
+          uu[q] = ok ? __ldcg(U2 + i) : make_double2(0.0, 0.0);
+          vv[q] = ok && mom ? __ldcg(V2 + i) : make_double2(0.0, 0.0);
+          yy[q] = ok ? Y2[i] : make_double2(0.0, 0.0);  // padded rows of y are zero
+        }
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const int64_t i = i0 + q * kThreads;
+          if (i >= n2) continue;
+          const double e0[2] = {uu[q].x, uu[q].y}, v0[2] = {vv[q].x, vv[q].y}, y0[2] = {yy[q].x, yy[q].y};
+          double rr[2];
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int64_t row = 2 * i + h;
+            const double u = e0[h];
+            const double uw = mom ? (1.0 + momentum) * u - momentum * v0[h] : u;
+            const double yi = y0[h];
+            const double r = row < n ? yi - uw : 0.0;
+            rr[h] = r;
+            arr = fma(r, r, arr);
+            ary = fma(yi, r, ary);
+            if (mom && row < n) {
+              const double e = yi - u;
+              aee = fma(e, e, aee);
+            }
+          }
+          R2[i] = make_double2(rr[0], rr[1]);
+          if (p.observe && blockIdx.x == 0) reinterpret_cast<double2*>(p.rho)[i] = make_double2(rr[0], rr[1]);
         }
       }
+      __syncthreads();
       double v[3] = {arr, ary, aee};
       const bool mx[3] = {false, false, false};
       block_reduce<3>(v, mx, sh);
@@ -1312,8 +1376,7 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
       // u = A_S x_next over the kept nonzeros (131-146); v fix for dropped atoms
       const bool need_fix = shrink && fista;
       ApplySrc as{bk.idx, bk.x, nullptr, 1.0, bk.keep, need_fix ? bk.xp : nullptr};
-      C_apply = op_apply_partials(p, sh, lv, as, S, sh.nnz + (need_fix ? 8 : 0), p.up, need_fix ? p.dvp : nullptr,
-                                  sc.list, sc.coef, sc.fixc);
+      C_apply = op_apply_partials(p, sh, lv, as, S, p.up, need_fix ? p.dvp : nullptr, sc.red);
     }
     if (threadIdx.x == 0) {  // ledger + trace (611-623)
       s.ledger += row_flops(p, s.dict_index, S, sh.nnz);
@@ -1438,7 +1501,7 @@ cudaError_t screen_kernel_launch(int64_t n, const double* dots, const double* ep
 }
 
 size_t engine_smem_bytes(int64_t ld, int64_t sukro_m) {
-  const int64_t scratch = std::max<int64_t>(3 * kApplyCap, sukro_m * (sukro_m + 1));
+  const int64_t scratch = std::max<int64_t>(static_cast<int64_t>(kWarps) * kUnit, sukro_m * (sukro_m + 1));
   return static_cast<size_t>(ld + scratch) * sizeof(double);
 }
 

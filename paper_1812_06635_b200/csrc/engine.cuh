@@ -13,12 +13,15 @@ namespace fl1 {
 
 constexpr int kMaxLevels = 8;
 #ifndef FL1_THREADS
-#define FL1_THREADS 512
+#define FL1_THREADS 256
+#endif
+#ifndef FL1_RING
+#define FL1_RING 2  // register ring depth of the streaming passes (2: no spills at 255 regs)
 #endif
 #ifndef FL1_UNIT
-#define FL1_UNIT 256
+#define FL1_UNIT 512
 #endif
-constexpr int kThreads = FL1_THREADS;  // one persistent CTA per SM
+constexpr int kThreads = FL1_THREADS;  // one persistent CTA of 8 warps per SM (255 registers/thread)
 constexpr int kWarps = kThreads / 32;
 constexpr int kUnit = FL1_UNIT;  // doubles per A^T r work unit (one column segment)
 
@@ -111,6 +114,7 @@ struct EngineState {
   double prof_bytes;
   double prof_apply_bytes;
   double prof_power_bytes;
+  double prof_pw[4];  // power-iteration sub-phases: apply, combine, adjoint+norms, reduce
 };
 
 struct EngineParams {

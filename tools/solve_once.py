@@ -13,4 +13,4 @@ out = F.run_lasso(seq, inst.y, inst.lam, cfg, F.RunOptions(variant=F.VARIANT_SCR
 pr = out.profile
 print(f"lib={os.path.basename(os.environ.get('FL1_LIB','default'))} {name} it={out.iterations} dev_ms={out.device_ms:.3f} "
       f"A={pr[0]/1e6:.3f} B={pr[1]/1e6:.3f} D={pr[2]/1e6:.3f} power={pr[3]/1e6:.3f} ({out.power_iterations} steps) "
-      f"A_GBps={pr[5]/max(pr[0],1):.0f} gap={out.final_gap:.6e}")
+      f"A_GBps={pr[5]/max(pr[0],1):.0f} gap={out.final_gap:.6e} pw[apply,comb,adj,red]_ms={[round(v/1e6,3) for v in pr[8:12]]}")
