@@ -89,7 +89,7 @@ struct DevBuf {
   }
 };
 
-int64_t even_ld(int64_t n) { return (n + 1) / 2 * 2; }
+int64_t even_ld(int64_t n) { return (n + 3) / 4 * 4; }  // 32-byte aligned columns
 
 }  // namespace
 
@@ -245,6 +245,7 @@ size_t carve(EngineParams& p, char* base, int64_t n, int64_t k, int64_t ld, int 
   p.U = c.take<double>(ld);
   p.V = c.take<double>(ld);
   p.rho = c.take<double>(ld);
+  p.rho_obs = c.take<double>(ld);
   p.up = c.take<double>(static_cast<int64_t>(grid) * ld);
   p.dvp = c.take<double>(static_cast<int64_t>(grid) * ld);
   p.pup = c.take<double>(static_cast<int64_t>(grid) * ld);
@@ -571,7 +572,7 @@ void do_solve(fl1_seq* s, const double* y, bool y_device, double lambda, const f
         ck(cudaMemcpy(h_idx.data(), ob.idx, static_cast<size_t>(S0) * sizeof(int32_t), cudaMemcpyDeviceToHost), "obs");
         ck(cudaMemcpy(h_keep.data(), ob.keep, static_cast<size_t>(S0), cudaMemcpyDeviceToHost), "obs");
       }
-      ck(cudaMemcpy(h_rho.data(), p.rho, static_cast<size_t>(w.ld) * sizeof(double), cudaMemcpyDeviceToHost), "obs");
+      ck(cudaMemcpy(h_rho.data(), p.rho_obs, static_cast<size_t>(w.ld) * sizeof(double), cudaMemcpyDeviceToHost), "obs");
       if (h_y.empty()) {
         h_y.resize(static_cast<size_t>(n));
         ck(cudaMemcpy(h_y.data(), p.y, static_cast<size_t>(n) * sizeof(double), cudaMemcpyDeviceToHost), "obs");

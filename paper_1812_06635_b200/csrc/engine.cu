@@ -62,7 +62,13 @@ enum Slot {
   kSlMaxPlainY = 10,
   kSlMaxStableY = 11,
   kSlLead2 = 12,
+  kSlRhoSq = 13,   // ||rho_g||^2 partials (written by the combine phase)
+  kSlRhoY = 14,    // rho_g . y
+  kSlRhoE = 15,    // ||y - u||^2 (momentum != 0)
 };
+// ||x||_1 partials for iteration t live in kSlL1 (t even) / kSlL1b (t odd); written
+// by phase B of iteration t-1 (over the kept new iterate) or by the constructor.
+constexpr int kSlL1b = 16;
 
 struct Frag {
   int64_t pos;
@@ -152,6 +158,13 @@ __device__ __forceinline__ double2 ldg_stream2(const double2* ptr) {
   return r;
 }
 
+// 256-bit streaming load (sm_100: LDG.E.NA.ENL2.256); p must be 32-byte aligned.
+__device__ __forceinline__ void ldg_stream4(const double* ptr, double2& lo, double2& hi) {
+  asm volatile("ld.global.nc.L1::no_allocate.v4.f64 {%0, %1, %2, %3}, [%4];"
+               : "=d"(lo.x), "=d"(lo.y), "=d"(hi.x), "=d"(hi.y)
+               : "l"(ptr));
+}
+
 __device__ __forceinline__ double soft_threshold(double z, double u) {  // solver.cpp:9-13
   const double mag = fabs(z) - u;
   if (mag <= 0.0) return 0.0;
@@ -194,15 +207,25 @@ __device__ __forceinline__ double warp_sum_partials(const double* __restrict__ p
 }
 
 // Calls f(i, value) for rows i in [lo, hi) (by one thread per row).
+// Few chunks: one thread per row with every load in flight. More: 8 lanes per
+// row (lane g adds chunks g, g+8, ...; a fixed 3-step shuffle tree), so 32 rows
+// are combined per 256-thread pass with ~C/8 loads in flight per lane.
 template <class Fn>
 __device__ __forceinline__ void combine_rows(const double* __restrict__ part, int C, int64_t ld, int64_t lo, int64_t hi,
                                              Fn&& f) {
   if (C <= kThreadCombineMax) {
     for (int64_t i = lo + threadIdx.x; i < hi; i += kThreads) f(i, thread_sum_partials(part, C, ld, i));
   } else {
-    for (int64_t i = lo + (threadIdx.x >> 5); i < hi; i += kWarps) {
-      const double t = warp_sum_partials(part, C, ld, i);
-      if ((threadIdx.x & 31) == 0) f(i, t);
+    const int g = threadIdx.x & 7;
+    for (int64_t i0 = lo; i0 < hi; i0 += kThreads / 8) {  // uniform trip count (shuffles below)
+      const int64_t i = i0 + (threadIdx.x >> 3);
+      double acc = 0.0;
+      if (i < hi)
+        for (int c = g; c < C; c += 8) acc += __ldcg(part + static_cast<int64_t>(c) * ld + i);
+      acc += __shfl_xor_sync(kFull, acc, 4);
+      acc += __shfl_xor_sync(kFull, acc, 2);
+      acc += __shfl_xor_sync(kFull, acc, 1);
+      if (g == 0 && i < hi) f(i, acc);
     }
   }
 }
@@ -286,6 +309,8 @@ __device__ __noinline__ void dense_adjoint(const EngineParams& p, Sh& sh, const 
   const int64_t n = p.n;
   const int U = static_cast<int>((n + kUnit - 1) / kUnit);
   const int last_nd2 = static_cast<int>(((n - static_cast<int64_t>(U - 1) * kUnit) + 1) >> 1);
+  const int last_nd = static_cast<int>(n - static_cast<int64_t>(U - 1) * kUnit);
+  (void)last_nd;
   const int64_t ld2 = p.ld >> 1;
   int64_t c0, c1;
   slice(S, c0, c1);
@@ -309,6 +334,30 @@ __device__ __noinline__ void dense_adjoint(const EngineParams& p, Sh& sh, const 
   int cc = ic, ch = ih;
   const double2* colp = nullptr;
   int colp_c = -1;
+#if FL1_V4
+  // 256-bit loads: lane l owns doubles [4(l + 32 q), 4(l + 32 q) + 4) of the unit
+#define FL1_ISSUE(B)                                                                                  \
+  do {                                                                                                \
+    if (ic != colp_c) {                                                                               \
+      colp = A2 + static_cast<int64_t>(__ldg(idx + c0 + ic)) * ld2;                                   \
+      colp_c = ic;                                                                                    \
+    }                                                                                                 \
+    const double* src_ = reinterpret_cast<const double*>(colp - l) + ih * kUnit + 4 * l;              \
+    const int lim_ = (ih == U - 1 ? last_nd : kUnit) - 4 * l;                                         \
+    _Pragma("unroll") for (int q = 0; q < kV / 2; ++q) {                                              \
+      if (128 * q < lim_) {                                                                           \
+        ldg_stream4(src_ + 128 * q, B[2 * q], B[2 * q + 1]);                                          \
+      } else {                                                                                        \
+        B[2 * q] = make_double2(0.0, 0.0);                                                            \
+        B[2 * q + 1] = make_double2(0.0, 0.0);                                                        \
+      }                                                                                               \
+    }                                                                                                 \
+    if (++ih == U) {                                                                                  \
+      ih = 0;                                                                                         \
+      ++ic;                                                                                           \
+    }                                                                                                 \
+  } while (0)
+#else
 #define FL1_ISSUE(B)                                                                                  \
   do {                                                                                                \
     if (ic != colp_c) {                                                                               \
@@ -324,11 +373,17 @@ __device__ __noinline__ void dense_adjoint(const EngineParams& p, Sh& sh, const 
       ++ic;                                                                                           \
     }                                                                                                 \
   } while (0)
+#endif
+#if FL1_V4
+#define FL1_RV(q) rr_[(q & 1) + 64 * (q >> 1) + 2 * l]  /* double2 index of element pair q */
+#else
+#define FL1_RV(q) rr_[32 * q]
+#endif
 #define FL1_CONSUME(B, U_)                                                                            \
   do {                                                                                                \
-    const double2* rr_ = r2 + ch * (kUnit / 2);                                                       \
+    const double2* rr_ = r2 + ch * (kUnit / 2) - (FL1_V4 ? l : 0);                                    \
     _Pragma("unroll") for (int q = 0; q < kV; ++q) {                                                  \
-      const double2 rv_ = rr_[32 * q];                                                                \
+      const double2 rv_ = FL1_RV(q);                                                                  \
       s = fma(B[q].x, rv_.x, s);                                                                      \
       s = fma(B[q].y, rv_.y, s);                                                                      \
     }                                                                                                 \
@@ -386,6 +441,7 @@ __device__ __noinline__ void dense_adjoint(const EngineParams& p, Sh& sh, const 
   }
 #undef FL1_ISSUE
 #undef FL1_CONSUME
+#undef FL1_RV
   if (l == 0) sh.nfrag[w] = nf;
   __syncthreads();
   // merge columns split between warps, in warp (= unit) order
@@ -861,19 +917,56 @@ __device__ void gather_metadata(const EngineParams& p, Sh& sh, const DevLevel& l
 }
 
 
-// Combine apply partials into U by row slices. shift: v <- u_old - fix
-// (FISTA bookkeeping 581-590 + apply_restriction 673-684).
-__device__ void combine_u(const EngineParams& p, int C, bool shift, bool fix) {
+// Phase E: combine the apply partials into U by row slices; shift: v <- u_old - fix
+// (FISTA bookkeeping 581-590 + apply_restriction 673-684); then, for the same
+// rows, the NEXT iteration's compute_products (359-369):
+//   rho_g = y - ((1+m)u - m v)  into p.rho,
+// with per-CTA partials of ||rho_g||^2, rho_g.y and ||y-u||^2 in slots, so phase A
+// only loads rho_g and reduces three slots. m is the next iteration's momentum.
+__device__ void combine_u(const EngineParams& p, Sh& sh, int C, bool shift, bool fix, double m) {
   int64_t lo, hi;
   slice(p.ld, lo, hi);
   if (shift) {
-    // v first (reads the old u), then u; both passes touch the same rows of this CTA only
     combine_rows(fix ? p.dvp : p.up, fix ? C : 0, p.ld, lo, hi,
                  [&](int64_t i, double f) { __stcg(p.V + i, __ldcg(p.U + i) - f); });
     __syncthreads();
   }
   combine_rows(p.up, C, p.ld, lo, hi, [&](int64_t i, double u) { __stcg(p.U + i, u); });
+  __syncthreads();
+  double arr = 0.0, ary = 0.0, aee = 0.0;
+  const bool mom = m != 0.0;
+  for (int64_t i = lo + threadIdx.x; i < hi; i += kThreads) {
+    const double u = __ldcg(p.U + i);
+    const double uw = mom ? (1.0 + m) * u - m * __ldcg(p.V + i) : u;
+    const double yi = p.y[i];  // zero on padded rows
+    const double r = i < p.n ? yi - uw : 0.0;
+    __stcg(p.rho + i, r);
+    arr = fma(r, r, arr);
+    ary = fma(yi, r, ary);
+    if (mom && i < p.n) {
+      const double e = yi - u;
+      aee = fma(e, e, aee);
+    }
+  }
+  double v[3] = {arr, ary, aee};
+  const bool mx[3] = {false, false, false};
+  block_reduce<3>(v, mx, sh);
+  if (threadIdx.x == 0) {
+    put_slot(p, kSlRhoSq, v[0]);
+    put_slot(p, kSlRhoY, v[1]);
+    put_slot(p, kSlRhoE, v[2]);
+  }
 }
+
+// momentum of the next iteration from the FISTA state (fastl1.cpp:465-470)
+__device__ __forceinline__ double next_momentum(const EngineParams& p, double t_k, bool ready) {
+  if (p.solver != FL1_FISTA || !ready) return 0.0;
+  const double t_next = 0.5 * (1.0 + sqrt(1.0 + 4.0 * t_k * t_k));
+  return (t_k - 1.0) / t_next;
+}
+
+// ||x||_1 partial of this CTA's slice into the slot of iteration t
+__device__ __forceinline__ int l1_slot(uint64_t t) { return (t & 1) ? kSlL1b : kSlL1; }
 
 // setup_dictionary (fastl1.cpp:283-324). first: constructor call.
 __device__ __noinline__ void setup_dictionary(const EngineParams& p, Sh& sh, bool first, const Scratch& sc) {
@@ -918,7 +1011,7 @@ __device__ __noinline__ void setup_dictionary(const EngineParams& p, Sh& sh, boo
   ApplySrc as{bk.idx, bk.x, nullptr, 1.0, nullptr, nullptr};
   const int C = op_apply_partials(p, sh, lv, as, s.S, p.up, nullptr, sc.red);
   grid.sync();
-  combine_u(p, C, false, false);
+  combine_u(p, sh, C, false, false, 0.0);  // momentum restarts (fastl1.cpp:322-323)
   if (threadIdx.x == 0) {
     s.momentum_ready = 0;
     s.t_k = 1.0;
@@ -1008,6 +1101,14 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
     }
     __syncthreads();
     gather_metadata(p, sh, p.lv[s.dict_index], bk, k);
+    {  // ||x_0||_1 for iteration 0
+      double acc = 0.0;
+      for (int64_t q = lo + threadIdx.x; q < hi; q += kThreads) acc += p.has_x_init ? fabs(p.x_init[q]) : 0.0;
+      double v[1] = {acc};
+      const bool mx[1] = {false};
+      block_reduce<1>(v, mx, sh);
+      if (threadIdx.x == 0) put_slot(p, l1_slot(0), v[0]);
+    }
     grid.sync();
     grid_reduce(p, sh, 0u, 1u << kSlMaxEps);
     if (threadIdx.x == 0) s.max_eps = sh.res[kSlMaxEps];
@@ -1047,68 +1148,19 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
       t_next = 0.5 * (1.0 + sqrt(1.0 + 4.0 * s.t_k * s.t_k));
       momentum = (s.t_k - 1.0) / t_next;
     }
-    {  // compute_products (359-369): rho_g in shared memory (128-bit loads, 2 per array in flight)
-      double arr = 0.0, ary = 0.0, aee = 0.0;
-      const int64_t n2 = ld >> 1;
-      const double2* __restrict__ U2 = reinterpret_cast<const double2*>(p.U);
-      const double2* __restrict__ V2 = reinterpret_cast<const double2*>(p.V);
-      const double2* __restrict__ Y2 = reinterpret_cast<const double2*>(p.y);
-      double2* R2 = reinterpret_cast<double2*>(sc.vec);
-      const bool mom = momentum != 0.0;
-      for (int64_t i0 = threadIdx.x; i0 < n2; i0 += 2 * kThreads) {
-        double2 uu[2], vv[2], yy[2];
-#pragma unroll
-        for (int q = 0; q < 2; ++q) {
-          const int64_t i = i0 + q * kThreads;
-          const bool ok = i < n2;
-          uu[q] = ok ? __ldcg(U2 + i) : make_double2(0.0, 0.0);
-          vv[q] = ok && mom ? __ldcg(V2 + i) : make_double2(0.0, 0.0);
-          yy[q] = ok ? Y2[i] : make_double2(0.0, 0.0);  // padded rows of y are zero
-        }
-#pragma unroll
-        for (int q = 0; q < 2; ++q) {
-          const int64_t i = i0 + q * kThreads;
-          if (i >= n2) continue;
-          const double e0[2] = {uu[q].x, uu[q].y}, v0[2] = {vv[q].x, vv[q].y}, y0[2] = {yy[q].x, yy[q].y};
-          double rr[2];
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const int64_t row = 2 * i + h;
-            const double u = e0[h];
-            const double uw = mom ? (1.0 + momentum) * u - momentum * v0[h] : u;
-            const double yi = y0[h];
-            const double r = row < n ? yi - uw : 0.0;
-            rr[h] = r;
-            arr = fma(r, r, arr);
-            ary = fma(yi, r, ary);
-            if (mom && row < n) {
-              const double e = yi - u;
-              aee = fma(e, e, aee);
-            }
-          }
-          R2[i] = make_double2(rr[0], rr[1]);
-          if (p.observe && blockIdx.x == 0) reinterpret_cast<double2*>(p.rho)[i] = make_double2(rr[0], rr[1]);
-        }
-      }
-      __syncthreads();
-      double v[3] = {arr, ary, aee};
-      const bool mx[3] = {false, false, false};
-      block_reduce<3>(v, mx, sh);
+    {  // compute_products (359-369): rho_g was formed by the previous combine phase
+      load_vec_smem(p, p.rho, sc.vec);
+      if (p.observe && blockIdx.x == 0)
+        for (int64_t i = threadIdx.x; i < ld; i += kThreads) p.rho_obs[i] = sc.vec[i];
+      grid_reduce(p, sh, (1u << kSlRhoSq) | (1u << kSlRhoY) | (1u << kSlRhoE), 0u);
       if (threadIdx.x == 0) {
         sh.t_next = t_next;
-        sh.rho_sq = v[0];
-        sh.rho_dot_y = v[1];
-        sh.rho_x_sq = momentum != 0.0 ? v[2] : v[0];
-        sh.rho_norm = sqrt(v[0]);
+        sh.rho_sq = sh.res[kSlRhoSq];
+        sh.rho_dot_y = sh.res[kSlRhoY];
+        sh.rho_x_sq = momentum != 0.0 ? sh.res[kSlRhoE] : sh.res[kSlRhoSq];
+        sh.rho_norm = sqrt(sh.res[kSlRhoSq]);
       }
-    }
-    {  // ||x||_1 partial on this CTA's slice (473)
-      double acc = 0.0;
-      for (int64_t q = lo + threadIdx.x; q < hi; q += kThreads) acc += fabs(bk.x[q]);
-      double v[1] = {acc};
-      const bool mx[1] = {false};
-      block_reduce<1>(v, mx, sh);
-      if (threadIdx.x == 0) put_slot(p, kSlL1, v[0]);
+      __syncthreads();
     }
     const bool exact_fit = !(sh.rho_sq > 0.0);
     if (!exact_fit) {
@@ -1149,11 +1201,12 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
     }
 
     // ---------------------------------------------------------- phase B
-    grid_reduce(p, sh, 1u << kSlL1,
+    const int l1s = l1_slot(s.t);
+    grid_reduce(p, sh, 1u << l1s,
                 exact_fit ? ((1u << kSlMaxPlainY) | (1u << kSlMaxStableY))
                           : ((1u << kSlMaxPlain) | (1u << kSlMaxStable)));
     if (threadIdx.x == 0) {
-      const double x_l1 = sh.res[kSlL1];
+      const double x_l1 = sh.res[l1s];
       const double primal = 0.5 * sh.rho_x_sq + lambda * x_l1;
       double sp, st, ray_sq, ray_dot_y;  // dual_scalars (406-450)
       if (!exact_fit) {
@@ -1228,7 +1281,7 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
       const double inv_l = s.inv_l, thresh = lambda * s.inv_l;
       const bool fista = p.solver == FL1_FISTA;
       const bool use_atye = p.precompute_aty && s.atye_valid;
-      double kept = 0.0, look = 0.0, nnz = 0.0;
+      double kept = 0.0, look = 0.0, nnz = 0.0, l1n = 0.0;
       for (int64_t q = lo + threadIdx.x; q < hi; q += kThreads) {
         const double c = p.corr[q];
         const double xo = bk.x[q];
@@ -1258,16 +1311,18 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
           if (keep) {
             kept += 1.0;
             nnz += xn != 0.0 ? 1.0 : 0.0;
+            l1n += fabs(xn);  // ||x_{t+1}||_1 over the preserved set (next iteration's 473)
           }
         }
       }
-      double v[3] = {kept, look, nnz};
-      const bool mx[3] = {false, false, false};
-      block_reduce<3>(v, mx, sh);
+      double v[4] = {kept, look, nnz, l1n};
+      const bool mx[4] = {false, false, false, false};
+      block_reduce<4>(v, mx, sh);
       if (threadIdx.x == 0) {
         put_slot(p, kSlKept, v[0]);
         put_slot(p, kSlLook, v[1]);
         put_slot(p, kSlNnz, v[2]);
+        if (!stop_now) put_slot(p, l1_slot(s.t + 1), v[3]);
       }
     }
     grid.sync();  // ------------------------------------------------ sync 2
@@ -1410,7 +1465,10 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
     }
     grid.sync();  // ------------------------------------------------ sync 3
     // ---------------------------------------------------------- phase E
-    combine_u(p, C_apply, fista, shrink && fista);
+    {
+      const double tk_next = fista ? (s.momentum_ready ? sh.t_next : s.t_k) : s.t_k;
+      combine_u(p, sh, C_apply, fista, shrink && fista, next_momentum(p, tk_next, fista));
+    }
     if (threadIdx.x == 0) {
       if (fista) {  // 581-590
         if (s.momentum_ready) s.t_k = sh.t_next;

@@ -18,6 +18,9 @@ constexpr int kMaxLevels = 8;
 #ifndef FL1_RING
 #define FL1_RING 2  // register ring depth of the streaming passes (2: no spills at 255 regs)
 #endif
+#ifndef FL1_V4
+#define FL1_V4 0  // 256-bit loads in the A^T r pass (needs ld % 4 == 0)
+#endif
 #ifndef FL1_UNIT
 #define FL1_UNIT 512
 #endif
@@ -144,7 +147,8 @@ struct EngineParams {
   const double* x_init;  // length K (solve) or K (apply mode input)
   double* U;    // u = A x (combined)
   double* V;    // v = A x_prev (before a pending fix)
-  double* rho;  // residual snapshot (observer)
+  double* rho;  // rho_g of the next iteration (written by the combine phase)
+  double* rho_obs;  // rho_g snapshot of the last screening instant (observer)
   double* up;   // apply partials: chunk-major, ld each
   double* dvp;  // v-fix partials
   double* pup;  // power-iteration apply partials
@@ -169,7 +173,7 @@ struct EngineParams {
   EngineState* st;
 };
 
-constexpr int kBred = 16;  // doubles of per-CTA partials
+constexpr int kBred = 20;  // doubles of per-CTA partials (slots, see engine.cu)
 constexpr int kApplyCap = 1024;  // positions compacted per apply sub-chunk
 constexpr int kSukroMaxM = 128;
 constexpr int kSukroMaxQ = 256;
