@@ -11,6 +11,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <limits>
@@ -251,6 +252,7 @@ size_t carve(EngineParams& p, char* base, int64_t n, int64_t k, int64_t ld, int 
   p.pup = c.take<double>(static_cast<int64_t>(grid) * ld);
   p.vec_out = c.take<double>(vec);
   p.corr = c.take<double>(kk);
+  p.xnew = c.take<double>(kk);
   p.corr_y = c.take<double>(kk);
   p.part = c.take<double>(kk * units);
   p.cnt = c.take<int32_t>(kk);
@@ -278,6 +280,7 @@ size_t carve(EngineParams& p, char* base, int64_t n, int64_t k, int64_t ld, int 
   p.trace = c.take<fl1_trace_row>(std::max<int64_t>(trace_cap, 1));
   p.sw = c.take<fl1_switch_event>(fl1::kMaxLevels);
   p.st = c.take<EngineState>(1);
+  p.timeline = nullptr;
   return c.off + 256;
 }
 
@@ -519,6 +522,13 @@ void do_solve(fl1_seq* s, const double* y, bool y_device, double lambda, const f
   p.has_x_init = opts->x_init ? 1 : 0;
   p.gauss0 = ctx->gauss0(k);
   p.trace_cap = cap;  // <= w.trace_cap (a cached workspace may be larger)
+  std::unique_ptr<DevBuf> timeline;
+  const char* tl_path = std::getenv("FL1_TIMELINE_OUT");  // instrumented builds only
+  if (tl_path) {
+    timeline = std::make_unique<DevBuf>(static_cast<size_t>(4096) * w.grid * 8 * sizeof(uint64_t));
+    ck(cudaMemset(timeline->p, 0, timeline->bytes), "timeline memset");
+    p.timeline = timeline->as<uint64_t>();
+  }
 
   auto res = std::make_unique<fl1_result>();
   res->k = k;
@@ -629,6 +639,14 @@ void do_solve(fl1_seq* s, const double* y, bool y_device, double lambda, const f
   ck(cudaStreamSynchronize(w.stream), "finish sync");
   float ms = 0.f;
   ck(cudaEventElapsedTime(&ms, w.ev0, w.ev1), "elapsed");
+  if (timeline) {
+    std::vector<uint64_t> h(timeline->bytes / sizeof(uint64_t));
+    ck(cudaMemcpy(h.data(), timeline->p, timeline->bytes, cudaMemcpyDeviceToHost), "timeline");
+    if (FILE* f = std::fopen(tl_path, "wb")) {
+      std::fwrite(h.data(), sizeof(uint64_t), h.size(), f);
+      std::fclose(f);
+    }
+  }
   res->x.assign(static_cast<size_t>(k), 0.0);
   for (size_t q = 0; q < idx.size(); ++q) res->x[static_cast<size_t>(idx[q])] = xs[q];
   res->final_active = std::move(idx);

@@ -45,6 +45,26 @@ namespace fl1 {
 namespace {
 
 constexpr unsigned kFull = 0xffffffffu;
+
+// FL1_TIMELINE builds record, per iteration (< 4096) and per CTA, %globaltimer at
+// 8 points (phase boundaries before / after each grid sync) into p.timeline.
+#ifndef FL1_TIMELINE
+#define FL1_TIMELINE 0
+#endif
+#if FL1_TIMELINE
+#define FL1_MARK(pt)                                                                                      \
+  do {                                                                                                    \
+    if (threadIdx.x == 0 && s.t < 4096 && p.timeline) {                                                   \
+      uint64_t t_;                                                                                        \
+      asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_));                                              \
+      p.timeline[(static_cast<int64_t>(s.t) * gridDim.x + blockIdx.x) * 8 + (pt)] = t_;                  \
+    }                                                                                                     \
+  } while (0)
+#else
+#define FL1_MARK(pt) \
+  do {               \
+  } while (0)
+#endif
 constexpr int64_t kRedundantCombine = 8192;  // doubles of partials each CTA may re-sum instead of a sync
 
 // per-CTA partial slots (bred[cta * kBred + slot])
@@ -276,6 +296,18 @@ struct PassAcc {
       vw = fma(po.vdot[pos], total, vw);
     }
   }
+  // same statistics with the per-atom operand (eps or vdot) already in a register
+  __device__ __forceinline__ void add_v(const EngineParams& p, const PassOut& po, double total, double aux) {
+    if (po.track) {
+      const double ac = po.div_lambda ? fabs(total) / p.lambda : fabs(total);
+      mp = fmax(mp, ac);
+      ms = fmax(ms, ac + aux * po.eps_scale);
+    }
+    if (po.vdot) {
+      w2 = fma(total, total, w2);
+      vw = fma(aux, total, vw);
+    }
+  }
 };
 
 __device__ void finish_pass(const EngineParams& p, Sh& sh, const PassOut& po, PassAcc& acc) {
@@ -462,7 +494,8 @@ __device__ __noinline__ void dense_adjoint(const EngineParams& p, Sh& sh, const 
     if (cp >= 0) out[cp] = cs;
   }
   __syncthreads();
-  // per-CTA statistics over this CTA's columns (fixed thread -> position map)
+  // per-CTA statistics over this CTA's columns (fixed thread -> position map); a
+  // separate short pass is cheaper than statistics inside the streaming loop
   if (po.track || po.vdot) {
     for (int64_t pos = c0 + threadIdx.x; pos < c1; pos += kThreads) acc.add(p, po, eps, pos, out[pos]);
   }
@@ -551,6 +584,64 @@ __device__ void op_adjoint(const EngineParams& p, Sh& sh, const DevLevel& lv, co
 // ----------------------------------------------------------------------------
 // Apply: partial sums of u = sum_pos coef(pos) a_{idx[pos]}.
 // ----------------------------------------------------------------------------
+// Per-atom screening test + prox step of one iteration (fastl1.cpp:519-548, 572-579,
+// screening.cpp:136-150, solver.cpp:9-13), written with explicit rounding
+// intrinsics so every caller (the slice owner in phase B and the apply work items
+// that re-derive coefficients on the fly) gets bit-identical results.
+struct ProxCtx {
+  const double* corr;
+  const double* corr_y;
+  const double* x;
+  const double* xp;
+  const double* eps;
+  const double* en;
+  const double* an;
+  const double* aty;
+  const double* atye;
+  double m, inv_l, thresh, sp, cn, R, lambda;
+  int screen_now, stable_test, rule_gap, ray_is_y, use_atye;
+  // per-atom inputs, loaded once (prefetchable)
+  struct Atom {
+    double c, cy, xo, xpv, eps, en, an, aty;
+  };
+  __device__ __forceinline__ Atom load(int64_t q) const {
+    Atom a;
+    a.c = corr[q];
+    a.xo = x[q];
+    a.xpv = m != 0.0 ? xp[q] : 0.0;
+    a.cy = (screen_now && rule_gap && ray_is_y) ? corr_y[q] : 0.0;
+    a.eps = (screen_now && stable_test) ? eps[q] : 0.0;
+    a.en = screen_now ? en[q] : 0.0;
+    a.an = (screen_now && stable_test) ? an[q] : 0.0;
+    a.aty = (screen_now && !rule_gap) ? (use_atye ? atye[q] : aty[q]) : 0.0;
+    return a;
+  }
+  __device__ __forceinline__ double dot(const Atom& a) const {
+    if (rule_gap) return fabs(__dmul_rn(sp, ray_is_y ? a.cy : a.c));
+    return fabs(__ddiv_rn(a.aty, lambda));
+  }
+  __device__ __forceinline__ bool keep(const Atom& a, double d) const {
+    if (!screen_now) return true;
+    if (stable_test) return __fma_rn(R, a.en, __fma_rn(a.eps, cn, d)) >= 1.0;  // stable_zone_test
+    return __fma_rn(R, a.en, d) >= 1.0;                                          // sphere_test
+  }
+  __device__ __forceinline__ bool look(const Atom& a, double d, bool kp) const {
+    if (!screen_now) return false;
+    if (stable_test) return __fma_rn(R, a.an, d) >= 1.0;  // lookahead on approx norms
+    return kp;
+  }
+  __device__ __forceinline__ double xnew(const Atom& a) const {
+    const double g = m != 0.0 ? __fma_rn(1.0 + m, a.xo, -__dmul_rn(m, a.xpv)) : a.xo;
+    const double z = __fma_rn(inv_l, a.c, g);
+    const double mag = fabs(z) - thresh;
+    if (mag <= 0.0) return 0.0;
+    return z > 0.0 ? mag : -mag;
+  }
+  __device__ __forceinline__ bool keep_at(int64_t q, const Atom& a) const {
+    return keep(a, screen_now ? dot(a) : 0.0);
+  }
+};
+
 struct ApplySrc {
   const int32_t* idx;
   const double* coef;      // values (x or power vector)
@@ -558,10 +649,17 @@ struct ApplySrc {
   double div;
   const int8_t* keep;      // nullable: only keep != 0 contribute
   const double* xp;        // nullable: keep == 0 && xp != 0 feed the v fix (apply_restriction 673-684)
+  const ProxCtx* prox;     // non-null: coefficients re-derived on the fly (phase B)
   __device__ __forceinline__ double c(int64_t pos) const { return coef_div ? coef_div[pos] / div : coef[pos]; }
   __device__ __forceinline__ bool kept(int64_t pos) const { return keep == nullptr || keep[pos] != 0; }
   // coefficient of position pos for pass `fix` (0: kept atoms, 1: dropped atoms' history)
   __device__ __forceinline__ double coef_for(int64_t pos, bool fix) const {
+    if (prox) {
+      const ProxCtx::Atom a = prox->load(pos);
+      const bool kp = prox->keep_at(pos, a);
+      if (!fix) return kp ? prox->xnew(a) : 0.0;
+      return kp ? 0.0 : a.xo;
+    }
     if (!fix) return kept(pos) ? c(pos) : 0.0;
     return keep[pos] == 0 ? xp[pos] : 0.0;
   }
@@ -845,7 +943,7 @@ __device__ __noinline__ double power_iteration(const EngineParams& p, Sh& sh, co
     for (int64_t q = lo + threadIdx.x; q < hi; q += kThreads) p.pv[q] = cur_src[q] / cur_div;
     double tq0 = 0.0;
     if (threadIdx.x == 0) tq0 = globaltimer_ns();
-    ApplySrc as{bk.idx, nullptr, cur_src, cur_div, nullptr, nullptr};
+    ApplySrc as{bk.idx, nullptr, cur_src, cur_div, nullptr, nullptr, nullptr};
     const int C = op_apply_partials(p, sh, lv, as, S, p.pup, nullptr, sc.red);
     grid.sync();
     double tq1 = 0.0;
@@ -926,26 +1024,58 @@ __device__ void gather_metadata(const EngineParams& p, Sh& sh, const DevLevel& l
 __device__ void combine_u(const EngineParams& p, Sh& sh, int C, bool shift, bool fix, double m) {
   int64_t lo, hi;
   slice(p.ld, lo, hi);
-  if (shift) {
-    combine_rows(fix ? p.dvp : p.up, fix ? C : 0, p.ld, lo, hi,
-                 [&](int64_t i, double f) { __stcg(p.V + i, __ldcg(p.U + i) - f); });
-    __syncthreads();
-  }
-  combine_rows(p.up, C, p.ld, lo, hi, [&](int64_t i, double u) { __stcg(p.U + i, u); });
-  __syncthreads();
-  double arr = 0.0, ary = 0.0, aee = 0.0;
+  // one pass per row: a group of G lanes sums the chunk partials (G = 1 for few
+  // chunks, else 8 with a fixed shuffle tree); the group leader's loads of
+  // u_old / v / y are issued together with the partials.
+  const int G = C <= kThreadCombineMax ? 1 : 8;
+  const int g = threadIdx.x % G;
   const bool mom = m != 0.0;
-  for (int64_t i = lo + threadIdx.x; i < hi; i += kThreads) {
-    const double u = __ldcg(p.U + i);
-    const double uw = mom ? (1.0 + m) * u - m * __ldcg(p.V + i) : u;
-    const double yi = p.y[i];  // zero on padded rows
-    const double r = i < p.n ? yi - uw : 0.0;
-    __stcg(p.rho + i, r);
-    arr = fma(r, r, arr);
-    ary = fma(yi, r, ary);
-    if (mom && i < p.n) {
-      const double e = yi - u;
-      aee = fma(e, e, aee);
+  double arr = 0.0, ary = 0.0, aee = 0.0;
+  for (int64_t i0 = lo; i0 < hi; i0 += kThreads / G) {  // uniform trip count (shuffles)
+    const int64_t i = i0 + threadIdx.x / G;
+    const bool ok = i < hi;
+    double u = 0.0, f = 0.0, u_old = 0.0, v_old = 0.0, yi = 0.0;
+    if (ok) {
+      if (g == 0) {
+        if (shift) u_old = __ldcg(p.U + i);
+        else if (mom) v_old = __ldcg(p.V + i);
+        yi = p.y[i];  // zero on padded rows
+      }
+      if (G == 1) {
+        u = thread_sum_partials(p.up, C, p.ld, i);
+        if (fix) f = thread_sum_partials(p.dvp, C, p.ld, i);
+      } else {
+        for (int c = g; c < C; c += 8) u += __ldcg(p.up + static_cast<int64_t>(c) * p.ld + i);
+        if (fix)
+          for (int c = g; c < C; c += 8) f += __ldcg(p.dvp + static_cast<int64_t>(c) * p.ld + i);
+      }
+    }
+    if (G == 8) {
+      u += __shfl_xor_sync(kFull, u, 4);
+      u += __shfl_xor_sync(kFull, u, 2);
+      u += __shfl_xor_sync(kFull, u, 1);
+      if (fix) {
+        f += __shfl_xor_sync(kFull, f, 4);
+        f += __shfl_xor_sync(kFull, f, 2);
+        f += __shfl_xor_sync(kFull, f, 1);
+      }
+    }
+    if (ok && g == 0) {
+      double v = v_old;
+      if (shift) {
+        v = u_old - f;  // v = u_old with the history fix (581-590, 673-684)
+        __stcg(p.V + i, v);
+      }
+      __stcg(p.U + i, u);
+      const double uw = mom ? (1.0 + m) * u - m * v : u;
+      const double r = i < p.n ? yi - uw : 0.0;
+      __stcg(p.rho + i, r);
+      arr = fma(r, r, arr);
+      ary = fma(yi, r, ary);
+      if (mom && i < p.n) {
+        const double e = yi - u;
+        aee = fma(e, e, aee);
+      }
     }
   }
   double v[3] = {arr, ary, aee};
@@ -1008,7 +1138,7 @@ __device__ __noinline__ void setup_dictionary(const EngineParams& p, Sh& sh, boo
     s.active_at_last_l = s.S;
   }
   // u = op.apply(x)
-  ApplySrc as{bk.idx, bk.x, nullptr, 1.0, nullptr, nullptr};
+  ApplySrc as{bk.idx, bk.x, nullptr, 1.0, nullptr, nullptr, nullptr};
   const int C = op_apply_partials(p, sh, lv, as, s.S, p.up, nullptr, sc.red);
   grid.sync();
   combine_u(p, sh, C, false, false, 0.0);  // momentum restarts (fastl1.cpp:322-323)
@@ -1056,7 +1186,7 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
       PassOut po{p.vec_out, 0, 0.0, false, 0, 0, nullptr};
       op_adjoint(p, sh, lv, bk.idx, bk.eps, k, sc.vec, sc.rt, po);
     } else if (p.mode == kModeApply) {
-      ApplySrc as{bk.idx, p.x_init, nullptr, 1.0, nullptr, nullptr};
+      ApplySrc as{bk.idx, p.x_init, nullptr, 1.0, nullptr, nullptr, nullptr};
       const int C = op_apply_partials(p, sh, lv, as, k, p.up, nullptr, sc.red);
       grid.sync();
       int64_t lo, hi;
@@ -1139,6 +1269,7 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
     const int64_t S = s.S;
     int64_t lo, hi;
     slice(S, lo, hi);
+    FL1_MARK(0);
     double tp0 = 0.0;
     if (threadIdx.x == 0) tp0 = globaltimer_ns();
 
@@ -1149,10 +1280,23 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
       momentum = (s.t_k - 1.0) / t_next;
     }
     {  // compute_products (359-369): rho_g was formed by the previous combine phase
-      load_vec_smem(p, p.rho, sc.vec);
+      // the three slot sums are reduced by warps 0-2 while every thread's rho loads are in flight
+      {
+        const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+        double sacc = 0.0;
+        if (w < 3) {
+          const int slot = kSlRhoSq + w;
+          for (int b = l; b < p.grid; b += 32) sacc += __ldcg(p.bred + static_cast<int64_t>(b) * kBred + slot);
+        }
+        load_vec_smem(p, p.rho, sc.vec);  // ends with __syncthreads
+        if (w < 3) {
+          sacc = warp_sum(sacc);
+          if (l == 0) sh.res[kSlRhoSq + w] = sacc;
+        }
+        __syncthreads();
+      }
       if (p.observe && blockIdx.x == 0)
         for (int64_t i = threadIdx.x; i < ld; i += kThreads) p.rho_obs[i] = sc.vec[i];
-      grid_reduce(p, sh, (1u << kSlRhoSq) | (1u << kSlRhoY) | (1u << kSlRhoE), 0u);
       if (threadIdx.x == 0) {
         sh.t_next = t_next;
         sh.rho_sq = sh.res[kSlRhoSq];
@@ -1192,7 +1336,9 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
         op_adjoint(p, sh, lv, bk.idx, bk.eps, S, sc.vec, sc.rt, po);
       }
     }
+    FL1_MARK(1);
     grid.sync();  // ------------------------------------------------ sync 1
+    FL1_MARK(2);
     double tp1 = 0.0;
     if (threadIdx.x == 0) {
       tp1 = globaltimer_ns();
@@ -1201,6 +1347,21 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
     }
 
     // ---------------------------------------------------------- phase B
+    // prefetch this thread's first atom (independent of the scalar reduction below)
+    ProxCtx::Atom pre{};
+    {
+      const int64_t q = lo + threadIdx.x;
+      if (q < hi) {
+        pre.c = p.corr[q];
+        pre.xo = bk.x[q];
+        pre.xpv = bk.xp[q];
+        pre.cy = exact_fit ? p.corr_y[q] : 0.0;
+        pre.eps = bk.eps[q];
+        pre.en = bk.en[q];
+        pre.an = bk.an[q];
+        pre.aty = p.rule == FL1_RULE_DYNAMIC ? ((p.precompute_aty && s.atye_valid) ? bk.atye[q] : bk.aty[q]) : 0.0;
+      }
+    }
     const int l1s = l1_slot(s.t);
     grid_reduce(p, sh, 1u << l1s,
                 exact_fit ? ((1u << kSlMaxPlainY) | (1u << kSlMaxStableY))
@@ -1275,44 +1436,54 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
       sh.stable_test = stable_test;
     }
     __syncthreads();
-    {
-      const bool stop_now = sh.stop_now, screen_now = sh.screen_now;
-      const double sp = sh.scale_prime, cn = sh.center_norm, R = sh.radius;
-      const double inv_l = s.inv_l, thresh = lambda * s.inv_l;
-      const bool fista = p.solver == FL1_FISTA;
-      const bool use_atye = p.precompute_aty && s.atye_valid;
+    const bool stop_now = sh.stop_now;
+    const bool fista = p.solver == FL1_FISTA;
+    ProxCtx px;
+    px.corr = p.corr;
+    px.corr_y = p.corr_y;
+    px.x = bk.x;
+    px.xp = bk.xp;
+    px.eps = bk.eps;
+    px.en = bk.en;
+    px.an = bk.an;
+    px.aty = bk.aty;
+    px.atye = bk.atye;
+    px.m = momentum;
+    px.inv_l = s.inv_l;
+    px.thresh = lambda * s.inv_l;
+    px.sp = sh.scale_prime;
+    px.cn = sh.center_norm;
+    px.R = sh.radius;
+    px.lambda = lambda;
+    px.screen_now = sh.screen_now;
+    px.stable_test = sh.stable_test;
+    px.rule_gap = p.rule == FL1_RULE_GAP;
+    px.ray_is_y = sh.ray_is_y;
+    px.use_atye = p.precompute_aty && s.atye_valid;
+    {  // per-atom sphere test + prox on this CTA's slice (results to xnew / keep)
       double kept = 0.0, look = 0.0, nnz = 0.0, l1n = 0.0;
       for (int64_t q = lo + threadIdx.x; q < hi; q += kThreads) {
-        const double c = p.corr[q];
-        const double xo = bk.x[q];
-        int keep = 1;
-        if (screen_now) {
-          double d;
-          if (p.rule == FL1_RULE_GAP)
-            d = fabs(sp * (sh.ray_is_y ? p.corr_y[q] : c));
-          else
-            d = use_atye ? fabs(bk.atye[q] / lambda) : fabs(bk.aty[q] / lambda);
-          if (sh.stable_test) {
-            keep = (d + bk.eps[q] * cn + R * bk.en[q]) >= 1.0;  // stable_zone_test
-            look += (d + R * bk.an[q]) >= 1.0 ? 1.0 : 0.0;      // sphere_test, approx norms
-          } else {
-            keep = (d + R * bk.en[q]) >= 1.0;
-            look += keep ? 1.0 : 0.0;
-          }
+        ProxCtx::Atom a;
+        if (q == lo + threadIdx.x) {
+          a = pre;
+          if (px.m == 0.0) a.xpv = 0.0;
+        } else {
+          a = px.load(q);
         }
         if (stop_now) {
-          nnz += xo != 0.0 ? 1.0 : 0.0;
-        } else {
-          const double g = momentum != 0.0 ? (1.0 + momentum) * xo - momentum * bk.xp[q] : xo;
-          const double xn = soft_threshold(g + inv_l * c, thresh);
-          if (fista) bk.xp[q] = xo;
-          bk.x[q] = xn;
-          bk.keep[q] = static_cast<int8_t>(keep);
-          if (keep) {
-            kept += 1.0;
-            nnz += xn != 0.0 ? 1.0 : 0.0;
-            l1n += fabs(xn);  // ||x_{t+1}||_1 over the preserved set (next iteration's 473)
-          }
+          nnz += a.xo != 0.0 ? 1.0 : 0.0;
+          continue;
+        }
+        const double d = px.screen_now ? px.dot(a) : 0.0;
+        const bool kp = px.keep(a, d);
+        look += px.look(a, d, kp) ? 1.0 : 0.0;
+        const double xn = px.xnew(a);
+        p.xnew[q] = xn;
+        bk.keep[q] = static_cast<int8_t>(kp);
+        if (kp) {
+          kept += 1.0;
+          nnz += xn != 0.0 ? 1.0 : 0.0;
+          l1n += fabs(xn);  // ||x_{t+1}||_1 over the preserved set (next iteration's 473)
         }
       }
       double v[4] = {kept, look, nnz, l1n};
@@ -1325,17 +1496,34 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
         if (!stop_now) put_slot(p, l1_slot(s.t + 1), v[3]);
       }
     }
+    // u = A_S x_next over the kept nonzeros (131-146) and the v history fix for atoms
+    // dropped by this screening pass (FISTA, 673-684), in the same phase: dense work
+    // items re-derive the coefficients with ProxCtx; the SuKro scatter is slice-owned.
+    int C_apply = 0;
+    const bool fix_pass = !stop_now && fista && sh.screen_now;
+    if (!stop_now) {
+      if (lv.kind == kDense) {
+        ApplySrc as{bk.idx, nullptr, nullptr, 1.0, nullptr, nullptr, &px};
+        C_apply = op_apply_partials(p, sh, lv, as, S, p.up, fix_pass ? p.dvp : nullptr, sc.red);
+      } else {
+        __syncthreads();
+        ApplySrc as{bk.idx, p.xnew, nullptr, 1.0, bk.keep, fix_pass ? bk.x : nullptr, nullptr};
+        C_apply = op_apply_partials(p, sh, lv, as, S, p.up, fix_pass ? p.dvp : nullptr, sc.red);
+      }
+    }
+    FL1_MARK(3);
     grid.sync();  // ------------------------------------------------ sync 2
+    FL1_MARK(4);
     double tp2 = 0.0;
     if (threadIdx.x == 0) {
       tp2 = globaltimer_ns();
       s.prof_ns[1] += tp2 - tp1;
     }
 
-    // ---------------------------------------------------------- phase D
+    // ---------------------------------------------------------- phase E
     grid_reduce(p, sh, (1u << kSlKept) | (1u << kSlLook) | (1u << kSlNnz), 0u);
     if (threadIdx.x == 0) {
-      sh.S_new = sh.stop_now ? S : static_cast<int64_t>(sh.res[kSlKept]);
+      sh.S_new = stop_now ? S : static_cast<int64_t>(sh.res[kSlKept]);
       sh.look = static_cast<int64_t>(sh.res[kSlLook]);
       sh.nnz = static_cast<int64_t>(sh.res[kSlNnz]);
       sh.gamma = -1.0;
@@ -1371,71 +1559,9 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
         s.obs_bank = s.cur;
         s.obs_ray_is_y = sh.ray_is_y;
       }
-    }
-    __syncthreads();
-    const bool stop_now = sh.stop_now;
-    const int64_t S_new = sh.S_new;
-    const bool shrink = !stop_now && S_new < S;
-    const bool fista = p.solver == FL1_FISTA;
-    int C_apply = 0;
-    if (!stop_now) {
-      if (shrink) {  // apply_restriction: stream compaction into the other bank (686-701)
-        const Bank nb = p.bank[s.cur ^ 1];
-        if (threadIdx.x < 32) {
-          double acc = 0.0;
-          for (int b = threadIdx.x; b < static_cast<int>(blockIdx.x); b += 32)
-            acc += __ldcg(p.bred + static_cast<int64_t>(b) * kBred + kSlKept);
-          acc = warp_sum(acc);
-          if (threadIdx.x == 0) sh.scan_base = static_cast<int64_t>(acc);
-        }
-        __syncthreads();
-        const bool lead_ok = s.lead_valid != 0;
-        const bool dyn = p.rule == FL1_RULE_DYNAMIC;
-        const bool atye = s.atye_valid != 0;
-        int64_t out_base = sh.scan_base;
-        double me = -DBL_MAX;
-        const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-        for (int64_t q0 = lo; q0 < hi; q0 += kThreads) {
-          const int64_t q = q0 + threadIdx.x;
-          const int kp = q < hi ? bk.keep[q] : 0;
-          const unsigned bal = __ballot_sync(kFull, kp);
-          if (l == 0) sh.wscan[w] = __popc(bal);
-          __syncthreads();
-          int64_t off = out_base;
-          int tot = 0;
-          for (int ww = 0; ww < kWarps; ++ww) {
-            if (ww < w) off += sh.wscan[ww];
-            tot += sh.wscan[ww];
-          }
-          off += __popc(bal & ((1u << l) - 1u));
-          if (kp) {
-            nb.idx[off] = bk.idx[q];
-            nb.x[off] = bk.x[q];
-            if (fista) nb.xp[off] = bk.xp[q];
-            nb.eps[off] = bk.eps[q];
-            nb.en[off] = bk.en[q];
-            nb.an[off] = bk.an[q];
-            if (dyn) nb.aty[off] = bk.aty[q];
-            if (atye) nb.atye[off] = bk.atye[q];
-            if (lead_ok) nb.lead[off] = bk.lead[q];
-            me = fmax(me, bk.eps[q]);
-          }
-          out_base += tot;
-          __syncthreads();
-        }
-        double v[1] = {me};
-        const bool mx[1] = {true};
-        block_reduce<1>(v, mx, sh);
-        if (threadIdx.x == 0) put_slot(p, kSlMaxEps, v[0]);
-      }
-      // u = A_S x_next over the kept nonzeros (131-146); v fix for dropped atoms
-      const bool need_fix = shrink && fista;
-      ApplySrc as{bk.idx, bk.x, nullptr, 1.0, bk.keep, need_fix ? bk.xp : nullptr};
-      C_apply = op_apply_partials(p, sh, lv, as, S, p.up, need_fix ? p.dvp : nullptr, sc.red);
-    }
-    if (threadIdx.x == 0) {  // ledger + trace (611-623)
-      s.ledger += row_flops(p, s.dict_index, S, sh.nnz);
-      if (!stop_now && lv.kind == kDense) s.prof_apply_bytes += 8.0 * static_cast<double>(p.n) * static_cast<double>(sh.nnz);
+      s.ledger += row_flops(p, s.dict_index, S, sh.nnz);  // ledger + trace (611-623)
+      if (!stop_now && lv.kind == kDense)
+        s.prof_apply_bytes += 8.0 * static_cast<double>(p.n) * static_cast<double>(sh.nnz);
       if (p.collect_trace && blockIdx.x == 0) {
         fl1_trace_row row;
         row.iter = s.t;
@@ -1451,6 +1577,7 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
       }
       if (p.collect_trace) s.n_trace += 1;
     }
+    __syncthreads();
     if (stop_now) {
       if (threadIdx.x == 0) {
         s.converged = 1;
@@ -1463,11 +1590,65 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
       __syncthreads();
       break;
     }
-    grid.sync();  // ------------------------------------------------ sync 3
-    // ---------------------------------------------------------- phase E
-    {
+    const int64_t S_new = sh.S_new;
+    const bool shrink = S_new < S;
+    if (shrink) {  // apply_restriction: stream compaction into the other bank (686-701)
+      const Bank nb = p.bank[s.cur ^ 1];
+      if (threadIdx.x < 32) {
+        double acc = 0.0;
+        for (int b = threadIdx.x; b < static_cast<int>(blockIdx.x); b += 32)
+          acc += __ldcg(p.bred + static_cast<int64_t>(b) * kBred + kSlKept);
+        acc = warp_sum(acc);
+        if (threadIdx.x == 0) sh.scan_base = static_cast<int64_t>(acc);
+      }
+      __syncthreads();
+      const bool lead_ok = s.lead_valid != 0;
+      const bool dyn = p.rule == FL1_RULE_DYNAMIC;
+      const bool atye = s.atye_valid != 0;
+      int64_t out_base = sh.scan_base;
+      double me = -DBL_MAX;
+      const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+      for (int64_t q0 = lo; q0 < hi; q0 += kThreads) {
+        const int64_t q = q0 + threadIdx.x;
+        const int kp = q < hi ? bk.keep[q] : 0;
+        const unsigned bal = __ballot_sync(kFull, kp);
+        if (l == 0) sh.wscan[w] = __popc(bal);
+        __syncthreads();
+        int64_t off = out_base;
+        int tot = 0;
+        for (int ww = 0; ww < kWarps; ++ww) {
+          if (ww < w) off += sh.wscan[ww];
+          tot += sh.wscan[ww];
+        }
+        off += __popc(bal & ((1u << l) - 1u));
+        if (kp) {
+          nb.idx[off] = bk.idx[q];
+          nb.x[off] = p.xnew[q];
+          if (fista) nb.xp[off] = bk.x[q];  // x_prev = x (581-590)
+          nb.eps[off] = bk.eps[q];
+          nb.en[off] = bk.en[q];
+          nb.an[off] = bk.an[q];
+          if (dyn) nb.aty[off] = bk.aty[q];
+          if (atye) nb.atye[off] = bk.atye[q];
+          if (lead_ok) nb.lead[off] = bk.lead[q];
+          me = fmax(me, bk.eps[q]);
+        }
+        out_base += tot;
+        __syncthreads();
+      }
+      double v[1] = {me};
+      const bool mx[1] = {true};
+      block_reduce<1>(v, mx, sh);
+      if (threadIdx.x == 0) put_slot(p, kSlMaxEps, v[0]);
+    } else {  // same positions: x_prev = x, x = x_next on this CTA's slice
+      for (int64_t q = lo + threadIdx.x; q < hi; q += kThreads) {
+        if (fista) bk.xp[q] = bk.x[q];
+        bk.x[q] = p.xnew[q];
+      }
+    }
+    {  // combine u (and v <- u_old - fix), then the next iteration's rho_g
       const double tk_next = fista ? (s.momentum_ready ? sh.t_next : s.t_k) : s.t_k;
-      combine_u(p, sh, C_apply, fista, shrink && fista, next_momentum(p, tk_next, fista));
+      combine_u(p, sh, C_apply, fista, fix_pass, next_momentum(p, tk_next, fista));
     }
     if (threadIdx.x == 0) {
       if (fista) {  // 581-590
@@ -1479,12 +1660,14 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
         s.S = S_new;
       }
     }
-    __syncthreads();
+    FL1_MARK(5);
+    grid.sync();  // ------------------------------------------------ sync 3
+    FL1_MARK(6);
     if (shrink) {
-      grid_reduce(p, sh, 0u, 1u << kSlMaxEps);  // slot written before sync 3
+      grid_reduce(p, sh, 0u, 1u << kSlMaxEps);
       if (threadIdx.x == 0) s.max_eps = S_new > 0 ? sh.res[kSlMaxEps] : 0.0;
+      __syncthreads();
     }
-    grid.sync();  // ------------------------------------------------ sync 4
     double tp3 = 0.0;
     if (threadIdx.x == 0) {
       tp3 = globaltimer_ns();

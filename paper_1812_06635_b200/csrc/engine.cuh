@@ -154,6 +154,7 @@ struct EngineParams {
   double* pup;  // power-iteration apply partials
   double* vec_out;  // Apply/Adjoint mode output (length ld or K)
   double* corr;     // K
+  double* xnew;     // K: prox output of the current bank positions (phase B -> E)
   double* corr_y;   // K (exact-fit fallback)
   double* part;     // K * units-per-column
   int32_t* cnt;     // K column-completion counters
@@ -171,6 +172,7 @@ struct EngineParams {
   int64_t trace_cap;
   fl1_switch_event* sw;
   EngineState* st;
+  uint64_t* timeline;  // FL1_TIMELINE builds only: [iter][cta][8] %globaltimer marks
 };
 
 constexpr int kBred = 20;  // doubles of per-CTA partials (slots, see engine.cu)
