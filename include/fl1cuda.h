@@ -187,6 +187,19 @@ int fl1_solve(fl1_seq* s, const double* y, double lambda, const fl1_switch_confi
 int fl1_solve_device(fl1_seq* s, const double* y_dev, double lambda,
                      const fl1_switch_config* cfg, const fl1_run_options* opts,
                      fl1_result** out);
+/* Batched many-signal solve (BASELINE config 5): B independent run_lasso calls on one
+ * sequence — per-signal FISTA state, preserved set, Lipschitz refreshes and stop —
+ * executed as `concurrency` concurrent sub-grid engine launches (own stream and
+ * workspace each; 0 = default 4). Y is N x B column-major with leading dimension
+ * ldy (host), lambdas has B entries, out receives B results. Observers and x_init
+ * are per-signal features of fl1_solve and are rejected here. */
+int fl1_solve_batched(fl1_seq* s, const double* Y, int64_t ldy, const double* lambdas, int32_t batch,
+                      const fl1_switch_config* cfg, const fl1_run_options* opts, int32_t concurrency,
+                      fl1_result** out);
+/* Same with Y (N x B, leading dimension ldy) resident in HBM. */
+int fl1_solve_batched_device(fl1_seq* s, const double* Y_dev, int64_t ldy, const double* lambdas, int32_t batch,
+                             const fl1_switch_config* cfg, const fl1_run_options* opts, int32_t concurrency,
+                             fl1_result** out);
 int fl1_result_info_get(const fl1_result* r, fl1_result_info* out);
 int fl1_result_x(const fl1_result* r, double* out);  /* length K, zero over screened atoms */
 int fl1_result_trace(const fl1_result* r, fl1_trace_row* out);

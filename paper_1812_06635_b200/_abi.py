@@ -158,6 +158,10 @@ PRODUCT_ONLY = {
     "ctx_info": (C.c_int, [_P, _PI32, _PI64, _PI64]),
     "dict_dense_device": (C.c_int, [_P, C.c_void_p, C.c_int64, C.c_int64, _PP]),
     "result_profile": (C.c_int, [_P, _PD]),
+    "solve_batched": (C.c_int, [_P, _PD, C.c_int64, _PD, C.c_int32, C.POINTER(SwitchConfigC), C.POINTER(RunOptionsC),
+                                C.c_int32, _PP]),
+    "solve_batched_device": (C.c_int, [_P, C.c_void_p, C.c_int64, _PD, C.c_int32, C.POINTER(SwitchConfigC),
+                                       C.POINTER(RunOptionsC), C.c_int32, _PP]),
     "solve_device": (C.c_int, [_P, C.c_void_p, C.c_double, C.POINTER(SwitchConfigC), C.POINTER(RunOptionsC), _PP]),
 }
 

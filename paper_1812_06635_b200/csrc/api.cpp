@@ -16,7 +16,9 @@
 #include <cstring>
 #include <limits>
 #include <memory>
+#include <atomic>
 #include <mutex>
+#include <thread>
 #include <random>
 #include <stdexcept>
 #include <string>
@@ -97,6 +99,7 @@ int64_t even_ld(int64_t n) { return (n + 3) / 4 * 4; }  // 32-byte aligned colum
 // ---------------------------------------------------------------- handles
 struct Workspace {
   int64_t n = 0, k = 0, ld = 0;
+  int grid_cap = 0;  // 0: one CTA per SM; else the sub-grid of a concurrent batched solve
   int64_t sk_elems = 0;  // SuKro scratch capacity (nterms * m * q)
   int64_t sk_m = 0;
   int grid = 0;
@@ -106,7 +109,17 @@ struct Workspace {
   cudaStream_t stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   EngineParams base{};  // pointers filled
+  // pinned host staging: state, y, final (idx, x), switch events, trace rows
+  void* pinned = nullptr;
+  EngineState* h_st = nullptr;
+  double* h_y = nullptr;
+  int32_t* h_idx = nullptr;
+  double* h_x = nullptr;
+  fl1_switch_event* h_sw = nullptr;
+  fl1_trace_row* h_trace = nullptr;
+  int64_t h_trace_cap = 0;
   ~Workspace() {
+    if (pinned) cudaFreeHost(pinned);
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
     if (stream) cudaStreamDestroy(stream);
@@ -140,10 +153,11 @@ struct fl1_ctx {
     return gauss->as<double>();
   }
 
-  std::unique_ptr<Workspace> acquire(int64_t n, int64_t k, int64_t trace_cap, int64_t sk_elems, int64_t sk_m);
+  std::unique_ptr<Workspace> acquire(int64_t n, int64_t k, int64_t trace_cap, int64_t sk_elems, int64_t sk_m,
+                                     int grid_cap = 0);
   void release(std::unique_ptr<Workspace> w) {
     std::lock_guard<std::mutex> g(mu);
-    if (pool.size() < 4) pool.push_back(std::move(w));
+    if (pool.size() < 64) pool.push_back(std::move(w));
   }
 };
 
@@ -287,13 +301,14 @@ size_t carve(EngineParams& p, char* base, int64_t n, int64_t k, int64_t ld, int 
 }  // namespace
 
 std::unique_ptr<Workspace> fl1_ctx::acquire(int64_t n, int64_t k, int64_t trace_cap, int64_t sk_elems,
-                                            int64_t sk_m) {
+                                            int64_t sk_m, int grid_cap) {
   const int64_t ld = even_ld(n);
   {
     std::lock_guard<std::mutex> g(mu);
     for (size_t i = 0; i < pool.size(); ++i) {
       Workspace& w = *pool[i];
-      if (w.n == n && w.k == k && w.trace_cap >= trace_cap && w.sk_elems >= sk_elems && w.sk_m >= sk_m) {
+      if (w.n == n && w.k == k && w.trace_cap >= trace_cap && w.sk_elems >= sk_elems && w.sk_m >= sk_m &&
+          w.grid_cap == grid_cap) {
         auto r = std::move(pool[i]);
         pool.erase(pool.begin() + static_cast<long>(i));
         return r;
@@ -313,6 +328,8 @@ std::unique_ptr<Workspace> fl1_ctx::acquire(int64_t n, int64_t k, int64_t trace_
     if (e == cudaErrorInvalidConfiguration)
       throw std::logic_error("signal length too large for the shared-memory resident residual");
     ck(e, "engine_configure");
+    if (grid_cap > 0 && grid_cap < w->grid) w->grid = grid_cap;  // sub-grid for concurrent solves
+    w->grid_cap = grid_cap;
   }
   EngineParams p{};
   const size_t bytes = carve(p, nullptr, n, k, ld, w->grid, w->units, trace_cap, sk_elems);
@@ -326,6 +343,28 @@ std::unique_ptr<Workspace> fl1_ctx::acquire(int64_t n, int64_t k, int64_t trace_
   p.trace_cap = trace_cap;
   w->base = p;
   ck(cudaStreamCreateWithFlags(&w->stream, cudaStreamNonBlocking), "stream");
+  {
+    w->h_trace_cap = std::min<int64_t>(trace_cap, 1 << 16);
+    auto up = [](size_t x) { return (x + 255) / 256 * 256; };
+    const size_t kk = static_cast<size_t>(std::max<int64_t>(k, 1));
+    const size_t bytes = up(sizeof(EngineState)) + up(sizeof(double) * static_cast<size_t>(ld)) +
+                         up(sizeof(int32_t) * kk) + up(sizeof(double) * kk) +
+                         up(sizeof(fl1_switch_event) * fl1::kMaxLevels) +
+                         up(sizeof(fl1_trace_row) * static_cast<size_t>(std::max<int64_t>(w->h_trace_cap, 1)));
+    ck(cudaHostAlloc(&w->pinned, bytes, cudaHostAllocDefault), "cudaHostAlloc");
+    char* c = static_cast<char*>(w->pinned);
+    w->h_st = reinterpret_cast<EngineState*>(c);
+    c += up(sizeof(EngineState));
+    w->h_y = reinterpret_cast<double*>(c);
+    c += up(sizeof(double) * static_cast<size_t>(ld));
+    w->h_idx = reinterpret_cast<int32_t*>(c);
+    c += up(sizeof(int32_t) * kk);
+    w->h_x = reinterpret_cast<double*>(c);
+    c += up(sizeof(double) * kk);
+    w->h_sw = reinterpret_cast<fl1_switch_event*>(c);
+    c += up(sizeof(fl1_switch_event) * fl1::kMaxLevels);
+    w->h_trace = reinterpret_cast<fl1_trace_row*>(c);
+  }
   ck(cudaEventCreate(&w->ev0), "event");
   ck(cudaEventCreate(&w->ev1), "event");
   return w;
@@ -336,8 +375,8 @@ namespace {
 struct WsLease {
   fl1_ctx* ctx;
   std::unique_ptr<Workspace> w;
-  WsLease(fl1_ctx* c, int64_t n, int64_t k, int64_t cap, int64_t sk_elems, int64_t sk_m)
-      : ctx(c), w(c->acquire(n, k, cap, sk_elems, sk_m)) {}
+  WsLease(fl1_ctx* c, int64_t n, int64_t k, int64_t cap, int64_t sk_elems, int64_t sk_m, int grid_cap = 0)
+      : ctx(c), w(c->acquire(n, k, cap, sk_elems, sk_m, grid_cap)) {}
   ~WsLease() {
     if (w) ctx->release(std::move(w));
   }
@@ -464,7 +503,7 @@ std::unique_ptr<DevBuf> upload(const std::vector<double>& v) {
 
 // ---------------------------------------------------------------- solve
 void do_solve(fl1_seq* s, const double* y, bool y_device, double lambda, const fl1_switch_config* cfg,
-              const fl1_run_options* opts, fl1_result** out) {
+              const fl1_run_options* opts, fl1_result** out, int grid_cap = 0) {
   if (!s || !cfg || !opts || !out) throw std::invalid_argument("null argument");
   s->validate();  // run_lasso (fastl1.cpp:755)
   const ApproxImpl& exact = *s->lv.back();
@@ -499,7 +538,7 @@ void do_solve(fl1_seq* s, const double* y, bool y_device, double lambda, const f
   uint64_t cap_limit = 1u << 20;  // device trace rows per launch; full buffers are flushed and the solve resumes
   if (const char* e = std::getenv("FL1_TRACE_CAP")) cap_limit = std::max<uint64_t>(1, std::strtoull(e, nullptr, 10));
   const int64_t cap = static_cast<int64_t>(std::min<uint64_t>(std::max<uint64_t>(want_rows, 1), cap_limit));
-  WsLease lease(ctx, n, k, cap, sk_elems, sk_m);
+  WsLease lease(ctx, n, k, cap, sk_elems, sk_m, grid_cap);
   Workspace& w = *lease.w;
   EngineParams p = w.base;
   p.mode = fl1::kModeSolve;
@@ -537,11 +576,20 @@ void do_solve(fl1_seq* s, const double* y, bool y_device, double lambda, const f
   st.t_k = 1.0;
 
   ck(cudaEventRecord(w.ev0, w.stream), "event");
-  ck(cudaMemcpyAsync(p.st, &st, sizeof(st), cudaMemcpyHostToDevice, w.stream), "state upload");
+  EngineState& hst = *w.h_st;  // pinned: every transfer below is asynchronous on the solve stream
+  hst = st;
+  ck(cudaMemcpyAsync(p.st, &hst, sizeof(st), cudaMemcpyHostToDevice, w.stream), "state upload");
   ck(cudaMemsetAsync(const_cast<double*>(p.y), 0, static_cast<size_t>(w.ld) * sizeof(double), w.stream), "memset");
-  ck(cudaMemcpyAsync(const_cast<double*>(p.y), y, static_cast<size_t>(n) * sizeof(double),
-                     y_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, w.stream),
-     "y upload");
+  if (y_device) {
+    ck(cudaMemcpyAsync(const_cast<double*>(p.y), y, static_cast<size_t>(n) * sizeof(double), cudaMemcpyDeviceToDevice,
+                       w.stream),
+       "y copy");
+  } else {
+    std::copy(y, y + n, w.h_y);
+    ck(cudaMemcpyAsync(const_cast<double*>(p.y), w.h_y, static_cast<size_t>(n) * sizeof(double),
+                       cudaMemcpyHostToDevice, w.stream),
+       "y upload");
+  }
   if (opts->x_init)
     ck(cudaMemcpyAsync(const_cast<double*>(p.x_init), opts->x_init, static_cast<size_t>(k) * sizeof(double),
                        cudaMemcpyHostToDevice, w.stream),
@@ -556,17 +604,21 @@ void do_solve(fl1_seq* s, const double* y, bool y_device, double lambda, const f
   while (true) {
     ck(fl1::engine_launch(p, w.sk_m, w.stream), "engine launch");
     ++launches;
-    ck(cudaMemcpyAsync(&st, p.st, sizeof(st), cudaMemcpyDeviceToHost, w.stream), "state download");
+    ck(cudaMemcpyAsync(&hst, p.st, sizeof(st), cudaMemcpyDeviceToHost, w.stream), "state download");
     ck(cudaStreamSynchronize(w.stream), "engine sync");
+    st = hst;
     d2h += static_cast<int64_t>(sizeof(st));
     if (st.event == fl1::kEvTraceFull || st.event == fl1::kEvDone) {
       if (p.collect_trace && st.n_trace > 0) {
         d2h += st.n_trace * static_cast<int64_t>(sizeof(fl1_trace_row));
-        const size_t old = host_rows.size();
-        host_rows.resize(old + static_cast<size_t>(st.n_trace));
-        ck(cudaMemcpy(host_rows.data() + old, p.trace, static_cast<size_t>(st.n_trace) * sizeof(fl1_trace_row),
-                      cudaMemcpyDeviceToHost),
-           "trace download");
+        for (int64_t off = 0; off < st.n_trace; off += w.h_trace_cap) {
+          const int64_t cnt = std::min(w.h_trace_cap, st.n_trace - off);
+          ck(cudaMemcpyAsync(w.h_trace, p.trace + off, static_cast<size_t>(cnt) * sizeof(fl1_trace_row),
+                             cudaMemcpyDeviceToHost, w.stream),
+             "trace download");
+          ck(cudaStreamSynchronize(w.stream), "trace sync");
+          host_rows.insert(host_rows.end(), w.h_trace, w.h_trace + cnt);
+        }
         st.trace_base += static_cast<uint64_t>(st.n_trace);
         st.n_trace = 0;
       }
@@ -620,23 +672,27 @@ void do_solve(fl1_seq* s, const double* y, bool y_device, double lambda, const f
     st.event = fl1::kEvNone;
     p.mode = fl1::kModeResume;
     h2d += static_cast<int64_t>(sizeof(st));
-    ck(cudaMemcpyAsync(p.st, &st, sizeof(st), cudaMemcpyHostToDevice, w.stream), "state upload");
+    hst = st;
+    ck(cudaMemcpyAsync(p.st, &hst, sizeof(st), cudaMemcpyHostToDevice, w.stream), "state upload");
   }
   // finish (fastl1.cpp:741-748)
   const fl1::Bank& fb = p.bank[st.cur];
-  std::vector<int32_t> idx(static_cast<size_t>(st.S));
-  std::vector<double> xs(static_cast<size_t>(st.S));
   if (st.S > 0) {
-    ck(cudaMemcpyAsync(idx.data(), fb.idx, idx.size() * sizeof(int32_t), cudaMemcpyDeviceToHost, w.stream), "x");
-    ck(cudaMemcpyAsync(xs.data(), fb.x, xs.size() * sizeof(double), cudaMemcpyDeviceToHost, w.stream), "x");
+    ck(cudaMemcpyAsync(w.h_idx, fb.idx, static_cast<size_t>(st.S) * sizeof(int32_t), cudaMemcpyDeviceToHost,
+                       w.stream),
+       "x");
+    ck(cudaMemcpyAsync(w.h_x, fb.x, static_cast<size_t>(st.S) * sizeof(double), cudaMemcpyDeviceToHost, w.stream), "x");
   }
-  std::vector<fl1_switch_event> sws(static_cast<size_t>(st.n_switches));
   if (st.n_switches > 0)
-    ck(cudaMemcpyAsync(sws.data(), p.sw, sws.size() * sizeof(fl1_switch_event), cudaMemcpyDeviceToHost, w.stream),
+    ck(cudaMemcpyAsync(w.h_sw, p.sw, static_cast<size_t>(st.n_switches) * sizeof(fl1_switch_event),
+                       cudaMemcpyDeviceToHost, w.stream),
        "switches");
   d2h += st.S * 12 + st.n_switches * static_cast<int64_t>(sizeof(fl1_switch_event));
   ck(cudaEventRecord(w.ev1, w.stream), "event");
   ck(cudaStreamSynchronize(w.stream), "finish sync");
+  std::vector<int32_t> idx(w.h_idx, w.h_idx + st.S);
+  std::vector<double> xs(w.h_x, w.h_x + st.S);
+  std::vector<fl1_switch_event> sws(w.h_sw, w.h_sw + st.n_switches);
   float ms = 0.f;
   ck(cudaEventElapsedTime(&ms, w.ev0, w.ev1), "elapsed");
   if (timeline) {
@@ -874,6 +930,70 @@ int fl1_solve(fl1_seq* s, const double* y, double lambda, const fl1_switch_confi
 int fl1_solve_device(fl1_seq* s, const double* y, double lambda, const fl1_switch_config* cfg,
                      const fl1_run_options* opts, fl1_result** out) {
   return guard([&] { do_solve(s, y, true, lambda, cfg, opts, out); });
+}
+namespace {
+int solve_batched_impl(fl1_seq* s, const double* Y, bool y_device, int64_t ldy, const double* lambdas, int32_t batch,
+                       const fl1_switch_config* cfg, const fl1_run_options* opts, int32_t concurrency,
+                       fl1_result** out) {
+  return guard([&] {
+    if (!s || !Y || !lambdas || !out || batch < 0) throw std::invalid_argument("null argument");
+    if (opts && opts->observer) throw std::invalid_argument("observers are not supported in batched solves");
+    if (opts && opts->x_init) throw std::invalid_argument("x_init is per signal: use fl1_solve");
+    const int64_t n = s->lv.back()->dict->n;
+    if (ldy < n) throw std::invalid_argument("ldy must be >= N");
+    fl1_ctx* ctx = s->lv.back()->dict->ctx;
+    ctx->bind();
+    int M = concurrency;
+    if (M <= 0) M = 4;  // default: 4 concurrent sub-grid solves (measured best on B200)
+    M = std::max(1, std::min({M, ctx->sms, std::max<int>(batch, 1)}));
+    const int grid_cap = std::max(1, ctx->sms / M);
+    for (int32_t b = 0; b < batch; ++b) out[b] = nullptr;
+    std::vector<std::thread> pool;
+    std::mutex mu;
+    std::string first_err;
+    int first_code = FL1_OK;
+    std::atomic<int32_t> next{0};
+    for (int wkr = 0; wkr < M; ++wkr) {
+      pool.emplace_back([&] {
+        const int dev = ctx->device;
+        cudaSetDevice(dev);
+        while (true) {
+          const int32_t b = next.fetch_add(1);
+          if (b >= batch) break;
+          const int st = guard([&] { do_solve(s, Y + static_cast<int64_t>(b) * ldy, y_device, lambdas[b], cfg, opts,
+                                              &out[b], grid_cap); });
+          if (st != FL1_OK) {
+            std::lock_guard<std::mutex> g(mu);
+            if (first_code == FL1_OK) {
+              first_code = st;
+              first_err = g_err;
+            }
+          }
+        }
+      });
+    }
+    for (auto& t : pool) t.join();
+    if (first_code != FL1_OK) {
+      for (int32_t b = 0; b < batch; ++b) {
+        delete out[b];
+        out[b] = nullptr;
+      }
+      if (first_code == FL1_EINVAL) throw std::invalid_argument(first_err);
+      throw std::runtime_error(first_err);
+    }
+  });
+}
+}  // namespace
+
+int fl1_solve_batched(fl1_seq* s, const double* Y, int64_t ldy, const double* lambdas, int32_t batch,
+                      const fl1_switch_config* cfg, const fl1_run_options* opts, int32_t concurrency,
+                      fl1_result** out) {
+  return solve_batched_impl(s, Y, false, ldy, lambdas, batch, cfg, opts, concurrency, out);
+}
+int fl1_solve_batched_device(fl1_seq* s, const double* Y, int64_t ldy, const double* lambdas, int32_t batch,
+                             const fl1_switch_config* cfg, const fl1_run_options* opts, int32_t concurrency,
+                             fl1_result** out) {
+  return solve_batched_impl(s, Y, true, ldy, lambdas, batch, cfg, opts, concurrency, out);
 }
 int fl1_result_info_get(const fl1_result* r, fl1_result_info* o) {
   return guard([&] {

@@ -448,6 +448,41 @@ def run_lasso_device(seq: ApproxSequence, y_dev_ptr: int, lam: float, cfg: Switc
         lib.result_free(h)
 
 
+def run_lasso_batched(seq: ApproxSequence, Y, lambdas, cfg: SwitchConfig, opts: RunOptions,
+                      concurrency: int = 0, y_dev_ptr: Optional[int] = None) -> list:
+    """B independent run_lasso solves (columns of Y, N x B) on the GPU at once
+    (BASELINE config 5); product library only. With y_dev_ptr, Y (N x B column-major,
+    leading dimension N) is already in HBM and `Y` only gives the shape."""
+    lib = seq.backend.lib
+    if y_dev_ptr is None:
+        Ym = np.asfortranarray(np.asarray(Y, dtype=np.float64))
+        if Ym.ndim == 1:
+            Ym = Ym.reshape(-1, 1, order="F")
+        n, B = Ym.shape
+    else:
+        n, B = Y
+    if n != seq.exact().op.rows():
+        raise InvalidArgument("y has wrong length")
+    lam = _vec(lambdas, B, "lambdas")
+    keep: list = []
+    o = _run_options_c(opts, keep)
+    c = cfg.c()
+    hs = (C.c_void_p * max(B, 1))()
+    if y_dev_ptr is None:
+        lib.check(lib.solve_batched(seq._h, _dptr(Ym), n, _dptr(lam), B, C.byref(c), C.byref(o), concurrency, hs))
+    else:
+        lib.check(lib.solve_batched_device(seq._h, C.c_void_p(y_dev_ptr), n, _dptr(lam), B, C.byref(c), C.byref(o),
+                                           concurrency, hs))
+    out = []
+    try:
+        for b in range(B):
+            out.append(_collect_result(lib, hs[b]))
+    finally:
+        for b in range(B):
+            lib.result_free(hs[b])
+    return out
+
+
 def fastl1_solve(seq, y, lam, cfg, solver=SOLVER_FISTA, rule=RULE_GAP) -> SolveResult:  # fastl1.hpp:104-111
     return run_lasso(seq, y, lam, cfg, RunOptions(solver=solver, rule=rule, variant=VARIANT_MULTI_DICT))
 

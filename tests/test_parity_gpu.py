@@ -224,3 +224,28 @@ def test_large_path_properties(cuda):
         nz = np.nonzero(r.x)[0]
         assert set(nz.tolist()) <= set(r.final_active.tolist())
         x = r.x
+
+
+@pytest.mark.parametrize("concurrency", [1, 4, 16])
+def test_batched_many_signal(cuda, oracle16, concurrency):
+    """BASELINE configs[4] semantics (independent solves per signal), reduced batch:
+    every batched result matches the oracle's own solve of that signal."""
+    rng = np.random.default_rng(5)
+    n, k, B = 128, 512, 12
+    a = syn.gaussian_dictionary(rng, n, k)
+    Y = np.empty((n, B), order="F")
+    lams = np.empty(B)
+    for b in range(B):
+        x0 = syn.sparse_signal(rng, k, 5)
+        Y[:, b] = syn.observe(rng, a @ x0, None, 30.0)
+        lams[b] = 0.25 * np.max(np.abs(a.T @ Y[:, b]))
+    cfg = F.SwitchConfig(screening_interval=10, max_iterations=5000, rel_tolerance=1e-6)
+    opts = F.RunOptions(variant=F.VARIANT_SCREENED)
+    seq_g = F.ApproxSequence([F.make_exact_approx(F.DenseDictionary(a, backend=cuda))])
+    seq_o = F.ApproxSequence([F.make_exact_approx(F.DenseDictionary(a, backend=oracle16))])
+    res = F.run_lasso_batched(seq_g, Y, lams, cfg, opts, concurrency=concurrency)
+    assert len(res) == B
+    for b in range(B):
+        o = F.run_lasso(seq_o, Y[:, b], lams[b], cfg, opts)
+        assert res[b].converged
+        assert_parity(res[b], o, a, Y[:, b], lams[b])
