@@ -189,8 +189,11 @@ int fl1_solve_device(fl1_seq* s, const double* y_dev, double lambda,
                      fl1_result** out);
 /* Batched many-signal solve (BASELINE config 5): B independent run_lasso calls on one
  * sequence — per-signal FISTA state, preserved set, Lipschitz refreshes and stop —
- * executed as `concurrency` concurrent sub-grid engine launches (own stream and
- * workspace each; 0 = default 4). Y is N x B column-major with leading dimension
+ * on one device. concurrency <= 0: ONE launch in which every thread-block cluster
+ * of -concurrency CTAs (0 = default 2; at most 16) is an engine with its own
+ * workspace that takes signals from a device-side queue. concurrency > 0: that
+ * many concurrent sub-grid engine launches (own stream and workspace each).
+ * Both give the same per-signal results as fl1_solve. Y is N x B column-major with leading dimension
  * ldy (host), lambdas has B entries, out receives B results. Observers and x_init
  * are per-signal features of fl1_solve and are rejected here. */
 int fl1_solve_batched(fl1_seq* s, const double* Y, int64_t ldy, const double* lambdas, int32_t batch,

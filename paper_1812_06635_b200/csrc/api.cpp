@@ -30,6 +30,9 @@ namespace fl1 {
 size_t engine_smem_bytes(int64_t ld, int64_t sukro_m);
 cudaError_t engine_configure(int64_t ld, int64_t sukro_m, int device, int* grid_out);
 cudaError_t engine_launch(const EngineParams& p, int64_t sukro_m, cudaStream_t stream);
+cudaError_t engine_cluster_capacity(int64_t ld, int64_t sukro_m, int csize, int* n_clusters);
+cudaError_t engine_launch_clusters(const EngineParams& p0, int n_clusters, int csize, int64_t sukro_m,
+                                   cudaStream_t stream);
 cudaError_t screen_kernel_launch(int64_t n, const double* dots, const double* eps, const double* en,
                                  const double* an, double cn, double r, int8_t* keep, int8_t* look,
                                  cudaStream_t stream);
@@ -91,6 +94,8 @@ struct DevBuf {
     return static_cast<T*>(p);
   }
 };
+
+constexpr int kDefaultClusterSize = 2;  // batched solves: CTAs per signal
 
 int64_t even_ld(int64_t n) { return (n + 3) / 4 * 4; }  // 32-byte aligned columns
 
@@ -261,9 +266,11 @@ size_t carve(EngineParams& p, char* base, int64_t n, int64_t k, int64_t ld, int 
   p.V = c.take<double>(ld);
   p.rho = c.take<double>(ld);
   p.rho_obs = c.take<double>(ld);
-  p.up = c.take<double>(static_cast<int64_t>(grid) * ld);
-  p.dvp = c.take<double>(static_cast<int64_t>(grid) * ld);
-  p.pup = c.take<double>(static_cast<int64_t>(grid) * ld);
+  // apply partials: one chunk per CTA (dense) or sk_ks split-K chunks (SuKro)
+  const int64_t chunks = std::max<int64_t>(grid, 8);
+  p.up = c.take<double>(chunks * ld);
+  p.dvp = c.take<double>(chunks * ld);
+  p.pup = c.take<double>(chunks * ld);
   p.vec_out = c.take<double>(vec);
   p.corr = c.take<double>(kk);
   p.xnew = c.take<double>(kk);
@@ -502,48 +509,50 @@ std::unique_ptr<DevBuf> upload(const std::vector<double>& v) {
 }
 
 // ---------------------------------------------------------------- solve
-void do_solve(fl1_seq* s, const double* y, bool y_device, double lambda, const fl1_switch_config* cfg,
-              const fl1_run_options* opts, fl1_result** out, int grid_cap = 0) {
-  if (!s || !cfg || !opts || !out) throw std::invalid_argument("null argument");
+// run_lasso / Engine ctor validation shared by the single and batched entries.
+struct SolvePlan {
+  fl1_ctx* ctx = nullptr;
+  int64_t n = 0, k = 0, sk_elems = 0, sk_m = 0;
+  int levels = 0, start_level = 0;
+};
+
+SolvePlan plan_solve(fl1_seq* s, const fl1_switch_config* cfg, const fl1_run_options* opts) {
+  if (!s || !cfg || !opts) throw std::invalid_argument("null argument");
   s->validate();  // run_lasso (fastl1.cpp:755)
+  SolvePlan pl;
   const ApproxImpl& exact = *s->lv.back();
   const DictImpl& ed = *exact.dict;
-  fl1_ctx* ctx = ed.ctx;
-  const int64_t n = ed.n, k = ed.k;
+  pl.ctx = ed.ctx;
+  pl.n = ed.n;
+  pl.k = ed.k;
   for (const auto& l : s->lv) {
-    if (l->dict->ctx != ctx) throw std::invalid_argument("levels live on different contexts");
-    if (l->dict->n != n) throw std::invalid_argument("sequence has mismatched signal lengths");
+    if (l->dict->ctx != pl.ctx) throw std::invalid_argument("levels live on different contexts");
+    if (l->dict->n != pl.n) throw std::invalid_argument("sequence has mismatched signal lengths");
   }
-  int64_t sk_elems = 0, sk_m = 0;
   for (const auto& l : s->lv) {
-    sk_elems = std::max(sk_elems, sk_elems_of(*l->dict));
-    if (l->dict->kind == fl1::kSukro) sk_m = std::max(sk_m, l->dict->m);
+    pl.sk_elems = std::max(pl.sk_elems, sk_elems_of(*l->dict));
+    if (l->dict->kind == fl1::kSukro) pl.sk_m = std::max(pl.sk_m, l->dict->m);
   }
   if (s->lv.size() > static_cast<size_t>(fl1::kMaxLevels)) throw std::invalid_argument("too many levels");
   // Engine ctor validation (fastl1.cpp:268-273)
-  if (lambda <= 0) throw std::invalid_argument("lambda must be positive");
   if (cfg->gamma_threshold <= 0.0 || cfg->gamma_threshold >= 1.0)
     throw std::invalid_argument("gamma threshold must lie in (0, 1)");
   if (cfg->screening_interval < 1) throw std::invalid_argument("screening interval must be >= 1");
   if (opts->solver != FL1_ISTA && opts->solver != FL1_FISTA) throw std::invalid_argument("unknown solver");
   if (opts->rule != FL1_RULE_GAP && opts->rule != FL1_RULE_DYNAMIC) throw std::invalid_argument("unknown rule");
   if (opts->variant < FL1_PLAIN || opts->variant > FL1_MULTI_DICT) throw std::invalid_argument("unknown variant");
-  const int levels = static_cast<int>(s->lv.size());
-  const int start_level = opts->variant == FL1_MULTI_DICT ? 0 : levels - 1;
-  if (opts->full_lipschitz && opts->n_full_lipschitz < levels)
+  pl.levels = static_cast<int>(s->lv.size());
+  pl.start_level = opts->variant == FL1_MULTI_DICT ? 0 : pl.levels - 1;
+  if (opts->full_lipschitz && opts->n_full_lipschitz < pl.levels)
     throw std::invalid_argument("full_lipschitz must list one value per level");
+  return pl;
+}
 
-  ctx->bind();
-  const uint64_t want_rows = opts->collect_trace ? cfg->max_iterations : 1;
-  uint64_t cap_limit = 1u << 20;  // device trace rows per launch; full buffers are flushed and the solve resumes
-  if (const char* e = std::getenv("FL1_TRACE_CAP")) cap_limit = std::max<uint64_t>(1, std::strtoull(e, nullptr, 10));
-  const int64_t cap = static_cast<int64_t>(std::min<uint64_t>(std::max<uint64_t>(want_rows, 1), cap_limit));
-  WsLease lease(ctx, n, k, cap, sk_elems, sk_m, grid_cap);
-  Workspace& w = *lease.w;
-  EngineParams p = w.base;
+void fill_params(EngineParams& p, const SolvePlan& pl, fl1_seq* s, double lambda, const fl1_switch_config* cfg,
+                 const fl1_run_options* opts) {
   p.mode = fl1::kModeSolve;
-  p.n_levels = levels;
-  for (int i = 0; i < levels; ++i) p.lv[i] = make_level(s->lv[static_cast<size_t>(i)].get());
+  p.n_levels = pl.levels;
+  for (int i = 0; i < pl.levels; ++i) p.lv[i] = make_level(s->lv[static_cast<size_t>(i)].get());
   p.lambda = lambda;
   p.gamma_threshold = cfg->gamma_threshold;
   p.interval = cfg->screening_interval;
@@ -555,11 +564,52 @@ void do_solve(fl1_seq* s, const double* y, bool y_device, double lambda, const f
   p.rule = opts->rule;
   p.variant = opts->variant;
   p.has_full_l = opts->full_lipschitz != nullptr;
-  for (int i = 0; i < levels && p.has_full_l; ++i) p.full_l[i] = opts->full_lipschitz[i];
+  for (int i = 0; i < pl.levels && p.has_full_l; ++i) p.full_l[i] = opts->full_lipschitz[i];
   p.collect_trace = opts->collect_trace ? 1 : 0;
   p.observe = opts->observer ? 1 : 0;
   p.has_x_init = opts->x_init ? 1 : 0;
-  p.gauss0 = ctx->gauss0(k);
+  p.gauss0 = pl.ctx->gauss0(pl.k);
+}
+
+// finish (fastl1.cpp:741-748) and SolveResult fields from the final device state
+void fill_result(fl1_result& r, const EngineState& st, const fl1_switch_config* cfg, int64_t k,
+                 std::vector<int32_t> idx, const double* xs, std::vector<fl1_switch_event> sws) {
+  r.k = k;
+  r.x.assign(static_cast<size_t>(k), 0.0);
+  for (size_t q = 0; q < idx.size(); ++q) r.x[static_cast<size_t>(idx[q])] = xs[q];
+  r.final_active = std::move(idx);
+  r.converged = st.converged != 0;
+  r.iterations = st.converged ? st.t : cfg->max_iterations;
+  r.final_gap = st.converged ? st.final_gap : std::numeric_limits<double>::quiet_NaN();
+  r.total_flops = st.ledger;
+  r.gap_warning = st.warning != 0;
+  r.switches = std::move(sws);
+  r.setup_ms = (st.t0_ns - st.start_ns) * 1e-6;
+  r.power_steps = st.power_steps;
+  for (int i = 0; i < 5; ++i) r.prof[i] = st.prof_ns[i];
+  r.prof[5] = st.prof_bytes;
+  r.prof[6] = st.prof_apply_bytes;
+  r.prof[7] = st.prof_power_bytes;
+  for (int i = 0; i < 4; ++i) r.prof[8 + i] = st.prof_pw[i];
+}
+
+void do_solve(fl1_seq* s, const double* y, bool y_device, double lambda, const fl1_switch_config* cfg,
+              const fl1_run_options* opts, fl1_result** out, int grid_cap = 0) {
+  if (!out) throw std::invalid_argument("null argument");
+  const SolvePlan pl = plan_solve(s, cfg, opts);
+  if (lambda <= 0) throw std::invalid_argument("lambda must be positive");
+  fl1_ctx* ctx = pl.ctx;
+  const int64_t n = pl.n, k = pl.k, sk_elems = pl.sk_elems, sk_m = pl.sk_m;
+  const int start_level = pl.start_level;
+  ctx->bind();
+  const uint64_t want_rows = opts->collect_trace ? cfg->max_iterations : 1;
+  uint64_t cap_limit = 1u << 20;  // device trace rows per launch; full buffers are flushed and the solve resumes
+  if (const char* e = std::getenv("FL1_TRACE_CAP")) cap_limit = std::max<uint64_t>(1, std::strtoull(e, nullptr, 10));
+  const int64_t cap = static_cast<int64_t>(std::min<uint64_t>(std::max<uint64_t>(want_rows, 1), cap_limit));
+  WsLease lease(ctx, n, k, cap, sk_elems, sk_m, grid_cap);
+  Workspace& w = *lease.w;
+  EngineParams p = w.base;
+  fill_params(p, pl, s, lambda, cfg, opts);
   p.trace_cap = cap;  // <= w.trace_cap (a cached workspace may be larger)
   std::unique_ptr<DevBuf> timeline;
   const char* tl_path = std::getenv("FL1_TIMELINE_OUT");  // instrumented builds only
@@ -703,25 +753,10 @@ void do_solve(fl1_seq* s, const double* y, bool y_device, double lambda, const f
       std::fclose(f);
     }
   }
-  res->x.assign(static_cast<size_t>(k), 0.0);
-  for (size_t q = 0; q < idx.size(); ++q) res->x[static_cast<size_t>(idx[q])] = xs[q];
-  res->final_active = std::move(idx);
-  res->converged = st.converged != 0;
-  res->iterations = st.converged ? st.t : cfg->max_iterations;
-  res->final_gap = st.converged ? st.final_gap : std::numeric_limits<double>::quiet_NaN();
-  res->total_flops = st.ledger;
-  res->gap_warning = st.warning != 0;
+  fill_result(*res, st, cfg, k, std::move(idx), xs.data(), std::move(sws));
   res->trace = std::move(host_rows);
-  res->switches = std::move(sws);
   res->device_ms = ms;
-  res->setup_ms = (st.t0_ns - st.start_ns) * 1e-6;
   res->launches = launches;
-  res->power_steps = st.power_steps;
-  for (int i = 0; i < 5; ++i) res->prof[i] = st.prof_ns[i];
-  res->prof[5] = st.prof_bytes;
-  res->prof[6] = st.prof_apply_bytes;
-  res->prof[7] = st.prof_power_bytes;
-  for (int i = 0; i < 4; ++i) res->prof[8 + i] = st.prof_pw[i];
   res->h2d = h2d;
   res->d2h = d2h;
   *out = res.release();
@@ -932,6 +967,178 @@ int fl1_solve_device(fl1_seq* s, const double* y, double lambda, const fl1_switc
   return guard([&] { do_solve(s, y, true, lambda, cfg, opts, out); });
 }
 namespace {
+// Batched solves in ONE launch: every thread-block cluster of `csize` CTAs is a
+// virtual grid with its own workspace and pulls signals from a device queue
+// (each signal runs the same Engine::run as fl1_solve, with cluster barriers).
+void solve_clusters(fl1_seq* s, const double* Y, bool y_device, int64_t ldy, const double* lambdas, int32_t batch,
+                    const fl1_switch_config* cfg, const fl1_run_options* opts, int csize, fl1_result** out) {
+  const SolvePlan pl = plan_solve(s, cfg, opts);
+  for (int32_t b = 0; b < batch; ++b)
+    if (!(lambdas[b] > 0)) throw std::invalid_argument("lambda must be positive");
+  if (csize < 1 || csize > 16) throw std::invalid_argument("cluster size must lie in [1, 16]");
+  fl1_ctx* ctx = pl.ctx;
+  ctx->bind();
+  const int64_t n = pl.n, k = pl.k, ld = even_ld(n), units = (n + fl1::kUnit - 1) / fl1::kUnit;
+  int grid = 0;
+  {
+    const cudaError_t e = fl1::engine_configure(ld, pl.sk_m, ctx->device, &grid);
+    if (e == cudaErrorInvalidConfiguration)
+      throw std::logic_error("signal length too large for the shared-memory resident residual");
+    ck(e, "engine_configure");
+  }
+  int n_clusters = 0;
+  ck(fl1::engine_cluster_capacity(ld, pl.sk_m, csize, &n_clusters), "cluster capacity");
+  if (n_clusters < 1) throw std::runtime_error("no cluster of this size fits on the device");
+  n_clusters = std::min<int>(n_clusters, std::max<int32_t>(batch, 1));
+  const int64_t cap = opts->collect_trace ? static_cast<int64_t>(std::max<uint64_t>(cfg->max_iterations, 1)) : 1;
+  const int64_t B = std::max<int32_t>(batch, 1);
+
+  EngineParams tmpl{};
+  const size_t ws_bytes = (carve(tmpl, nullptr, n, k, ld, csize, units, 1, pl.sk_elems) + 255) / 256 * 256;
+  size_t top = ws_bytes * static_cast<size_t>(n_clusters);  // cluster workspaces first, then:
+  auto region = [&](size_t bytes) {
+    top = (top + 255) / 256 * 256;
+    const size_t o = top;
+    top += bytes;
+    return o;
+  };
+  const size_t ub = static_cast<size_t>(B), kb = static_cast<size_t>(k);
+  const size_t o_params = region(sizeof(EngineParams) * static_cast<size_t>(n_clusters));
+  const size_t o_desc = region(sizeof(fl1::BatchDesc));
+  const size_t o_y = region(y_device ? 0 : sizeof(double) * static_cast<size_t>(ld) * ub);
+  const size_t o_lam = region(sizeof(double) * ub);
+  const size_t o_st = region(sizeof(EngineState) * ub);
+  const size_t o_tr = region(sizeof(fl1_trace_row) * static_cast<size_t>(cap) * ub);
+  const size_t o_sw = region(sizeof(fl1_switch_event) * fl1::kMaxLevels * ub);
+  const size_t o_cnt = region(sizeof(int64_t) * static_cast<size_t>(2 + n_clusters));
+  const size_t o_off = region(sizeof(int64_t) * ub);
+  const size_t o_idx = region(sizeof(int32_t) * kb * ub);
+  const size_t o_x = region(sizeof(double) * kb * ub);
+  DevBuf mem(top + 256);
+  char* base = mem.as<char>();
+  cudaStream_t stream = nullptr;
+  ck(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking), "stream");
+  struct StreamGuard {
+    cudaStream_t s;
+    ~StreamGuard() { cudaStreamDestroy(s); }
+  } sg{stream};
+  cudaEvent_t ev0, ev1;
+  ck(cudaEventCreate(&ev0), "event");
+  ck(cudaEventCreate(&ev1), "event");
+  struct EventGuard {
+    cudaEvent_t a, b;
+    ~EventGuard() {
+      cudaEventDestroy(a);
+      cudaEventDestroy(b);
+    }
+  } eg{ev0, ev1};
+
+  std::vector<EngineParams> params(static_cast<size_t>(n_clusters));
+  for (int q = 0; q < n_clusters; ++q) {
+    EngineParams& p = params[static_cast<size_t>(q)];
+    carve(p, base + static_cast<size_t>(q) * ws_bytes, n, k, ld, csize, units, 1, pl.sk_elems);
+    fill_params(p, pl, s, 1.0, cfg, opts);
+    p.grid = csize;
+    p.n = n;
+    p.k = k;
+    p.ld = ld;
+    p.trace_cap = cap;
+  }
+  fl1::BatchDesc bd{};
+  bd.batch = batch;
+  int64_t* counters = reinterpret_cast<int64_t*>(base + o_cnt);
+  bd.next = reinterpret_cast<int32_t*>(counters);
+  bd.out_used = counters + 1;
+  bd.cluster_sig = reinterpret_cast<int32_t*>(counters + 2);
+  bd.cluster_params = reinterpret_cast<const EngineParams*>(base + o_params);
+  bd.Y = y_device ? Y : reinterpret_cast<const double*>(base + o_y);
+  bd.ldy = y_device ? ldy : ld;
+  bd.lambdas = reinterpret_cast<const double*>(base + o_lam);
+  bd.states = reinterpret_cast<EngineState*>(base + o_st);
+  bd.traces = reinterpret_cast<fl1_trace_row*>(base + o_tr);
+  bd.trace_cap = cap;
+  bd.sws = reinterpret_cast<fl1_switch_event*>(base + o_sw);
+  bd.out_off = reinterpret_cast<int64_t*>(base + o_off);
+  bd.out_idx = reinterpret_cast<int32_t*>(base + o_idx);
+  bd.out_x = reinterpret_cast<double*>(base + o_x);
+  EngineParams p0{};
+  p0.batch = reinterpret_cast<const fl1::BatchDesc*>(base + o_desc);
+  p0.ld = ld;
+
+  std::vector<EngineState> hst(static_cast<size_t>(B));
+  for (auto& st : hst) {
+    st = EngineState{};
+    st.dict_index = pl.start_level;
+    st.t_k = 1.0;
+  }
+  ck(cudaEventRecord(ev0, stream), "event");
+  ck(cudaMemsetAsync(base, 0, ws_bytes * static_cast<size_t>(n_clusters), stream), "workspace memset");
+  ck(cudaMemsetAsync(counters, 0, sizeof(int64_t) * (2 + n_clusters), stream), "counter memset");
+  ck(cudaMemcpyAsync(base + o_params, params.data(), sizeof(EngineParams) * params.size(), cudaMemcpyHostToDevice,
+                     stream),
+     "params upload");
+  ck(cudaMemcpyAsync(base + o_desc, &bd, sizeof(bd), cudaMemcpyHostToDevice, stream), "desc upload");
+  ck(cudaMemcpyAsync(base + o_lam, lambdas, sizeof(double) * batch, cudaMemcpyHostToDevice, stream), "lambda upload");
+  ck(cudaMemcpyAsync(base + o_st, hst.data(), sizeof(EngineState) * batch, cudaMemcpyHostToDevice, stream),
+     "state upload");
+  int64_t h2d_sig = static_cast<int64_t>(sizeof(EngineState) + sizeof(double));
+  if (!y_device && batch > 0) {
+    ck(cudaMemcpy2DAsync(base + o_y, sizeof(double) * ld, Y, sizeof(double) * ldy, sizeof(double) * n, batch,
+                         cudaMemcpyHostToDevice, stream),
+       "signal upload");
+    h2d_sig += 8 * n;
+  }
+  if (batch > 0) ck(fl1::engine_launch_clusters(p0, n_clusters, csize, pl.sk_m, stream), "cluster launch");
+  ck(cudaMemcpyAsync(hst.data(), base + o_st, sizeof(EngineState) * batch, cudaMemcpyDeviceToHost, stream),
+     "state download");
+  int64_t used = 0;
+  ck(cudaMemcpyAsync(&used, counters + 1, sizeof(int64_t), cudaMemcpyDeviceToHost, stream), "count download");
+  ck(cudaStreamSynchronize(stream), "batched sync");
+  std::vector<int64_t> offs(static_cast<size_t>(B));
+  std::vector<int32_t> all_idx(static_cast<size_t>(std::max<int64_t>(used, 1)));
+  std::vector<double> all_x(static_cast<size_t>(std::max<int64_t>(used, 1)));
+  std::vector<fl1_switch_event> all_sw(static_cast<size_t>(fl1::kMaxLevels * B));
+  ck(cudaMemcpyAsync(offs.data(), base + o_off, sizeof(int64_t) * batch, cudaMemcpyDeviceToHost, stream), "offsets");
+  if (used > 0) {
+    ck(cudaMemcpyAsync(all_idx.data(), base + o_idx, sizeof(int32_t) * used, cudaMemcpyDeviceToHost, stream), "idx");
+    ck(cudaMemcpyAsync(all_x.data(), base + o_x, sizeof(double) * used, cudaMemcpyDeviceToHost, stream), "x");
+  }
+  ck(cudaMemcpyAsync(all_sw.data(), base + o_sw, sizeof(fl1_switch_event) * fl1::kMaxLevels * batch,
+                     cudaMemcpyDeviceToHost, stream),
+     "switches");
+  std::vector<std::vector<fl1_trace_row>> traces(static_cast<size_t>(B));
+  for (int32_t b = 0; b < batch && opts->collect_trace; ++b) {
+    const int64_t rows = hst[static_cast<size_t>(b)].n_trace;
+    traces[static_cast<size_t>(b)].resize(static_cast<size_t>(rows));
+    if (rows > 0)
+      ck(cudaMemcpyAsync(traces[static_cast<size_t>(b)].data(),
+                         base + o_tr + sizeof(fl1_trace_row) * static_cast<size_t>(b * cap),
+                         sizeof(fl1_trace_row) * rows, cudaMemcpyDeviceToHost, stream),
+         "trace download");
+  }
+  ck(cudaEventRecord(ev1, stream), "event");
+  ck(cudaStreamSynchronize(stream), "download sync");
+  for (int32_t b = 0; b < batch; ++b) {
+    const EngineState& st = hst[static_cast<size_t>(b)];
+    if (!st.done) throw std::runtime_error("batched solve did not finish");
+    const int32_t* ib = all_idx.data() + offs[static_cast<size_t>(b)];
+    const double* xb = all_x.data() + offs[static_cast<size_t>(b)];
+    auto res = std::make_unique<fl1_result>();
+    const fl1_switch_event* sb = all_sw.data() + static_cast<size_t>(b) * fl1::kMaxLevels;
+    fill_result(*res, st, cfg, k, std::vector<int32_t>(ib, ib + st.S), xb,
+                std::vector<fl1_switch_event>(sb, sb + st.n_switches));
+    res->trace = std::move(traces[static_cast<size_t>(b)]);
+    res->device_ms = (st.end_ns - st.start_ns) * 1e-6;
+    res->launches = 0;  // one launch for the whole batch (fl1_result_info.kernel_launches of signal 0 = 1)
+    if (b == 0) res->launches = 1;
+    res->h2d = h2d_sig;
+    res->d2h = static_cast<int64_t>(sizeof(EngineState)) + 12 * st.S +
+               st.n_switches * static_cast<int64_t>(sizeof(fl1_switch_event)) +
+               st.n_trace * static_cast<int64_t>(sizeof(fl1_trace_row));
+    out[b] = res.release();
+  }
+}
+
 int solve_batched_impl(fl1_seq* s, const double* Y, bool y_device, int64_t ldy, const double* lambdas, int32_t batch,
                        const fl1_switch_config* cfg, const fl1_run_options* opts, int32_t concurrency,
                        fl1_result** out) {
@@ -943,8 +1150,21 @@ int solve_batched_impl(fl1_seq* s, const double* Y, bool y_device, int64_t ldy, 
     if (ldy < n) throw std::invalid_argument("ldy must be >= N");
     fl1_ctx* ctx = s->lv.back()->dict->ctx;
     ctx->bind();
+    for (int32_t b = 0; b < batch; ++b) out[b] = nullptr;
+    if (concurrency <= 0) {  // one launch, thread-block clusters as virtual grids
+      const int csize = concurrency == 0 ? kDefaultClusterSize : -concurrency;
+      try {
+        solve_clusters(s, Y, y_device, ldy, lambdas, batch, cfg, opts, csize, out);
+      } catch (...) {
+        for (int32_t b = 0; b < batch; ++b) {
+          delete out[b];
+          out[b] = nullptr;
+        }
+        throw;
+      }
+      return;
+    }
     int M = concurrency;
-    if (M <= 0) M = 4;  // default: 4 concurrent sub-grid solves (measured best on B200)
     M = std::max(1, std::min({M, ctx->sms, std::max<int>(batch, 1)}));
     const int grid_cap = std::max(1, ctx->sms / M);
     for (int32_t b = 0; b < batch; ++b) out[b] = nullptr;

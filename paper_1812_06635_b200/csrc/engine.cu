@@ -57,7 +57,7 @@ constexpr unsigned kFull = 0xffffffffu;
     if (threadIdx.x == 0 && s.t < 4096 && p.timeline) {                                                   \
       uint64_t t_;                                                                                        \
       asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_));                                              \
-      p.timeline[(static_cast<int64_t>(s.t) * gridDim.x + blockIdx.x) * 8 + (pt)] = t_;                  \
+      p.timeline[(static_cast<int64_t>(s.t) * vsize() + vrank()) * 8 + (pt)] = t_;                  \
     }                                                                                                     \
   } while (0)
 #else
@@ -89,6 +89,21 @@ enum Slot {
 // ||x||_1 partials for iteration t live in kSlL1 (t even) / kSlL1b (t odd); written
 // by phase B of iteration t-1 (over the kept new iterate) or by the constructor.
 constexpr int kSlL1b = 16;
+
+// Virtual grid: the engine runs either on the whole GPU (one cooperative launch,
+// grid-wide barrier) or inside one thread-block cluster per solve (batched mode,
+// cluster barrier). Every slice / work partition / barrier below goes through these.
+__shared__ int s_vsize;     // CTAs of the virtual grid
+__shared__ int s_vrank;     // this CTA's rank in it
+__shared__ int s_vcluster;  // 1: cluster mode
+__device__ __forceinline__ int vsize() { return s_vsize; }
+__device__ __forceinline__ int vrank() { return s_vrank; }
+__device__ __forceinline__ void vsync() {
+  if (s_vcluster)
+    cg::this_cluster().sync();
+  else
+    cg::this_grid().sync();
+}
 
 struct Frag {
   int64_t pos;
@@ -169,7 +184,7 @@ __device__ void grid_reduce(const EngineParams& p, Sh& sh, unsigned mask_sum, un
 }
 
 __device__ __forceinline__ void put_slot(const EngineParams& p, int slot, double v) {
-  __stcg(p.bred + static_cast<int64_t>(blockIdx.x) * kBred + slot, v);
+  __stcg(p.bred + static_cast<int64_t>(vrank()) * kBred + slot, v);
 }
 
 __device__ __forceinline__ double2 ldg_stream2(const double2* ptr) {
@@ -193,8 +208,8 @@ __device__ __forceinline__ double soft_threshold(double z, double u) {  // solve
 
 // CTA slice [lo, hi) of n items (balanced, contiguous).
 __device__ __forceinline__ void slice(int64_t n, int64_t& lo, int64_t& hi) {
-  lo = n * blockIdx.x / gridDim.x;
-  hi = n * (blockIdx.x + 1) / gridDim.x;
+  lo = n * vrank() / vsize();
+  hi = n * (vrank() + 1) / vsize();
 }
 
 __device__ __forceinline__ double globaltimer_ns() {
@@ -512,7 +527,6 @@ __device__ __noinline__ void dense_adjoint(const EngineParams& p, Sh& sh, const 
 __device__ __noinline__ void sukro_adjoint(const EngineParams& p, Sh& sh, const DevLevel& lv, const int32_t* __restrict__ idx,
                               const double* __restrict__ eps, int64_t S, const double* __restrict__ r,
                               double* __restrict__ rt, const PassOut& po) {
-  cg::grid_group grid = cg::this_grid();
   const int64_t m = lv.m, q = lv.q;
   const int nt = lv.nterms;
   const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
@@ -524,7 +538,7 @@ __device__ __noinline__ void sukro_adjoint(const EngineParams& p, Sh& sh, const 
   __syncthreads();
   // stage 1: warp task (t, s): lanes over rb
   const int64_t tasks = static_cast<int64_t>(nt) * q;
-  const int64_t gw = static_cast<int64_t>(blockIdx.x) * kWarps + w, nw = static_cast<int64_t>(gridDim.x) * kWarps;
+  const int64_t gw = static_cast<int64_t>(vrank()) * kWarps + w, nw = static_cast<int64_t>(vsize()) * kWarps;
   for (int64_t task = gw; task < tasks; task += nw) {
     const int64_t t = task / q, s = task - t * q;
     const double* __restrict__ ccol = lv.right + t * m * q + s * m;
@@ -550,7 +564,7 @@ __device__ __noinline__ void sukro_adjoint(const EngineParams& p, Sh& sh, const 
     for (int e = 0; e < kSukroMaxM / 32; ++e)
       if (l + 32 * e < m) __stcg(dst + l + 32 * e, a[e]);
   }
-  grid.sync();
+  vsync();
   // stage 2: warp per preserved atom, lanes over rb
   int64_t lo, hi;
   slice(S, lo, hi);
@@ -689,7 +703,7 @@ __device__ __noinline__ void dense_apply_units(const EngineParams& p, const DevL
   const int C = dense_apply_chunks(p, S);
   const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
   const double2* __restrict__ A2 = reinterpret_cast<const double2*>(lv.a) + l;
-  for (int64_t item = blockIdx.x; item < static_cast<int64_t>(U) * C; item += gridDim.x) {
+  for (int64_t item = vrank(); item < static_cast<int64_t>(U) * C; item += vsize()) {
     const int h = static_cast<int>(item % U);
     const int64_t c = item / U;
     const int64_t clo = S * c / C, chi = S * (c + 1) / C;
@@ -788,7 +802,6 @@ __device__ __noinline__ void dense_apply_units(const EngineParams& p, const DevL
 // the padded operands stay zero between calls. A second source carries the v fix.
 __device__ __noinline__ int sukro_apply_partials(const EngineParams& p, const DevLevel& lv, const ApplySrc& src, int64_t S,
                                     double* __restrict__ out, double* __restrict__ fix_out) {
-  cg::grid_group grid = cg::this_grid();
   const int64_t m = lv.m, q = lv.q, K = p.k, ld = p.ld;
   const int nt = lv.nterms;
   const int nsrc = fix_out ? 2 : 1;
@@ -805,9 +818,9 @@ __device__ __noinline__ int sukro_apply_partials(const EngineParams& p, const De
       p.sk_x[K + j] = d * src.xp[pos];
     }
   }
-  grid.sync();
+  vsync();
   // stage 1: W_t(s, rb) = sum_jj X(s, jj) B_t(rb, jj); warp task (src, t, rb), lanes over s
-  const int64_t gw = static_cast<int64_t>(blockIdx.x) * kWarps + w, nw = static_cast<int64_t>(gridDim.x) * kWarps;
+  const int64_t gw = static_cast<int64_t>(vrank()) * kWarps + w, nw = static_cast<int64_t>(vsize()) * kWarps;
   const int64_t tasks1 = static_cast<int64_t>(nsrc) * nt * m;
   for (int64_t task = gw; task < tasks1; task += nw) {
     const int64_t sr = task / (nt * m);
@@ -836,7 +849,7 @@ __device__ __noinline__ int sukro_apply_partials(const EngineParams& p, const De
     for (int e = 0; e < kSukroMaxQ / 32; ++e)
       if (l + 32 * e < q) __stcg(dst + l + 32 * e, a[e]);
   }
-  grid.sync();
+  vsync();
   // stage 2: out(rc, rb) = sum_t sum_s C_t(rc, s) W_t(s, rb), split over s into KS chunks
   const int KS = p.sk_ks;
   const int64_t tasks2 = static_cast<int64_t>(nsrc) * KS * m;
@@ -907,7 +920,6 @@ struct Scratch {
 
 __device__ __noinline__ double power_iteration(const EngineParams& p, Sh& sh, const DevLevel& lv, const Bank& bk, int64_t S,
                                   bool try_warm, const Scratch& sc) {
-  cg::grid_group grid = cg::this_grid();
   int64_t lo, hi;
   slice(S, lo, hi);
   {
@@ -924,7 +936,7 @@ __device__ __noinline__ double power_iteration(const EngineParams& p, Sh& sh, co
       put_slot(p, kSlSum, v[1]);
     }
   }
-  grid.sync();
+  vsync();
   grid_reduce(p, sh, (1u << kSlLead2) | (1u << kSlSum), 0u);
   const bool warm = try_warm && sh.res[kSlLead2] > 0.0;
   const double* cur_src = warm ? bk.lead : p.gauss0;
@@ -945,7 +957,7 @@ __device__ __noinline__ double power_iteration(const EngineParams& p, Sh& sh, co
     if (threadIdx.x == 0) tq0 = globaltimer_ns();
     ApplySrc as{bk.idx, nullptr, cur_src, cur_div, nullptr, nullptr, nullptr};
     const int C = op_apply_partials(p, sh, lv, as, S, p.pup, nullptr, sc.red);
-    grid.sync();
+    vsync();
     double tq1 = 0.0;
     if (threadIdx.x == 0) {
       tq1 = globaltimer_ns();
@@ -958,7 +970,7 @@ __device__ __noinline__ double power_iteration(const EngineParams& p, Sh& sh, co
       int64_t ilo, ihi;
       slice(p.ld, ilo, ihi);
       combine_rows(p.pup, C, p.ld, ilo, ihi, [&](int64_t i, double t) { __stcg(p.PU + i, t); });
-      grid.sync();
+      vsync();
         load_vec_smem(p, p.PU, sc.vec);
     }
     __syncthreads();
@@ -969,7 +981,7 @@ __device__ __noinline__ double power_iteration(const EngineParams& p, Sh& sh, co
     }
     PassOut po{p.pw, 0, 0.0, false, 0, 0, p.pv};
     op_adjoint(p, sh, lv, bk.idx, bk.eps, S, sc.vec, sc.rt, po);
-    grid.sync();
+    vsync();
     double tq3 = 0.0;
     if (threadIdx.x == 0) {
       tq3 = globaltimer_ns();
@@ -991,7 +1003,7 @@ __device__ __noinline__ double power_iteration(const EngineParams& p, Sh& sh, co
   }
   // leading vector (v after the last update)
   for (int64_t q = lo + threadIdx.x; q < hi; q += kThreads) bk.lead[q] = have_w ? p.pw[q] / cur_div : p.pv[q];
-  grid.sync();
+  vsync();
   return estimate;
 }
 
@@ -1100,13 +1112,12 @@ __device__ __forceinline__ int l1_slot(uint64_t t) { return (t & 1) ? kSlL1b : k
 
 // setup_dictionary (fastl1.cpp:283-324). first: constructor call.
 __device__ __noinline__ void setup_dictionary(const EngineParams& p, Sh& sh, bool first, const Scratch& sc) {
-  cg::grid_group grid = cg::this_grid();
   EngineState& s = sh.s;
   const DevLevel& lv = p.lv[s.dict_index];
   Bank bk = p.bank[s.cur];
   if (!first) {  // ActiveOp::rebase (105-112)
     gather_metadata(p, sh, lv, bk, s.S);
-    grid.sync();
+    vsync();
     grid_reduce(p, sh, 0u, 1u << kSlMaxEps);
     if (threadIdx.x == 0) s.max_eps = s.S > 0 ? sh.res[kSlMaxEps] : 0.0;
     __syncthreads();
@@ -1116,12 +1127,12 @@ __device__ __noinline__ void setup_dictionary(const EngineParams& p, Sh& sh, boo
     PassOut po{bk.aty, 0, 0.0, false, 0, 0, nullptr};
     op_adjoint(p, sh, lv, bk.idx, bk.eps, s.S, sc.vec, sc.rt, po);
     if (p.precompute_aty && !s.atye_valid) {
-      grid.sync();
+      vsync();
       PassOut pe{bk.atye, 0, 0.0, false, 0, 0, nullptr};
       op_adjoint(p, sh, p.lv[p.n_levels - 1], bk.idx, bk.eps, s.S, sc.vec, sc.rt, pe);
       if (threadIdx.x == 0) s.atye_valid = 1;
     }
-    grid.sync();
+    vsync();
   }
   if (p.has_full_l && s.S == p.k) {
     if (threadIdx.x == 0) s.lipschitz = p.full_l[s.dict_index];
@@ -1140,13 +1151,13 @@ __device__ __noinline__ void setup_dictionary(const EngineParams& p, Sh& sh, boo
   // u = op.apply(x)
   ApplySrc as{bk.idx, bk.x, nullptr, 1.0, nullptr, nullptr, nullptr};
   const int C = op_apply_partials(p, sh, lv, as, s.S, p.up, nullptr, sc.red);
-  grid.sync();
+  vsync();
   combine_u(p, sh, C, false, false, 0.0);  // momentum restarts (fastl1.cpp:322-323)
   if (threadIdx.x == 0) {
     s.momentum_ready = 0;
     s.t_k = 1.0;
   }
-  grid.sync();
+  vsync();
 }
 
 __device__ uint64_t row_flops(const EngineParams& p, int dict, int64_t active, int64_t nnz) {  // 647-665
@@ -1161,10 +1172,8 @@ __device__ uint64_t row_flops(const EngineParams& p, int dict, int64_t active, i
 }  // namespace
 
 // ============================================================================
-__global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_constant__ EngineParams p) {
-  cg::grid_group grid = cg::this_grid();
-  extern __shared__ __align__(16) double dyn[];
-  __shared__ Sh sh;
+// The whole solve (Engine ctor + Engine::run) or a utility mode, on the virtual grid.
+__device__ __noinline__ void engine_body(const EngineParams& p, Sh& sh, double* dyn) {
   EngineState& s = sh.s;
   Scratch sc;
   sc.vec = dyn;
@@ -1188,13 +1197,13 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
     } else if (p.mode == kModeApply) {
       ApplySrc as{bk.idx, p.x_init, nullptr, 1.0, nullptr, nullptr, nullptr};
       const int C = op_apply_partials(p, sh, lv, as, k, p.up, nullptr, sc.red);
-      grid.sync();
+      vsync();
       int64_t lo, hi;
       slice(ld, lo, hi);
       combine_rows(p.up, C, ld, lo, hi, [&](int64_t i, double t) { p.vec_out[i] = t; });
     } else {
       const double sq = power_iteration(p, sh, lv, bk, k, false, sc);
-      if (blockIdx.x == 0 && threadIdx.x == 0) {
+      if (vrank() == 0 && threadIdx.x == 0) {
         s.power_est = sq;
         *p.st = s;
       }
@@ -1239,7 +1248,7 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
       block_reduce<1>(v, mx, sh);
       if (threadIdx.x == 0) put_slot(p, l1_slot(0), v[0]);
     }
-    grid.sync();
+    vsync();
     grid_reduce(p, sh, 0u, 1u << kSlMaxEps);
     if (threadIdx.x == 0) s.max_eps = sh.res[kSlMaxEps];
     __syncthreads();
@@ -1295,7 +1304,7 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
         }
         __syncthreads();
       }
-      if (p.observe && blockIdx.x == 0)
+      if (p.observe && vrank() == 0)
         for (int64_t i = threadIdx.x; i < ld; i += kThreads) p.rho_obs[i] = sc.vec[i];
       if (threadIdx.x == 0) {
         sh.t_next = t_next;
@@ -1337,7 +1346,7 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
       }
     }
     FL1_MARK(1);
-    grid.sync();  // ------------------------------------------------ sync 1
+    vsync();  // ------------------------------------------------ sync 1
     FL1_MARK(2);
     double tp1 = 0.0;
     if (threadIdx.x == 0) {
@@ -1512,7 +1521,7 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
       }
     }
     FL1_MARK(3);
-    grid.sync();  // ------------------------------------------------ sync 2
+    vsync();  // ------------------------------------------------ sync 2
     FL1_MARK(4);
     double tp2 = 0.0;
     if (threadIdx.x == 0) {
@@ -1562,7 +1571,7 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
       s.ledger += row_flops(p, s.dict_index, S, sh.nnz);  // ledger + trace (611-623)
       if (!stop_now && lv.kind == kDense)
         s.prof_apply_bytes += 8.0 * static_cast<double>(p.n) * static_cast<double>(sh.nnz);
-      if (p.collect_trace && blockIdx.x == 0) {
+      if (p.collect_trace && vrank() == 0) {
         fl1_trace_row row;
         row.iter = s.t;
         row.dict_index = s.dict_index;
@@ -1596,7 +1605,7 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
       const Bank nb = p.bank[s.cur ^ 1];
       if (threadIdx.x < 32) {
         double acc = 0.0;
-        for (int b = threadIdx.x; b < static_cast<int>(blockIdx.x); b += 32)
+        for (int b = threadIdx.x; b < vrank(); b += 32)
           acc += __ldcg(p.bred + static_cast<int64_t>(b) * kBred + kSlKept);
         acc = warp_sum(acc);
         if (threadIdx.x == 0) sh.scan_base = static_cast<int64_t>(acc);
@@ -1661,7 +1670,7 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
       }
     }
     FL1_MARK(5);
-    grid.sync();  // ------------------------------------------------ sync 3
+    vsync();  // ------------------------------------------------ sync 3
     FL1_MARK(6);
     if (shrink) {
       grid_reduce(p, sh, 0u, 1u << kSlMaxEps);
@@ -1691,7 +1700,7 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
     __syncthreads();
     if (next_dict != s.dict_index) {  // switch (633-637)
       if (threadIdx.x == 0) {
-        if (blockIdx.x == 0) {
+        if (vrank() == 0) {
           fl1_switch_event ev;
           ev.iter = s.t - 1;
           ev.from = s.dict_index;
@@ -1716,7 +1725,93 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
     }
   }
   __syncthreads();
-  if (blockIdx.x == 0 && threadIdx.x == 0) *p.st = s;
+  if (vrank() == 0 && threadIdx.x == 0) {
+    s.end_ns = globaltimer_ns();
+    *p.st = s;
+  }
+}
+
+// ============================================================================
+// Grid mode (p0.batch == nullptr): one cooperative launch over every SM runs one
+// solve. Cluster mode: each thread-block cluster is a virtual grid with its own
+// workspace and takes signals from a shared queue (BASELINE config 5: B
+// independent run_lasso solves in one launch, cluster barriers instead of grid
+// barriers).
+__global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_constant__ EngineParams p0) {
+  extern __shared__ __align__(16) double dyn[];
+  __shared__ Sh sh;
+  __shared__ __align__(16) EngineParams sp;
+  auto copy_params = [&](const EngineParams* src) {
+    const int4* a = reinterpret_cast<const int4*>(src);
+    int4* b = reinterpret_cast<int4*>(&sp);
+    for (int i = threadIdx.x; i < static_cast<int>(sizeof(EngineParams) / sizeof(int4)); i += kThreads) b[i] = a[i];
+  };
+  if (p0.batch == nullptr) {
+    if (threadIdx.x == 0) {
+      s_vsize = gridDim.x;
+      s_vrank = blockIdx.x;
+      s_vcluster = 0;
+    }
+    copy_params(&p0);
+    __syncthreads();
+    engine_body(sp, sh, dyn);
+    return;
+  }
+  cg::cluster_group cl = cg::this_cluster();
+  const int csize = static_cast<int>(cl.num_blocks());
+  const int cid = blockIdx.x / csize;
+  if (threadIdx.x == 0) {
+    s_vsize = csize;
+    s_vrank = static_cast<int>(cl.block_rank());
+    s_vcluster = 1;
+  }
+  const BatchDesc& bd = *p0.batch;
+  copy_params(bd.cluster_params + cid);
+  __syncthreads();
+  while (true) {
+    if (s_vrank == 0 && threadIdx.x == 0) __stcg(bd.cluster_sig + cid, atomicAdd(bd.next, 1));
+    cl.sync();
+    const int b = __ldcg(bd.cluster_sig + cid);
+    cl.sync();
+    if (b >= bd.batch) break;
+    if (threadIdx.x == 0) {
+      sp.mode = kModeSolve;
+      sp.lambda = bd.lambdas[b];
+      sp.st = bd.states + b;
+      sp.trace = bd.traces + static_cast<int64_t>(b) * bd.trace_cap;
+      sp.sw = bd.sws + static_cast<int64_t>(b) * kMaxLevels;
+    }
+    {  // y_b into the workspace (zero padded to ld), by CTA slices
+      int64_t lo, hi;
+      slice(sp.ld, lo, hi);
+      double* yw = const_cast<double*>(sp.y);
+      for (int64_t i = lo + threadIdx.x; i < hi; i += kThreads)
+        yw[i] = i < sp.n ? bd.Y[static_cast<int64_t>(b) * bd.ldy + i] : 0.0;
+    }
+    __syncthreads();
+    cl.sync();
+    engine_body(sp, sh, dyn);
+    cl.sync();
+    {  // finish (fastl1.cpp:741-748): the preserved set and its iterate to the signal's outputs
+      // packed: rank 0 reserves S slots and publishes the offset through the state
+      const Bank fb = sp.bank[sh.s.cur];
+      if (s_vrank == 0 && threadIdx.x == 0) {
+        const unsigned long long off =
+            atomicAdd(reinterpret_cast<unsigned long long*>(bd.out_used), static_cast<unsigned long long>(sh.s.S));
+        bd.out_off[b] = static_cast<int64_t>(off);
+      }
+      cl.sync();
+      const int64_t off = __ldcg(bd.out_off + b);
+      int64_t lo, hi;
+      slice(sh.s.S, lo, hi);
+      for (int64_t q = lo + threadIdx.x; q < hi; q += kThreads) {
+        bd.out_idx[off + q] = fb.idx[q];
+        bd.out_x[off + q] = fb.x[q];
+      }
+    }
+    __syncthreads();
+    cl.sync();
+  }
 }
 
 // screen_precomputed (screening.cpp:136-150) as a standalone device kernel.
@@ -1751,9 +1846,12 @@ cudaError_t engine_configure(int64_t ld, int64_t sukro_m, int device, int* grid_
   int optin = 0;
   cudaError_t e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
   if (e != cudaSuccess) return e;
-  if (smem + sizeof(Sh) + 1024 > static_cast<size_t>(optin)) return cudaErrorInvalidConfiguration;
-  e = cudaFuncSetAttribute(engine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           optin - static_cast<int>(sizeof(Sh)) - 1024);
+  cudaFuncAttributes fa{};
+  e = cudaFuncGetAttributes(&fa, engine_kernel);
+  if (e != cudaSuccess) return e;
+  const int room = optin - static_cast<int>(fa.sharedSizeBytes);  // static: Sh, EngineParams, reduction scratch
+  if (static_cast<int64_t>(smem) > room) return cudaErrorInvalidConfiguration;
+  e = cudaFuncSetAttribute(engine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, room);
   if (e != cudaSuccess) return e;
   int per_sm = 0;
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, engine_kernel, kThreads, smem);
@@ -1764,6 +1862,41 @@ cudaError_t engine_configure(int64_t ld, int64_t sukro_m, int device, int* grid_
   if (per_sm < 1) return cudaErrorInvalidConfiguration;
   *grid_out = sms;  // one persistent CTA per SM
   return cudaSuccess;
+}
+
+namespace {
+cudaLaunchConfig_t cluster_config(int n_clusters, int csize, int64_t ld, int64_t sukro_m, cudaLaunchAttribute* at) {
+  cudaLaunchConfig_t c{};
+  c.gridDim = dim3(static_cast<unsigned>(n_clusters * csize));
+  c.blockDim = dim3(kThreads);
+  c.dynamicSmemBytes = engine_smem_bytes(ld, sukro_m);
+  at->id = cudaLaunchAttributeClusterDimension;
+  at->val.clusterDim.x = static_cast<unsigned>(csize);
+  at->val.clusterDim.y = 1;
+  at->val.clusterDim.z = 1;
+  c.attrs = at;
+  c.numAttrs = 1;
+  return c;
+}
+}  // namespace
+
+// How many clusters of csize CTAs can be co-resident (engine_configure first).
+cudaError_t engine_cluster_capacity(int64_t ld, int64_t sukro_m, int csize, int* n_clusters) {
+  if (csize > 8) {
+    const cudaError_t e = cudaFuncSetAttribute(engine_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) return e;
+  }
+  cudaLaunchAttribute at;
+  cudaLaunchConfig_t c = cluster_config(1, csize, ld, sukro_m, &at);
+  return cudaOccupancyMaxActiveClusters(n_clusters, engine_kernel, &c);
+}
+
+cudaError_t engine_launch_clusters(const EngineParams& p0, int n_clusters, int csize, int64_t sukro_m,
+                                   cudaStream_t stream) {
+  cudaLaunchAttribute at;
+  cudaLaunchConfig_t c = cluster_config(n_clusters, csize, p0.ld, sukro_m, &at);
+  c.stream = stream;
+  return cudaLaunchKernelEx(&c, engine_kernel, p0);
 }
 
 cudaError_t engine_launch(const EngineParams& p, int64_t sukro_m, cudaStream_t stream) {

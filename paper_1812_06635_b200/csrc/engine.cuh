@@ -86,6 +86,7 @@ struct EngineState {
   double final_gap;
   double t0_ns;          // %globaltimer at run() start
   double start_ns;       // %globaltimer at kernel start (solve mode)
+  double end_ns;         // %globaltimer at the final state write
   int32_t dict_index;
   int32_t cur;           // current bank
   int32_t momentum_ready;
@@ -120,7 +121,29 @@ struct EngineState {
   double prof_pw[4];  // power-iteration sub-phases: apply, combine, adjoint+norms, reduce
 };
 
-struct EngineParams {
+struct EngineParams;
+
+// Batched (cluster) mode: B independent solves of one sequence, one per signal,
+// taken from a queue by thread-block clusters (each cluster = one workspace).
+struct BatchDesc {
+  int32_t batch;
+  int32_t* next;                        // work counter (starts at 0)
+  int32_t* cluster_sig;                 // per cluster: signal being solved
+  const EngineParams* cluster_params;   // per cluster: workspace + problem (grid = cluster size)
+  const double* Y;                      // N x B, leading dimension ldy
+  int64_t ldy;
+  const double* lambdas;                // B
+  EngineState* states;                  // B: initial state in, final state out
+  fl1_trace_row* traces;                // B x trace_cap
+  int64_t trace_cap;
+  fl1_switch_event* sws;                // B x kMaxLevels
+  int64_t* out_used;                    // packed-output counter (starts at 0)
+  int64_t* out_off;                     // B: offset of each signal's final set
+  int32_t* out_idx;                     // packed final preserved sets (capacity B x K)
+  double* out_x;                        // iterate on them
+};
+
+struct alignas(16) EngineParams {
   int32_t mode;
   int32_t grid;
   int64_t n, k, ld;
@@ -173,6 +196,7 @@ struct EngineParams {
   fl1_switch_event* sw;
   EngineState* st;
   uint64_t* timeline;  // FL1_TIMELINE builds only: [iter][cta][8] %globaltimer marks
+  const BatchDesc* batch;  // non-null: cluster (batched) mode
 };
 
 constexpr int kBred = 20;  // doubles of per-CTA partials (slots, see engine.cu)

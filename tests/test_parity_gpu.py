@@ -226,10 +226,12 @@ def test_large_path_properties(cuda):
         x = r.x
 
 
-@pytest.mark.parametrize("concurrency", [1, 4, 16])
+@pytest.mark.parametrize("concurrency", [1, 4, 16, 0, -1, -4, -16])
 def test_batched_many_signal(cuda, oracle16, concurrency):
     """BASELINE configs[4] semantics (independent solves per signal), reduced batch:
-    every batched result matches the oracle's own solve of that signal."""
+    every batched result matches the oracle's own solve of that signal, both for
+    concurrent sub-grid launches (concurrency > 0) and for the single launch of
+    thread-block clusters (concurrency <= 0: cluster size -concurrency, 0 = default)."""
     rng = np.random.default_rng(5)
     n, k, B = 128, 512, 12
     a = syn.gaussian_dictionary(rng, n, k)
@@ -249,3 +251,54 @@ def test_batched_many_signal(cuda, oracle16, concurrency):
         o = F.run_lasso(seq_o, Y[:, b], lams[b], cfg, opts)
         assert res[b].converged
         assert_parity(res[b], o, a, Y[:, b], lams[b])
+
+
+@pytest.mark.parametrize("csize", [1, 2, 8])
+def test_batched_clusters_switching_and_trace(cuda, oracle16, csize):
+    """Cluster mode with per-signal dictionary switching (stable screening over the
+    SuKro levels) and full traces: every signal equals its own oracle solve,
+    including the switch events and the per-iteration trace."""
+    inst = syn.sukro_instance(seed=3, m=16, q=32, nnz=30)
+    rng = np.random.default_rng(11)
+    B = 6
+    Y = np.empty((inst.a.shape[0], B), order="F")
+    lams = np.empty(B)
+    for b in range(B):
+        Y[:, b] = syn.observe(rng, inst.a @ syn.sparse_signal(rng, inst.a.shape[1], 20 + 3 * b), None, 30.0)
+        lams[b] = (0.2 + 0.05 * b) * np.max(np.abs(inst.a.T @ Y[:, b]))
+    cfg = F.SwitchConfig(screening_interval=10, max_iterations=5000, rel_tolerance=1e-6, gamma_threshold=0.5)
+    opts = F.RunOptions(collect_trace=True)
+    res = F.run_lasso_batched(_sukro_seq(inst, cuda), Y, lams, cfg, opts, concurrency=-csize)
+    seq_o = _sukro_seq(inst, oracle16)
+    n_sw = 0
+    for b in range(B):
+        o = F.run_lasso(seq_o, Y[:, b], lams[b], cfg, opts)
+        assert res[b].converged
+        assert_parity(res[b], o, inst.a, Y[:, b], lams[b])
+        assert len(res[b].trace) == len(o.trace)
+        n_sw += res[b].switches.size
+    assert n_sw >= 1
+
+
+def test_batched_clusters_device_input(cuda):
+    """Y resident in HBM (fl1_solve_batched_device) gives the same results as host Y,
+    with no signal bytes copied host->device; an empty batch is a no-op."""
+    import torch
+
+    rng = np.random.default_rng(7)
+    n, k, B = 200, 700, 9
+    a = syn.gaussian_dictionary(rng, n, k)
+    Y = np.empty((n, B), order="F")
+    for b in range(B):
+        Y[:, b] = syn.observe(rng, a @ syn.sparse_signal(rng, k, 8), None, 30.0)
+    lams = 0.25 * np.max(np.abs(a.T @ Y), axis=0)
+    seq = F.ApproxSequence([F.make_exact_approx(F.DenseDictionary(a, backend=cuda))])
+    cfg = F.SwitchConfig(screening_interval=10, max_iterations=5000, rel_tolerance=1e-6)
+    opts = F.RunOptions(variant=F.VARIANT_SCREENED)
+    r_host = F.run_lasso_batched(seq, Y, lams, cfg, opts, concurrency=-2)
+    y_dev = torch.from_numpy(np.ascontiguousarray(Y.T)).cuda()  # row b = signal b: N x B column-major
+    r_dev = F.run_lasso_batched(seq, (n, B), lams, cfg, opts, concurrency=-2, y_dev_ptr=y_dev.data_ptr())
+    for b in range(B):
+        assert np.array_equal(r_host[b].x, r_dev[b].x)
+        assert r_dev[b].h2d_bytes < r_host[b].h2d_bytes
+    assert F.run_lasso_batched(seq, Y[:, :0], lams[:0], cfg, opts, concurrency=0) == []
