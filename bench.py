@@ -25,6 +25,7 @@ every rank solves its own seeded instance, no collective on the data path.
 from __future__ import annotations
 
 import argparse
+from dataclasses import replace
 import json
 import os
 import statistics
@@ -261,6 +262,119 @@ def run_gpu(args) -> None:
         "cpu_baseline": cpu,
         "parity": {"final_gap": r0.final_gap, "nnz": int(np.count_nonzero(r0.x)),
                    "converged": r0.converged},
+    }
+    print(json.dumps(line))
+    if dist:
+        dist.destroy_process_group()
+
+
+def run_sukro(args) -> None:
+    """configs[2]: Kronecker-sum dictionary (6 terms, 4096 x 16384) with stable GAP
+    screening and switching A1 -> A2 -> A4 -> A (multi_dict, Gamma = 0.5). A step =
+    one solve; value = device time per solve (y resident in HBM)."""
+    import torch
+
+    from paper_1812_06635_b200 import fastl1 as F, synthetic as syn
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    os.environ["FL1_DEVICE"] = str(local)
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist_mod
+
+        dist_mod.init_process_group("nccl", device_id=torch.device("cuda", local))
+        dist = dist_mod
+    inst = syn.sukro_instance(seed=3 + 1000 * rank)
+    n, k = inst.a.shape
+    seq = syn.sukro_sequence(inst)
+    # per-level Lipschitz constants cached outside run_lasso, as the reference harness does
+    Ls = [F.lipschitz_bound(dd.op) for dd in seq.dicts]
+    cfg = F.SwitchConfig(screening_interval=10, max_iterations=5000, rel_tolerance=1e-6, gamma_threshold=0.5)
+    opts = F.RunOptions(variant=F.VARIANT_MULTI_DICT, full_lipschitz=Ls)
+    y_dev = torch.from_numpy(inst.y).to(f"cuda:{local}")
+    for _ in range(args.warmup):
+        F.run_lasso_device(seq, y_dev.data_ptr(), inst.lam, cfg, opts)
+        F.run_lasso(seq, inst.y, inst.lam, cfg, opts)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        dev_ms, iters, launches = [], 0, 0
+        for _ in range(args.steps):
+            r = F.run_lasso_device(seq, y_dev.data_ptr(), inst.lam, cfg, opts)
+            dev_ms.append(r.device_ms)
+            iters += r.iterations
+            launches += r.kernel_launches
+        torch.cuda.synchronize()
+        t1 = time.perf_counter()
+        e2e_r = None
+        for _ in range(args.steps):
+            e2e_r = F.run_lasso(seq, inst.y, inst.lam, cfg, opts)
+        torch.cuda.synchronize()
+        wall_e2e = (time.perf_counter() - t1) / args.steps
+    per_solve_s = float(np.mean(dev_ms)) / 1e3
+    per_solve_s, e2e_s, iters_total = reduce_over_ranks(dist, f"cuda:{local}", per_solve_s, wall_e2e, float(iters))
+    if rank != 0:
+        if dist:
+            dist.destroy_process_group()
+        return
+    # breakdown from one traced solve: SuKro levels (flops) vs the exact dense phase (bytes)
+    rt = F.run_lasso_device(seq, y_dev.data_ptr(), inst.lam, replace(cfg), replace(opts, collect_trace=True))
+    tr = rt.trace
+    exact = seq.levels() - 1
+    sk = tr["dict_index"] < exact
+    sk_flops = 0.0
+    for li in range(exact):
+        mv = float(seq.dicts[li].op.matvec_flops())
+        sk_flops += 4.0 * mv * float(np.count_nonzero(tr["dict_index"] == li))  # adjoint + apply, 2 flops per MAC
+    first_exact = int(np.argmax(~sk)) if np.any(~sk) else len(tr)
+    sk_ms = float(tr["wall_ms"][first_exact]) if first_exact < len(tr) else float(tr["wall_ms"][-1])
+    dense_bytes = 8.0 * n * float(np.sum((tr["active_size"][~sk] + tr["x_nnz"][~sk]).astype(np.float64)))
+    dense_bytes += float(rt.profile[7])
+    dense_ms = max(rt.device_ms - sk_ms, 1e-9)
+    peak, peak_src = _peaks()
+    achieved = dense_bytes / (dense_ms / 1e3) / 1e9
+    cpu = None
+    if not args.no_cpu_baseline:
+        b = _oracle_backend(1)
+        seq_o = syn.sukro_sequence(inst, backend=b)
+        t = time.perf_counter()
+        F.run_lasso(seq_o, inst.y, inst.lam, cfg, opts)
+        cpu = {"value": time.perf_counter() - t, "unit": "s", "cores": 1, "kind": "port",
+               "sample": "1 full c3 solve by the Eigen-free CPU restatement (oracle/), 1 thread"}
+    line = {
+        "metric": METRIC, "value": per_solve_s, "unit": "s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": per_solve_s * 1e3, "higher_is_better": False, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (BASELINE c3: 6-term Kronecker sum of seeded Gaussian 64x128 factors, column-normalised; "
+                "numpy PCG64 seed 3)",
+        "config": {"workload": f"c3: SuKro {n}x{k}, levels A1 -> A2 -> A4 -> A, stable GAP every 10, Gamma 0.5, "
+                               "gap<=1e-6*P(x), cap 5000",
+                   "parallelism": f"replicas x{world}",
+                   "l2_policy": "exact A = 512 MiB >> L2; SuKro factors L2-resident"},
+        "iterations_per_solve": rt.iterations, "iters_per_s": iters_total / (per_solve_s * args.steps),
+        "switches": [(int(e["iter"]), int(e["from"]), int(e["to"])) for e in rt.switches],
+        "e2e": {"value": e2e_s, "unit": "s", "h2d_bytes_per_step": int(e2e_r.h2d_bytes),
+                "d2h_bytes_per_step": int(e2e_r.d2h_bytes)},
+        "gpu_launches": int(launches),
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": None, "peak_source": peak_src,
+                     "algorithmic_bytes_per_launch": dense_bytes,
+                     "kernel": "fl1::engine_kernel, exact dense phase (after the last switch)",
+                     "sukro_phase": {"flops": sk_flops, "ms": sk_ms, "TFLOPs": sk_flops / (sk_ms / 1e3) / 1e12,
+                                     "iterations": int(np.count_nonzero(sk)),
+                                     "note": "2 products per iteration at 2 * matvec_flops each (SURVEY 8d); "
+                                             "latency-bound small contractions, includes switch-time power "
+                                             "iterations"}},
+        "phase_ms": {"A_products_pass": rt.profile[0] / 1e6, "B_dual_screen_prox": rt.profile[1] / 1e6,
+                     "D_compact_apply": rt.profile[2] / 1e6, "power_iterations": rt.profile[3] / 1e6,
+                     "switch_setup": rt.profile[4] / 1e6},
+        "clocks": clk.summary(),
+        "cpu_baseline": cpu,
+        "parity": {"final_gap": rt.final_gap, "converged": rt.converged, "nnz": int(np.count_nonzero(rt.x))},
     }
     print(json.dumps(line))
     if dist:
@@ -625,12 +739,14 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
-    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c4", "c5"])
-    ap.add_argument("--concurrency", type=int, default=0, help="c5: concurrent sub-grid solves (0 = 4)")
+    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--concurrency", type=int, default=0, help="c5: <=0 one launch of thread-block clusters of -N CTAs (0 = default 2); >0 that many concurrent sub-grid launches")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
+    elif args.config == "c3":
+        run_sukro(args)
     elif args.config == "c4":
         run_path(args)
     elif args.config == "c5":

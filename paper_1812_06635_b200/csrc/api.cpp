@@ -28,6 +28,7 @@
 
 namespace fl1 {
 size_t engine_smem_bytes(int64_t ld, int64_t sukro_m);
+int64_t engine_scratch_len(int64_t ld, int64_t sukro_m);
 cudaError_t engine_configure(int64_t ld, int64_t sukro_m, int device, int* grid_out);
 cudaError_t engine_launch(const EngineParams& p, int64_t sukro_m, cudaStream_t stream);
 cudaError_t engine_cluster_capacity(int64_t ld, int64_t sukro_m, int csize, int* n_clusters);
@@ -255,7 +256,7 @@ struct Carver {
 };
 
 size_t carve(EngineParams& p, char* base, int64_t n, int64_t k, int64_t ld, int grid, int64_t units,
-             int64_t trace_cap, int64_t sk_elems) {
+             int64_t trace_cap, int64_t sk_m) {
   (void)n;
   Carver c{base};
   const int64_t kk = std::max<int64_t>(k, 1);
@@ -266,7 +267,7 @@ size_t carve(EngineParams& p, char* base, int64_t n, int64_t k, int64_t ld, int 
   p.V = c.take<double>(ld);
   p.rho = c.take<double>(ld);
   p.rho_obs = c.take<double>(ld);
-  // apply partials: one chunk per CTA (dense) or sk_ks split-K chunks (SuKro)
+  // apply partials: at most one chunk per CTA
   const int64_t chunks = std::max<int64_t>(grid, 8);
   p.up = c.take<double>(chunks * ld);
   p.dvp = c.take<double>(chunks * ld);
@@ -280,10 +281,8 @@ size_t carve(EngineParams& p, char* base, int64_t n, int64_t k, int64_t ld, int 
   p.pv = c.take<double>(kk);
   p.pw = c.take<double>(kk);
   p.PU = c.take<double>(ld);
-  p.sk_scat = nullptr;
-  p.sk_t = sk_elems > 0 ? c.take<double>(2 * sk_elems) : nullptr;
-  p.sk_x = sk_elems > 0 ? c.take<double>(2 * kk) : nullptr;
-  p.sk_ks = 8;
+  p.sk_z = sk_m > 0 ? c.take<double>(kk) : nullptr;
+  p.scratch_len = fl1::engine_scratch_len(ld, sk_m);
   p.bred = c.take<double>(static_cast<int64_t>(grid) * fl1::kBred);
   for (int b = 0; b < 2; ++b) {
     fl1::Bank& bk = p.bank[b];
@@ -339,10 +338,10 @@ std::unique_ptr<Workspace> fl1_ctx::acquire(int64_t n, int64_t k, int64_t trace_
     w->grid_cap = grid_cap;
   }
   EngineParams p{};
-  const size_t bytes = carve(p, nullptr, n, k, ld, w->grid, w->units, trace_cap, sk_elems);
+  const size_t bytes = carve(p, nullptr, n, k, ld, w->grid, w->units, trace_cap, sk_m);
   w->mem = std::make_unique<DevBuf>(bytes);
   ck(cudaMemset(w->mem->p, 0, bytes), "workspace memset");
-  carve(p, w->mem->as<char>(), n, k, ld, w->grid, w->units, trace_cap, sk_elems);
+  carve(p, w->mem->as<char>(), n, k, ld, w->grid, w->units, trace_cap, sk_m);
   p.grid = w->grid;
   p.n = n;
   p.k = k;
@@ -994,7 +993,7 @@ void solve_clusters(fl1_seq* s, const double* Y, bool y_device, int64_t ldy, con
   const int64_t B = std::max<int32_t>(batch, 1);
 
   EngineParams tmpl{};
-  const size_t ws_bytes = (carve(tmpl, nullptr, n, k, ld, csize, units, 1, pl.sk_elems) + 255) / 256 * 256;
+  const size_t ws_bytes = (carve(tmpl, nullptr, n, k, ld, csize, units, 1, pl.sk_m) + 255) / 256 * 256;
   size_t top = ws_bytes * static_cast<size_t>(n_clusters);  // cluster workspaces first, then:
   auto region = [&](size_t bytes) {
     top = (top + 255) / 256 * 256;
@@ -1036,7 +1035,7 @@ void solve_clusters(fl1_seq* s, const double* Y, bool y_device, int64_t ldy, con
   std::vector<EngineParams> params(static_cast<size_t>(n_clusters));
   for (int q = 0; q < n_clusters; ++q) {
     EngineParams& p = params[static_cast<size_t>(q)];
-    carve(p, base + static_cast<size_t>(q) * ws_bytes, n, k, ld, csize, units, 1, pl.sk_elems);
+    carve(p, base + static_cast<size_t>(q) * ws_bytes, n, k, ld, csize, units, 1, pl.sk_m);
     fill_params(p, pl, s, 1.0, cfg, opts);
     p.grid = csize;
     p.n = n;

@@ -519,70 +519,120 @@ __device__ __noinline__ void dense_adjoint(const EngineParams& p, Sh& sh, const 
 }
 
 // ----------------------------------------------------------------------------
+// fp64 tensor-core MMA (DMMA): D(8x8) += A(8x4, row) B(4x8, col). Fragments:
+// a = A[g][t], b = B[t][g], c[i] = D[g][2t+i] with g = lane/4, t = lane%4.
+// ----------------------------------------------------------------------------
+__device__ __forceinline__ void dmma884(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
+
+// ----------------------------------------------------------------------------
 // SuKro adjoint (SukroDictionary::apply_adjoint, dictionary.cpp:158-164, then the
-// ActiveOp gather 157-160): out[pos] = d_j * [sum_t C_t^T R B_t](s, jj) for
-// j = idx[pos] = jj*q + s. Stage 1 (all CTAs): T_t(s, rb) = sum_rc C_t(rc,s) R(rc,rb);
-// grid sync; stage 2: one warp per preserved atom. r is in shared memory.
+// ActiveOp gather 157-160): out[pos] = d_j * Z(s, jj), j = idx[pos] = jj*q + s,
+// Z = sum_t C_t^T R B_t (q x q), R = reshape(r, m, m) resident in shared memory.
+// Each CTA owns (8 columns jj) x (SB rows s) tiles of Z and needs no other CTA:
+//   V_t = R B_t(:, jj-block)          (m x 8, DMMA, K = m)
+//   Z  += C_t(:, s-block)^T V_t       (SB x 8, DMMA, K = m; split-K over warps)
+// Z goes to HBM/L2, one virtual-grid barrier, then every CTA gathers its own
+// slice of preserved positions with the pass statistics.
 // ----------------------------------------------------------------------------
 __device__ __noinline__ void sukro_adjoint(const EngineParams& p, Sh& sh, const DevLevel& lv, const int32_t* __restrict__ idx,
                               const double* __restrict__ eps, int64_t S, const double* __restrict__ r,
-                              double* __restrict__ rt, const PassOut& po) {
-  const int64_t m = lv.m, q = lv.q;
+                              double* __restrict__ scratch, const PassOut& po) {
+  const int m = static_cast<int>(lv.m), q = static_cast<int>(lv.q);
   const int nt = lv.nterms;
-  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-  // R^T with a padded row stride (bank-conflict free): rt[rb*(m+1) + rc] = R(rc, rb)
-  for (int64_t e = threadIdx.x; e < m * m; e += kThreads) {
-    const int64_t rb = e / m, rc = e - rb * m;
-    rt[rb * (m + 1) + rc] = r[e];
-  }
-  __syncthreads();
-  // stage 1: warp task (t, s): lanes over rb
-  const int64_t tasks = static_cast<int64_t>(nt) * q;
-  const int64_t gw = static_cast<int64_t>(vrank()) * kWarps + w, nw = static_cast<int64_t>(vsize()) * kWarps;
-  for (int64_t task = gw; task < tasks; task += nw) {
-    const int64_t t = task / q, s = task - t * q;
-    const double* __restrict__ ccol = lv.right + t * m * q + s * m;
-    double cv[kSukroMaxM / 32];
-#pragma unroll
-    for (int e = 0; e < kSukroMaxM / 32; ++e) cv[e] = (l + 32 * e < m) ? ccol[l + 32 * e] : 0.0;
-    double a[kSukroMaxM / 32];
-#pragma unroll
-    for (int e = 0; e < kSukroMaxM / 32; ++e) a[e] = 0.0;
-    for (int64_t rc = 0; rc < m; ++rc) {
-      double cb = 0.0;
-#pragma unroll
-      for (int e = 0; e < kSukroMaxM / 32; ++e)
-        if ((rc >> 5) == e) cb = __shfl_sync(kFull, cv[e], static_cast<int>(rc & 31));
-#pragma unroll
-      for (int e = 0; e < kSukroMaxM / 32; ++e) {
-        const int64_t rb = l + 32 * e;
-        if (rb < m) a[e] = fma(cb, rt[rb * (m + 1) + rc], a[e]);
+  const int64_t mq = static_cast<int64_t>(m) * q;
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31, g = l >> 2, tg = l & 3;
+  const int m4 = (m + 3) & ~3, mt = (m + 7) >> 3, ks_n = m4 >> 2;
+  const int q8 = (q + 7) >> 3, n_jb = q8;
+  int n_sb = vsize() / n_jb;
+  n_sb = max(n_sb, (q8 + 3) / 4);
+  n_sb = min(n_sb, q8);
+  int sb8 = (q8 + n_sb - 1) / n_sb;  // 8-row tiles per s-block: 1, 2 or 4
+  if (sb8 == 3) sb8 = 4;
+  n_sb = (q8 + sb8 - 1) / sb8;
+  const int SB = sb8 * 8, ksplit = 8 / sb8;
+  const int my_mt = w % sb8, kpart = w / sb8;
+  const int k_lo = ks_n * kpart / ksplit, k_hi = ks_n * (kpart + 1) / ksplit;
+  // per term: B block (m4 x 8), V (m4 x 8), C block (SB x (m4+1)); as many terms
+  // per staging round as the scratch holds (one load latency per round)
+  const int per_term = 16 * m4 + SB * (m4 + 1);
+  const int G = max(1, min(nt, static_cast<int>((p.scratch_len - kWarps * 64) / per_term)));
+  double* Red = scratch;                // split-K partials: kWarps x 64
+  double* Z = p.sk_z;
+  const int tiles = n_jb * n_sb;
+  for (int tile = vrank(); tile < tiles; tile += vsize()) {
+    const int jj0 = (tile % n_jb) * 8, s0 = (tile / n_jb) * SB;
+    double acc[2] = {0.0, 0.0};
+    for (int t0 = 0; t0 < nt; t0 += G) {
+      const int gn = min(G, nt - t0);
+      __syncthreads();  // previous users of the staging area are done
+      for (int e = threadIdx.x; e < gn * 8 * m4; e += kThreads) {
+        const int tt = e / (8 * m4), e2 = e - tt * 8 * m4;
+        const int n = e2 / m4, k = e2 - n * m4;
+        double* Bs = scratch + kWarps * 64 + tt * per_term;
+        Bs[k * 8 + n] = (k < m && jj0 + n < q)
+                            ? __ldg(lv.left + (t0 + tt) * mq + static_cast<int64_t>(jj0 + n) * m + k) : 0.0;
+      }
+      for (int e = threadIdx.x; e < gn * SB * m4; e += kThreads) {
+        const int tt = e / (SB * m4), e2 = e - tt * SB * m4;
+        const int i = e2 / m4, rc = e2 - i * m4;
+        double* Cs = scratch + kWarps * 64 + tt * per_term + 16 * m4;
+        Cs[i * (m4 + 1) + rc] = (rc < m && s0 + i < q)
+                                    ? __ldg(lv.right + (t0 + tt) * mq + static_cast<int64_t>(s0 + i) * m + rc) : 0.0;
+      }
+      __syncthreads();
+      // V_t = R B_t(:, jj-block): warp w owns (row tile, term) items w, w + 8, ...
+      for (int it = w; it < mt * gn; it += kWarps) {
+        const int rt = it % mt, tt = it / mt;
+        const double* Bs = scratch + kWarps * 64 + tt * per_term;
+        double* Vs = scratch + kWarps * 64 + tt * per_term + 8 * m4;
+        double c[2] = {0.0, 0.0};
+        const int rc = rt * 8 + g;
+        for (int ks = 0; ks < ks_n; ++ks) {
+          const int k = ks * 4 + tg;
+          const double a = (rc < m && k < m) ? r[rc + k * m] : 0.0;
+          dmma884(c, a, Bs[k * 8 + g]);
+        }
+        if (rc < m4) {
+          Vs[rc * 8 + 2 * tg] = c[0];
+          Vs[rc * 8 + 2 * tg + 1] = c[1];
+        }
+      }
+      __syncthreads();
+      // Z(s-block, jj-block) += C_t(:, s-block)^T V_t: warp = (row tile, K part)
+      for (int tt = 0; tt < gn; ++tt) {
+        const double* Vs = scratch + kWarps * 64 + tt * per_term + 8 * m4;
+        const double* Cs = scratch + kWarps * 64 + tt * per_term + 16 * m4;
+        for (int ks = k_lo; ks < k_hi; ++ks) {
+          const int k = ks * 4 + tg;
+          dmma884(acc, Cs[(my_mt * 8 + g) * (m4 + 1) + k], Vs[k * 8 + g]);
+        }
       }
     }
-    double* __restrict__ dst = p.sk_t + (t * q + s) * m;
-#pragma unroll
-    for (int e = 0; e < kSukroMaxM / 32; ++e)
-      if (l + 32 * e < m) __stcg(dst + l + 32 * e, a[e]);
+    // fixed-order sum of the K parts, then Z tile to memory (Z[j], j = jj*q + s)
+    __syncthreads();
+    Red[w * 64 + g * 8 + 2 * tg] = acc[0];
+    Red[w * 64 + g * 8 + 2 * tg + 1] = acc[1];
+    __syncthreads();
+    for (int e = threadIdx.x; e < SB * 8; e += kThreads) {
+      const int i = e >> 3, n = e & 7;  // tile row i (s), column n (jj)
+      const int rt = i >> 3, gi = i & 7;
+      double z = 0.0;
+      for (int kp = 0; kp < ksplit; ++kp) z += Red[(kp * sb8 + rt) * 64 + gi * 8 + n];
+      if (s0 + i < q && jj0 + n < q) __stcg(Z + static_cast<int64_t>(jj0 + n) * q + s0 + i, z);
+    }
   }
   vsync();
-  // stage 2: warp per preserved atom, lanes over rb
   int64_t lo, hi;
   slice(S, lo, hi);
   PassAcc acc;
-  for (int64_t pos = lo + w; pos < hi; pos += kWarps) {
+  for (int64_t pos = lo + threadIdx.x; pos < hi; pos += kThreads) {
     const int64_t j = idx[pos];
-    const int64_t jj = j / q, s = j - jj * q;
-    double a = 0.0;
-    for (int t = 0; t < nt; ++t) {
-      const double* __restrict__ trow = p.sk_t + (static_cast<int64_t>(t) * q + s) * m;
-      const double* __restrict__ bcol = lv.left + static_cast<int64_t>(t) * m * q + jj * m;
-      for (int64_t rb = l; rb < m; rb += 32) a = fma(__ldcg(trow + rb), bcol[rb], a);
-    }
-    a = warp_sum(a);
-    if (l == 0) {
-      const double total = lv.col_scale ? lv.col_scale[j] * a : a;
-      acc.add(p, po, eps, pos, total, true);
-    }
+    const double z = __ldcg(Z + j);
+    acc.add(p, po, eps, pos, lv.col_scale ? lv.col_scale[j] * z : z, true);
   }
   finish_pass(p, sh, po, acc);
 }
@@ -797,114 +847,123 @@ __device__ __noinline__ void dense_apply_units(const EngineParams& p, const DevL
 
 // SuKro apply (SukroDictionary::apply, dictionary.cpp:150-156, on the ActiveOp
 // zero-padded iterate 141-145): u = vec(sum_t C_t X B_t^T), X = reshape(d o x, q, q).
-// Scatter (own slice) -> sync -> W_t = X B_t^T -> sync -> split-K partials of
-// sum_t C_t W_t into out[ks*ld + i]; the scatter is undone in the last stage so
-// the padded operands stay zero between calls. A second source carries the v fix.
-__device__ __noinline__ int sukro_apply_partials(const EngineParams& p, const DevLevel& lv, const ApplySrc& src, int64_t S,
-                                    double* __restrict__ out, double* __restrict__ fix_out) {
-  const int64_t m = lv.m, q = lv.q, K = p.k, ld = p.ld;
+// Every nonzero x_j (j = jj*q + s) adds sum_t (d_j x_j C_t(:, s)) B_t(:, jj)^T, so
+// each CTA forms the partial U of its own slice of positions as one DMMA rank-k
+// update U_c = Cg Bg^T over the gathered columns (k = entry x term), staged through
+// shared memory in chunks — no grid barrier. Partials go to chunk vrank of out
+// (and of fix_out for the v-fix source: dropped atoms' previous iterate).
+__device__ __noinline__ int sukro_apply_partials(const EngineParams& p, Sh& sh, const DevLevel& lv, const ApplySrc& src,
+                                                 int64_t S, double* __restrict__ out, double* __restrict__ fix_out,
+                                                 double* __restrict__ scratch) {
+  const int m = static_cast<int>(lv.m), q = static_cast<int>(lv.q);
   const int nt = lv.nterms;
+  const int64_t mq = static_cast<int64_t>(m) * q, nn = static_cast<int64_t>(m) * m, ld = p.ld;
   const int nsrc = fix_out ? 2 : 1;
-  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31, g = l >> 2, tg = l & 3;
+  const int mt = (m + 7) >> 3, ntile = mt * mt, passes = (ntile + 63) / 64;
+  const int m1 = m + 1;
+  double* ent_v = scratch;                                   // kThreads entry values
+  int32_t* ent_j = reinterpret_cast<int32_t*>(scratch + kThreads);  // kThreads atom indices
+  double* stage = scratch + kThreads + kThreads / 2;
+  const int64_t room = p.scratch_len - (kThreads + kThreads / 2);
+  int kc = static_cast<int>(min(static_cast<int64_t>(128), room / (2 * m1))) & ~3;
+  const int E = max(1, kc / nt);  // entries per chunk
+  kc = (E * nt + 3) & ~3;
+  double* Cg = stage;           // column k: Cg[k*m1 + row]
+  double* Bg = stage + kc * m1;
   int64_t lo, hi;
   slice(S, lo, hi);
-  for (int64_t pos = lo + threadIdx.x; pos < hi; pos += kThreads) {
-    const int64_t j = src.idx[pos];
-    const double d = lv.col_scale ? lv.col_scale[j] : 1.0;
-    if (src.kept(pos)) {
-      const double cf = src.c(pos);
-      if (cf != 0.0) p.sk_x[j] = d * cf;
-    } else if (nsrc == 2 && src.xp[pos] != 0.0) {
-      p.sk_x[K + j] = d * src.xp[pos];
-    }
-  }
-  vsync();
-  // stage 1: W_t(s, rb) = sum_jj X(s, jj) B_t(rb, jj); warp task (src, t, rb), lanes over s
-  const int64_t gw = static_cast<int64_t>(vrank()) * kWarps + w, nw = static_cast<int64_t>(vsize()) * kWarps;
-  const int64_t tasks1 = static_cast<int64_t>(nsrc) * nt * m;
-  for (int64_t task = gw; task < tasks1; task += nw) {
-    const int64_t sr = task / (nt * m);
-    const int64_t rem = task - sr * nt * m;
-    const int64_t t = rem / m, rb = rem - t * m;
-    const double* __restrict__ X = p.sk_x + sr * K;
-    const double* __restrict__ B = lv.left + t * m * q;
-    double a[kSukroMaxQ / 32];
+  for (int sr = 0; sr < nsrc; ++sr) {
+    double* __restrict__ dst = (sr == 0 ? out : fix_out) + static_cast<int64_t>(vrank()) * ld;
+    for (int pass = 0; pass < passes; ++pass) {
+      double acc[8][2];
 #pragma unroll
-    for (int e = 0; e < kSukroMaxQ / 32; ++e) a[e] = 0.0;
-    for (int64_t j0 = 0; j0 < q; j0 += 32) {
-      const double bl = (j0 + l < q) ? B[(j0 + l) * m + rb] : 0.0;  // B_t(rb, jj) for jj = j0 + lane
-      const int jn = static_cast<int>(min(static_cast<int64_t>(32), q - j0));
-      for (int jq = 0; jq < jn; ++jq) {
-        const double bv = __shfl_sync(kFull, bl, jq);
-        const double* __restrict__ xcol = X + (j0 + jq) * q;
+      for (int i = 0; i < 8; ++i) acc[i][0] = acc[i][1] = 0.0;
+      for (int64_t base = lo; base < hi; base += kThreads) {
+        // entries of this batch of positions, compacted in position order
+        const int64_t pos = base + threadIdx.x;
+        double v = 0.0;
+        int32_t j = 0;
+        if (pos < hi) {
+          j = src.idx[pos];
+          if (sr == 0) {
+            if (src.kept(pos)) v = src.c(pos);
+          } else if (!src.kept(pos)) {
+            v = src.xp[pos];
+          }
+          if (v != 0.0 && lv.col_scale) v *= lv.col_scale[j];
+        }
+        const unsigned bal = __ballot_sync(kFull, v != 0.0);
+        if (l == 0) sh.wscan[w] = __popc(bal);
+        __syncthreads();
+        int off = 0, tot = 0;
+        for (int ww = 0; ww < kWarps; ++ww) {
+          if (ww < w) off += sh.wscan[ww];
+          tot += sh.wscan[ww];
+        }
+        if (v != 0.0) {
+          const int at = off + __popc(bal & ((1u << l) - 1u));
+          ent_v[at] = v;
+          ent_j[at] = j;
+        }
+        __syncthreads();
+        for (int e0 = 0; e0 < tot; e0 += E) {
+          const int ne = min(E, tot - e0), ncol = ne * nt, ncol4 = (ncol + 3) & ~3;
+          for (int e = threadIdx.x; e < ncol4 * m; e += kThreads) {
+            const int col = e / m, row = e - col * m;
+            double cv = 0.0, bv = 0.0;
+            if (col < ncol) {
+              const int en = e0 + col / nt, t = col - (col / nt) * nt;
+              const int32_t jj = ent_j[en] / q, ss = ent_j[en] - jj * q;
+              cv = ent_v[en] * __ldg(lv.right + t * mq + static_cast<int64_t>(ss) * m + row);
+              bv = __ldg(lv.left + t * mq + static_cast<int64_t>(jj) * m + row);
+            }
+            Cg[col * m1 + row] = cv;
+            Bg[col * m1 + row] = bv;
+          }
+          __syncthreads();
+          for (int ks = 0; ks < (ncol4 >> 2); ++ks) {
+            const int k = ks * 4 + tg;
 #pragma unroll
-        for (int e = 0; e < kSukroMaxQ / 32; ++e) {
-          const int64_t s = l + 32 * e;
-          if (s < q) a[e] = fma(__ldcg(xcol + s), bv, a[e]);
+            for (int i = 0; i < 8; ++i) {
+              const int T = pass * 64 + w * 8 + i;
+              if (T < ntile) {
+                const int rc = (T / mt) * 8 + g, rb = (T % mt) * 8 + g;
+                dmma884(acc[i], rc < m ? Cg[k * m1 + rc] : 0.0, rb < m ? Bg[k * m1 + rb] : 0.0);
+              }
+            }
+          }
+          __syncthreads();
         }
       }
-    }
-    double* __restrict__ dst = p.sk_t + (sr * nt + t) * m * q + rb * q;
+      // U_c(rc, rb) at rc + rb*m
 #pragma unroll
-    for (int e = 0; e < kSukroMaxQ / 32; ++e)
-      if (l + 32 * e < q) __stcg(dst + l + 32 * e, a[e]);
-  }
-  vsync();
-  // stage 2: out(rc, rb) = sum_t sum_s C_t(rc, s) W_t(s, rb), split over s into KS chunks
-  const int KS = p.sk_ks;
-  const int64_t tasks2 = static_cast<int64_t>(nsrc) * KS * m;
-  for (int64_t task = gw; task < tasks2; task += nw) {
-    const int64_t sr = task / (KS * m);
-    const int64_t rem = task - sr * KS * m;
-    const int64_t ks = rem / m, rb = rem - ks * m;
-    const int64_t s_lo = q * ks / KS, s_hi = q * (ks + 1) / KS;
-    double a[kSukroMaxM / 32];
+      for (int i = 0; i < 8; ++i) {
+        const int T = pass * 64 + w * 8 + i;
+        if (T < ntile) {
+          const int rc = (T / mt) * 8 + g;
 #pragma unroll
-    for (int e = 0; e < kSukroMaxM / 32; ++e) a[e] = 0.0;
-    for (int t = 0; t < nt; ++t) {
-      const double* __restrict__ Wr = p.sk_t + (sr * nt + t) * m * q + rb * q;
-      const double* __restrict__ Ct = lv.right + static_cast<int64_t>(t) * m * q;
-      for (int64_t s0 = s_lo; s0 < s_hi; s0 += 32) {
-        const double wl = (s0 + l < s_hi) ? __ldcg(Wr + s0 + l) : 0.0;
-        const int sn = static_cast<int>(min(static_cast<int64_t>(32), s_hi - s0));
-        for (int sq = 0; sq < sn; ++sq) {
-          const double wv = __shfl_sync(kFull, wl, sq);
-          const double* __restrict__ ccol = Ct + (s0 + sq) * m;
-#pragma unroll
-          for (int e = 0; e < kSukroMaxM / 32; ++e) {
-            const int64_t rc = l + 32 * e;
-            if (rc < m) a[e] = fma(ccol[rc], wv, a[e]);
+          for (int c = 0; c < 2; ++c) {
+            const int rb = (T % mt) * 8 + 2 * tg + c;
+            if (rc < m && rb < m) __stcg(dst + rc + static_cast<int64_t>(rb) * m, acc[i][c]);
           }
         }
       }
     }
-    double* __restrict__ dst = (sr == 0 ? out : fix_out) + ks * ld + rb * m;
-#pragma unroll
-    for (int e = 0; e < kSukroMaxM / 32; ++e)
-      if (l + 32 * e < m) __stcg(dst + l + 32 * e, a[e]);
+    for (int64_t i = nn + threadIdx.x; i < ld; i += kThreads) __stcg(dst + i, 0.0);  // padding rows
   }
-  // undo the scatter (own slice, same predicate as above)
-  for (int64_t pos = lo + threadIdx.x; pos < hi; pos += kThreads) {
-    const int64_t j = src.idx[pos];
-    if (src.kept(pos)) {
-      if (src.c(pos) != 0.0) p.sk_x[j] = 0.0;
-    } else if (nsrc == 2 && src.xp[pos] != 0.0) {
-      p.sk_x[K + j] = 0.0;
-    }
-  }
-  return KS;
+  return vsize();
 }
 
 // Returns the number of partial chunks written to out (and fix_out).
 __device__ int op_apply_partials(const EngineParams& p, Sh& sh, const DevLevel& lv, const ApplySrc& src, int64_t S,
                                  double* out, double* fix_out, double* red) {
-  (void)sh;
   if (lv.kind == kDense) {
     dense_apply_units(p, lv, src, S, false, out, red);
     if (fix_out) dense_apply_units(p, lv, src, S, true, fix_out, red);
     return dense_apply_chunks(p, S);
   }
-  return sukro_apply_partials(p, lv, src, S, out, fix_out);
+  return sukro_apply_partials(p, sh, lv, src, S, out, fix_out, red);
 }
 
 // ----------------------------------------------------------------------------
@@ -1836,9 +1895,23 @@ cudaError_t screen_kernel_launch(int64_t n, const double* dots, const double* ep
   return cudaGetLastError();
 }
 
+// Shared scratch after the resident residual: dense apply warp partials, or the
+// SuKro staging (adjoint tiles; apply entry list + 64-column Cg / Bg chunks).
+int64_t engine_scratch_len(int64_t ld, int64_t sukro_m) {
+  int64_t s = static_cast<int64_t>(kWarps) * kUnit;
+  if (sukro_m > 0) {
+    const int64_t m4 = (sukro_m + 3) / 4 * 4;
+    const int64_t term = 16 * m4 + 32 * (m4 + 1);
+    s = std::max(s, term + kWarps * 64);                             // adjoint, one term per round
+    s = std::max(s, kThreads + kThreads / 2 + 2 * (sukro_m + 1) * 64);  // apply
+    const int64_t room = 200 * 1024 / 8 - ld;                        // up to 4 adjoint terms per round
+    s = std::max(s, std::min(room, 4 * term + kWarps * 64));
+  }
+  return s;
+}
+
 size_t engine_smem_bytes(int64_t ld, int64_t sukro_m) {
-  const int64_t scratch = std::max<int64_t>(static_cast<int64_t>(kWarps) * kUnit, sukro_m * (sukro_m + 1));
-  return static_cast<size_t>(ld + scratch) * sizeof(double);
+  return static_cast<size_t>(ld + engine_scratch_len(ld, sukro_m)) * sizeof(double);
 }
 
 cudaError_t engine_configure(int64_t ld, int64_t sukro_m, int device, int* grid_out) {

@@ -184,11 +184,9 @@ struct alignas(16) EngineParams {
   double* pv;       // K
   double* pw;       // K
   double* PU;       // ld: power-iteration A v (combined)
-  int32_t* sk_scat; // SuKro: per-CTA count of scattered entries (unscatter bookkeeping)
   const double* gauss0;  // K: mt19937_64(0x11b5c417) normals (solver.cpp:80-82)
-  double* sk_t;     // SuKro scratch: 2 * nterms * q * m (T_t / W_t for two sources)
-  double* sk_x;     // SuKro scratch: 2 * K zero-padded operands (iterate, v-fix)
-  int32_t sk_ks;    // SuKro apply split-K chunks
+  double* sk_z;     // SuKro adjoint: Z = sum_t C_t^T R B_t (K doubles)
+  int64_t scratch_len;  // doubles of shared scratch after the residual (engine_scratch_len)
   double* bred;     // per-CTA partials: grid * kBred doubles
   Bank bank[2];
   fl1_trace_row* trace;

@@ -128,3 +128,19 @@ def sukro_instance(seed: int = 3, m: int = 64, q: int = 128, terms: int = 6, lev
     return SukroInstance(lefts=lefts, rights=rights, col_scale=scale, a=a, levels=tuple(levels), eps=eps,
                          approx_norms=an, exact_norms=exact_norms, rc=rc, x0=x0, y=y, lam_max=lam_max,
                          lam=lam_ratio * lam_max, seed=seed)
+
+
+def sukro_sequence(inst: SukroInstance, backend=None):
+    """The configs[2] ApproxSequence: SuKro truncations to the first q in inst.levels
+    terms (same column scale, exact per-atom error norms) followed by the exact dense
+    dictionary (dictionary.cpp:216-251 invariants)."""
+    from . import fastl1 as F
+
+    levels = []
+    for li, nt in enumerate(inst.levels):
+        op = F.SukroDictionary(list(zip(inst.lefts[:nt], inst.rights[:nt])), col_scale=inst.col_scale,
+                               backend=backend)
+        levels.append(F.ApproxDictionary(op, inst.eps[li], float(inst.eps[li].max()), inst.rc[li],
+                                         inst.approx_norms[li], inst.exact_norms))
+    levels.append(F.make_exact_approx(F.DenseDictionary(inst.a, backend=backend)))
+    return F.ApproxSequence(levels)

@@ -85,13 +85,7 @@ def test_cold_lipschitz_matches_oracle(cuda, oracle16):
 
 
 def _sukro_seq(inst, b):
-    levels = []
-    for li, nt in enumerate(inst.levels):
-        op = F.SukroDictionary(list(zip(inst.lefts[:nt], inst.rights[:nt])), col_scale=inst.col_scale, backend=b)
-        levels.append(F.ApproxDictionary(op, inst.eps[li], float(inst.eps[li].max()), inst.rc[li],
-                                         inst.approx_norms[li], inst.exact_norms))
-    levels.append(F.make_exact_approx(F.DenseDictionary(inst.a, backend=b)))
-    return F.ApproxSequence(levels)
+    return syn.sukro_sequence(inst, b)
 
 
 @pytest.mark.parametrize("size", ["small", "full"])
