@@ -582,11 +582,12 @@ def run_batched(args) -> None:
     torch.cuda.synchronize()
     with ClockSampler(local) as clk:
         t0 = time.perf_counter()
-        its, launches, last = 0, 0, None
+        its, launches, last, dev = 0, 0, None, []
         for _ in range(args.steps):
             last = F.run_lasso_batched(seq, (n, B), lams, cfg, opts, args.concurrency, y_dev_ptr=Yd.data_ptr())
             its += sum(r.iterations for r in last)
             launches += sum(r.kernel_launches for r in last)
+            dev.append(last[0].batch_device_ms)
         torch.cuda.synchronize()
         wall = (time.perf_counter() - t0) / args.steps
         t1 = time.perf_counter()
@@ -595,14 +596,16 @@ def run_batched(args) -> None:
             e2e_last = F.run_lasso_batched(seq, Y, lams, cfg, opts, args.concurrency)
         torch.cuda.synchronize()
         wall_e2e = (time.perf_counter() - t1) / args.steps
-    per_batch, e2e_s, its_total = reduce_over_ranks(dist, f"cuda:{local}", wall, wall_e2e, float(its))
+    per_batch = float(np.mean(dev)) / 1e3
+    per_batch, e2e_s, its_total = reduce_over_ranks(dist, f"cuda:{local}", per_batch, wall_e2e, float(its))
     if rank != 0:
         if dist:
             dist.destroy_process_group()
         return
-    peak, peak_src = _peaks()
-    alg = sum(algorithmic_bytes(r, n) for r in last)
-    achieved = alg / per_batch / 1e9
+    # C5 FLOPs_t = 2 N K B_active per iteration (the dense masked A^T R)
+    flops = 2.0 * n * k * float(sum(r.iterations for r in last))
+    peak_t, peak_src_t = _fp64_peak()
+    achieved = flops / per_batch / 1e12
     cpu = None if args.no_cpu_baseline else cpu_baseline_batched(a, Y, lams, L)
     line = {
         "metric": METRIC, "value": per_batch, "unit": "s", "n_gpus": world, "steps": args.steps,
@@ -610,23 +613,38 @@ def run_batched(args) -> None:
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (BASELINE c5 shape/distribution, numpy PCG64 seed 5)",
         "config": {"workload": f"c5: {B} independent Lasso signals on one dense {n}x{k} dictionary, per-signal "
                                "FISTA + GAP every 10 to gap<=1e-6*P(x), lambda_b = 0.25 lambda_max_b",
-                   "parallelism": f"replicas x{world}; {args.concurrency or 4} concurrent sub-grid solves per GPU",
+                   "parallelism": f"replicas x{world}; per GPU: lockstep batched engine (DMMA contractions over "
+                                  f"all signals) then thread-block clusters of {-args.concurrency or 2} CTAs",
                    "l2_policy": "A = 33.5 MB, L2-resident"},
-        "timing": "host wall clock per batch bracketed by device synchronisation (solves run on concurrent streams)",
+        "timing": "CUDA events around the whole batched call on its stream (lockstep + cluster launches), "
+                  "Y resident in HBM",
+        "wall_s_device_loop": wall,
         "signals_per_s": world * B / per_batch, "iters_per_s": its_total / (per_batch * args.steps),
         "e2e": {"value": e2e_s, "unit": "s", "h2d_bytes_per_step": int(sum(r.h2d_bytes for r in e2e_last)),
                 "d2h_bytes_per_step": int(sum(r.d2h_bytes for r in e2e_last))},
         "gpu_launches": int(launches),
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": None, "peak_source": peak_src, "algorithmic_bytes_per_launch": alg / B,
-                     "kernel": "fl1::engine_kernel (one sub-grid launch per signal)",
-                     "note": "A is L2-resident, so the algorithmic bytes are served from L2"},
+        "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak_t, "unit": "TFLOP/s",
+                     "frac": achieved / peak_t, "traffic": None, "peak_source": peak_src_t,
+                     "algorithmic_flops_per_launch": flops,
+                     "kernel": "fl1::prefix_kernel (lockstep batched engine, DMMA m8n8k4) + fl1::engine_kernel",
+                     "note": "algorithmic FLOPs = 2 N K per signal-iteration (SURVEY 8d); the lockstep also runs "
+                             "the restricted power iterations as contractions, not counted"},
         "clocks": clk.summary(),
         "cpu_baseline": cpu,
     }
     print(json.dumps(line))
     if dist:
         dist.destroy_process_group()
+
+
+def _fp64_peak():
+    """fp64 DMMA peak measured on B200 by tools/dmma_peak.cu (profiles/r01_dmma_peak.txt)."""
+    f = ROOT / "profiles" / "r01_dmma_peak.txt"
+    try:
+        vals = [float(l.split()[-2]) for l in f.read_text().splitlines() if l.startswith("DMMA")]
+        return max(vals), "measured (tools/dmma_peak.cu, profiles/r01_dmma_peak.txt)"
+    except Exception:
+        return 40.0, "nominal B200 fp64 tensor (40 TFLOP/s)"
 
 
 def cpu_baseline_batched(a, Y, lams, L, sample: int = 64) -> dict:

@@ -135,6 +135,8 @@ typedef struct fl1_result_info {
   int64_t power_iterations; /* total power-iteration steps (all L estimates) */
   int64_t h2d_bytes;        /* host->device bytes moved by this solve */
   int64_t d2h_bytes;        /* device->host bytes moved by this solve */
+  double batch_device_ms;   /* batched solves: device time of the whole batch (every launch,
+                               CUDA events on the batch stream); single solves: device_ms */
 } fl1_result_info;
 
 /* ---- errors ---- */

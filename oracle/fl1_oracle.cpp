@@ -1064,6 +1064,7 @@ int orc_result_info_get(const orc_result* r, fl1_result_info* o) {
   o->n_switches = static_cast<int64_t>(r->r.switches.size());
   o->n_final_active = static_cast<int64_t>(r->r.final_active.size());
   o->device_ms = r->r.run_ms;
+  o->batch_device_ms = r->r.run_ms;
   o->setup_ms = r->r.setup_ms;
   o->kernel_launches = 0;
   o->power_iterations = r->r.power_steps;

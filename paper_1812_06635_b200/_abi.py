@@ -100,6 +100,7 @@ class ResultInfoC(C.Structure):
         ("power_iterations", C.c_int64),
         ("h2d_bytes", C.c_int64),
         ("d2h_bytes", C.c_int64),
+        ("batch_device_ms", C.c_double),
     ]
 
 

@@ -31,6 +31,9 @@ size_t engine_smem_bytes(int64_t ld, int64_t sukro_m);
 int64_t engine_scratch_len(int64_t ld, int64_t sukro_m);
 cudaError_t engine_configure(int64_t ld, int64_t sukro_m, int device, int* grid_out);
 cudaError_t engine_launch(const EngineParams& p, int64_t sukro_m, cudaStream_t stream);
+size_t prefix_smem_bytes(int64_t ld, int64_t batch);
+cudaError_t prefix_launch(const PrefixParams& p, int device, cudaStream_t stream);
+int prefix_split_max();
 cudaError_t engine_cluster_capacity(int64_t ld, int64_t sukro_m, int csize, int* n_clusters);
 cudaError_t engine_launch_clusters(const EngineParams& p0, int n_clusters, int csize, int64_t sukro_m,
                                    cudaStream_t stream);
@@ -161,6 +164,17 @@ struct fl1_ctx {
 
   std::unique_ptr<Workspace> acquire(int64_t n, int64_t k, int64_t trace_cap, int64_t sk_elems, int64_t sk_m,
                                      int grid_cap = 0);
+  // device scratch of the batched entry, kept between calls (one batched call at a time)
+  std::mutex batch_mu;
+  std::unique_ptr<DevBuf> batch_buf[2];
+  DevBuf& batch_scratch(int slot, size_t bytes) {
+    auto& b = batch_buf[slot];
+    if (!b || b->bytes < bytes) {
+      b.reset();
+      b = std::make_unique<DevBuf>(bytes + bytes / 8);
+    }
+    return *b;
+  }
   void release(std::unique_ptr<Workspace> w) {
     std::lock_guard<std::mutex> g(mu);
     if (pool.size() < 64) pool.push_back(std::move(w));
@@ -234,7 +248,7 @@ struct fl1_result {
   std::vector<fl1_switch_event> switches;
   std::vector<int32_t> final_active;
   bool gap_warning = false;
-  double device_ms = 0.0, setup_ms = 0.0;
+  double device_ms = 0.0, setup_ms = 0.0, batch_ms = -1.0;
   int64_t launches = 0, power_steps = 0;
   double prof[12] = {0};
   int64_t h2d = 0, d2h = 0;
@@ -1013,8 +1027,8 @@ void solve_clusters(fl1_seq* s, const double* Y, bool y_device, int64_t ldy, con
   const size_t o_off = region(sizeof(int64_t) * ub);
   const size_t o_idx = region(sizeof(int32_t) * kb * ub);
   const size_t o_x = region(sizeof(double) * kb * ub);
-  DevBuf mem(top + 256);
-  char* base = mem.as<char>();
+  std::lock_guard<std::mutex> batch_lock(ctx->batch_mu);
+  char* base = ctx->batch_scratch(0, top + 256).as<char>();
   cudaStream_t stream = nullptr;
   ck(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking), "stream");
   struct StreamGuard {
@@ -1087,7 +1101,96 @@ void solve_clusters(fl1_seq* s, const double* Y, bool y_device, int64_t ldy, con
        "signal upload");
     h2d_sig += 8 * n;
   }
+  // lockstep engine (batched.cu): dense exact dictionary, GAP rule, cached full L
+  std::unique_ptr<DevBuf> step_log;
+  int32_t* d_steps = nullptr;
+  const ApproxImpl& ex = *s->lv.back();
+  const char* pe = std::getenv("FL1_BATCH_PREFIX");
+  const bool use_prefix = batch > 0 && pl.levels == 1 && ex.dict->kind == fl1::kDense &&
+                          opts->rule == FL1_RULE_GAP &&
+                          (opts->variant == FL1_SCREENED || opts->variant == FL1_PLAIN) &&
+                          opts->full_lipschitz != nullptr && !(pe && pe[0] == '0');
+  if (use_prefix) {
+    const int64_t bcap = (B + 63) / 64 * 64, kt = (k + 63) / 64;
+    size_t ptop = 0;
+    auto preg = [&](size_t bytes) {
+      ptop = (ptop + 255) / 256 * 256;
+      const size_t o = ptop;
+      ptop += bytes;
+      return o;
+    };
+    const size_t kb8 = sizeof(double) * static_cast<size_t>(k) * ub, lb8 = sizeof(double) * static_cast<size_t>(ld) * ub;
+    const size_t sm = static_cast<size_t>(fl1::prefix_split_max());
+    const size_t q_x0 = preg(kb8), q_x1 = preg(kb8), q_x2 = preg(kb8), q_u0 = preg(lb8), q_u1 = preg(lb8);
+    const size_t q_mk = preg(static_cast<size_t>(k) * ub), q_ld = preg(kb8), q_ps = preg(kb8), q_vp = preg(kb8);
+    const size_t q_hi = preg(sizeof(int32_t) * static_cast<size_t>(k) * ub);
+    const size_t q_r = preg(sizeof(double) * static_cast<size_t>(ld * bcap));
+    const size_t q_np = preg(sizeof(double) * static_cast<size_t>(ld * bcap) * sm);
+    const size_t q_c = preg(sizeof(double) * static_cast<size_t>(k * bcap) * sm);
+    const size_t q_s = preg(sizeof(fl1::PrefixSig) * ub), q_h = preg(sizeof(fl1::Handoff) * ub);
+    const size_t q_n = preg(sizeof(int32_t));
+    (void)kt;
+    char* pb = ctx->batch_scratch(1, ptop + 256).as<char>();
+    fl1::PrefixParams pp{};
+    pp.n = n;
+    pp.k = k;
+    pp.ld = ld;
+    pp.batch = batch;
+    pp.bcap = static_cast<int32_t>(bcap);
+    pp.a = ex.dict->a->as<double>();
+    pp.en = ex.d_en->as<double>();
+    pp.gauss0 = ctx->gauss0(k);
+    pp.y = bd.Y;
+    pp.ldy = bd.ldy;
+    pp.lambdas = bd.lambdas;
+    pp.lipschitz = opts->full_lipschitz[pl.levels - 1];
+    pp.tol = cfg->tolerance;
+    pp.rel_tol = cfg->rel_tolerance;
+    pp.max_it = cfg->max_iterations;
+    pp.interval = cfg->screening_interval;
+    pp.solver = opts->solver;
+    pp.variant = opts->variant;
+    pp.collect_trace = opts->collect_trace ? 1 : 0;
+    // default: signals stay in the lockstep through their first (cold) restricted power
+    // iteration — the dense part of the solve — and the per-signal engine finishes the
+    // short, small-set tail (measured best on B200; 0 and 1 are the other policies)
+    pp.policy = 2;
+    if (const char* pol = std::getenv("FL1_LOCKSTEP_POLICY")) pp.policy = std::atoi(pol);
+    pp.X3[0] = reinterpret_cast<double*>(pb + q_x0);
+    pp.X3[1] = reinterpret_cast<double*>(pb + q_x1);
+    pp.X3[2] = reinterpret_cast<double*>(pb + q_x2);
+    pp.U2[0] = reinterpret_cast<double*>(pb + q_u0);
+    pp.U2[1] = reinterpret_cast<double*>(pb + q_u1);
+    pp.mask = reinterpret_cast<int8_t*>(pb + q_mk);
+    pp.lead = reinterpret_cast<double*>(pb + q_ld);
+    pp.psrc = reinterpret_cast<double*>(pb + q_ps);
+    pp.vp = reinterpret_cast<double*>(pb + q_vp);
+    pp.hidx = reinterpret_cast<int32_t*>(pb + q_hi);
+    pp.R = reinterpret_cast<double*>(pb + q_r);
+    pp.np = reinterpret_cast<double*>(pb + q_np);
+    pp.corr = reinterpret_cast<double*>(pb + q_c);
+    pp.sig = reinterpret_cast<fl1::PrefixSig*>(pb + q_s);
+    pp.hand = reinterpret_cast<fl1::Handoff*>(pb + q_h);
+    pp.states = bd.states;
+    pp.out_used = bd.out_used;
+    pp.out_off = bd.out_off;
+    pp.out_idx = bd.out_idx;
+    pp.out_x = bd.out_x;
+    pp.traces = bd.traces;
+    pp.trace_cap = cap;
+    pp.steps_out = reinterpret_cast<int32_t*>(pb + q_n);
+    if (std::getenv("FL1_STEP_LOG")) {  // diagnostics: per-step occupancy of the lockstep engine
+      pp.max_log = 4096;
+      step_log = std::make_unique<DevBuf>(sizeof(double) * 3 * pp.max_log);
+      pp.step_log = step_log->as<double>();
+    }
+    bd.handoff = pp.hand;
+    ck(cudaMemcpyAsync(base + o_desc, &bd, sizeof(bd), cudaMemcpyHostToDevice, stream), "desc upload");
+    d_steps = pp.steps_out;
+    ck(fl1::prefix_launch(pp, ctx->device, stream), "prefix launch");
+  }
   if (batch > 0) ck(fl1::engine_launch_clusters(p0, n_clusters, csize, pl.sk_m, stream), "cluster launch");
+  ck(cudaEventRecord(ev1, stream), "event");
   ck(cudaMemcpyAsync(hst.data(), base + o_st, sizeof(EngineState) * batch, cudaMemcpyDeviceToHost, stream),
      "state download");
   int64_t used = 0;
@@ -1115,8 +1218,19 @@ void solve_clusters(fl1_seq* s, const double* Y, bool y_device, int64_t ldy, con
                          sizeof(fl1_trace_row) * rows, cudaMemcpyDeviceToHost, stream),
          "trace download");
   }
-  ck(cudaEventRecord(ev1, stream), "event");
   ck(cudaStreamSynchronize(stream), "download sync");
+  float batch_ms = 0.f;
+  ck(cudaEventElapsedTime(&batch_ms, ev0, ev1), "elapsed");
+  if (step_log && d_steps) {
+    int32_t steps = 0;
+    ck(cudaMemcpy(&steps, d_steps, sizeof(steps), cudaMemcpyDeviceToHost), "steps");
+    std::vector<double> lg(3 * static_cast<size_t>(std::min(steps, 4096)));
+    if (!lg.empty()) ck(cudaMemcpy(lg.data(), step_log->p, lg.size() * sizeof(double), cudaMemcpyDeviceToHost), "log");
+    if (FILE* f = std::fopen(std::getenv("FL1_STEP_LOG"), "w")) {
+      for (size_t i = 0; i + 2 < lg.size(); i += 3) std::fprintf(f, "%g %g %g\n", lg[i], lg[i + 1], lg[i + 2]);
+      std::fclose(f);
+    }
+  }
   for (int32_t b = 0; b < batch; ++b) {
     const EngineState& st = hst[static_cast<size_t>(b)];
     if (!st.done) throw std::runtime_error("batched solve did not finish");
@@ -1128,8 +1242,9 @@ void solve_clusters(fl1_seq* s, const double* Y, bool y_device, int64_t ldy, con
                 std::vector<fl1_switch_event>(sb, sb + st.n_switches));
     res->trace = std::move(traces[static_cast<size_t>(b)]);
     res->device_ms = (st.end_ns - st.start_ns) * 1e-6;
+    res->batch_ms = batch_ms;
     res->launches = 0;  // one launch for the whole batch (fl1_result_info.kernel_launches of signal 0 = 1)
-    if (b == 0) res->launches = 1;
+    if (b == 0) res->launches = use_prefix ? 2 : 1;
     res->h2d = h2d_sig;
     res->d2h = static_cast<int64_t>(sizeof(EngineState)) + 12 * st.S +
                st.n_switches * static_cast<int64_t>(sizeof(fl1_switch_event)) +
@@ -1232,6 +1347,7 @@ int fl1_result_info_get(const fl1_result* r, fl1_result_info* o) {
     o->power_iterations = r->power_steps;
     o->h2d_bytes = r->h2d;
     o->d2h_bytes = r->d2h;
+    o->batch_device_ms = r->batch_ms >= 0.0 ? r->batch_ms : r->device_ms;
   });
 }
 int fl1_result_x(const fl1_result* r, double* out) {

@@ -1285,34 +1285,65 @@ __device__ __noinline__ void engine_body(const EngineParams& p, Sh& sh, double* 
       }
     }
     Bank bk = p.bank[0];
+    const Handoff* hd = p.handoff;  // resume from the batched lockstep engine
+    const int64_t S0 = hd ? hd->S : k;
     int64_t lo, hi;
-    slice(k, lo, hi);
+    slice(S0, lo, hi);
     for (int64_t q = lo + threadIdx.x; q < hi; q += kThreads) {
-      bk.idx[q] = static_cast<int32_t>(q);
-      bk.x[q] = p.has_x_init ? p.x_init[q] : 0.0;
-      bk.xp[q] = 0.0;
+      bk.idx[q] = hd ? __ldcg(hd->idx + q) : static_cast<int32_t>(q);
+      bk.x[q] = hd ? __ldcg(hd->x + q) : (p.has_x_init ? p.x_init[q] : 0.0);
+      bk.xp[q] = hd ? __ldcg(hd->xp + q) : 0.0;
+      if (hd && hd->lead_valid) bk.lead[q] = __ldcg(hd->lead + q);
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-      s.S = k;
+      s.S = S0;
       s.cur = 0;
     }
     __syncthreads();
-    gather_metadata(p, sh, p.lv[s.dict_index], bk, k);
+    gather_metadata(p, sh, p.lv[s.dict_index], bk, S0);
     {  // ||x_0||_1 for iteration 0
       double acc = 0.0;
-      for (int64_t q = lo + threadIdx.x; q < hi; q += kThreads) acc += p.has_x_init ? fabs(p.x_init[q]) : 0.0;
+      for (int64_t q = lo + threadIdx.x; q < hi; q += kThreads) acc += fabs(bk.x[q]);
       double v[1] = {acc};
       const bool mx[1] = {false};
       block_reduce<1>(v, mx, sh);
-      if (threadIdx.x == 0) put_slot(p, l1_slot(0), v[0]);
+      if (threadIdx.x == 0) put_slot(p, l1_slot(hd ? hd->t : 0), v[0]);
     }
     vsync();
     grid_reduce(p, sh, 0u, 1u << kSlMaxEps);
     if (threadIdx.x == 0) s.max_eps = sh.res[kSlMaxEps];
     __syncthreads();
-    setup_dictionary(p, sh, true, sc);
-    if (threadIdx.x == 0) s.t0_ns = globaltimer_ns();
+    if (!hd) {
+      setup_dictionary(p, sh, true, sc);
+    } else {
+      // the lockstep engine ran iterations 0..t-1 (setup_dictionary 311-323 there):
+      // continue its FISTA state, Lipschitz estimate, leading vector, ledger and trace
+      if (threadIdx.x == 0) {
+        s.lipschitz = hd->lipschitz;
+        s.inv_l = 1.0 / s.lipschitz;
+        s.active_at_last_l = hd->active_at_last_l;
+        s.lead_valid = hd->lead_valid;
+        s.power_steps = hd->power_steps;
+        s.t = hd->t;
+        s.t_k = hd->t_k;
+        s.momentum_ready = hd->ready;
+        s.ledger = hd->ledger;
+        s.warning = hd->warning;
+        s.n_trace = hd->n_trace;
+      }
+      int64_t rlo, rhi;
+      slice(ld, rlo, rhi);
+      for (int64_t i = rlo + threadIdx.x; i < rhi; i += kThreads) {
+        __stcg(p.up + i, __ldcg(hd->u + i));  // one partial chunk holding u
+        __stcg(p.V + i, __ldcg(hd->v + i));
+      }
+      __syncthreads();
+      vsync();
+      combine_u(p, sh, 1, false, false, next_momentum(p, hd->t_k, hd->ready != 0));
+      vsync();
+    }
+    if (threadIdx.x == 0) s.t0_ns = globaltimer_ns() - (hd ? hd->elapsed_ns : 0.0);
     __syncthreads();
   }
 
@@ -1833,12 +1864,14 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
     const int b = __ldcg(bd.cluster_sig + cid);
     cl.sync();
     if (b >= bd.batch) break;
+    if (bd.handoff && __ldcg(&bd.handoff[b].state) == 2) continue;  // finished in the lockstep engine
     if (threadIdx.x == 0) {
       sp.mode = kModeSolve;
       sp.lambda = bd.lambdas[b];
       sp.st = bd.states + b;
       sp.trace = bd.traces + static_cast<int64_t>(b) * bd.trace_cap;
       sp.sw = bd.sws + static_cast<int64_t>(b) * kMaxLevels;
+      sp.handoff = (bd.handoff && bd.handoff[b].state == 1) ? bd.handoff + b : nullptr;
     }
     {  // y_b into the workspace (zero padded to ld), by CTA slices
       int64_t lo, hi;

@@ -123,6 +123,90 @@ struct EngineState {
 
 struct EngineParams;
 
+// Batched lockstep engine -> per-signal engine hand-off (batched solves): the state
+// of one signal at the START of iteration t, preserved set compacted in atom order.
+struct Handoff {
+  const int32_t* idx;   // S preserved atoms, ascending
+  const double* x;      // S
+  const double* xp;     // S
+  const double* lead;   // S (valid if lead_valid)
+  const double* u;      // ld
+  const double* v;      // ld
+  uint64_t t;
+  uint64_t ledger;
+  int64_t n_trace;
+  int64_t S;
+  int64_t active_at_last_l;
+  int64_t power_steps;
+  double t_k;
+  double lipschitz;
+  double elapsed_ns;    // device time the lockstep spent on this signal
+  int32_t ready;
+  int32_t warning;
+  int32_t lead_valid;
+  int32_t state;        // 0: not handled, 1: resume from this state, 2: finished in the lockstep
+};
+
+// Per-signal state of the lockstep engine.
+struct PrefixSig {
+  double t_k, x_l1, y_sq, rsq, rdy, ree;
+  double lipschitz, inv_l;
+  double p_est, p_div, p_tol;   // power iteration: estimate, |cur_src|, tolerance
+  uint64_t t, ledger;
+  int64_t n_trace, S, active_at_last_l, power_steps;
+  int32_t ready, warning, lead_valid;
+  int32_t mode;                 // 0: FISTA iteration, 1: power step, 2: finished, 3: handed off
+  int32_t rot;                  // roles of X3: x = X3[rot], x_prev = X3[rot+1], x_next = X3[rot+2] (mod 3)
+  int32_t uswap;                // u = U2[uswap], v = U2[1 - uswap]
+  int32_t p_it, p_max, p_min, p_have_w;
+};
+
+// Lockstep batched engine: B independent solves on one dense exact dictionary (GAP
+// rule, cached full Lipschitz constant). Every global step, each unfinished signal
+// performs its own next unit of Engine::run — one FISTA iteration, or one step of
+// its restricted power iteration — and the dictionary products of all of them are
+// two dense contractions on the fp64 tensor cores: W = A V for the signals in a
+// power step, Corr = A^T [rho | w] for all. Preserved sets are per-signal masks
+// (atom order = the reference's compacted order).
+struct PrefixParams {
+  int64_t n, k, ld;
+  int32_t batch, bcap;        // signals; column capacity of R / corr (multiple of 64)
+  const double* a;            // ld x k, zero-padded rows
+  const double* en;           // exact atom norms
+  const double* gauss0;       // cold power-iteration start (by preserved position)
+  const double* y;            // N x B, leading dimension ldy
+  int64_t ldy;
+  const double* lambdas;
+  double lipschitz;           // cached full-dictionary L
+  double tol, rel_tol;
+  uint64_t max_it;
+  int32_t interval, solver, variant, collect_trace;
+  int32_t policy;             // hand-off: 0 never, 1 at the first shrink, 2 after the first power iteration
+  double* X3[3];              // three k x B iterate buffers (roles rotate, PrefixSig::rot)
+  double* U2[2];              // two ld x B buffers for u and v (PrefixSig::uswap)
+  int8_t* mask;               // k x B preserved-set masks
+  double* lead;               // k x B leading vectors (masked)
+  double* psrc;               // k x B power iteration: cur_src
+  double* vp;                 // k x B power iteration: v = cur_src / |cur_src| (contraction input)
+  int32_t* hidx;              // k x B hand-off: compacted preserved atoms
+  double* R;                  // ld x bcap: contraction input columns (rho or w)
+  double* np;                 // kSplitMax x bcap x ld: W = A V split-K partials
+  double* corr;               // kSplitMax x k x bcap: A^T R split-K partials
+  PrefixSig* sig;             // B
+  Handoff* hand;              // B (out)
+  EngineState* states;        // B final states of signals finished here (host reads them)
+  fl1_switch_event* sws;      // unused (single level)
+  int64_t* out_used;          // packed final sets (shared with the cluster engine)
+  int64_t* out_off;
+  int32_t* out_idx;
+  double* out_x;
+  fl1_trace_row* traces;      // B x trace_cap
+  int64_t trace_cap;
+  int32_t* steps_out;         // global steps executed
+  double* step_log;           // nullable: per step (n_act, n_pow, %globaltimer) x max_log
+  int32_t max_log;
+};
+
 // Batched (cluster) mode: B independent solves of one sequence, one per signal,
 // taken from a queue by thread-block clusters (each cluster = one workspace).
 struct BatchDesc {
@@ -138,6 +222,7 @@ struct BatchDesc {
   int64_t trace_cap;
   fl1_switch_event* sws;                // B x kMaxLevels
   int64_t* out_used;                    // packed-output counter (starts at 0)
+  const Handoff* handoff;               // nullable: B lockstep-prefix states to resume from
   int64_t* out_off;                     // B: offset of each signal's final set
   int32_t* out_idx;                     // packed final preserved sets (capacity B x K)
   double* out_x;                        // iterate on them
@@ -195,6 +280,7 @@ struct alignas(16) EngineParams {
   EngineState* st;
   uint64_t* timeline;  // FL1_TIMELINE builds only: [iter][cta][8] %globaltimer marks
   const BatchDesc* batch;  // non-null: cluster (batched) mode
+  const Handoff* handoff;  // non-null: solve resumes from a lockstep-prefix state
 };
 
 constexpr int kBred = 20;  // doubles of per-CTA partials (slots, see engine.cu)

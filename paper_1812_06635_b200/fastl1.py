@@ -350,6 +350,7 @@ class SolveResult:  # fastl1.hpp:61-71
     profile: Optional[np.ndarray] = None  # product library only: see fl1_result_profile
     h2d_bytes: int = 0
     d2h_bytes: int = 0
+    batch_device_ms: float = 0.0  # batched calls: device time of the whole batch
 
 
 def _collect_result(lib: Library, h) -> SolveResult:
@@ -374,7 +375,8 @@ def _collect_result(lib: Library, h) -> SolveResult:
                        total_flops=int(info.total_flops), trace=trace, switches=sws, final_active=fa,
                        gap_warning=bool(info.gap_warning), device_ms=info.device_ms, setup_ms=info.setup_ms,
                        kernel_launches=int(info.kernel_launches), power_iterations=int(info.power_iterations),
-                       h2d_bytes=int(info.h2d_bytes), d2h_bytes=int(info.d2h_bytes))
+                       h2d_bytes=int(info.h2d_bytes), d2h_bytes=int(info.d2h_bytes),
+                       batch_device_ms=float(info.batch_device_ms))
 
 
 def _run_options_c(opts: RunOptions, keep: list) -> _abi.RunOptionsC:

@@ -296,3 +296,58 @@ def test_batched_clusters_device_input(cuda):
         assert np.array_equal(r_host[b].x, r_dev[b].x)
         assert r_dev[b].h2d_bytes < r_host[b].h2d_bytes
     assert F.run_lasso_batched(seq, Y[:, :0], lams[:0], cfg, opts, concurrency=0) == []
+
+
+@pytest.mark.parametrize("variant", [F.VARIANT_SCREENED, F.VARIANT_PLAIN])
+@pytest.mark.parametrize("solver", [F.SOLVER_FISTA, F.SOLVER_ISTA])
+def test_batched_lockstep_prefix(cuda, oracle16, variant, solver):
+    """Batched solves with a cached full Lipschitz constant run in the lockstep
+    engine (every step: DMMA contractions W = A V for power steps, Corr = A^T R for
+    all signals; screening by per-signal masks) and, by the default policy, move to
+    the per-signal engine after their first restricted power iteration: every signal
+    still equals its own oracle solve, trace and ledger included. Ragged shapes: K
+    not a multiple of the atom tile, B not a multiple of 64."""
+    rng = np.random.default_rng(17)
+    n, k, B = 230, 1000, 70
+    a = syn.gaussian_dictionary(rng, n, k)
+    Y = np.empty((n, B), order="F")
+    for b in range(B):
+        Y[:, b] = syn.observe(rng, a @ syn.sparse_signal(rng, k, 6 + b % 7), None, 30.0)
+    lams = (0.2 + 0.1 * (np.arange(B) % 3)) * np.max(np.abs(a.T @ Y), axis=0)
+    L = F.lipschitz_bound(F.DenseDictionary(a, backend=cuda))
+    cfg = F.SwitchConfig(screening_interval=10, max_iterations=3000, rel_tolerance=1e-6)
+    opts = F.RunOptions(solver=solver, variant=variant, full_lipschitz=[L], collect_trace=True)
+    seq_g = F.ApproxSequence([F.make_exact_approx(F.DenseDictionary(a, backend=cuda))])
+    seq_o = F.ApproxSequence([F.make_exact_approx(F.DenseDictionary(a, backend=oracle16))])
+    res = F.run_lasso_batched(seq_g, Y, lams, cfg, opts, concurrency=-2)
+    assert res[0].kernel_launches == 2  # prefix + cluster engine
+    for b in range(0, B, 3 if variant == F.VARIANT_PLAIN else 1):
+        o = F.run_lasso(seq_o, Y[:, b], lams[b], cfg, opts)
+        assert_parity(res[b], o, a, Y[:, b], lams[b])
+        assert len(res[b].trace) == len(o.trace)
+
+
+@pytest.mark.parametrize("policy", ["0", "1", "2"])
+def test_batched_prefix_matches_engine_only(cuda, monkeypatch, policy):
+    """The lockstep engine changes only the route, not the answer, under every
+    hand-off policy (0: never, 1: at the first shrink, 2: after the first power
+    iteration): same supports, iteration counts and ledgers as the engine-only path."""
+    monkeypatch.setenv("FL1_LOCKSTEP_POLICY", policy)
+    rng = np.random.default_rng(23)
+    n, k, B = 128, 512, 20
+    a = syn.gaussian_dictionary(rng, n, k)
+    Y = np.empty((n, B), order="F")
+    for b in range(B):
+        Y[:, b] = syn.observe(rng, a @ syn.sparse_signal(rng, k, 5), None, 30.0)
+    lams = 0.25 * np.max(np.abs(a.T @ Y), axis=0)
+    L = F.lipschitz_bound(F.DenseDictionary(a, backend=cuda))
+    seq = F.ApproxSequence([F.make_exact_approx(F.DenseDictionary(a, backend=cuda))])
+    cfg = F.SwitchConfig(screening_interval=10, max_iterations=5000, rel_tolerance=1e-6)
+    opts = F.RunOptions(variant=F.VARIANT_SCREENED, full_lipschitz=[L])
+    r1 = F.run_lasso_batched(seq, Y, lams, cfg, opts, concurrency=0)
+    monkeypatch.setenv("FL1_BATCH_PREFIX", "0")
+    r2 = F.run_lasso_batched(seq, Y, lams, cfg, opts, concurrency=0)
+    for x, y in zip(r1, r2):
+        assert x.iterations == y.iterations and x.total_flops == y.total_flops
+        assert np.array_equal(x.final_active, y.final_active)
+        assert np.max(np.abs(x.x - y.x)) <= 1e-9 * max(1.0, np.max(np.abs(y.x)))
