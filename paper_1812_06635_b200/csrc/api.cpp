@@ -29,6 +29,7 @@
 namespace fl1 {
 size_t engine_smem_bytes(int64_t ld, int64_t sukro_m);
 int64_t engine_scratch_len(int64_t ld, int64_t sukro_m);
+int engine_bulk_stages(int64_t ld);
 cudaError_t engine_configure(int64_t ld, int64_t sukro_m, int device, int* grid_out);
 cudaError_t engine_launch(const EngineParams& p, int64_t sukro_m, cudaStream_t stream);
 size_t prefix_smem_bytes(int64_t ld, int64_t batch);
@@ -297,6 +298,7 @@ size_t carve(EngineParams& p, char* base, int64_t n, int64_t k, int64_t ld, int 
   p.PU = c.take<double>(ld);
   p.sk_z = sk_m > 0 ? c.take<double>(kk) : nullptr;
   p.scratch_len = fl1::engine_scratch_len(ld, sk_m);
+  p.bulk_stages = fl1::engine_bulk_stages(ld);
   p.bred = c.take<double>(static_cast<int64_t>(grid) * fl1::kBred);
   for (int b = 0; b < 2; ++b) {
     fl1::Bank& bk = p.bank[b];

@@ -36,6 +36,7 @@
 #include <cfloat>
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 
 #include "engine.cuh"
 
@@ -96,6 +97,42 @@ constexpr int kSlL1b = 16;
 __shared__ int s_vsize;     // CTAs of the virtual grid
 __shared__ int s_vrank;     // this CTA's rank in it
 __shared__ int s_vcluster;  // 1: cluster mode
+
+// Bulk-copy (TMA 1D) streaming ring of the dense adjoint pass: per warp up to
+// kMaxBulk 4 KiB stages in shared memory, one mbarrier each; phase bits persist
+// across passes (and across solves of a cluster).
+constexpr int kMaxBulk = 6;
+__shared__ __align__(8) uint64_t s_bar[FL1_THREADS / 32 * kMaxBulk];
+__shared__ uint32_t s_bphase[FL1_THREADS / 32];
+__device__ __forceinline__ uint32_t smem_u32(const void* ptr) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(ptr));
+}
+__device__ __forceinline__ void bulk_init_barriers() {
+  if ((threadIdx.x & 31) == 0) {
+    const int w = threadIdx.x >> 5;
+    for (int s = 0; s < kMaxBulk; ++s)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&s_bar[w * kMaxBulk + s])));
+    s_bphase[w] = 0u;
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+}
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void bulk_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t ok = 0;
+  while (!ok) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  }
+}
 __device__ __forceinline__ int vsize() { return s_vsize; }
 __device__ __forceinline__ int vrank() { return s_vrank; }
 __device__ __forceinline__ void vsync() {
@@ -352,7 +389,8 @@ __device__ void finish_pass(const EngineParams& p, Sh& sh, const PassOut& po, Pa
 // ----------------------------------------------------------------------------
 __device__ __noinline__ void dense_adjoint(const EngineParams& p, Sh& sh, const DevLevel& lv,
                                            const int32_t* __restrict__ idx, const double* __restrict__ eps, int64_t S,
-                                           const double* __restrict__ r, const PassOut& po) {
+                                           const double* __restrict__ r, double* __restrict__ ring,
+                                           const PassOut& po) {
   const int64_t n = p.n;
   const int U = static_cast<int>((n + kUnit - 1) / kUnit);
   const int last_nd2 = static_cast<int>(((n - static_cast<int64_t>(U - 1) * kUnit) + 1) >> 1);
@@ -455,7 +493,47 @@ __device__ __noinline__ void dense_adjoint(const EngineParams& p, Sh& sh, const 
       ++cc;                                                                                           \
     }                                                                                                 \
   } while (0)
-  if (u_lo < u_hi) {
+  if (u_lo < u_hi && p.bulk_stages >= 2) {
+    // bulk-copy ring: lane 0 streams whole units into shared memory (one mbarrier per
+    // stage), so R units per warp are in flight instead of two register units
+    const int R = p.bulk_stages;
+    double2* wring = reinterpret_cast<double2*>(ring) + static_cast<int64_t>(w) * R * (kUnit / 2);
+    uint64_t* bars = &s_bar[w * kMaxBulk];
+    uint32_t ph = s_bphase[w];
+    const double* __restrict__ A = lv.a;
+    auto bulk_issue = [&](int st) {
+      if (l == 0) {
+        const double* src = A + static_cast<int64_t>(__ldg(idx + c0 + ic)) * p.ld + static_cast<int64_t>(ih) * kUnit;
+        const uint32_t bytes =
+            static_cast<uint32_t>(((ih == U - 1) ? (p.ld - static_cast<int64_t>(ih) * kUnit) : kUnit) * 8);
+        bulk_load(wring + st * (kUnit / 2), src, bytes, bars + st);
+      }
+      if (++ih == U) {
+        ih = 0;
+        ++ic;
+      }
+    };
+    int iu = u_lo;
+    for (int st = 0; st < R && iu < u_hi; ++st, ++iu) bulk_issue(st);
+    int st = 0;
+    for (int u = u_lo; u < u_hi; ++u) {
+      bulk_wait(bars + st, (ph >> st) & 1u);
+      ph ^= 1u << st;
+      double2 b0[kV];
+      const double2* sp = wring + st * (kUnit / 2) + l;
+      const int lim = (ch == U - 1 ? last_nd2 : kUnit / 2) - l;
+#pragma unroll
+      for (int q = 0; q < kV; ++q) b0[q] = (32 * q < lim) ? sp[32 * q] : make_double2(0.0, 0.0);
+      __syncwarp();
+      if (iu < u_hi) {
+        bulk_issue(st);
+        ++iu;
+      }
+      FL1_CONSUME(b0, u);
+      if (++st == R) st = 0;
+    }
+    if (l == 0) s_bphase[w] = ph;
+  } else if (u_lo < u_hi) {
 #if FL1_RING == 3
     double2 b0[kV], b1[kV], b2[kV];
     FL1_ISSUE(b0);
@@ -640,7 +718,7 @@ __device__ __noinline__ void sukro_adjoint(const EngineParams& p, Sh& sh, const 
 __device__ void op_adjoint(const EngineParams& p, Sh& sh, const DevLevel& lv, const int32_t* idx, const double* eps,
                            int64_t S, const double* r, double* scratch, const PassOut& po) {
   if (lv.kind == kDense)
-    dense_adjoint(p, sh, lv, idx, eps, S, r, po);
+    dense_adjoint(p, sh, lv, idx, eps, S, r, scratch, po);
   else
     sukro_adjoint(p, sh, lv, idx, eps, S, r, scratch, po);
 }
@@ -1836,6 +1914,7 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
     int4* b = reinterpret_cast<int4*>(&sp);
     for (int i = threadIdx.x; i < static_cast<int>(sizeof(EngineParams) / sizeof(int4)); i += kThreads) b[i] = a[i];
   };
+  bulk_init_barriers();
   if (p0.batch == nullptr) {
     if (threadIdx.x == 0) {
       s_vsize = gridDim.x;
@@ -1930,8 +2009,23 @@ cudaError_t screen_kernel_launch(int64_t n, const double* dots, const double* ep
 
 // Shared scratch after the resident residual: dense apply warp partials, or the
 // SuKro staging (adjoint tiles; apply entry list + 64-column Cg / Bg chunks).
+// Bulk-copy ring stages per warp for a residual of ld doubles (4 KiB each, 8 warps).
+// Off by default: on B200 the register ring already keeps the dense pass at the HBM
+// roofline (measured: 2-4 stages change the c2 pass by < 3%), while the larger
+// shared-memory carve-out shrinks L1 for the other phases. FL1_BULK_STAGES=R enables it.
+int engine_bulk_stages(int64_t ld) {
+  const char* e = std::getenv("FL1_BULK_STAGES");
+  if (!e) return 0;
+  const int64_t room = 200 * 1024 / 8 - ld;  // doubles left beside the resident residual
+  const int64_t fit = std::max<int64_t>(0, std::min<int64_t>(kMaxBulk, room / (kWarps * kUnit)));
+  const int64_t r = std::min<int64_t>(fit, std::atoi(e));
+  return r >= 2 ? static_cast<int>(r) : 0;
+}
+
 int64_t engine_scratch_len(int64_t ld, int64_t sukro_m) {
   int64_t s = static_cast<int64_t>(kWarps) * kUnit;
+  const int R = engine_bulk_stages(ld);
+  if (R >= 2) s = std::max<int64_t>(s, static_cast<int64_t>(R) * kWarps * kUnit);
   if (sukro_m > 0) {
     const int64_t m4 = (sukro_m + 3) / 4 * 4;
     const int64_t term = 16 * m4 + 32 * (m4 + 1);

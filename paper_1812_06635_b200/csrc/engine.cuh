@@ -272,6 +272,7 @@ struct alignas(16) EngineParams {
   const double* gauss0;  // K: mt19937_64(0x11b5c417) normals (solver.cpp:80-82)
   double* sk_z;     // SuKro adjoint: Z = sum_t C_t^T R B_t (K doubles)
   int64_t scratch_len;  // doubles of shared scratch after the residual (engine_scratch_len)
+  int32_t bulk_stages;  // dense adjoint bulk-copy ring depth per warp (0: register ring)
   double* bred;     // per-CTA partials: grid * kBred doubles
   Bank bank[2];
   fl1_trace_row* trace;
