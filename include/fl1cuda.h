@@ -224,6 +224,16 @@ void fl1_result_free(fl1_result* r);
 int fl1_lambda_max(fl1_dict* d, const double* y, double* out);
 /* lipschitz_bound (solver.cpp:108-114): cold power iteration x 1.05 on the GPU. */
 int fl1_lipschitz_bound(fl1_dict* d, double* out);
+
+/* ---- harness generators (host; the reference's own <random> streams) ---- */
+/* count draws of std::normal_distribution<double>(0, 1) on std::mt19937_64(seed): the
+ * stream behind synthesize_scenario (dictionary.cpp:396-409, seed ^ 0xd1c7) and
+ * truncated_svd (dictionary.cpp:258-262, seed 0x5eedf00d). */
+int fl1_rng_normals(uint64_t seed, int64_t count, double* out);
+/* draw_signal (bench.cpp:141-166): Bernoulli(p)-Gaussian x over K atoms from
+ * mt19937_64(mix_seed(seed, trial)), y = A x on the GPU, both scaled so |y| = 1;
+ * draws with an empty support or |y| <= 1e-12 are redrawn. y: N, x: K. */
+int fl1_draw_signal(fl1_dict* d, double bernoulli_p, uint64_t seed, int32_t trial, double* y, double* x);
 /* screen_precomputed (screening.cpp:136-150) as a device kernel; kept gets positions. */
 int fl1_screen_precomputed(fl1_ctx* ctx, int64_t n, const double* abs_dots, const double* eps,
                            const double* exact_norms, const double* approx_norms,

@@ -164,6 +164,8 @@ PRODUCT_ONLY = {
     "solve_batched_device": (C.c_int, [_P, C.c_void_p, C.c_int64, _PD, C.c_int32, C.POINTER(SwitchConfigC),
                                        C.POINTER(RunOptionsC), C.c_int32, _PP]),
     "solve_device": (C.c_int, [_P, C.c_void_p, C.c_double, C.POINTER(SwitchConfigC), C.POINTER(RunOptionsC), _PP]),
+    "rng_normals": (C.c_int, [C.c_uint64, C.c_int64, _PD]),
+    "draw_signal": (C.c_int, [_P, C.c_double, C.c_uint64, C.c_int32, _PD, _PD]),
 }
 
 # oracle-only entry points (test infrastructure)

@@ -1378,6 +1378,51 @@ int fl1_lambda_max(fl1_dict* d, const double* y, double* out) {  // screening.cp
     *out = m;
   });
 }
+int fl1_rng_normals(uint64_t seed, int64_t count, double* out) {
+  return guard([&] {
+    if (count < 0 || (count > 0 && !out)) throw std::invalid_argument("bad output");
+    std::mt19937_64 rng(seed);
+    std::normal_distribution<double> gauss(0.0, 1.0);
+    for (int64_t i = 0; i < count; ++i) out[i] = gauss(rng);
+  });
+}
+
+int fl1_draw_signal(fl1_dict* dh, double p, uint64_t seed, int32_t trial, double* y, double* x) {  // bench.cpp:141-166
+  return guard([&] {
+    if (!dh || !y || !x) throw std::invalid_argument("null argument");
+    if (!(p > 0.0 && p <= 1.0)) throw std::invalid_argument("bernoulli-p must lie in (0, 1]");
+    DictImpl& d = *dh->d;
+    uint64_t z = seed + 0x9e3779b97f4a7c15ULL * (static_cast<uint64_t>(trial) + 1);  // mix_seed (bench.cpp:45-50)
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+    std::mt19937_64 rng(z ^ (z >> 31));
+    std::bernoulli_distribution coin(p);
+    std::normal_distribution<double> gauss(0.0, 1.0);
+    std::vector<double> yy(static_cast<size_t>(d.n));
+    for (int attempt = 0;; ++attempt) {
+      if (attempt > 100000) throw std::runtime_error("signal draw kept failing");
+      std::fill(x, x + d.k, 0.0);
+      bool any = false;
+      for (int64_t j = 0; j < d.k; ++j) {
+        if (coin(rng)) {
+          x[j] = gauss(rng);
+          any = true;
+        }
+      }
+      if (!any) continue;
+      std::vector<double> out(static_cast<size_t>(even_ld(d.n)), 0.0);
+      run_utility(d, fl1::kModeApply, x, out.data(), static_cast<size_t>(d.n));
+      double nrm = 0.0;
+      for (int64_t i = 0; i < d.n; ++i) nrm += out[static_cast<size_t>(i)] * out[static_cast<size_t>(i)];
+      nrm = std::sqrt(nrm);
+      if (nrm <= 1e-12) continue;
+      for (int64_t j = 0; j < d.k; ++j) x[j] /= nrm;
+      for (int64_t i = 0; i < d.n; ++i) y[i] = out[static_cast<size_t>(i)] / nrm;
+      return;
+    }
+  });
+}
+
 int fl1_lipschitz_bound(fl1_dict* d, double* out) {  // solver.cpp:108-114
   return guard([&] {
     const EngineState st = run_utility(*d->d, fl1::kModePower, nullptr, nullptr, 0);

@@ -1,0 +1,268 @@
+"""The reference's experiment harness over the CUDA solver (paper_1812_06635_b200/
+harness.py): ports of test_bench.cpp plus format / stream / SuKro-construction
+parity checks. CPU tests need only the library's host code; -m gpu tests solve."""
+from __future__ import annotations
+
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+from paper_1812_06635_b200 import fastl1 as F, harness as H
+
+from _refgen import RefGen
+
+
+def small_config(tmp=None) -> H.ExperimentConfig:  # test_bench.cpp:15-28
+    return H.ExperimentConfig(n=36, k=100, scenario="moderate", lambda_ratios=[0.3], tol=1e-6, ranks=[1, 3],
+                              trials=2, seed=11, out="" if tmp is None else str(tmp), use_gram=False)
+
+
+# ---------------------------------------------------------------- host-only
+def test_rng_stream_is_the_reference_stream(oracle):
+    rg = RefGen(oracle)
+    for seed in (0, 11 ^ 0xD1C7, 0x5EEDF00D):
+        assert np.array_equal(H.rng_normals(seed, 1000), rg.normals(seed, 1000))
+
+
+def test_config_validation():  # test_bench.cpp:39-54
+    cfg = small_config()
+    cfg.validate()
+    for field, value in (("bernoulli_p", 0.0), ("lambda_ratios", [1.5]), ("gamma", 1.0), ("trials", 0),
+                         ("jobs", 0), ("screen_interval", 0), ("ranks", []), ("tol", 0.0)):
+        c = small_config()
+        setattr(c, field, value)
+        with pytest.raises(F.InvalidArgument):
+            c.validate()
+    c = small_config()
+    c.lambda_ratios, c.lambda_grid = [], 0
+    with pytest.raises(F.InvalidArgument):
+        c.validate()
+    c = small_config()
+    c.rc_override = [0.1]
+    with pytest.raises(F.InvalidArgument):
+        c.validate()
+
+
+def test_lambda_grid_log_spaced():  # test_bench.cpp:56-67
+    cfg = small_config()
+    cfg.lambda_ratios, cfg.lambda_grid = [], 5
+    g = cfg.resolved_lambda_ratios()
+    assert len(g) == 5 and abs(g[0] - 1e-2) < 1e-15 and g[-1] == 1.0
+    for i in range(1, len(g)):
+        assert abs(g[i] / g[i - 1] - g[1] / g[0]) <= 1e-12 * g[1] / g[0]
+    cfg.lambda_grid = 1
+    assert cfg.resolved_lambda_ratios() == [0.1]
+
+
+def test_gamma_defaults():  # test_bench.cpp:69-78
+    assert H.default_gamma("hard") == 0.5 and H.default_gamma("moderate") == 0.25 and H.default_gamma("easy") == 0.2
+    cfg = small_config()
+    cfg.scenario = "easy"
+    assert cfg.resolved_gamma() == 0.2
+    cfg.gamma = 0.33
+    assert cfg.resolved_gamma() == 0.33
+
+
+def test_config_json(tmp_path):  # test_bench.cpp:272-291
+    p = tmp_path / "cfg.json"
+    p.write_text('{"n": 36, "k": 100, "scenario": "easy", "lambda_ratio": 0.4, "tol": 1e-5, "ranks": [2, 5], '
+                 '"trials": 3, "seed": 9, "solver": "ista", "rule": "dynamic"}')
+    cfg = H.load_config_json(str(p))
+    assert (cfg.n, cfg.k, cfg.scenario, cfg.lambda_ratios, cfg.trials) == (36, 100, "easy", [0.4], 3)
+    assert cfg.solver == F.SOLVER_ISTA and cfg.rule == F.RULE_DYNAMIC and cfg.ranks == [2, 5] and cfg.seed == 9
+    cfg.validate()
+    p.write_text('{"rule": "gap_safe"}')
+    with pytest.raises(F.InvalidArgument):
+        H.load_config_json(str(p))
+    p.write_text("{not json")
+    with pytest.raises(F.InvalidArgument):
+        H.load_config_json(str(p))
+    with pytest.raises(F.InvalidArgument):
+        H.load_config_json(str(tmp_path / "missing.json"))
+
+
+def test_percentile_oracle():  # test_bench.cpp:221-227
+    assert H.percentile([1.0, 2.0, 3.0, 4.0], 0.5) == pytest.approx(2.5)
+    assert H.percentile([5.0], 0.25) == 5.0
+    assert H.percentile([1.0, 2.0, 3.0, 4.0, 5.0], 0.25) == pytest.approx(2.0)
+    assert H.percentile([4.0, 1.0, 3.0, 2.0], 0.0) == 1.0
+    assert H.percentile([4.0, 1.0, 3.0, 2.0], 1.0) == 4.0
+    assert math.isnan(H.percentile([], 0.5))
+
+
+def _record(run_id, trial, ratio, variant, rows):
+    tr = np.zeros(len(rows), dtype=F.TRACE_DTYPE)
+    for i, (it, d, a, gap, gamma, fl, wall, nnz) in enumerate(rows):
+        tr[i] = (it, d, a, gap, gamma, fl, wall, nnz, 0)
+    return H.RunRecord(run_id=run_id, trial=trial, lambda_ratio=ratio, variant=variant, iterations=len(rows),
+                       flops=rows[-1][5], wall_ms=rows[-1][6], converged=True, final_gap=0.0, trace=tr)
+
+
+def test_csv_formats(tmp_path):
+    """Headers, %.17g / %.3f formatting and column order of bench.cpp:336-414."""
+    runs = [_record(0, 1, 0.3, F.VARIANT_PLAIN, [(0, 0, 100, 0.5, -1.0, 1234, 0.0123456, 7)]),
+            _record(1, 1, 0.3, F.VARIANT_SCREENED, [(0, 1, 90, -1.0, 0.25, 1000, 1.5, 6)]),
+            _record(2, 1, 0.3, F.VARIANT_MULTI_DICT, [(0, 2, 80, 1e-7, 0.1, 500, 2.25, 5)])]
+    H.write_trace_csv(str(tmp_path / "trace.csv"), runs)
+    lines = (tmp_path / "trace.csv").read_text().splitlines()
+    assert lines[0] == "run_id,trial,lambda_ratio,variant,iter,dict_index,active_size,gap,gamma,flops_cum,wall_ms,x_nnz"
+    assert lines[1] == "0,1,0.29999999999999999,plain,0,0,100,0.5,-1,1234,0.012,7"
+    assert lines[2] == "1,1,0.29999999999999999,screened,0,1,90,-1,0.25,1000,1.500,6"
+    assert lines[3] == "2,1,0.29999999999999999,fastl1,0,2,80,9.9999999999999995e-08,0.10000000000000001,500,2.250,5"
+    row = H.SweepSummaryRow(trial=1, lambda_ratio=0.3, flops_plain=1234, flops_screened=1000, flops_multi=500,
+                            time_plain=0.0123456, time_screened=1.5, time_multi=2.25, iters_plain=1, iters_screened=1,
+                            iters_multi=1)
+    H.write_summary_csv(str(tmp_path / "summary.csv"), [row])
+    s = (tmp_path / "summary.csv").read_text().splitlines()
+    assert s[0].startswith("trial,lambda_ratio,flops_plain,flops_screened,flops_fastl1,time_plain_ms")
+    assert s[0].endswith("time_ratio_screened,time_ratio_fastl1,capped")
+    cells = s[1].split(",")
+    assert cells[:11] == ["1", "0.29999999999999999", "1234", "1000", "500", "0.012", "1.500", "2.250", "1", "1", "1"]
+    assert float(cells[11]) == 1000 / 1234 and float(cells[12]) == 500 / 1234 and cells[-1] == "0"
+    H.write_percentiles_csv(str(tmp_path / "pct.csv"), [row, row])
+    p = (tmp_path / "pct.csv").read_text().splitlines()
+    assert p[0] == "lambda_ratio,metric,p25,median,p75" and len(p) == 5
+    assert p[1].startswith("0.29999999999999999,flops_ratio_screened,")
+
+
+def test_emit_plot_data(tmp_path):  # test_bench.cpp:229-270 (empty trace + sentinel filtering)
+    hdr = "run_id,trial,lambda_ratio,variant,iter,dict_index,active_size,gap,gamma,flops_cum,wall_ms,x_nnz\n"
+    (tmp_path / "trace.csv").write_text(hdr)
+    H.emit_plot_data(str(tmp_path / "trace.csv"), str(tmp_path / "plots"))
+    assert (tmp_path / "plots" / "gap_iter.csv").read_text() == "lambda_ratio,trial,variant,iter,gap\n"
+    runs = [_record(0, 0, 0.5, F.VARIANT_MULTI_DICT, [(0, 0, 100, -1.0, 0.9, 10, 0.1, 3), (1, 1, 50, 0.25, -1.0, 20, 0.2, 2)])]
+    H.write_trace_csv(str(tmp_path / "t2.csv"), runs)
+    H.emit_plot_data(str(tmp_path / "t2.csv"), str(tmp_path / "p2"))
+    gap = (tmp_path / "p2" / "gap_iter.csv").read_text().splitlines()
+    assert gap == ["lambda_ratio,trial,variant,iter,gap", "0.5,0,fastl1,1,0.25"]
+    assert len((tmp_path / "p2" / "flops_iter.csv").read_text().splitlines()) == 3
+    assert (tmp_path / "p2" / "gap_time.csv").read_text().splitlines()[1] == "0.5,0,fastl1,0.200,0.25"
+    (tmp_path / "bad.csv").write_text(hdr + "1,2,3\n")
+    with pytest.raises(F.InvalidArgument):
+        H.emit_plot_data(str(tmp_path / "bad.csv"), str(tmp_path / "p3"))
+
+
+def test_dictionary_files_roundtrip(tmp_path):  # dictionary.cpp:76-135
+    rng = np.random.default_rng(3)
+    a = np.asfortranarray(rng.standard_normal((7, 5)))
+    H.save_blob(a, str(tmp_path / "a.blob"))
+    raw = (tmp_path / "a.blob").read_bytes()
+    assert raw[:8] == (7).to_bytes(4, "little") + (5).to_bytes(4, "little") and len(raw) == 8 + 8 * 35
+    assert np.array_equal(H.load_blob(str(tmp_path / "a.blob")), a)
+    H.save_csv(a, str(tmp_path / "a.csv"))
+    assert np.array_equal(H.load_csv(str(tmp_path / "a.csv")), a)  # %.17g round-trips exactly
+    (tmp_path / "r.csv").write_text("1,2\n3\n")
+    (tmp_path / "e.csv").write_text("\n\n")
+    (tmp_path / "t.blob").write_bytes(raw[:20])
+    (tmp_path / "h.blob").write_bytes(b"\x00" * 8)
+    for bad, fn in (("r.csv", H.load_csv), ("e.csv", H.load_csv), ("t.blob", H.load_blob), ("h.blob", H.load_blob),
+                    ("missing.blob", H.load_blob)):
+        with pytest.raises(F.InvalidArgument):
+            fn(str(tmp_path / bad))
+
+
+def test_synthesize_scenario_matches_restatement(oracle):
+    rg = RefGen(oracle)
+    a = H.synthesize_scenario(36, 100, "moderate", 11)
+    b = rg.synthesize_scenario(36, 100, "moderate", 11)
+    assert np.array_equal(a, b)
+    assert np.allclose(np.linalg.norm(a, axis=0), 1.0, atol=1e-14)
+    with pytest.raises(F.InvalidArgument):
+        H.synthesize_scenario(35, 100, "moderate", 1)
+    with pytest.raises(F.InvalidArgument):
+        H.synthesize_scenario(36, 100, "medium", 1)
+
+
+def test_sukro_construction_matches_restatement(oracle):
+    """build_sukro_sequence through torch (here on the CPU device) against the numpy
+    restatement: same per-level error bounds, norms, RC and Kronecker sums."""
+    torch = pytest.importorskip("torch")
+    rg = RefGen(oracle)
+    a = rg.synthesize_scenario(64, 256, "moderate", 5)
+    ours = H.build_sukro_levels(a, [1, 2, 4], device="cpu")
+    ref = rg.build_sukro_sequence(a, [1, 2, 4])
+    assert len(ours) == len(ref) == 3
+    for o, r in zip(ours, ref):
+        assert o.rc == r["rc"]
+        assert np.allclose(o.eps, r["eps"], rtol=1e-9, atol=1e-12)
+        assert np.allclose(o.approx_norms, r["approx_norms"], rtol=1e-9, atol=1e-12)
+        ko = sum(np.kron(l, rr) for l, rr in o.terms)
+        kr = sum(np.kron(l, rr) for l, rr in r["terms"])
+        assert np.allclose(ko, kr, atol=1e-10)
+    with pytest.raises(F.InvalidArgument):
+        H.build_sukro_levels(a, [3, 1], device="cpu")
+    del torch
+
+
+# ---------------------------------------------------------------- on the GPU
+@pytest.mark.gpu
+def test_generate_problem(cuda):  # test_bench.cpp:80-99
+    cfg = small_config()
+    a, b = H.generate_problem(cfg, 0), H.generate_problem(cfg, 0)
+    assert np.array_equal(a.y, b.y) and np.array_equal(a.x_true, b.x_true)
+    c = H.generate_problem(cfg, 1)
+    assert np.max(np.abs(a.y - c.y)) > 0
+    assert abs(np.linalg.norm(a.y) - 1.0) <= 1e-12
+    assert np.max(np.abs(a.dict @ a.x_true - a.y)) <= 1e-12
+    cfg.bernoulli_p = 1e-4
+    for trial in range(20):
+        assert np.count_nonzero(H.generate_problem(cfg, trial).x_true) >= 1
+
+
+@pytest.mark.gpu
+def test_sweep_summaries_and_deterministic_csvs(cuda, tmp_path):  # test_bench.cpp:120-190
+    cfg = small_config(tmp_path / "sweep")
+    out = H.run_sweep(cfg)
+    assert len(out.runs) == 6 and len(out.summary) == 2 and not out.any_capped
+    for r in out.runs:
+        assert len(r.trace) and r.flops == int(r.trace["flops_cum"][-1])
+    ta = (tmp_path / "sweep" / "trace.csv").read_text()
+    sa = (tmp_path / "sweep" / "summary.csv").read_text()
+    H.run_sweep(cfg)
+    tb = (tmp_path / "sweep" / "trace.csv").read_text()
+    sb = (tmp_path / "sweep" / "summary.csv").read_text()
+
+    def strip(csv, cols):
+        return [[c for i, c in enumerate(l.split(",")) if i not in cols] for l in csv.splitlines()]
+
+    assert strip(ta, {10}) == strip(tb, {10})
+    assert strip(sa, {5, 6, 7, 13, 14}) == strip(sb, {5, 6, 7, 13, 14})
+    H.emit_plot_data(str(tmp_path / "sweep" / "trace.csv"), str(tmp_path / "plots"))
+    total = sum(len(r.trace) for r in out.runs)
+    gap_ok = sum(int(np.count_nonzero(r.trace["gap"] >= 0)) for r in out.runs)
+    assert len((tmp_path / "plots" / "flops_iter.csv").read_text().splitlines()) - 1 == total
+    assert len((tmp_path / "plots" / "gap_iter.csv").read_text().splitlines()) - 1 == gap_ok
+
+
+@pytest.mark.gpu
+def test_sweep_variants_agree(cuda):  # test_bench.cpp:192-219
+    cfg = small_config()
+    cfg.tol = 1e-7
+    a = H.synthesize_scenario(cfg.n, cfg.k, cfg.scenario, cfg.seed)
+    seq = H.sukro_sequence(a, cfg.ranks)
+    d = seq.exact().op
+    for trial in range(cfg.trials):
+        y, _ = H.draw_signal(d, cfg.bernoulli_p, cfg.seed, trial)
+        lam = cfg.lambda_ratios[0] * F.lambda_max(d, y)
+        sw = F.SwitchConfig(tolerance=cfg.tol, gamma_threshold=cfg.resolved_gamma())
+        vals = []
+        for v in (F.VARIANT_PLAIN, F.VARIANT_SCREENED, F.VARIANT_MULTI_DICT):
+            r = F.run_lasso(seq, y, lam, sw, F.RunOptions(variant=v))
+            assert r.converged
+            res = y - a @ r.x
+            vals.append(0.5 * res @ res + lam * np.abs(r.x).sum())
+        assert max(vals) - min(vals) <= 2.0 * cfg.tol
+
+
+@pytest.mark.gpu
+def test_sukro_construction_on_gpu_matches_restatement(cuda, oracle):
+    rg = RefGen(oracle)
+    a = rg.synthesize_scenario(64, 256, "hard", 2)
+    ours = H.build_sukro_levels(a, [2, 4], device="cuda")
+    ref = rg.build_sukro_sequence(a, [2, 4])
+    for o, r in zip(ours, ref):
+        assert np.allclose(o.eps, r["eps"], rtol=1e-9, atol=1e-12)
+        assert o.op_err == pytest.approx(r["op_err"], rel=1e-9)
