@@ -20,6 +20,8 @@
 // (size, rows, cols, data, operator(), resize, Zero). Only .data()/.size() cross
 // the boundary, so both layouts are zero-copy into the C-ABI.
 //
+//   DenseDictionary::load_csv / save_csv / load_blob / save_blob  dictionary.cpp:76-135
+//
 // Extensions (defaults reproduce the reference): SwitchConfig::rel_tolerance,
 // RunOptions::x_init, SukroDictionary column scale. The exact_gram option of the
 // reference (out of scope) is accepted and ignored, as the reference ignores it
@@ -27,6 +29,7 @@
 #pragma once
 
 #include <cstdint>
+#include <cstdio>
 #include <cstdlib>
 #include <functional>
 #include <limits>
@@ -156,11 +159,88 @@ class LinearOp {
 class DenseDictionary : public LinearOp {  // dictionary.hpp:19-48, resident in HBM
  public:
   DenseDictionary() = default;
-  explicit DenseDictionary(const Matrix& entries) {
+  explicit DenseDictionary(Matrix entries) : entries_(std::move(entries)) {
     fl1_dict* d = nullptr;
-    detail::check(fl1_dict_dense(detail::context(), entries.data(), entries.rows(), entries.cols(), &d));
+    detail::check(fl1_dict_dense(detail::context(), entries_.data(), entries_.rows(), entries_.cols(), &d));
     adopt(d);
   }
+  const Matrix& entries() const { return entries_; }
+
+  // File formats of dictionary.cpp:76-135: CSV one row per line (%.17g, commas),
+  // blob = uint32 N, uint32 K, then the column-major doubles.
+  static DenseDictionary load_csv(const std::string& path) {
+    std::FILE* f = std::fopen(path.c_str(), "r");
+    if (!f) throw std::invalid_argument("cannot open " + path);
+    std::vector<std::vector<double>> rows;
+    std::string line;
+    int ch;
+    auto flush_line = [&]() {
+      if (line.empty()) return;
+      std::vector<double> row;
+      size_t pos = 0;
+      while (true) {
+        const size_t comma = line.find(',', pos);
+        row.push_back(std::stod(line.substr(pos, comma == std::string::npos ? std::string::npos : comma - pos)));
+        if (comma == std::string::npos) break;
+        pos = comma + 1;
+      }
+      if (!rows.empty() && row.size() != rows.front().size()) {
+        std::fclose(f);
+        throw std::invalid_argument("ragged CSV in " + path);
+      }
+      rows.push_back(std::move(row));
+      line.clear();
+    };
+    while ((ch = std::fgetc(f)) != EOF) {
+      if (ch == '\n') flush_line();
+      else line.push_back(static_cast<char>(ch));
+    }
+    flush_line();
+    std::fclose(f);
+    if (rows.empty()) throw std::invalid_argument("empty CSV in " + path);
+    Matrix m(static_cast<Index>(rows.size()), static_cast<Index>(rows.front().size()));
+    for (Index i = 0; i < m.rows(); ++i)
+      for (Index j = 0; j < m.cols(); ++j) m(i, j) = rows[static_cast<size_t>(i)][static_cast<size_t>(j)];
+    return DenseDictionary(std::move(m));
+  }
+  void save_csv(const std::string& path) const {
+    std::FILE* f = std::fopen(path.c_str(), "w");
+    if (!f) throw std::invalid_argument("cannot open " + path + " for writing");
+    for (Index i = 0; i < entries_.rows(); ++i) {
+      for (Index j = 0; j < entries_.cols(); ++j)
+        std::fprintf(f, j + 1 < entries_.cols() ? "%.17g," : "%.17g", entries_(i, j));
+      std::fputc('\n', f);
+    }
+    std::fclose(f);
+  }
+  static DenseDictionary load_blob(const std::string& path) {
+    std::FILE* f = std::fopen(path.c_str(), "rb");
+    if (!f) throw std::invalid_argument("cannot open " + path);
+    std::uint32_t n = 0, k = 0;
+    const bool ok = std::fread(&n, 4, 1, f) == 1 && std::fread(&k, 4, 1, f) == 1;
+    if (!ok || n == 0 || k == 0) {
+      std::fclose(f);
+      throw std::invalid_argument("bad blob header in " + path);
+    }
+    Matrix m(static_cast<Index>(n), static_cast<Index>(k));
+    const size_t got = std::fread(m.data(), sizeof(double), static_cast<size_t>(n) * k, f);
+    std::fclose(f);
+    if (got != static_cast<size_t>(n) * k) throw std::invalid_argument("truncated blob " + path);
+    return DenseDictionary(std::move(m));
+  }
+  void save_blob(const std::string& path) const {
+    std::FILE* f = std::fopen(path.c_str(), "wb");
+    if (!f) throw std::invalid_argument("cannot open " + path + " for writing");
+    const auto n = static_cast<std::uint32_t>(entries_.rows());
+    const auto k = static_cast<std::uint32_t>(entries_.cols());
+    std::fwrite(&n, 4, 1, f);
+    std::fwrite(&k, 4, 1, f);
+    std::fwrite(entries_.data(), sizeof(double), static_cast<size_t>(n) * k, f);
+    std::fclose(f);
+  }
+
+ private:
+  Matrix entries_;
 };
 
 class SukroDictionary : public LinearOp {  // dictionary.hpp:53-81

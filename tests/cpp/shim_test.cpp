@@ -83,6 +83,24 @@ int main() {
     threw = true;
   }
   CHECK(threw);
+
+  // DenseDictionary file formats (dictionary.cpp:76-135): exact round trips
+  dict.save_blob("/tmp/fl1_shim_dict.blob");
+  dict.save_csv("/tmp/fl1_shim_dict.csv");
+  const DenseDictionary from_blob = DenseDictionary::load_blob("/tmp/fl1_shim_dict.blob");
+  const DenseDictionary from_csv = DenseDictionary::load_csv("/tmp/fl1_shim_dict.csv");
+  bool same = from_blob.rows() == n && from_blob.cols() == k && from_csv.rows() == n && from_csv.cols() == k;
+  for (Index j = 0; same && j < k; ++j)
+    for (Index i = 0; i < n; ++i)
+      same = same && from_blob.entries()(i, j) == a(i, j) && from_csv.entries()(i, j) == a(i, j);
+  CHECK(same);
+  threw = false;
+  try {
+    DenseDictionary::load_blob("/tmp/fl1_shim_missing.blob");
+  } catch (const std::invalid_argument&) {
+    threw = true;
+  }
+  CHECK(threw);
   std::printf("shim ok: %llu iterations, gap %.3e, %d screening events\n",
               static_cast<unsigned long long>(res.iterations), res.final_gap, screens);
   return 0;
