@@ -35,6 +35,7 @@ cudaError_t engine_launch(const EngineParams& p, int64_t sukro_m, cudaStream_t s
 size_t prefix_smem_bytes(int64_t ld, int64_t batch);
 cudaError_t prefix_launch(const PrefixParams& p, int device, cudaStream_t stream);
 int prefix_split_max();
+int64_t prefix_max_atoms();
 cudaError_t engine_cluster_capacity(int64_t ld, int64_t sukro_m, int csize, int* n_clusters);
 cudaError_t engine_launch_clusters(const EngineParams& p0, int n_clusters, int csize, int64_t sukro_m,
                                    cudaStream_t stream);
@@ -1111,7 +1112,8 @@ void solve_clusters(fl1_seq* s, const double* Y, bool y_device, int64_t ldy, con
   const bool use_prefix = batch > 0 && pl.levels == 1 && ex.dict->kind == fl1::kDense &&
                           opts->rule == FL1_RULE_GAP &&
                           (opts->variant == FL1_SCREENED || opts->variant == FL1_PLAIN) &&
-                          opts->full_lipschitz != nullptr && !(pe && pe[0] == '0');
+                          opts->full_lipschitz != nullptr && k <= fl1::prefix_max_atoms() &&
+                          !(pe && pe[0] == '0');
   if (use_prefix) {
     const int64_t bcap = (B + 63) / 64 * 64, kt = (k + 63) / 64;
     size_t ptop = 0;
@@ -1126,7 +1128,7 @@ void solve_clusters(fl1_seq* s, const double* Y, bool y_device, int64_t ldy, con
     const size_t q_x0 = preg(kb8), q_x1 = preg(kb8), q_x2 = preg(kb8), q_u0 = preg(lb8), q_u1 = preg(lb8);
     const size_t q_mk = preg(static_cast<size_t>(k) * ub), q_ld = preg(kb8), q_ps = preg(kb8), q_vp = preg(kb8);
     const size_t q_hi = preg(sizeof(int32_t) * static_cast<size_t>(k) * ub);
-    const size_t q_r = preg(sizeof(double) * static_cast<size_t>(ld * bcap));
+    const size_t q_r = preg(sizeof(double) * static_cast<size_t>(ld) * ub);  // per-signal R columns
     const size_t q_np = preg(sizeof(double) * static_cast<size_t>(ld * bcap) * sm);
     const size_t q_c = preg(sizeof(double) * static_cast<size_t>(k * bcap) * sm);
     const size_t q_s = preg(sizeof(fl1::PrefixSig) * ub), q_h = preg(sizeof(fl1::Handoff) * ub);
@@ -1183,7 +1185,7 @@ void solve_clusters(fl1_seq* s, const double* Y, bool y_device, int64_t ldy, con
     pp.steps_out = reinterpret_cast<int32_t*>(pb + q_n);
     if (std::getenv("FL1_STEP_LOG")) {  // diagnostics: per-step occupancy of the lockstep engine
       pp.max_log = 4096;
-      step_log = std::make_unique<DevBuf>(sizeof(double) * 3 * pp.max_log);
+      step_log = std::make_unique<DevBuf>(sizeof(double) * 5 * pp.max_log);
       pp.step_log = step_log->as<double>();
     }
     bd.handoff = pp.hand;
@@ -1226,10 +1228,11 @@ void solve_clusters(fl1_seq* s, const double* Y, bool y_device, int64_t ldy, con
   if (step_log && d_steps) {
     int32_t steps = 0;
     ck(cudaMemcpy(&steps, d_steps, sizeof(steps), cudaMemcpyDeviceToHost), "steps");
-    std::vector<double> lg(3 * static_cast<size_t>(std::min(steps, 4096)));
+    std::vector<double> lg(5 * static_cast<size_t>(std::min(steps, 4096)));
     if (!lg.empty()) ck(cudaMemcpy(lg.data(), step_log->p, lg.size() * sizeof(double), cudaMemcpyDeviceToHost), "log");
     if (FILE* f = std::fopen(std::getenv("FL1_STEP_LOG"), "w")) {
-      for (size_t i = 0; i + 2 < lg.size(); i += 3) std::fprintf(f, "%g %g %g\n", lg[i], lg[i + 1], lg[i + 2]);
+      for (size_t i = 0; i + 4 < lg.size(); i += 5)
+        std::fprintf(f, "%g %g %g %g %g\n", lg[i], lg[i + 1], lg[i + 2], lg[i + 3], lg[i + 4]);
       std::fclose(f);
     }
   }

@@ -38,7 +38,7 @@ constexpr int kTK = 32;             // K chunk (rows of A / rho)
 constexpr int kSS = kTK + 4;        // padded smem row stride (doubles)
 constexpr int kStage = (kTM + kTN) * kSS;  // doubles per pipeline stage
 constexpr unsigned kAll = 0xffffffffu;
-constexpr int kSplitMax = 4;       // split-K parts of the contraction (load balance)
+constexpr int kSplitMax = 16;      // split-K parts of the contractions (load balance)
 
 __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
@@ -69,6 +69,7 @@ struct PSh {
   double m, t_next, sp, radius, gap_tilde, primal;
   int release, screen;
   int64_t n_act, off;
+  int32_t nzc[kPW], fxc[kPW];
 };
 
 // deterministic block reductions (fixed tree)
@@ -128,7 +129,7 @@ __device__ void block_sum3(double (&v)[3], PSh& sh) {
 // Corr tile (atoms j0..j0+63) x (slots a0..a0+63) over K-part kp of sk (rows of A /
 // rho), DMMA, into the split-K partial buffer kp.
 __device__ __noinline__ void gemm_tile(const PrefixParams& p, int rt, int ct, int kp, int sk, int64_t n_act,
-                                       double* stage) {
+                                       const int32_t* act, double* stage) {
   const int w = threadIdx.x >> 5, l = threadIdx.x & 31, g = l >> 2, tg = l & 3;
   const int64_t j0 = static_cast<int64_t>(rt) * kTM, a0 = static_cast<int64_t>(ct) * kTN;
   const int64_t K = p.k, ld = p.ld;
@@ -157,7 +158,8 @@ __device__ __noinline__ void gemm_tile(const PrefixParams& p, int rt, int ct, in
       const int c = e / (kTK / 2), kk = (e % (kTK / 2)) * 2;
       const int64_t a = a0 + c, kg = k0 + kk;
       const bool ok = a < n_act && kg < ld;
-      cp16(Rs + c * kSS + kk, ok ? p.R + a * ld + kg : p.R, ok);
+      const int64_t b = ok ? act[a] : 0;  // R columns are per signal
+      cp16(Rs + c * kSS + kk, ok ? p.R + b * ld + kg : p.R, ok);
     }
   };
   if (c_lo < c_hi) issue(0, c_lo);
@@ -442,45 +444,125 @@ __device__ double combine_corr(const PrefixParams& p, PSh& sh, int64_t a, int64_
   return block_max(dp, sh);
 }
 
+// compute_products (fastl1.cpp:359-369) for signal b's NEXT iteration: rho_g =
+// y - ((1+m)u - m v) into its R column, with ||rho_g||^2, rho_g.y, ||y - u||^2.
+__device__ void compute_rho(const PrefixParams& p, PSh& sh, int64_t b) {
+  PrefixSig& sg = p.sig[b];
+  const int64_t N = p.n, ld = p.ld;
+  double m = 0.0;
+  if (p.solver == FL1_FISTA && sg.ready) m = (sg.t_k - 1.0) / (0.5 * (1.0 + sqrt(1.0 + 4.0 * sg.t_k * sg.t_k)));
+  const bool mom = m != 0.0;
+  const double* uc = p.U2[sg.uswap] + b * ld;
+  const double* vc = p.U2[1 - sg.uswap] + b * ld;
+  double v[3] = {0.0, 0.0, 0.0};
+  for (int64_t i = threadIdx.x; i < ld; i += kPT) {
+    double r = 0.0;
+    if (i < N) {
+      const double u = uc[i];
+      const double uw = mom ? (1.0 + m) * u - m * vc[i] : u;
+      const double yi = p.y[b * p.ldy + i];
+      r = yi - uw;
+      v[0] = fma(r, r, v[0]);
+      v[1] = fma(yi, r, v[1]);
+      if (mom) {
+        const double e = yi - u;
+        v[2] = fma(e, e, v[2]);
+      }
+    }
+    __stcg(p.R + b * ld + i, r);
+  }
+  block_sum3(v, sh);
+  if (threadIdx.x == 0) {
+    sg.rsq = v[0];
+    sg.rdy = v[1];
+    sg.ree = v[2];
+  }
+  __syncthreads();
+}
+
+// Per-signal passes over the K atoms: warp w owns the contiguous atom range
+// [w Kw, (w+1) Kw), so lists built by per-warp ballots are in atom order when read
+// warp by warp -- no block barrier per 256 atoms.
+struct WarpRange {
+  int64_t lo, hi;
+  __device__ WarpRange(int64_t K) {
+    const int64_t kw = (K + kPW - 1) / kPW;
+    const int w = threadIdx.x >> 5;
+    lo = min(K, kw * w);
+    hi = min(K, lo + kw);
+  }
+};
+
+// append (v, j) to this warp's list segment when flag; returns the new count
+__device__ __forceinline__ int warp_append(bool flag, double v, int32_t j, double* ev, int32_t* ej, int cnt) {
+  const int l = threadIdx.x & 31;
+  const unsigned bal = __ballot_sync(kAll, flag);
+  if (flag) {
+    const int at = cnt + __popc(bal & ((1u << l) - 1u));
+    ev[at] = v;
+    ej[at] = j;
+  }
+  return cnt + __popc(bal);
+}
+
+// rows over threads: acc_i += sum over the warp segments (in warp = atom order)
+__device__ __forceinline__ void apply_segments(const PrefixParams& p, double* us, const double* ev, const int32_t* ej,
+                                               int64_t seg, const int32_t* cnt, double sign) {
+  for (int64_t i = threadIdx.x; i < p.ld; i += kPT) {
+    double acc = us[i];
+    for (int w = 0; w < kPW; ++w) {
+      const double* v = ev + w * seg;
+      const int32_t* jj = ej + w * seg;
+#pragma unroll 4
+      for (int e = 0; e < cnt[w]; ++e) acc = fma(sign * v[e], __ldg(p.a + static_cast<int64_t>(jj[e]) * p.ld + i), acc);
+    }
+    us[i] = acc;
+  }
+  __syncthreads();
+}
+
 // Enter the restricted power iteration (power_iteration_sq_norm, solver.cpp:72-104):
 // warm from the gathered leading vector when it is nonzero, else the fixed Gaussian
-// start by preserved position.
+// start by preserved position (rank among unmasked atoms).
 __device__ void enter_power(const PrefixParams& p, PSh& sh, int64_t b) {
   PrefixSig& sg = p.sig[b];
   const int64_t K = p.k;
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
   const int8_t* mk = p.mask + b * K;
   const double* ldv = p.lead + b * K;
   double* src = p.psrc + b * K;
   double* vp = p.vp + b * K;
+  const WarpRange wr(K);
+  // pass 1: |lead|^2 over the set and the warp's active count (rank offsets)
   double a_lead = 0.0;
-  if (sg.lead_valid)
-    for (int64_t j = threadIdx.x; j < K; j += kPT)
-      if (mk[j]) a_lead = fma(ldv[j], ldv[j], a_lead);
+  int cnt = 0;
+  for (int64_t base = wr.lo; base < wr.hi; base += 32) {
+    const int64_t j = base + l;
+    const bool on = j < wr.hi && mk[j] != 0;
+    if (on && sg.lead_valid) a_lead = fma(ldv[j], ldv[j], a_lead);
+    cnt += __popc(__ballot_sync(kAll, on));
+  }
+  if (l == 0) sh.wcnt[w] = cnt;
   a_lead = block_sum(a_lead, sh);
   const bool warm = sg.lead_valid && a_lead > 0.0;
-  double nrm2 = 0.0;
-  if (warm) {
-    for (int64_t j = threadIdx.x; j < K; j += kPT) src[j] = mk[j] ? ldv[j] : 0.0;
-    nrm2 = a_lead;
-  } else {
-    int tot = 0;
-    double acc = 0.0;
-    for (int64_t base = 0; base < K; base += kPT) {
-      const int64_t j = base + threadIdx.x;
-      const bool on = j < K && mk[j] != 0;
-      int at;
-      tot = block_compact(sh, on, tot, &at);
-      if (j < K) {
-        const double gv = on ? p.gauss0[at] : 0.0;
-        src[j] = gv;
-        acc = fma(gv, gv, acc);
-      }
+  int off = 0;
+  for (int ww = 0; ww < w; ++ww) off += sh.wcnt[ww];
+  // pass 2: the start vector
+  double acc = 0.0;
+  for (int64_t base = wr.lo; base < wr.hi; base += 32) {
+    const int64_t j = base + l;
+    const bool on = j < wr.hi && mk[j] != 0;
+    const unsigned bal = __ballot_sync(kAll, on);
+    if (j < wr.hi) {
+      const double gv = on ? (warm ? ldv[j] : p.gauss0[off + __popc(bal & ((1u << l) - 1u))]) : 0.0;
+      src[j] = gv;
+      acc = fma(gv, gv, acc);
     }
-    nrm2 = block_sum(acc, sh);
+    off += __popc(bal);
   }
+  const double nrm2 = warm ? a_lead : block_sum(acc, sh);
   const double div = sqrt(nrm2);
-  __syncthreads();
-  for (int64_t j = threadIdx.x; j < K; j += kPT) vp[j] = src[j] / div;
+  for (int64_t j = wr.lo + l; j < wr.hi; j += 32) vp[j] = src[j] / div;  // same thread wrote src[j]
   if (threadIdx.x == 0) {
     sg.mode = 1;
     sg.p_div = div;
@@ -494,27 +576,29 @@ __device__ void enter_power(const PrefixParams& p, PSh& sh, int64_t b) {
   __syncthreads();
 }
 
-// One power step's update after v_new = A_S^T A_S v (slot a's corr column).
+// One power step's update after v_new = A_S^T A_S v (slot a's corr column parts).
 __device__ __noinline__ void power_step(const PrefixParams& p, PSh& sh, int64_t a, int64_t b, int sk, double t0) {
   PrefixSig& sg = p.sig[b];
-  const int64_t K = p.k;
-  (void)combine_corr(p, sh, a, b, sk);
+  const int64_t K = p.k, part = K * p.bcap;
   const double* cr = p.corr + a * K;
   const int8_t* mk = p.mask + b * K;
   double* src = p.psrc + b * K;
   double* vp = p.vp + b * K;
-  double w2 = 0.0, vw = 0.0;
-  for (int64_t j = threadIdx.x; j < K; j += kPT) {
+  const WarpRange wr(K);
+  const int l = threadIdx.x & 31;
+  double v[3] = {0.0, 0.0, 0.0};  // |v_new|^2, v.v_new
+  for (int64_t j = wr.lo + l; j < wr.hi; j += 32) {
     if (!mk[j]) continue;
-    const double vn = __ldcg(cr + j);
-    w2 = fma(vn, vn, w2);
-    vw = fma(vp[j], vn, vw);
+    double c = __ldcg(cr + j);
+    for (int kp = 1; kp < sk; ++kp) c += __ldcg(cr + kp * part + j);
+    src[j] = c;  // v_new (unnormalised) = the next cur_src
+    v[0] = fma(c, c, v[0]);
+    v[1] = fma(vp[j], c, v[1]);
   }
-  w2 = block_sum(w2, sh);
-  vw = block_sum(vw, sh);
+  block_sum3(v, sh);
   if (threadIdx.x == 0) {
     sg.power_steps += 1;
-    const double nrm = sqrt(w2);
+    const double nrm = sqrt(v[0]);
     int stop = 0;
     double est = sg.p_est;
     if (nrm == 0.0) {
@@ -522,7 +606,7 @@ __device__ __noinline__ void power_step(const PrefixParams& p, PSh& sh, int64_t 
       stop = 2;  // lead = have_w ? w / div : v  (w = 0 here)
     } else {
       const double prev = est;
-      est = vw;
+      est = v[1];
       sg.p_div = nrm;
       sg.p_have_w = 1;
       if (sg.p_it > sg.p_min && fabs(est - prev) <= sg.p_tol * est) stop = 1;
@@ -536,13 +620,11 @@ __device__ __noinline__ void power_step(const PrefixParams& p, PSh& sh, int64_t 
   __syncthreads();
   const int stop = sh.release;
   const double div = sh.m;
-  if (stop == 2) {  // |w| == 0
-    for (int64_t j = threadIdx.x; j < K; j += kPT) p.lead[b * K + j] = sg.p_have_w ? 0.0 : vp[j];
-  } else {
-    for (int64_t j = threadIdx.x; j < K; j += kPT) {
-      const double vn = mk[j] ? __ldcg(cr + j) : 0.0;
-      src[j] = vn;
-      const double v1 = vn / div;
+  for (int64_t j = wr.lo + l; j < wr.hi; j += 32) {  // same thread mapping as above
+    if (stop == 2) {
+      p.lead[b * K + j] = sg.p_have_w ? 0.0 : vp[j];
+    } else {
+      const double v1 = mk[j] ? src[j] / div : 0.0;
       if (stop) p.lead[b * K + j] = v1;
       else vp[j] = v1;
     }
@@ -556,7 +638,11 @@ __device__ __noinline__ void power_step(const PrefixParams& p, PSh& sh, int64_t 
     sg.mode = 0;
   }
   __syncthreads();
-  if (stop && p.policy == 2) handoff_signal(p, sh, b, t0);
+  if (stop && p.policy == 2) {
+    handoff_signal(p, sh, b, t0);
+  } else if (stop) {
+    compute_rho(p, sh, b);
+  }
 }
 
 // One FISTA / ISTA iteration of signal b (slot a): fastl1.cpp:459-645 with the
@@ -564,12 +650,22 @@ __device__ __noinline__ void power_step(const PrefixParams& p, PSh& sh, int64_t 
 __device__ __noinline__ void fista_step(const PrefixParams& p, PSh& sh, int64_t a, int64_t b, double t0, int sk,
                                         double* us, double* stage) {
   PrefixSig& sg = p.sig[b];
-  const int64_t K = p.k, ld = p.ld;
+  const int64_t K = p.k, ld = p.ld, part = K * p.bcap;
   const double lambda = p.lambdas[b];
   const uint64_t t = sg.t;
-  const double dp = combine_corr(p, sh, a, b, sk);
-  const double* cr = p.corr + a * K;
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  const WarpRange wr(K);
+  double* cr = p.corr + a * K;
   int8_t* mk = p.mask + b * K;
+  // corr = sum of the split-K parts, written back to part 0; max |corr| over the set
+  double dp = 0.0;
+  for (int64_t j = wr.lo + l; j < wr.hi; j += 32) {
+    double c = __ldcg(cr + j);
+    for (int kp = 1; kp < sk; ++kp) c += __ldcg(cr + kp * part + j);
+    if (sk > 1) __stcg(cr + j, c);
+    if (mk[j]) dp = fmax(dp, fabs(c));
+  }
+  dp = block_max(dp, sh);
   if (threadIdx.x == 0) {
     double m = 0.0, t_next = sg.t_k;  // 465-470
     if (p.solver == FL1_FISTA && sg.ready) {
@@ -616,9 +712,6 @@ __device__ __noinline__ void fista_step(const PrefixParams& p, PSh& sh, int64_t 
   double* __restrict__ xpc = p.X3[(rot + 1) % 3] + b * K;
   double* __restrict__ xn = p.X3[(rot + 2) % 3] + b * K;
   const int64_t S_old = sg.S;
-  const int cap = 2 * kStage / 3 - kPT;  // list entries (value + index) in the staging area
-  double* ent_v = stage;
-  int32_t* ent_j = reinterpret_cast<int32_t*>(stage + 2 * kStage / 3);
   if (sh.release == 2) {  // stop (fastl1.cpp:568-571, 625-633)
     double nnz = 0.0;
     for (int64_t j = threadIdx.x; j < K; j += kPT) nnz += (mk[j] && xc[j] != 0.0) ? 1.0 : 0.0;
@@ -642,14 +735,34 @@ __device__ __noinline__ void fista_step(const PrefixParams& p, PSh& sh, int64_t 
     finish_signal(p, sh, b, true, sh.gap_tilde, t0);
     return;
   }
-  // screening (494-566; stable test with eps = 0) and prox (572-579) over the set
+  if (p.policy == 1 && sh.screen) {  // policy 1: leave at the start of an iteration that would shrink
+    double drops = 0.0;
+    for (int64_t j = threadIdx.x; j < K; j += kPT)
+      if (mk[j] && !(__fma_rn(sh.radius, p.en[j], fabs(__dmul_rn(sh.sp, __ldcg(cr + j)))) >= 1.0)) drops += 1.0;
+    drops = block_sum(drops, sh);
+    if (drops > 0.0) {
+      handoff_signal(p, sh, b, t0);
+      return;
+    }
+  }
+  // One pass: screening (494-566; stable test with eps = 0), prox (572-579), and the
+  // restriction (667-702) folded in: a dropped atom's x_next is discarded, its
+  // x_prev (the old x) feeds the v fix, and it leaves x, x_prev, lead and the mask.
+  // Lists per warp segment: nonzeros of the new x (u = A x) and the v-fix entries.
   const double m = sh.m, inv_l = sg.inv_l, thresh = lambda * sg.inv_l;
-  const bool screen = sh.screen != 0;
+  const bool screen = sh.screen != 0, fista = p.solver == FL1_FISTA;
   const double spv = sh.sp, rad = sh.radius;
-  double kept = 0.0;
-  for (int64_t j = threadIdx.x; j < K; j += kPT) {
-    double v = 0.0;
-    if (mk[j]) {
+  const int64_t seg = (K + kPW - 1) / kPW;
+  double* nz_v = stage;                                   // K values
+  double* fx_v = stage + seg * kPW;                       // K values
+  int32_t* nz_j = reinterpret_cast<int32_t*>(stage + 2 * seg * kPW);
+  int32_t* fx_j = nz_j + seg * kPW;
+  int nz_c = 0, fx_c = 0;
+  double red3[3] = {0.0, 0.0, 0.0};  // kept, nnz(x_new), |x_new|_1
+  for (int64_t base = wr.lo; base < wr.hi; base += 32) {
+    const int64_t j = base + l;
+    double v = 0.0, fixv = 0.0;
+    if (j < wr.hi && mk[j]) {
       const double c = __ldcg(cr + j);
       const double xo = xc[j];
       const double xpv = m != 0.0 ? xpc[j] : 0.0;
@@ -657,91 +770,44 @@ __device__ __noinline__ void fista_step(const PrefixParams& p, PSh& sh, int64_t 
       const double z = __fma_rn(inv_l, c, gg);
       const double mag = fabs(z) - thresh;
       v = mag <= 0.0 ? 0.0 : (z > 0.0 ? mag : -mag);
-      if (screen) {
-        const double d = fabs(__dmul_rn(spv, c));
-        if (__fma_rn(rad, p.en[j], d) >= 1.0) kept += 1.0;
-        else mk[j] = 2;  // dropped at this instant
-      } else {
-        kept += 1.0;
-      }
-    }
-    xn[j] = v;
-  }
-  kept = block_sum(kept, sh);
-  const int64_t S_new = static_cast<int64_t>(kept);
-  if (p.policy == 1 && S_new < S_old) {  // leave at the start of this iteration
-    for (int64_t j = threadIdx.x; j < K; j += kPT)
-      if (mk[j] == 2) mk[j] = 1;
-    __syncthreads();
-    handoff_signal(p, sh, b, t0);
-    return;
-  }
-  const bool fista = p.solver == FL1_FISTA;
-  // FISTA bookkeeping (581-590): x_prev = x, v = u; x = x_next. Roles rotate: the
-  // new x_prev is the old x buffer, the new x the x_next buffer; v takes u's buffer.
-  double* __restrict__ xnew = xn;
-  double* __restrict__ xprev = xc;
-  const double* __restrict__ uo = p.U2[sg.uswap] + b * ld;   // u = old u  -> becomes v
-  double* __restrict__ un = p.U2[1 - sg.uswap] + b * ld;      // new u
-  // apply_restriction (667-702): v -= x_prev_j a_j over dropped atoms (FISTA, momentum
-  // ready after the shift above), then the dropped atoms leave x, x_prev, lead
-  for (int64_t i = threadIdx.x; i < ld; i += kPT) us[i] = fista ? uo[i] : 0.0;
-  __syncthreads();
-  if (S_new < S_old) {
-    int tot = 0;
-    for (int64_t base = 0; base < K; base += kPT) {
-      const int64_t j = base + threadIdx.x;
-      double v = 0.0;
-      if (j < K && mk[j] == 2) {
-        if (fista && xprev[j] != 0.0) v = -xprev[j];
+      const bool keep = !screen || __fma_rn(rad, p.en[j], fabs(__dmul_rn(spv, c))) >= 1.0;
+      if (keep) {
+        red3[0] += 1.0;
+      } else {  // dropped: x_prev of the shifted history is the old x
+        if (fista && xo != 0.0) fixv = -xo;
+        v = 0.0;
         mk[j] = 0;
-        xnew[j] = 0.0;
-        xprev[j] = 0.0;
+        xc[j] = 0.0;  // becomes x_prev after the role rotation
         p.lead[b * K + j] = 0.0;
       }
-      int at;
-      const int ntot = block_compact(sh, v != 0.0, tot, &at);
-      if (v != 0.0) {
-        ent_v[at] = v;
-        ent_j[at] = static_cast<int32_t>(j);
-      }
-      tot = ntot;
-      if (tot > cap - kPT) {
-        apply_list(p, us, ent_v, ent_j, tot);
-        tot = 0;
-      }
+      red3[1] += v != 0.0 ? 1.0 : 0.0;
+      red3[2] += fabs(v);
     }
-    apply_list(p, us, ent_v, ent_j, tot);
+    if (j < wr.hi) xn[j] = v;
+    nz_c = warp_append(v != 0.0, v, static_cast<int32_t>(j), nz_v + w * seg, nz_j + w * seg, nz_c);
+    fx_c = warp_append(fixv != 0.0, fixv, static_cast<int32_t>(j), fx_v + w * seg, fx_j + w * seg, fx_c);
   }
-  // the v buffer (old u, fixed) is final; u = A x over the nonzeros of the new x
-  if (fista)
+  if (l == 0) {
+    sh.nzc[w] = nz_c;
+    sh.fxc[w] = fx_c;
+  }
+  block_sum3(red3, sh);  // (syncs: the warp counts are visible after it)
+  const int64_t S_new = static_cast<int64_t>(red3[0]);
+  const double nnz = red3[1], l1n = red3[2];
+  // FISTA bookkeeping (581-590): x_prev = x, v = u (the old u buffer, minus the fix), x = x_next
+  const double* __restrict__ uo = p.U2[sg.uswap] + b * ld;
+  double* __restrict__ un = p.U2[1 - sg.uswap] + b * ld;
+  int any_fix = 0;
+  for (int ww = 0; ww < kPW; ++ww) any_fix += sh.fxc[ww];
+  if (fista && any_fix) {
+    for (int64_t i = threadIdx.x; i < ld; i += kPT) us[i] = uo[i];
+    __syncthreads();
+    apply_segments(p, us, fx_v, fx_j, seg, sh.fxc, 1.0);
     for (int64_t i = threadIdx.x; i < ld; i += kPT) const_cast<double*>(uo)[i] = us[i];
+  }
   for (int64_t i = threadIdx.x; i < ld; i += kPT) us[i] = 0.0;
   __syncthreads();
-  double nnz = 0.0, l1n = 0.0;
-  {
-    int tot = 0;
-    for (int64_t base = 0; base < K; base += kPT) {
-      const int64_t j = base + threadIdx.x;
-      const double v = j < K ? xnew[j] : 0.0;
-      nnz += v != 0.0 ? 1.0 : 0.0;
-      l1n += fabs(v);
-      int at;
-      const int ntot = block_compact(sh, v != 0.0, tot, &at);
-      if (v != 0.0) {
-        ent_v[at] = v;
-        ent_j[at] = static_cast<int32_t>(j);
-      }
-      tot = ntot;
-      if (tot > cap - kPT) {
-        apply_list(p, us, ent_v, ent_j, tot);
-        tot = 0;
-      }
-    }
-    apply_list(p, us, ent_v, ent_j, tot);
-  }
-  nnz = block_sum(nnz, sh);
-  l1n = block_sum(l1n, sh);
+  apply_segments(p, us, nz_v, nz_j, seg, sh.nzc, 1.0);  // u = A x (ActiveOp::apply 131-146)
   for (int64_t i = threadIdx.x; i < ld; i += kPT) un[i] = us[i];
   if (threadIdx.x == 0) {
     if (fista) {
@@ -766,11 +832,18 @@ __device__ __noinline__ void fista_step(const PrefixParams& p, PSh& sh, int64_t 
       sg.n_trace += 1;
     }
     sg.t = t + 1;
-    // restricted Lipschitz refresh when the set halved (603-608)
+    // restricted Lipschitz refresh when the set halved (603-608); the cap ends the run (640-644)
     sh.screen = (S_new * 2 <= sg.active_at_last_l && S_new > 0) ? 1 : 0;
+    sh.release = sg.t >= p.max_it ? 1 : 0;
   }
   __syncthreads();
-  if (sh.screen) enter_power(p, sh, b);
+  if (sh.release) {
+    finish_signal(p, sh, b, false, 0.0, t0);
+  } else if (sh.screen) {
+    enter_power(p, sh, b);
+  } else {
+    compute_rho(p, sh, b);
+  }
 }
 
 }  // namespace
@@ -814,6 +887,9 @@ __global__ void __launch_bounds__(kPT, 1) prefix_kernel(const __grid_constant__ 
       s.inv_l = 1.0 / p.lipschitz;
       p.sig[b] = s;
     }
+    __syncthreads();
+    if (p.max_it == 0) finish_signal(p, sh, b, false, 0.0, t0);
+    else compute_rho(p, sh, b);
   }
   grid.sync();
   int32_t steps = 0;
@@ -834,53 +910,14 @@ __global__ void __launch_bounds__(kPT, 1) prefix_kernel(const __grid_constant__ 
       n_pow = np;
     }
     if (n_act == 0) break;
-    if (p.step_log && blockIdx.x == 0 && threadIdx.x == 0 && steps < p.max_log) {
-      p.step_log[3 * steps] = n_act;
-      p.step_log[3 * steps + 1] = n_pow;
-      p.step_log[3 * steps + 2] = gtimer() - t0;
-    }
-    // ---- FISTA signals: compute_products (359-369) rho_g with its norms; max_iterations
-    for (int64_t a = blockIdx.x; a < n_act; a += gridDim.x) {
-      const int64_t b = act[a];
-      PrefixSig& sg = p.sig[b];
-      if (__ldcg(&sg.mode) != 0) continue;
-      if (sg.t >= p.max_it) {  // fastl1.cpp:640-644
-        finish_signal(p, sh, b, false, 0.0, t0);
-        for (int64_t i = threadIdx.x; i < ld; i += kPT) __stcg(p.R + a * ld + i, 0.0);
-        continue;
-      }
-      double m = 0.0;
-      if (p.solver == FL1_FISTA && sg.ready) m = (sg.t_k - 1.0) / (0.5 * (1.0 + sqrt(1.0 + 4.0 * sg.t_k * sg.t_k)));
-      const bool mom = m != 0.0;
-      const double* uc = p.U2[sg.uswap] + b * ld;
-      const double* vc = p.U2[1 - sg.uswap] + b * ld;
-      double v[3] = {0.0, 0.0, 0.0};
-      for (int64_t i = threadIdx.x; i < ld; i += kPT) {
-        double r = 0.0;
-        if (i < N) {
-          const double u = uc[i];
-          const double uw = mom ? (1.0 + m) * u - m * vc[i] : u;
-          const double yi = p.y[b * p.ldy + i];
-          r = yi - uw;
-          v[0] = fma(r, r, v[0]);
-          v[1] = fma(yi, r, v[1]);
-          if (mom) {
-            const double e = yi - u;
-            v[2] = fma(e, e, v[2]);
-          }
-        }
-        __stcg(p.R + a * ld + i, r);
-      }
-      block_sum3(v, sh);
-      if (threadIdx.x == 0) {
-        sg.rsq = v[0];
-        sg.rdy = v[1];
-        sg.ree = v[2];
-      }
+    const bool logit = p.step_log && blockIdx.x == 0 && threadIdx.x == 0 && steps < p.max_log;
+    if (logit) {
+      p.step_log[5 * steps] = n_act;
+      p.step_log[5 * steps + 1] = n_pow;
+      p.step_log[5 * steps + 2] = gtimer() - t0;
     }
     // ---- power-step signals: w = A_S v (one contraction), then summed into R
     if (n_pow > 0) {
-      grid.sync();
       const int n_rt = static_cast<int>((ld + kTM - 1) / kTM);
       const int n_ct = (n_pow + kTN - 1) / kTN;
       const int sk = split_for(n_rt * n_ct, gridDim.x);
@@ -894,19 +931,21 @@ __global__ void __launch_bounds__(kPT, 1) prefix_kernel(const __grid_constant__ 
         const int64_t pc = e / ld, i = e - pc * ld;
         double w = 0.0;
         for (int kp = 0; kp < sk; ++kp) w += __ldcg(p.np + (static_cast<int64_t>(kp) * p.bcap + pc) * ld + i);
-        __stcg(p.R + static_cast<int64_t>(pact[pc]) * ld + i, i < N ? w : 0.0);
+        __stcg(p.R + static_cast<int64_t>(act[pact[pc]]) * ld + i, i < N ? w : 0.0);
       }
+      grid.sync();
     }
-    grid.sync();
+    if (logit) p.step_log[5 * steps + 3] = gtimer() - t0;
     // ---- Corr = A^T [rho | w] for every unfinished signal (fp64 tensor cores)
     const int n_rt = static_cast<int>((K + kTM - 1) / kTM);
     const int n_ct = (n_act + kTN - 1) / kTN;
     const int sk = split_for(n_rt * n_ct, gridDim.x);
     for (int item = blockIdx.x; item < n_rt * n_ct * sk; item += gridDim.x) {
       const int tile = item % (n_rt * n_ct), kp = item / (n_rt * n_ct);
-      gemm_tile(p, tile % n_rt, tile / n_rt, kp, sk, n_act, stage);
+      gemm_tile(p, tile % n_rt, tile / n_rt, kp, sk, n_act, act, stage);
     }
     grid.sync();
+    if (logit) p.step_log[5 * steps + 4] = gtimer() - t0;
     // ---- the rest of each signal's unit of work, one signal per CTA
     for (int64_t a = blockIdx.x; a < n_act; a += gridDim.x) {
       const int64_t b = act[a];
@@ -923,6 +962,8 @@ size_t prefix_smem_bytes(int64_t ld, int64_t batch) {
   return static_cast<size_t>(2 * kStage + ld) * sizeof(double) + static_cast<size_t>(2 * batch) * sizeof(int32_t);
 }
 int prefix_split_max() { return kSplitMax; }
+// two per-signal atom lists (12 bytes per entry each) live in the staging area
+int64_t prefix_max_atoms() { return (2 * kStage * 8) / 24 / kPW * kPW; }
 
 cudaError_t prefix_launch(const PrefixParams& p, int device, cudaStream_t stream) {
   const size_t smem = prefix_smem_bytes(p.ld, p.batch);

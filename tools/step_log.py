@@ -17,8 +17,11 @@ for _ in range(2):
 lg = np.loadtxt('/tmp/fl1_steps.txt')
 t = lg[:, 2] / 1e6
 dt = np.diff(t)
+gn = (lg[:, 3] - lg[:, 2]) / 1e3   # us: power contraction W = A V + combine
+gt = (lg[:, 4] - lg[:, 3]) / 1e3   # us: A^T R contraction
 print('batch ms', rs[0].batch_device_ms, 'steps', len(lg), 'lockstep ms', t[-1])
 for lo, hi in [(0, 40), (40, 80), (80, 120), (120, 160), (160, 200), (200, 240), (240, 300)]:
     sel = slice(lo, min(hi, len(dt)))
     if lo >= len(dt): break
-    print(f"steps {lo:3d}-{hi:3d}: n_act {lg[sel,0].mean():6.1f} n_pow {lg[sel,1].mean():6.1f} us/step {dt[sel].mean()*1e3:7.1f} total ms {dt[sel].sum():6.2f}")
+    print(f"steps {lo:3d}-{hi:3d}: n_act {lg[sel,0].mean():6.1f} n_pow {lg[sel,1].mean():6.1f} us/step {dt[sel].mean()*1e3:7.1f} "
+          f"[W=AV {gn[sel].mean():6.1f}  A^T R {gt[sel].mean():6.1f}  per-signal {dt[sel].mean()*1e3-gn[sel].mean()-gt[sel].mean():6.1f}] total ms {dt[sel].sum():6.2f}")
