@@ -505,18 +505,51 @@ __device__ __forceinline__ int warp_append(bool flag, double v, int32_t j, doubl
   return cnt + __popc(bal);
 }
 
-// rows over threads: acc_i += sum over the warp segments (in warp = atom order)
+// rows over threads: acc_i += sum over the warp segments (in warp = atom order);
+// four rows per thread and four entries per round keep 16 loads in flight
 __device__ __forceinline__ void apply_segments(const PrefixParams& p, double* us, const double* ev, const int32_t* ej,
                                                int64_t seg, const int32_t* cnt, double sign) {
-  for (int64_t i = threadIdx.x; i < p.ld; i += kPT) {
-    double acc = us[i];
+  const int64_t ld = p.ld;
+  const double* __restrict__ A = p.a;
+  for (int64_t i0 = threadIdx.x; i0 < ld; i0 += 4 * kPT) {
+    double acc[4];
+    bool ok[4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      ok[r] = i0 + r * kPT < ld;
+      acc[r] = ok[r] ? us[i0 + r * kPT] : 0.0;
+    }
     for (int w = 0; w < kPW; ++w) {
       const double* v = ev + w * seg;
       const int32_t* jj = ej + w * seg;
-#pragma unroll 4
-      for (int e = 0; e < cnt[w]; ++e) acc = fma(sign * v[e], __ldg(p.a + static_cast<int64_t>(jj[e]) * p.ld + i), acc);
+      const int n = cnt[w];
+      int e = 0;
+      for (; e + 4 <= n; e += 4) {
+        double a[4][4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const double* col = A + static_cast<int64_t>(jj[e + q]) * ld + i0;
+#pragma unroll
+          for (int r = 0; r < 4; ++r) a[q][r] = ok[r] ? __ldg(col + r * kPT) : 0.0;
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const double c = sign * v[e + q];
+#pragma unroll
+          for (int r = 0; r < 4; ++r) acc[r] = fma(c, a[q][r], acc[r]);
+        }
+      }
+      for (; e < n; ++e) {
+        const double* col = A + static_cast<int64_t>(jj[e]) * ld + i0;
+        const double c = sign * v[e];
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+          if (ok[r]) acc[r] = fma(c, __ldg(col + r * kPT), acc[r]);
+      }
     }
-    us[i] = acc;
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+      if (ok[r]) us[i0 + r * kPT] = acc[r];
   }
   __syncthreads();
 }
