@@ -351,3 +351,34 @@ def test_batched_prefix_matches_engine_only(cuda, monkeypatch, policy):
         assert x.iterations == y.iterations and x.total_flops == y.total_flops
         assert np.array_equal(x.final_active, y.final_active)
         assert np.max(np.abs(x.x - y.x)) <= 1e-9 * max(1.0, np.max(np.abs(y.x)))
+
+
+@pytest.mark.parametrize("policy", ["0", "2"])
+def test_batched_lockstep_edge_cases(cuda, oracle16, monkeypatch, policy):
+    """Lockstep corner cases against per-signal oracle solves: a zero signal (exact
+    fit: hand-off to the per-signal engine at iteration 0), lambda >= lambda_max
+    (immediate convergence), an iteration cap reached inside the lockstep, a single
+    signal, and a dictionary smaller than one contraction tile (K < 128, N < 64)."""
+    monkeypatch.setenv("FL1_LOCKSTEP_POLICY", policy)
+    rng = np.random.default_rng(29)
+    for n, k, B, cap in ((50, 40, 5, 5000), (120, 300, 1, 5000), (120, 300, 6, 7)):
+        a = syn.gaussian_dictionary(rng, n, k)
+        Y = np.empty((n, B), order="F")
+        lams = np.empty(B)
+        for b in range(B):
+            Y[:, b] = syn.observe(rng, a @ syn.sparse_signal(rng, k, 4), None, 30.0)
+            lams[b] = 0.3 * np.max(np.abs(a.T @ Y[:, b]))
+        if B >= 5:
+            Y[:, 1] = 0.0
+            lams[1] = 1.0                                      # exact fit from the start
+            lams[2] = 1.5 * np.max(np.abs(a.T @ Y[:, 2]))      # lambda above lambda_max
+        L = F.lipschitz_bound(F.DenseDictionary(a, backend=cuda))
+        cfg = F.SwitchConfig(screening_interval=10, max_iterations=cap, rel_tolerance=1e-6)
+        opts = F.RunOptions(variant=F.VARIANT_SCREENED, full_lipschitz=[L], collect_trace=True)
+        seq_g = F.ApproxSequence([F.make_exact_approx(F.DenseDictionary(a, backend=cuda))])
+        seq_o = F.ApproxSequence([F.make_exact_approx(F.DenseDictionary(a, backend=oracle16))])
+        res = F.run_lasso_batched(seq_g, Y, lams, cfg, opts, concurrency=0)
+        for b in range(B):
+            o = F.run_lasso(seq_o, Y[:, b], lams[b], cfg, opts)
+            assert res[b].converged == o.converged
+            assert_parity(res[b], o, a, Y[:, b], lams[b])
