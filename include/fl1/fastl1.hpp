@@ -23,7 +23,8 @@
 //   DenseDictionary::load_csv / save_csv / load_blob / save_blob  dictionary.cpp:76-135
 //
 // Extensions (defaults reproduce the reference): SwitchConfig::rel_tolerance,
-// RunOptions::x_init, SukroDictionary column scale. The exact_gram option of the
+// RunOptions::x_init, SukroDictionary column scale. RunOptions::exact_gram is honoured
+// (uploaded to the GPU once per matrix and cached by its data pointer); as in the
 // reference (out of scope) is accepted and ignored, as the reference ignores it
 // while an observer is attached.
 #pragma once
@@ -34,6 +35,7 @@
 #include <functional>
 #include <limits>
 #include <memory>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 #include <utility>
@@ -386,7 +388,7 @@ struct RunOptions {  // fastl1.hpp:85-96
   SolverKind solver = SolverKind::fista;
   RuleKind rule = RuleKind::gap_safe;
   Variant variant = Variant::multi_dict;
-  const Matrix* exact_gram = nullptr;  // accepted, not used (Gram-backed phase is out of scope)
+  const Matrix* exact_gram = nullptr;  // K x K Gram of the exact dictionary: exact phase on G
   const std::vector<double>* full_lipschitz = nullptr;
   bool collect_trace = true;
   ScreenObserver observer;
@@ -425,6 +427,22 @@ inline void observer_trampoline(const fl1_screen_event* ev, void* user) {
   e.dict = &c.seq->dicts[static_cast<size_t>(ev->dict_index)];
   (*c.fn)(e);
 }
+// The Gram matrix uploaded once (sweeps pass the same matrix to every run_lasso).
+inline std::shared_ptr<fl1_dict> gram_handle(const Matrix& g) {
+  static std::mutex mu;
+  static const double* key = nullptr;
+  static Index key_rows = 0;
+  static std::shared_ptr<fl1_dict> cached;
+  std::lock_guard<std::mutex> lock(mu);
+  if (key != g.data() || key_rows != g.rows() || !cached) {
+    fl1_dict* d = nullptr;
+    check(fl1_dict_dense(context(), g.data(), g.rows(), g.cols(), &d));
+    cached.reset(d, [](fl1_dict* p) { fl1_dict_destroy(p); });
+    key = g.data();
+    key_rows = g.rows();
+  }
+  return cached;
+}
 }  // namespace detail
 
 // run_lasso (fastl1.cpp:753-758): the whole solve runs on the GPU.
@@ -454,6 +472,13 @@ inline SolveResult run_lasso(const ApproxSequence& seq, const Vector& y, double 
   if (opts.x_init) {
     if (opts.x_init->size() != seq.exact().op->cols()) throw std::invalid_argument("x_init has wrong length");
     o.x_init = opts.x_init->data();
+  }
+  std::shared_ptr<fl1_dict> gram;
+  if (opts.exact_gram) {
+    if (opts.exact_gram->rows() != seq.exact().op->cols() || opts.exact_gram->cols() != seq.exact().op->cols())
+      throw std::invalid_argument("exact_gram must be K x K");
+    gram = detail::gram_handle(*opts.exact_gram);
+    o.exact_gram = gram.get();
   }
   fl1_result* r = nullptr;
   detail::check(fl1_solve(s.get(), y.data(), lambda, &c, &o, &r));

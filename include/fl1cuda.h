@@ -82,7 +82,7 @@ typedef struct fl1_screen_event {
 } fl1_screen_event;
 typedef void (*fl1_observer_fn)(const fl1_screen_event* ev, void* user);
 
-/* RunOptions (fastl1.hpp:85-96) minus exact_gram, plus warm start. */
+/* RunOptions (fastl1.hpp:85-96) plus warm start. */
 typedef struct fl1_run_options {
   int32_t solver;  /* FL1_FISTA */
   int32_t rule;    /* FL1_RULE_GAP */
@@ -95,6 +95,11 @@ typedef struct fl1_run_options {
   /* EXTENSION (BASELINE config 4): warm start, length K, nullable (reference: x = 0,
    * fastl1.cpp:274). */
   const double* x_init;
+  /* exact_gram (fastl1.hpp:89-91): the K x K Gram matrix of the exact dictionary as a
+   * dense dictionary handle (fl1_gram_create, or fl1_dict_dense of a host G); nullable.
+   * The exact phase then runs on G (fastl1.cpp:283-324, 335-394); ignored while an
+   * observer is attached (fastl1.cpp:278-281). */
+  const struct fl1_dict* exact_gram;
 } fl1_run_options;
 
 /* TraceRow (fastl1.hpp:43-52) */
@@ -224,6 +229,10 @@ void fl1_result_free(fl1_result* r);
 int fl1_lambda_max(fl1_dict* d, const double* y, double* out);
 /* lipschitz_bound (solver.cpp:108-114): cold power iteration x 1.05 on the GPU. */
 int fl1_lipschitz_bound(fl1_dict* d, double* out);
+
+/* G = A^T A of a dense dictionary, computed on the GPU (one fp64 GEMM), as a dense
+ * K x K dictionary handle for fl1_run_options.exact_gram (bench.cpp:180-200). */
+int fl1_gram_create(fl1_dict* a, fl1_dict** out);
 
 /* ---- harness generators (host; the reference's own <random> streams) ---- */
 /* count draws of std::normal_distribution<double>(0, 1) on std::mt19937_64(seed): the

@@ -449,6 +449,8 @@ struct Result {
   int64_t power_steps = 0;
 };
 
+const Op* gram_of(const fl1_dict* d);  // exact_gram handle -> its dense K x K operator
+
 // ---------------------------------------------------------------- Engine (fastl1.cpp:213-749)
 struct Engine {
   const Seq& seq;
@@ -469,6 +471,10 @@ struct Engine {
   double lipschitz = 0.0, inv_l = 0.0;
   Vec lead_vector;
   int64_t active_at_last_l = 0;
+  // Gram-backed exact phase (fastl1.cpp:232-237): tracked G x / G v and A^T y, full K
+  const Op* gram = nullptr;
+  bool gram_mode = false;
+  Vec gx, gv, aty_full;
   Result result;
   uint64_t ledger = 0;
   std::chrono::steady_clock::time_point t_start;
@@ -497,16 +503,44 @@ struct Engine {
     if (cfg.screening_interval < 1) throw std::invalid_argument("screening interval must be >= 1");
     x.assign(static_cast<size_t>(k), 0.0);
     if (opts.x_init) x.assign(opts.x_init, opts.x_init + k);  // extension
+    if (opts.exact_gram) {
+      gram = gram_of(opts.exact_gram);
+      if (!gram->dense || gram->n != k || gram->k != k) throw std::invalid_argument("exact_gram must be K x K");
+    }
     const auto t0 = std::chrono::steady_clock::now();
     setup_dictionary(true);
     result.setup_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
   }
 
-  void setup_dictionary(bool first) {  // 283-324 (gram_mode never set)
+  // use_gram_now (fastl1.cpp:278-281)
+  bool use_gram_now() const {
+    return gram != nullptr && !opts.observer && dict_index == last && seq.at(dict_index).op->dense;
+  }
+
+  void gather_from_full(const Vec& full, Vec& out) const {  // 343-346
+    out.resize(static_cast<size_t>(op.size()));
+    for (int64_t j = 0; j < op.size(); ++j) out[static_cast<size_t>(j)] = full[static_cast<size_t>(op.active()[static_cast<size_t>(j)])];
+  }
+
+  Vec gram_product(const Vec& compact) const {  // 335-341: sum over nonzeros of x_j G(:, active_j)
+    Vec out(static_cast<size_t>(k), 0.0);
+    for (int64_t j = 0; j < static_cast<int64_t>(compact.size()); ++j) {
+      const double xj = compact[static_cast<size_t>(j)];
+      if (xj == 0.0) continue;
+      const double* col = gram->a.data() + static_cast<size_t>(op.active()[static_cast<size_t>(j)]) * static_cast<size_t>(k);
+      for (int64_t i = 0; i < k; ++i) out[static_cast<size_t>(i)] += xj * col[i];
+    }
+    return out;
+  }
+
+  void setup_dictionary(bool first) {  // 283-324
     const Approx& d = seq.at(dict_index);
     if (!first) op.rebase(&d);
+    gram_mode = use_gram_now();
+    if (gram_mode && aty_full.empty()) aty_full = d.op->adjoint(y);
     if (opts.rule == FL1_RULE_DYNAMIC) {
-      aty_active = op.apply_adjoint(y);
+      if (gram_mode) gather_from_full(aty_full, aty_active);
+      else aty_active = op.apply_adjoint(y);
       if (cfg.precompute_aty && aty_exact_active.empty()) {
         const Vec full = seq.exact().op->adjoint(y);
         aty_exact_active.resize(static_cast<size_t>(op.size()));
@@ -522,8 +556,13 @@ struct Engine {
     }
     inv_l = 1.0 / lipschitz;
     active_at_last_l = op.size();
-    u = op.apply(x);
-    v.clear();
+    if (gram_mode) {  // tracked products restart with the new operator
+      gx = gram_product(x);
+      gv.clear();
+    } else {
+      u = op.apply(x);
+      v.clear();
+    }
     momentum_ready = false;
     t_k = 1.0;
   }
@@ -546,8 +585,35 @@ struct Engine {
     Vec rho_g;
   };
 
-  Products compute_products(double momentum) {  // 359-369
+  Products compute_products(double momentum) {  // 359-394
     Products p;
+    if (gram_mode) {  // 373-393: corr = A^T y - G w, residual norms from the dots
+      Vec gw = gx;
+      if (momentum != 0.0)
+        for (int64_t i = 0; i < k; ++i)
+          gw[static_cast<size_t>(i)] = (1.0 + momentum) * gx[static_cast<size_t>(i)] - momentum * gv[static_cast<size_t>(i)];
+      Vec corr_full(static_cast<size_t>(k));
+      for (int64_t i = 0; i < k; ++i) corr_full[static_cast<size_t>(i)] = aty_full[static_cast<size_t>(i)] - gw[static_cast<size_t>(i)];
+      gather_from_full(corr_full, p.corr);
+      Vec gw_active, aty_act;
+      gather_from_full(gw, gw_active);
+      gather_from_full(aty_full, aty_act);
+      Vec w = x;
+      if (momentum != 0.0)
+        for (size_t j = 0; j < w.size(); ++j) w[j] = (1.0 + momentum) * x[j] - momentum * x_prev[j];
+      const double w_aty = dot(w, aty_act), w_gw = dot(w, gw_active);
+      p.rho_g_sq = std::max(y_sqnorm - 2.0 * w_aty + w_gw, 0.0);
+      p.rho_g_dot_y = y_sqnorm - w_aty;
+      if (momentum != 0.0) {
+        Vec gx_active;
+        gather_from_full(gx, gx_active);
+        const double x_aty = dot(x, aty_act), x_gx = dot(x, gx_active);
+        p.rho_x_sq = std::max(y_sqnorm - 2.0 * x_aty + x_gx, 0.0);
+      } else {
+        p.rho_x_sq = p.rho_g_sq;
+      }
+      return p;
+    }
     Vec uw = u;
     if (momentum != 0.0)
       for (int64_t i = 0; i < n; ++i)
@@ -576,8 +642,13 @@ struct Engine {
     double ray_sq = 0, ray_dot_y = 0;
   };
 
-  Vec corr_of_y() const {  // 433-439 / 510-516 (gram branch absent)
+  Vec corr_of_y() const {  // 433-439
     if (opts.rule == FL1_RULE_DYNAMIC && static_cast<int64_t>(aty_active.size()) == op.size()) return aty_active;
+    if (gram_mode) {
+      Vec out;
+      gather_from_full(aty_full, out);
+      return out;
+    }
     return op.apply_adjoint(y);
   }
 
@@ -651,9 +722,14 @@ struct Engine {
       if (keep[static_cast<size_t>(j)]) continue;
       const int g = op.active()[static_cast<size_t>(j)];
       if (fix_history && static_cast<int64_t>(x_prev.size()) == op.size() && x_prev[static_cast<size_t>(j)] != 0.0) {
-        const Vec col = op.column_global(g);
         const double xp = x_prev[static_cast<size_t>(j)];
-        for (int64_t i = 0; i < n; ++i) v[static_cast<size_t>(i)] -= xp * col[static_cast<size_t>(i)];
+        if (gram_mode) {  // 678-679: gv -= x_prev_j G(:, g)
+          const double* col = gram->a.data() + static_cast<size_t>(g) * static_cast<size_t>(k);
+          for (int64_t i = 0; i < k; ++i) gv[static_cast<size_t>(i)] -= xp * col[i];
+        } else {
+          const Vec col = op.column_global(g);
+          for (int64_t i = 0; i < n; ++i) v[static_cast<size_t>(i)] -= xp * col[static_cast<size_t>(i)];
+        }
       }
     }
     auto gather = [&](Vec& vec) {
@@ -760,6 +836,8 @@ struct Engine {
             Vec corr_y;
             if (static_cast<int64_t>(aty_active.size()) == op.size())
               corr_y = aty_active;
+            else if (gram_mode)
+              gather_from_full(aty_full, corr_y);
             else
               corr_y = op.apply_adjoint(y);
             for (size_t j = 0; j < dots.size(); ++j) dots[j] = std::abs(ds.scale_prime * corr_y[j]);
@@ -812,12 +890,14 @@ struct Engine {
         if (opts.solver == FL1_FISTA) {
           if (momentum_ready) t_k = t_next;
           x_prev = x;
-          v = u;
+          if (gram_mode) gv = gx;  // 584-588
+          else v = u;
           momentum_ready = true;
         }
         x = std::move(x_next);
         if (kept_shrinks) apply_restriction(kept_local);
-        u = op.apply(x);
+        if (gram_mode) gx = gram_product(x);  // 596-600
+        else u = op.apply(x);
         x_nnz = count_nonzeros(x);
         if (op.size() * 2 <= active_at_last_l && op.size() > 0 && next_dict == dict_index) {
           lipschitz = restricted_lipschitz();
@@ -885,6 +965,9 @@ struct orc_ctx {
 struct orc_dict {
   std::shared_ptr<const Op> op;
 };
+namespace {
+const Op* gram_of(const fl1_dict* d) { return reinterpret_cast<const orc_dict*>(d)->op.get(); }
+}  // namespace
 struct orc_approx {
   std::shared_ptr<const Approx> a;
 };
@@ -909,6 +992,34 @@ int orc_ctx_create(int device, orc_ctx** out) {
 int orc_ctx_destroy(orc_ctx* ctx) {
   delete ctx;
   return FL1_OK;
+}
+
+int orc_gram_create(orc_dict* d, orc_dict** out) {  // G = A^T A (bench.cpp:190-197)
+  return guard([&] {
+    const Op& a = *d->op;
+    if (!a.dense) throw std::invalid_argument("exact_gram needs a dense dictionary");
+    const int64_t n = a.n, k = a.k;
+    auto op = std::make_shared<Op>();
+    op->dense = true;
+    op->n = k;
+    op->k = k;
+    op->a.assign(static_cast<size_t>(k * k), 0.0);
+#pragma omp parallel for schedule(static) num_threads(g_threads)
+    for (int64_t j = 0; j < k; ++j)
+      for (int64_t i = 0; i <= j; ++i) {
+        double s = 0.0;
+        for (int64_t r = 0; r < n; ++r) s += a.a[static_cast<size_t>(i * n + r)] * a.a[static_cast<size_t>(j * n + r)];
+        op->a[static_cast<size_t>(j * k + i)] = s;
+        op->a[static_cast<size_t>(i * k + j)] = s;
+      }
+    op->norms.resize(static_cast<size_t>(k));
+    for (int64_t j = 0; j < k; ++j) {
+      double s = 0.0;
+      for (int64_t i = 0; i < k; ++i) s += op->a[static_cast<size_t>(j * k + i)] * op->a[static_cast<size_t>(j * k + i)];
+      op->norms[static_cast<size_t>(j)] = std::sqrt(s);
+    }
+    *out = new orc_dict{op};
+  });
 }
 
 int orc_dict_dense(orc_ctx*, const double* a, int64_t n, int64_t k, orc_dict** out) {

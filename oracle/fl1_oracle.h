@@ -40,6 +40,7 @@ int orc_get_threads(void);
 int orc_ctx_create(int device, orc_ctx** out);
 int orc_ctx_destroy(orc_ctx* ctx);
 
+int orc_gram_create(orc_dict* d, orc_dict** out);
 int orc_dict_dense(orc_ctx* ctx, const double* colmajor, int64_t n, int64_t k, orc_dict** out);
 int orc_dict_sukro(orc_ctx* ctx, int32_t n_terms, int64_t m, int64_t q,
                    const double* const* left, const double* const* right,

@@ -56,6 +56,7 @@ class RunOptionsC(C.Structure):
         ("observer", OBSERVER_FN),
         ("observer_user", C.c_void_p),
         ("x_init", C.POINTER(C.c_double)),
+        ("exact_gram", C.c_void_p),
     ]
 
 
@@ -152,6 +153,7 @@ SIGNATURES = {
     "sphere_test": (C.c_double, [C.c_double, C.c_double, C.c_double]),
     "stable_zone_test": (C.c_double, [C.c_double, C.c_double, C.c_double, C.c_double, C.c_double]),
     "stable_ball_test": (C.c_double, [C.c_double, C.c_double, C.c_double, C.c_double, C.c_double]),
+    "gram_create": (C.c_int, [_P, _PP]),
 }
 
 # product-only entry points

@@ -35,6 +35,8 @@ cudaError_t engine_launch(const EngineParams& p, int64_t sukro_m, cudaStream_t s
 size_t prefix_smem_bytes(int64_t ld, int64_t batch);
 cudaError_t prefix_launch(const PrefixParams& p, int device, cudaStream_t stream);
 int prefix_split_max();
+cudaError_t gram_launch(const double* a, int64_t ld, int64_t k, double* g, int64_t ldg, int device,
+                        cudaStream_t stream);
 int64_t prefix_max_atoms();
 cudaError_t engine_cluster_capacity(int64_t ld, int64_t sukro_m, int csize, int* n_clusters);
 cudaError_t engine_launch_clusters(const EngineParams& p0, int n_clusters, int csize, int64_t sukro_m,
@@ -283,11 +285,17 @@ size_t carve(EngineParams& p, char* base, int64_t n, int64_t k, int64_t ld, int 
   p.V = c.take<double>(ld);
   p.rho = c.take<double>(ld);
   p.rho_obs = c.take<double>(ld);
-  // apply partials: at most one chunk per CTA
+  // apply partials: at most one chunk per CTA, of length ld (u = A x) or, in the
+  // Gram-backed exact phase, of the Gram's leading dimension (gx = G x)
   const int64_t chunks = std::max<int64_t>(grid, 8);
-  p.up = c.take<double>(chunks * ld);
-  p.dvp = c.take<double>(chunks * ld);
+  const int64_t plen = std::max(ld, even_ld(kk));
+  p.up = c.take<double>(chunks * plen);
+  p.dvp = c.take<double>(chunks * plen);
   p.pup = c.take<double>(chunks * ld);
+  p.GX = c.take<double>(kk);
+  p.GV = c.take<double>(kk);
+  p.ATYF = c.take<double>(kk);
+  p.ident = c.take<int32_t>(kk);
   p.vec_out = c.take<double>(vec);
   p.corr = c.take<double>(kk);
   p.xnew = c.take<double>(kk);
@@ -585,6 +593,15 @@ void fill_params(EngineParams& p, const SolvePlan& pl, fl1_seq* s, double lambda
   p.observe = opts->observer ? 1 : 0;
   p.has_x_init = opts->x_init ? 1 : 0;
   p.gauss0 = pl.ctx->gauss0(pl.k);
+  p.gram = nullptr;
+  p.gram_ld = 0;
+  if (opts->exact_gram) {  // RunOptions::exact_gram (fastl1.hpp:89-91)
+    const DictImpl& g = *reinterpret_cast<const fl1_dict*>(opts->exact_gram)->d;
+    if (g.kind != fl1::kDense || g.n != pl.k || g.k != pl.k) throw std::invalid_argument("exact_gram must be K x K");
+    if (g.ctx != pl.ctx) throw std::invalid_argument("exact_gram lives on another context");
+    p.gram = g.a->as<double>();
+    p.gram_ld = g.ld;
+  }
 }
 
 // finish (fastl1.cpp:741-748) and SolveResult fields from the final device state
@@ -1381,6 +1398,35 @@ int fl1_lambda_max(fl1_dict* d, const double* y, double* out) {  // screening.cp
     *out = m;
   });
 }
+int fl1_gram_create(fl1_dict* dh, fl1_dict** out) {  // bench.cpp:190-197
+  return guard([&] {
+    if (!dh || !out) throw std::invalid_argument("null argument");
+    const DictImpl& d = *dh->d;
+    if (d.kind != fl1::kDense) throw std::invalid_argument("exact_gram needs a dense dictionary");
+    d.ctx->bind();
+    auto g = std::make_shared<DictImpl>();
+    g->ctx = d.ctx;
+    g->kind = fl1::kDense;
+    g->n = d.k;
+    g->k = d.k;
+    g->ld = even_ld(d.k);
+    g->a = std::make_unique<DevBuf>(static_cast<size_t>(g->ld) * static_cast<size_t>(d.k) * sizeof(double));
+    ck(cudaMemset(g->a->p, 0, g->a->bytes), "memset");
+    ck(fl1::gram_launch(d.a->as<double>(), d.ld, d.k, g->a->as<double>(), g->ld, d.ctx->device, nullptr), "gram");
+    ck(cudaDeviceSynchronize(), "gram sync");
+    // column norms of G (LinearOp::atom_norms2 of the K x K operator)
+    std::vector<double> host(static_cast<size_t>(g->ld) * static_cast<size_t>(d.k));
+    ck(cudaMemcpy(host.data(), g->a->p, host.size() * sizeof(double), cudaMemcpyDeviceToHost), "gram download");
+    g->norms.resize(static_cast<size_t>(d.k));
+    for (int64_t j = 0; j < d.k; ++j) {
+      double s = 0.0;
+      for (int64_t i = 0; i < d.k; ++i) s += host[static_cast<size_t>(j * g->ld + i)] * host[static_cast<size_t>(j * g->ld + i)];
+      g->norms[static_cast<size_t>(j)] = std::sqrt(s);
+    }
+    *out = new fl1_dict{g};
+  });
+}
+
 int fl1_rng_normals(uint64_t seed, int64_t count, double* out) {
   return guard([&] {
     if (count < 0 || (count > 0 && !out)) throw std::invalid_argument("bad output");

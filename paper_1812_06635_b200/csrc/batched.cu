@@ -21,6 +21,7 @@
 #include <cuda_runtime.h>
 #include <math_constants.h>
 
+#include <algorithm>
 #include <cfloat>
 #include <cstdint>
 
@@ -989,6 +990,90 @@ __global__ void __launch_bounds__(kPT, 1) prefix_kernel(const __grid_constant__ 
     grid.sync();
   }
   if (blockIdx.x == 0 && threadIdx.x == 0 && p.steps_out) *p.steps_out = steps;
+}
+
+
+// ---------------------------------------------------------------------------
+// Gram matrix G = A^T A (K x K, leading dimension ldg) of a dense dictionary for
+// the Gram-backed exact phase (RunOptions::exact_gram, bench.cpp:190-197): the
+// same DMMA tiles as the lockstep contraction, both operands columns of A.
+__global__ void __launch_bounds__(kPT, 1) gram_kernel(const double* __restrict__ a, int64_t ld, int64_t k,
+                                                      double* __restrict__ g, int64_t ldg) {
+  extern __shared__ __align__(16) double dsm[];
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31, gi = l >> 2, tg = l & 3;
+  const int n_rt = static_cast<int>((k + kTM - 1) / kTM), n_ct = static_cast<int>((k + kTN - 1) / kTN);
+  const int nch = static_cast<int>((ld + kTK - 1) / kTK);
+  for (int tile = blockIdx.x; tile < n_rt * n_ct; tile += gridDim.x) {
+    const int64_t j0 = static_cast<int64_t>(tile % n_rt) * kTM, c0 = static_cast<int64_t>(tile / n_rt) * kTN;
+    double acc[2][8][2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+      for (int c = 0; c < 8; ++c) acc[h][c][0] = acc[h][c][1] = 0.0;
+    auto issue = [&](int s, int kc) {
+      double* As = dsm + s * kStage;
+      double* Bs = As + kTM * kSS;
+      const int64_t k0 = static_cast<int64_t>(kc) * kTK;
+      for (int e = threadIdx.x; e < kTM * (kTK / 2); e += kPT) {
+        const int r = e / (kTK / 2), kk = (e % (kTK / 2)) * 2;
+        const bool ok = j0 + r < k && k0 + kk < ld;
+        cp16(As + r * kSS + kk, ok ? a + (j0 + r) * ld + k0 + kk : a, ok);
+      }
+      for (int e = threadIdx.x; e < kTN * (kTK / 2); e += kPT) {
+        const int c = e / (kTK / 2), kk = (e % (kTK / 2)) * 2;
+        const bool ok = c0 + c < k && k0 + kk < ld;
+        cp16(Bs + c * kSS + kk, ok ? a + (c0 + c) * ld + k0 + kk : a, ok);
+      }
+    };
+    __syncthreads();
+    issue(0, 0);
+    cp_commit();
+    for (int kc = 0; kc < nch; ++kc) {
+      if (kc + 1 < nch) issue((kc + 1) & 1, kc + 1);
+      cp_commit();
+      cp_wait1();
+      __syncthreads();
+      const double* As = dsm + (kc & 1) * kStage;
+      const double* Bs = As + kTM * kSS;
+#pragma unroll
+      for (int ks = 0; ks < kTK / 4; ++ks) {
+        const double a0v = As[(w * 8 + gi) * kSS + ks * 4 + tg];
+        const double a1v = As[(64 + w * 8 + gi) * kSS + ks * 4 + tg];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          const double bv = Bs[(c * 8 + gi) * kSS + ks * 4 + tg];
+          dmma(acc[0][c], a0v, bv);
+          dmma(acc[1][c], a1v, bv);
+        }
+      }
+      __syncthreads();
+    }
+    cp_wait0();
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int64_t i = j0 + h * 64 + w * 8 + gi;
+#pragma unroll
+      for (int c = 0; c < 8; ++c)
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const int64_t j = c0 + c * 8 + 2 * tg + q;
+          if (i < k && j < k) g[j * ldg + i] = acc[h][c][q];
+        }
+    }
+  }
+}
+
+cudaError_t gram_launch(const double* a, int64_t ld, int64_t k, double* g, int64_t ldg, int device,
+                        cudaStream_t stream) {
+  const size_t smem = static_cast<size_t>(2 * kStage) * sizeof(double);
+  cudaError_t e = cudaFuncSetAttribute(gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  if (e != cudaSuccess) return e;
+  int sms = 0;
+  e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  if (e != cudaSuccess) return e;
+  const int64_t tiles = ((k + kTM - 1) / kTM) * ((k + kTN - 1) / kTN);
+  gram_kernel<<<static_cast<unsigned>(std::min<int64_t>(tiles, 4 * sms)), kPT, smem, stream>>>(a, ld, k, g, ldg);
+  return cudaGetLastError();
 }
 
 size_t prefix_smem_bytes(int64_t ld, int64_t batch) {

@@ -90,6 +90,10 @@ enum Slot {
 // ||x||_1 partials for iteration t live in kSlL1 (t even) / kSlL1b (t odd); written
 // by phase B of iteration t-1 (over the kept new iterate) or by the constructor.
 constexpr int kSlL1b = 16;
+constexpr int kSlGwa = 17;   // Gram mode: w . A^T y   (w = extrapolated x)
+constexpr int kSlGwg = 18;   //            w . G w
+constexpr int kSlGxa = 19;   //            x . A^T y
+constexpr int kSlGxg = 20;   //            x . G x
 
 // Virtual grid: the engine runs either on the whole GPU (one cooperative launch,
 // grid-wide barrier) or inside one thread-block cluster per solve (batched mode,
@@ -814,8 +818,8 @@ struct ApplySrc {
 // columns' units through the same three-stage register ring (kV x 128-bit
 // loads per lane) into per-lane accumulators. Warp partials are added in warp
 // order in shared memory; out[c*ld + row] holds chunk c's partial sum.
-__device__ __forceinline__ int dense_apply_chunks(const EngineParams& p, int64_t S) {
-  const int64_t U = (p.n + kUnit - 1) / kUnit;
+__device__ __forceinline__ int dense_apply_chunks(const EngineParams& p, const DevLevel& lv, int64_t S) {
+  const int64_t U = ((lv.rows ? lv.rows : p.n) + kUnit - 1) / kUnit;
   int64_t c = p.grid / U;
   const int64_t by_work = (S + 31) / 32;  // at least ~2 positions per warp
   if (c > by_work) c = by_work;
@@ -825,10 +829,10 @@ __device__ __forceinline__ int dense_apply_chunks(const EngineParams& p, int64_t
 __device__ __noinline__ void dense_apply_units(const EngineParams& p, const DevLevel& lv, const ApplySrc& src,
                                                int64_t S, bool fix, double* __restrict__ out, double* red) {
   constexpr int kV = kUnit / 64;
-  const int64_t n = p.n, ld = p.ld, ld2 = ld >> 1;
+  const int64_t n = lv.rows ? lv.rows : p.n, ld = lv.rows ? lv.ld : p.ld, ld2 = ld >> 1;
   const int U = static_cast<int>((n + kUnit - 1) / kUnit);
   const int last_nd2 = static_cast<int>(((n - static_cast<int64_t>(U - 1) * kUnit) + 1) >> 1);
-  const int C = dense_apply_chunks(p, S);
+  const int C = dense_apply_chunks(p, lv, S);
   const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
   const double2* __restrict__ A2 = reinterpret_cast<const double2*>(lv.a) + l;
   for (int64_t item = vrank(); item < static_cast<int64_t>(U) * C; item += vsize()) {
@@ -1039,7 +1043,7 @@ __device__ int op_apply_partials(const EngineParams& p, Sh& sh, const DevLevel& 
   if (lv.kind == kDense) {
     dense_apply_units(p, lv, src, S, false, out, red);
     if (fix_out) dense_apply_units(p, lv, src, S, true, fix_out, red);
-    return dense_apply_chunks(p, S);
+    return dense_apply_chunks(p, lv, S);
   }
   return sukro_apply_partials(p, sh, lv, src, S, out, fix_out, red);
 }
@@ -1247,6 +1251,77 @@ __device__ __forceinline__ double next_momentum(const EngineParams& p, double t_
 // ||x||_1 partial of this CTA's slice into the slot of iteration t
 __device__ __forceinline__ int l1_slot(uint64_t t) { return (t & 1) ? kSlL1b : kSlL1; }
 
+// Gram-mode compute_products (fastl1.cpp:373-393) on this CTA's slice: corr_j =
+// aty_j - gw_j with gw = (1+m) gx - m gv, the y-ray correlations aty_j, both pairs of
+// dual-scaling maxima (eps = 0 on the exact dictionary), and partials of w.aty, w.gw,
+// x.aty, x.gx (w = (1+m) x - m x_prev) for ||rho_g||^2, rho_g.y and ||y - A x||^2.
+__device__ __noinline__ void gram_products(const EngineParams& p, Sh& sh, const Bank& bk, int64_t S, double m) {
+  int64_t lo, hi;
+  slice(S, lo, hi);
+  const bool mom = m != 0.0;
+  double mp = 0.0, mpy = 0.0, wa = 0.0, wg = 0.0, xa = 0.0, xg = 0.0;
+  for (int64_t q = lo + threadIdx.x; q < hi; q += kThreads) {
+    const int64_t j = bk.idx[q];
+    const double gx = __ldcg(p.GX + j), aty = __ldcg(p.ATYF + j);
+    const double xo = bk.x[q];
+    const double gw = mom ? (1.0 + m) * gx - m * __ldcg(p.GV + j) : gx;
+    const double w = mom ? (1.0 + m) * xo - m * bk.xp[q] : xo;
+    const double c = aty - gw;
+    p.corr[q] = c;
+    p.corr_y[q] = aty;
+    mp = fmax(mp, fabs(c));
+    mpy = fmax(mpy, fabs(aty) / p.lambda);
+    wa = fma(w, aty, wa);
+    wg = fma(w, gw, wg);
+    if (mom) {
+      xa = fma(xo, aty, xa);
+      xg = fma(xo, gx, xg);
+    }
+  }
+  double v[4] = {mp, mpy, wa, wg};
+  const bool mx[4] = {true, true, false, false};
+  block_reduce<4>(v, mx, sh);
+  double v2[2] = {xa, xg};
+  const bool mx2[2] = {false, false};
+  block_reduce<2>(v2, mx2, sh);
+  if (threadIdx.x == 0) {
+    put_slot(p, kSlMaxPlain, v[0]);
+    put_slot(p, kSlMaxStable, v[0]);  // + eps_j |rho| with eps = 0
+    put_slot(p, kSlMaxPlainY, v[1]);
+    put_slot(p, kSlMaxStableY, v[1]);
+    put_slot(p, kSlGwa, v[2]);
+    put_slot(p, kSlGwg, v[3]);
+    put_slot(p, kSlGxa, v2[0]);
+    put_slot(p, kSlGxg, v2[1]);
+  }
+}
+
+// The Gram matrix as a dense K x K operator level (apply only).
+__device__ __forceinline__ DevLevel gram_level(const EngineParams& p) {
+  DevLevel g{};
+  g.kind = kDense;
+  g.a = p.gram;
+  g.rows = p.k;
+  g.ld = p.gram_ld;
+  return g;
+}
+
+// Gram-mode phase E (fastl1.cpp:584-600, 678-679): GX = sum of the G x partials; with
+// shift, GV = GX_old - fix (the history fix over dropped atoms, G columns).
+__device__ void combine_g(const EngineParams& p, int C, bool shift, bool fix) {
+  int64_t lo, hi;
+  slice(p.k, lo, hi);
+  const int64_t ldg = p.gram_ld;
+  for (int64_t i = lo + threadIdx.x; i < hi; i += kThreads) {
+    double u = 0.0, f = 0.0;
+    for (int c = 0; c < C; ++c) u += __ldcg(p.up + static_cast<int64_t>(c) * ldg + i);
+    if (fix)
+      for (int c = 0; c < C; ++c) f += __ldcg(p.dvp + static_cast<int64_t>(c) * ldg + i);
+    if (shift) __stcg(p.GV + i, __ldcg(p.GX + i) - f);
+    __stcg(p.GX + i, u);
+  }
+}
+
 // setup_dictionary (fastl1.cpp:283-324). first: constructor call.
 __device__ __noinline__ void setup_dictionary(const EngineParams& p, Sh& sh, bool first, const Scratch& sc) {
   EngineState& s = sh.s;
@@ -1285,11 +1360,23 @@ __device__ __noinline__ void setup_dictionary(const EngineParams& p, Sh& sh, boo
     s.inv_l = 1.0 / s.lipschitz;
     s.active_at_last_l = s.S;
   }
-  // u = op.apply(x)
+  // use_gram_now (278-281): exact level, a Gram matrix, no observer
+  const bool gram = p.gram && !p.observe && s.dict_index == p.n_levels - 1;
+  if (threadIdx.x == 0) s.gram_mode = gram ? 1 : 0;
+  if (gram && !s.atyf_valid) {  // aty_full = A^T y over every atom (288-290)
+    load_vec_smem(p, p.y, sc.vec);
+    PassOut pa{p.ATYF, 0, 0.0, false, 0, 0, nullptr};
+    op_adjoint(p, sh, lv, p.ident, lv.eps, p.k, sc.vec, sc.rt, pa);
+    if (threadIdx.x == 0) s.atyf_valid = 1;
+    vsync();
+  }
+  // u = op.apply(x), or gx = G x in Gram mode (315-321)
   ApplySrc as{bk.idx, bk.x, nullptr, 1.0, nullptr, nullptr, nullptr};
-  const int C = op_apply_partials(p, sh, lv, as, s.S, p.up, nullptr, sc.red);
+  const DevLevel glv = gram_level(p);
+  const int C = op_apply_partials(p, sh, gram ? glv : lv, as, s.S, p.up, nullptr, sc.red);
   vsync();
-  combine_u(p, sh, C, false, false, 0.0);  // momentum restarts (fastl1.cpp:322-323)
+  if (gram) combine_g(p, C, false, false);
+  else combine_u(p, sh, C, false, false, 0.0);  // momentum restarts (fastl1.cpp:322-323)
   if (threadIdx.x == 0) {
     s.momentum_ready = 0;
     s.t_k = 1.0;
@@ -1366,6 +1453,8 @@ __device__ __noinline__ void engine_body(const EngineParams& p, Sh& sh, double* 
     const Handoff* hd = p.handoff;  // resume from the batched lockstep engine
     const int64_t S0 = hd ? hd->S : k;
     int64_t lo, hi;
+    slice(k, lo, hi);
+    for (int64_t q = lo + threadIdx.x; q < hi; q += kThreads) p.ident[q] = static_cast<int32_t>(q);
     slice(S0, lo, hi);
     for (int64_t q = lo + threadIdx.x; q < hi; q += kThreads) {
       bk.idx[q] = hd ? __ldcg(hd->idx + q) : static_cast<int32_t>(q);
@@ -1456,7 +1545,8 @@ __device__ __noinline__ void engine_body(const EngineParams& p, Sh& sh, double* 
       t_next = 0.5 * (1.0 + sqrt(1.0 + 4.0 * s.t_k * s.t_k));
       momentum = (s.t_k - 1.0) / t_next;
     }
-    {  // compute_products (359-369): rho_g was formed by the previous combine phase
+    const bool gram = s.gram_mode != 0;
+    if (!gram) {  // compute_products (359-369): rho_g was formed by the previous combine phase
       // the three slot sums are reduced by warps 0-2 while every thread's rho loads are in flight
       {
         const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
@@ -1483,8 +1573,10 @@ __device__ __noinline__ void engine_body(const EngineParams& p, Sh& sh, double* 
       }
       __syncthreads();
     }
-    const bool exact_fit = !(sh.rho_sq > 0.0);
-    if (!exact_fit) {
+    bool exact_fit = !gram && !(sh.rho_sq > 0.0);  // Gram mode decides after the phase-B reduction
+    if (gram) {
+      gram_products(p, sh, bk, S, momentum);
+    } else if (!exact_fit) {
       // corr = A_S^T rho_g fused with the dual-scaling maxima (414-418)
       PassOut po{p.corr, 1, sh.rho_norm, false, kSlMaxPlain, kSlMaxStable, nullptr};
       op_adjoint(p, sh, lv, bk.idx, bk.eps, S, sc.vec, sc.rt, po);
@@ -1532,7 +1624,7 @@ __device__ __noinline__ void engine_body(const EngineParams& p, Sh& sh, double* 
         pre.c = p.corr[q];
         pre.xo = bk.x[q];
         pre.xpv = bk.xp[q];
-        pre.cy = exact_fit ? p.corr_y[q] : 0.0;
+        pre.cy = (exact_fit || gram) ? p.corr_y[q] : 0.0;
         pre.eps = bk.eps[q];
         pre.en = bk.en[q];
         pre.an = bk.an[q];
@@ -1540,9 +1632,26 @@ __device__ __noinline__ void engine_body(const EngineParams& p, Sh& sh, double* 
       }
     }
     const int l1s = l1_slot(s.t);
-    grid_reduce(p, sh, 1u << l1s,
-                exact_fit ? ((1u << kSlMaxPlainY) | (1u << kSlMaxStableY))
-                          : ((1u << kSlMaxPlain) | (1u << kSlMaxStable)));
+    if (gram) {
+      grid_reduce(p, sh, (1u << l1s) | (1u << kSlGwa) | (1u << kSlGwg) | (1u << kSlGxa) | (1u << kSlGxg),
+                  (1u << kSlMaxPlainY) | (1u << kSlMaxStableY) | (1u << kSlMaxPlain) | (1u << kSlMaxStable));
+      // residual norms from the Gram dots (fastl1.cpp:385-393)
+      const double ysq = s.y_sq;
+      const double rgs = fmax(ysq - 2.0 * sh.res[kSlGwa] + sh.res[kSlGwg], 0.0);
+      exact_fit = !(rgs > 0.0);
+      if (threadIdx.x == 0) {
+        sh.t_next = t_next;
+        sh.rho_sq = rgs;
+        sh.rho_dot_y = ysq - sh.res[kSlGwa];
+        sh.rho_x_sq = momentum != 0.0 ? fmax(ysq - 2.0 * sh.res[kSlGxa] + sh.res[kSlGxg], 0.0) : rgs;
+        sh.rho_norm = sqrt(rgs);
+      }
+      __syncthreads();
+    } else {
+      grid_reduce(p, sh, 1u << l1s,
+                  exact_fit ? ((1u << kSlMaxPlainY) | (1u << kSlMaxStableY))
+                            : ((1u << kSlMaxPlain) | (1u << kSlMaxStable)));
+    }
     if (threadIdx.x == 0) {
       const double x_l1 = sh.res[l1s];
       const double primal = 0.5 * sh.rho_x_sq + lambda * x_l1;
@@ -1681,7 +1790,8 @@ __device__ __noinline__ void engine_body(const EngineParams& p, Sh& sh, double* 
     if (!stop_now) {
       if (lv.kind == kDense) {
         ApplySrc as{bk.idx, nullptr, nullptr, 1.0, nullptr, nullptr, &px};
-        C_apply = op_apply_partials(p, sh, lv, as, S, p.up, fix_pass ? p.dvp : nullptr, sc.red);
+        const DevLevel glv = gram_level(p);  // Gram mode: gx = G x, gv fix over G columns (596-600, 678-679)
+        C_apply = op_apply_partials(p, sh, gram ? glv : lv, as, S, p.up, fix_pass ? p.dvp : nullptr, sc.red);
       } else {
         __syncthreads();
         ApplySrc as{bk.idx, p.xnew, nullptr, 1.0, bk.keep, fix_pass ? bk.x : nullptr, nullptr};
@@ -1825,7 +1935,8 @@ __device__ __noinline__ void engine_body(const EngineParams& p, Sh& sh, double* 
     }
     {  // combine u (and v <- u_old - fix), then the next iteration's rho_g
       const double tk_next = fista ? (s.momentum_ready ? sh.t_next : s.t_k) : s.t_k;
-      combine_u(p, sh, C_apply, fista, fix_pass, next_momentum(p, tk_next, fista));
+      if (gram) combine_g(p, C_apply, fista, fix_pass);
+      else combine_u(p, sh, C_apply, fista, fix_pass, next_momentum(p, tk_next, fista));
     }
     if (threadIdx.x == 0) {
       if (fista) {  // 581-590

@@ -45,6 +45,7 @@ struct DevLevel {
   double op_err;
   double rc;
   uint64_t matvec_flops;
+  int64_t rows, ld;         // dense operator shape when not the dictionary's (Gram: K, ldG); 0 = p.n, p.ld
 };
 
 // Per-atom arrays over the preserved set, in position order (ActiveOp state,
@@ -95,6 +96,8 @@ struct EngineState {
   int32_t fix_pending;   // dvp holds a v correction to apply
   int32_t lead_valid;    // bank lead holds S entries
   int32_t atye_valid;
+  int32_t gram_mode;     // exact phase on the Gram matrix (fastl1.cpp:278-281)
+  int32_t atyf_valid;    // aty_full holds A^T y over all K atoms
   int32_t n_switches;
   int32_t converged;
   int32_t event;
@@ -280,11 +283,17 @@ struct alignas(16) EngineParams {
   fl1_switch_event* sw;
   EngineState* st;
   uint64_t* timeline;  // FL1_TIMELINE builds only: [iter][cta][8] %globaltimer marks
+  const double* gram;      // nullable: K x K Gram of the exact dictionary (RunOptions::exact_gram)
+  int64_t gram_ld;
+  double* GX;              // K: G x (Gram mode's u)
+  double* GV;              // K: G x_prev history (Gram mode's v)
+  double* ATYF;            // K: A^T y over all atoms (Gram mode)
+  int32_t* ident;          // K: 0..K-1 (full-dictionary passes)
   const BatchDesc* batch;  // non-null: cluster (batched) mode
   const Handoff* handoff;  // non-null: solve resumes from a lockstep-prefix state
 };
 
-constexpr int kBred = 20;  // doubles of per-CTA partials (slots, see engine.cu)
+constexpr int kBred = 24;  // doubles of per-CTA partials (slots, see engine.cu)
 constexpr int kApplyCap = 1024;  // positions compacted per apply sub-chunk
 constexpr int kSukroMaxM = 128;
 constexpr int kSukroMaxQ = 256;

@@ -190,6 +190,23 @@ class DenseDictionary(LinearOp):
         self._lib().check(self._lib().dict_dense(self.backend.ctx, _dptr(a), n, k, C.byref(self._h)))
 
 
+class _Handle(LinearOp):
+    """A dictionary handle produced by the library (e.g. a Gram matrix)."""
+
+    def __init__(self, h, backend: Backend):
+        self.backend = backend
+        self._h = h
+
+
+def gram_matrix(d: LinearOp) -> LinearOp:
+    """G = A^T A of a dense dictionary as a dense K x K dictionary, computed by the
+    backend (one GPU GEMM; the oracle on the host) -- RunOptions.exact_gram
+    (fastl1.hpp:89-91), as the reference harness builds it (bench.cpp:190-197)."""
+    h = C.c_void_p()
+    d._lib().check(d._lib().gram_create(d._h, C.byref(h)))
+    return _Handle(h, d.backend)
+
+
 class DenseDictionaryDevice(LinearOp):
     """Dense dictionary uploaded from a device pointer (torch tensor data_ptr)."""
 
@@ -324,6 +341,7 @@ class RunOptions:  # fastl1.hpp:85-96
     collect_trace: bool = True
     observer: Optional[Callable[[ScreeningEvent], None]] = None
     x_init: Optional[np.ndarray] = None  # extension: warm start
+    exact_gram: Optional["LinearOp"] = None  # K x K Gram of the exact dictionary (gram_matrix)
 
 
 TRACE_DTYPE = np.dtype([("iter", "<u8"), ("dict_index", "<i4"), ("active_size", "<i4"), ("gap", "<f8"),
@@ -390,6 +408,9 @@ def _run_options_c(opts: RunOptions, keep: list) -> _abi.RunOptionsC:
         o.full_lipschitz = _dptr(fl)
         o.n_full_lipschitz = fl.size
     o.collect_trace = 1 if opts.collect_trace else 0
+    if opts.exact_gram is not None:
+        keep.append(opts.exact_gram)
+        o.exact_gram = opts.exact_gram._h
     if opts.observer is not None:
         user = opts.observer
 

@@ -17,10 +17,9 @@ normal / bernoulli distributions, exported by libfl1cuda.so), so a config and se
 give the reference's dictionaries and signals up to the rounding of the linear
 algebra (QR / SVD via LAPACK or cuSOLVER instead of Eigen).
 
-Every solve goes through fastl1.run_lasso / run_lasso_batched on the GPU. The
-reference's sweep passes an exact Gram matrix (use_gram) to speed up its CPU exact
-phase; the CUDA engine computes the same products directly (RunOptions.exact_gram
-is accepted and ignored, INTEGRATION.md).
+Every solve goes through fastl1.run_lasso on the GPU. With use_gram (the reference's
+default) the sweep builds the exact dictionary's Gram matrix once on the GPU and the
+exact phase of every run is Gram-backed, as in the reference.
 """
 from __future__ import annotations
 
@@ -489,13 +488,16 @@ class SweepContext:
     dense: F.DenseDictionary
     seq: F.ApproxSequence
     full_lipschitz: List[float]
+    gram: Optional[F.LinearOp] = None
 
 
 def build_context(config: ExperimentConfig, a: np.ndarray, backend: Optional[F.Backend] = None) -> SweepContext:
-    """bench.cpp:180-200 (the Gram matrix is not needed by the CUDA engine)."""
+    """bench.cpp:180-200: the approximation sequence, the per-level Lipschitz cache and
+    (use_gram) the exact dictionary's Gram matrix, built once per sweep on the GPU."""
     seq = sukro_sequence(a, config.ranks, backend=backend, rc_override=config.rc_override)
     full_l = [F.lipschitz_bound(d.op) for d in seq.dicts]
-    return SweepContext(seq.exact().op, seq, full_l)
+    gram = F.gram_matrix(seq.exact().op) if config.use_gram else None
+    return SweepContext(seq.exact().op, seq, full_l, gram)
 
 
 def execute_run(config: ExperimentConfig, ctx: SweepContext, y: np.ndarray, lambda_ratio: float, trial: int,
@@ -504,7 +506,7 @@ def execute_run(config: ExperimentConfig, ctx: SweepContext, y: np.ndarray, lamb
     sw = F.SwitchConfig(gamma_threshold=config.resolved_gamma(), screening_interval=config.screen_interval,
                         tolerance=config.tol, max_iterations=config.max_iter, precompute_aty=config.precompute_aty)
     opts = F.RunOptions(solver=config.solver, rule=config.rule, variant=variant, full_lipschitz=ctx.full_lipschitz,
-                        collect_trace=True)
+                        collect_trace=True, exact_gram=ctx.gram)
     res = F.run_lasso(ctx.seq, y, lambda_ratio * lmax, sw, opts)
     return RunRecord(run_id=run_id, trial=trial, lambda_ratio=lambda_ratio, variant=variant,
                      iterations=res.iterations if res.iterations else len(res.trace), flops=res.total_flops,

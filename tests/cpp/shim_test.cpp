@@ -75,6 +75,23 @@ int main() {
   bool rows_match = false;
   CHECK(recompute_flops(res.trace, seq, Variant::screened, n, k, &rows_match) == res.total_flops && rows_match);
 
+  // Gram-backed exact phase (fastl1.cpp:278-394): same trajectory as the direct products
+  Matrix gram(k, k);
+  for (Index j = 0; j < k; ++j)
+    for (Index i = 0; i < k; ++i) {
+      double acc = 0.0;
+      for (Index r = 0; r < n; ++r) acc += a(r, i) * a(r, j);
+      gram(i, j) = acc;
+    }
+  RunOptions gopts = opts;
+  gopts.observer = nullptr;  // the reference ignores the Gram while an observer is attached
+  gopts.exact_gram = &gram;
+  const SolveResult gres = run_lasso(seq, y, 0.2 * lmax, cfg, gopts);
+  CHECK(gres.converged && gres.iterations == res.iterations && gres.total_flops == res.total_flops);
+  double xdiff = 0.0;
+  for (Index j = 0; j < k; ++j) xdiff = std::max(xdiff, std::abs(gres.x(j) - res.x(j)));
+  CHECK(xdiff <= 1e-9);
+
   // invalid arguments surface as std::invalid_argument (fastl1.cpp:268-273)
   bool threw = false;
   try {
