@@ -37,6 +37,7 @@ cudaError_t prefix_launch(const PrefixParams& p, int device, cudaStream_t stream
 int prefix_split_max();
 cudaError_t gram_launch(const double* a, int64_t ld, int64_t k, double* g, int64_t ldg, int device,
                         cudaStream_t stream);
+cudaError_t colnorm_launch(const double* g, int64_t k, int64_t ldg, double* out, cudaStream_t stream);
 int64_t prefix_max_atoms();
 cudaError_t engine_cluster_capacity(int64_t ld, int64_t sukro_m, int csize, int* n_clusters);
 cudaError_t engine_launch_clusters(const EngineParams& p0, int n_clusters, int csize, int64_t sukro_m,
@@ -1414,15 +1415,11 @@ int fl1_gram_create(fl1_dict* dh, fl1_dict** out) {  // bench.cpp:190-197
     ck(cudaMemset(g->a->p, 0, g->a->bytes), "memset");
     ck(fl1::gram_launch(d.a->as<double>(), d.ld, d.k, g->a->as<double>(), g->ld, d.ctx->device, nullptr), "gram");
     ck(cudaDeviceSynchronize(), "gram sync");
-    // column norms of G (LinearOp::atom_norms2 of the K x K operator)
-    std::vector<double> host(static_cast<size_t>(g->ld) * static_cast<size_t>(d.k));
-    ck(cudaMemcpy(host.data(), g->a->p, host.size() * sizeof(double), cudaMemcpyDeviceToHost), "gram download");
+    // column norms of G (LinearOp::atom_norms2 of the K x K operator), on the device
+    DevBuf nrm(static_cast<size_t>(d.k) * sizeof(double));
+    ck(fl1::colnorm_launch(g->a->as<double>(), d.k, g->ld, nrm.as<double>(), nullptr), "gram norms");
     g->norms.resize(static_cast<size_t>(d.k));
-    for (int64_t j = 0; j < d.k; ++j) {
-      double s = 0.0;
-      for (int64_t i = 0; i < d.k; ++i) s += host[static_cast<size_t>(j * g->ld + i)] * host[static_cast<size_t>(j * g->ld + i)];
-      g->norms[static_cast<size_t>(j)] = std::sqrt(s);
-    }
+    ck(cudaMemcpy(g->norms.data(), nrm.p, nrm.bytes, cudaMemcpyDeviceToHost), "gram norms download");
     *out = new fl1_dict{g};
   });
 }

@@ -1063,6 +1063,27 @@ __global__ void __launch_bounds__(kPT, 1) gram_kernel(const double* __restrict__
   }
 }
 
+// column 2-norms of a column-major k x k matrix (one warp per column, fixed order)
+__global__ void colnorm_kernel(const double* __restrict__ g, int64_t k, int64_t ldg, double* __restrict__ out) {
+  const int64_t col = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int l = threadIdx.x & 31;
+  if (col >= k) return;
+  double s = 0.0;
+  for (int64_t i = l; i < k; i += 32) {
+    const double v = g[col * ldg + i];
+    s = fma(v, v, s);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(kAll, s, o);
+  if (l == 0) out[col] = sqrt(s);
+}
+
+cudaError_t colnorm_launch(const double* g, int64_t k, int64_t ldg, double* out, cudaStream_t stream) {
+  const int64_t threads = k * 32;
+  colnorm_kernel<<<static_cast<unsigned>((threads + 255) / 256), 256, 0, stream>>>(g, k, ldg, out);
+  return cudaGetLastError();
+}
+
 cudaError_t gram_launch(const double* a, int64_t ld, int64_t k, double* g, int64_t ldg, int device,
                         cudaStream_t stream) {
   const size_t smem = static_cast<size_t>(2 * kStage) * sizeof(double);
