@@ -992,20 +992,13 @@ int fl1_seq_destroy(fl1_seq* s) {
   return guard([&] { delete s; });
 }
 
-int fl1_solve(fl1_seq* s, const double* y, double lambda, const fl1_switch_config* cfg,
-              const fl1_run_options* opts, fl1_result** out) {
-  return guard([&] { do_solve(s, y, false, lambda, cfg, opts, out); });
-}
-int fl1_solve_device(fl1_seq* s, const double* y, double lambda, const fl1_switch_config* cfg,
-                     const fl1_run_options* opts, fl1_result** out) {
-  return guard([&] { do_solve(s, y, true, lambda, cfg, opts, out); });
-}
 namespace {
 // Batched solves in ONE launch: every thread-block cluster of `csize` CTAs is a
 // virtual grid with its own workspace and pulls signals from a device queue
 // (each signal runs the same Engine::run as fl1_solve, with cluster barriers).
 void solve_clusters(fl1_seq* s, const double* Y, bool y_device, int64_t ldy, const double* lambdas, int32_t batch,
-                    const fl1_switch_config* cfg, const fl1_run_options* opts, int csize, fl1_result** out) {
+                    const fl1_switch_config* cfg, const fl1_run_options* opts, int csize, fl1_result** out,
+                    bool allow_prefix = true) {
   const SolvePlan pl = plan_solve(s, cfg, opts);
   for (int32_t b = 0; b < batch; ++b)
     if (!(lambdas[b] > 0)) throw std::invalid_argument("lambda must be positive");
@@ -1127,7 +1120,7 @@ void solve_clusters(fl1_seq* s, const double* Y, bool y_device, int64_t ldy, con
   int32_t* d_steps = nullptr;
   const ApproxImpl& ex = *s->lv.back();
   const char* pe = std::getenv("FL1_BATCH_PREFIX");
-  const bool use_prefix = batch > 0 && pl.levels == 1 && ex.dict->kind == fl1::kDense &&
+  const bool use_prefix = allow_prefix && batch > 0 && pl.levels == 1 && ex.dict->kind == fl1::kDense &&
                           opts->rule == FL1_RULE_GAP &&
                           (opts->variant == FL1_SCREENED || opts->variant == FL1_PLAIN) &&
                           opts->full_lipschitz != nullptr && k <= fl1::prefix_max_atoms() &&
@@ -1276,6 +1269,33 @@ void solve_clusters(fl1_seq* s, const double* Y, bool y_device, int64_t ldy, con
   }
 }
 
+// A single solve on a small, L2-resident dictionary is latency-bound: one
+// thread-block cluster of 16 CTAs (cluster barriers instead of grid barriers) beats
+// the full cooperative grid (measured c1: 1.21 vs 1.58 ms). Larger dictionaries
+// need every SM's bandwidth. Observers, x_init and forced trace flushes keep the
+// grid path; FL1_SINGLE_CLUSTER=0 disables the route.
+constexpr int64_t kSingleClusterBytes = 16ll << 20;
+constexpr int kSingleClusterSize = 16;
+
+void solve_single(fl1_seq* s, const double* y, bool y_device, double lambda, const fl1_switch_config* cfg,
+                  const fl1_run_options* opts, fl1_result** out) {
+  if (s && cfg && opts && out && !opts->observer && !opts->x_init && !std::getenv("FL1_TRACE_CAP")) {
+    const char* e = std::getenv("FL1_SINGLE_CLUSTER");
+    int64_t bytes = 0;
+    for (const auto& l : s->lv) {
+      const DictImpl& d = *l->dict;
+      bytes += d.kind == fl1::kDense ? 8 * d.ld * d.k : 8 * 2 * static_cast<int64_t>(d.nterms) * d.m * d.q;
+    }
+    if (opts->exact_gram) bytes += 8 * s->lv.back()->dict->k * s->lv.back()->dict->k;
+    if (!(e && e[0] == '0') && bytes <= kSingleClusterBytes) {
+      solve_clusters(s, y, y_device, s->lv.back()->dict->n, &lambda, 1, cfg, opts, kSingleClusterSize, out, false);
+      return;
+    }
+  }
+  do_solve(s, y, y_device, lambda, cfg, opts, out);
+}
+
+
 int solve_batched_impl(fl1_seq* s, const double* Y, bool y_device, int64_t ldy, const double* lambdas, int32_t batch,
                        const fl1_switch_config* cfg, const fl1_run_options* opts, int32_t concurrency,
                        fl1_result** out) {
@@ -1342,6 +1362,14 @@ int solve_batched_impl(fl1_seq* s, const double* Y, bool y_device, int64_t ldy, 
 }
 }  // namespace
 
+int fl1_solve(fl1_seq* s, const double* y, double lambda, const fl1_switch_config* cfg,
+              const fl1_run_options* opts, fl1_result** out) {
+  return guard([&] { solve_single(s, y, false, lambda, cfg, opts, out); });
+}
+int fl1_solve_device(fl1_seq* s, const double* y, double lambda, const fl1_switch_config* cfg,
+                     const fl1_run_options* opts, fl1_result** out) {
+  return guard([&] { solve_single(s, y, true, lambda, cfg, opts, out); });
+}
 int fl1_solve_batched(fl1_seq* s, const double* Y, int64_t ldy, const double* lambdas, int32_t batch,
                       const fl1_switch_config* cfg, const fl1_run_options* opts, int32_t concurrency,
                       fl1_result** out) {

@@ -150,7 +150,9 @@ def test_bit_reproducible(cuda):
 
 def test_trace_flush_and_resume(cuda, monkeypatch):
     """A device trace buffer smaller than the run forces kernel exits + resumes; the
-    trajectory is unchanged bit for bit."""
+    trajectory is unchanged bit for bit (both runs on the full grid: the flush path
+    does not take the single-cluster route)."""
+    monkeypatch.setenv("FL1_SINGLE_CLUSTER", "0")
     inst = syn.dense_instance("c1")
     seq = F.ApproxSequence([F.make_exact_approx(F.DenseDictionary(inst.a, backend=cuda))])
     cfg = F.SwitchConfig(screening_interval=10, max_iterations=5000, rel_tolerance=1e-6)
@@ -382,3 +384,19 @@ def test_batched_lockstep_edge_cases(cuda, oracle16, monkeypatch, policy):
             o = F.run_lasso(seq_o, Y[:, b], lams[b], cfg, opts)
             assert res[b].converged == o.converged
             assert_parity(res[b], o, a, Y[:, b], lams[b])
+
+
+def test_single_cluster_route_matches_grid(cuda, oracle16, monkeypatch):
+    """Small dictionaries solve on one 16-CTA cluster (cheaper barriers); the grid
+    route gives the same trajectory and both match the oracle."""
+    inst = syn.dense_instance("c1")
+    seq = F.ApproxSequence([F.make_exact_approx(F.DenseDictionary(inst.a, backend=cuda))])
+    cfg = F.SwitchConfig(screening_interval=10, max_iterations=5000, rel_tolerance=1e-6)
+    opts = F.RunOptions(variant=F.VARIANT_SCREENED)
+    cl = F.run_lasso(seq, inst.y, inst.lam, cfg, opts)
+    monkeypatch.setenv("FL1_SINGLE_CLUSTER", "0")
+    gr = F.run_lasso(seq, inst.y, inst.lam, cfg, opts)
+    seq_o = F.ApproxSequence([F.make_exact_approx(F.DenseDictionary(inst.a, backend=oracle16))])
+    o = F.run_lasso(seq_o, inst.y, inst.lam, cfg, opts)
+    assert_parity(cl, o, inst.a, inst.y, inst.lam)
+    assert_parity(gr, o, inst.a, inst.y, inst.lam)
