@@ -17,7 +17,9 @@
 #include <limits>
 #include <memory>
 #include <atomic>
+#include <map>
 #include <mutex>
+#include <tuple>
 #include <thread>
 #include <random>
 #include <stdexcept>
@@ -172,6 +174,32 @@ struct fl1_ctx {
   // device scratch of the batched entry, kept between calls (one batched call at a time)
   std::mutex batch_mu;
   std::unique_ptr<DevBuf> batch_buf[2];
+  cudaStream_t batch_stream = nullptr;
+  cudaEvent_t batch_ev[2] = {nullptr, nullptr};
+  void* batch_pinned = nullptr;
+  size_t batch_pinned_bytes = 0;
+  std::map<std::tuple<int64_t, int64_t, int>, std::pair<int, int>> cluster_cfg;  // (ld, sk_m, csize) -> (grid, clusters)
+  char* pinned_scratch(size_t bytes) {
+    if (batch_pinned_bytes < bytes) {
+      if (batch_pinned) cudaFreeHost(batch_pinned);
+      batch_pinned = nullptr;
+      batch_pinned_bytes = 0;
+      ck(cudaHostAlloc(&batch_pinned, bytes + bytes / 8, cudaHostAllocDefault), "cudaHostAlloc");
+      batch_pinned_bytes = bytes + bytes / 8;
+    }
+    return static_cast<char*>(batch_pinned);
+  }
+  void batch_objects() {
+    if (!batch_stream) ck(cudaStreamCreateWithFlags(&batch_stream, cudaStreamNonBlocking), "stream");
+    for (auto& e : batch_ev)
+      if (!e) ck(cudaEventCreate(&e), "event");
+  }
+  ~fl1_ctx() {
+    if (batch_pinned) cudaFreeHost(batch_pinned);
+    for (auto e : batch_ev)
+      if (e) cudaEventDestroy(e);
+    if (batch_stream) cudaStreamDestroy(batch_stream);
+  }
   DevBuf& batch_scratch(int slot, size_t bytes) {
     auto& b = batch_buf[slot];
     if (!b || b->bytes < bytes) {
@@ -1006,15 +1034,23 @@ void solve_clusters(fl1_seq* s, const double* Y, bool y_device, int64_t ldy, con
   fl1_ctx* ctx = pl.ctx;
   ctx->bind();
   const int64_t n = pl.n, k = pl.k, ld = even_ld(n), units = (n + fl1::kUnit - 1) / fl1::kUnit;
-  int grid = 0;
-  {
-    const cudaError_t e = fl1::engine_configure(ld, pl.sk_m, ctx->device, &grid);
-    if (e == cudaErrorInvalidConfiguration)
-      throw std::logic_error("signal length too large for the shared-memory resident residual");
-    ck(e, "engine_configure");
-  }
+  std::lock_guard<std::mutex> batch_lock(ctx->batch_mu);
   int n_clusters = 0;
-  ck(fl1::engine_cluster_capacity(ld, pl.sk_m, csize, &n_clusters), "cluster capacity");
+  {  // launch shape, cached per (ld, SuKro m, cluster size)
+    const auto key = std::make_tuple(ld, pl.sk_m, csize);
+    auto it = ctx->cluster_cfg.find(key);
+    if (it == ctx->cluster_cfg.end()) {
+      int grid = 0;
+      const cudaError_t e = fl1::engine_configure(ld, pl.sk_m, ctx->device, &grid);
+      if (e == cudaErrorInvalidConfiguration)
+        throw std::logic_error("signal length too large for the shared-memory resident residual");
+      ck(e, "engine_configure");
+      int nc = 0;
+      ck(fl1::engine_cluster_capacity(ld, pl.sk_m, csize, &nc), "cluster capacity");
+      it = ctx->cluster_cfg.emplace(key, std::make_pair(grid, nc)).first;
+    }
+    n_clusters = it->second.second;
+  }
   if (n_clusters < 1) throw std::runtime_error("no cluster of this size fits on the device");
   n_clusters = std::min<int>(n_clusters, std::max<int32_t>(batch, 1));
   const int64_t cap = opts->collect_trace ? static_cast<int64_t>(std::max<uint64_t>(cfg->max_iterations, 1)) : 1;
@@ -1030,39 +1066,34 @@ void solve_clusters(fl1_seq* s, const double* Y, bool y_device, int64_t ldy, con
     return o;
   };
   const size_t ub = static_cast<size_t>(B), kb = static_cast<size_t>(k);
+  // upload block [params | desc | lambdas | states], download block [states | switches |
+  // counters | offsets]: one pinned copy each way
   const size_t o_params = region(sizeof(EngineParams) * static_cast<size_t>(n_clusters));
   const size_t o_desc = region(sizeof(fl1::BatchDesc));
-  const size_t o_y = region(y_device ? 0 : sizeof(double) * static_cast<size_t>(ld) * ub);
   const size_t o_lam = region(sizeof(double) * ub);
   const size_t o_st = region(sizeof(EngineState) * ub);
-  const size_t o_tr = region(sizeof(fl1_trace_row) * static_cast<size_t>(cap) * ub);
   const size_t o_sw = region(sizeof(fl1_switch_event) * fl1::kMaxLevels * ub);
   const size_t o_cnt = region(sizeof(int64_t) * static_cast<size_t>(2 + n_clusters));
   const size_t o_off = region(sizeof(int64_t) * ub);
+  const size_t up_end = o_st + sizeof(EngineState) * ub, down_end = top;
+  const size_t o_y = region(y_device ? 0 : sizeof(double) * static_cast<size_t>(ld) * ub);
+  const size_t o_tr = region(sizeof(fl1_trace_row) * static_cast<size_t>(cap) * ub);
   const size_t o_idx = region(sizeof(int32_t) * kb * ub);
   const size_t o_x = region(sizeof(double) * kb * ub);
-  std::lock_guard<std::mutex> batch_lock(ctx->batch_mu);
   char* base = ctx->batch_scratch(0, top + 256).as<char>();
-  cudaStream_t stream = nullptr;
-  ck(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking), "stream");
-  struct StreamGuard {
-    cudaStream_t s;
-    ~StreamGuard() { cudaStreamDestroy(s); }
-  } sg{stream};
-  cudaEvent_t ev0, ev1;
-  ck(cudaEventCreate(&ev0), "event");
-  ck(cudaEventCreate(&ev1), "event");
-  struct EventGuard {
-    cudaEvent_t a, b;
-    ~EventGuard() {
-      cudaEventDestroy(a);
-      cudaEventDestroy(b);
-    }
-  } eg{ev0, ev1};
+  ctx->batch_objects();
+  cudaStream_t stream = ctx->batch_stream;
+  cudaEvent_t ev0 = ctx->batch_ev[0], ev1 = ctx->batch_ev[1];
+  // pinned host image of [params .. offsets] (+ y), then the final sets
+  const size_t img = down_end - o_params;
+  const size_t ybytes = y_device ? 0 : sizeof(double) * static_cast<size_t>(ld) * ub;
+  char* pin = ctx->pinned_scratch(img + ybytes + 12 * kb * ub + 1024);
+  auto at = [&](size_t off) { return pin + (off - o_params); };
 
-  std::vector<EngineParams> params(static_cast<size_t>(n_clusters));
+  EngineParams* params = reinterpret_cast<EngineParams*>(at(o_params));
   for (int q = 0; q < n_clusters; ++q) {
-    EngineParams& p = params[static_cast<size_t>(q)];
+    EngineParams& p = params[q];
+    p = EngineParams{};
     carve(p, base + static_cast<size_t>(q) * ws_bytes, n, k, ld, csize, units, 1, pl.sk_m);
     fill_params(p, pl, s, 1.0, cfg, opts);
     p.grid = csize;
@@ -1092,27 +1123,24 @@ void solve_clusters(fl1_seq* s, const double* Y, bool y_device, int64_t ldy, con
   p0.batch = reinterpret_cast<const fl1::BatchDesc*>(base + o_desc);
   p0.ld = ld;
 
-  std::vector<EngineState> hst(static_cast<size_t>(B));
-  for (auto& st : hst) {
-    st = EngineState{};
-    st.dict_index = pl.start_level;
-    st.t_k = 1.0;
+  EngineState* hst = reinterpret_cast<EngineState*>(at(o_st));
+  for (int64_t b = 0; b < B; ++b) {
+    hst[b] = EngineState{};
+    hst[b].dict_index = pl.start_level;
+    hst[b].t_k = 1.0;
   }
+  std::copy(lambdas, lambdas + batch, reinterpret_cast<double*>(at(o_lam)));
   ck(cudaEventRecord(ev0, stream), "event");
   ck(cudaMemsetAsync(base, 0, ws_bytes * static_cast<size_t>(n_clusters), stream), "workspace memset");
   ck(cudaMemsetAsync(counters, 0, sizeof(int64_t) * (2 + n_clusters), stream), "counter memset");
-  ck(cudaMemcpyAsync(base + o_params, params.data(), sizeof(EngineParams) * params.size(), cudaMemcpyHostToDevice,
-                     stream),
-     "params upload");
-  ck(cudaMemcpyAsync(base + o_desc, &bd, sizeof(bd), cudaMemcpyHostToDevice, stream), "desc upload");
-  ck(cudaMemcpyAsync(base + o_lam, lambdas, sizeof(double) * batch, cudaMemcpyHostToDevice, stream), "lambda upload");
-  ck(cudaMemcpyAsync(base + o_st, hst.data(), sizeof(EngineState) * batch, cudaMemcpyHostToDevice, stream),
-     "state upload");
   int64_t h2d_sig = static_cast<int64_t>(sizeof(EngineState) + sizeof(double));
   if (!y_device && batch > 0) {
-    ck(cudaMemcpy2DAsync(base + o_y, sizeof(double) * ld, Y, sizeof(double) * ldy, sizeof(double) * n, batch,
-                         cudaMemcpyHostToDevice, stream),
-       "signal upload");
+    double* yp = reinterpret_cast<double*>(pin + img);
+    for (int32_t b = 0; b < batch; ++b) {
+      std::copy(Y + static_cast<int64_t>(b) * ldy, Y + static_cast<int64_t>(b) * ldy + n, yp + b * ld);
+      std::fill(yp + b * ld + n, yp + (b + 1) * ld, 0.0);
+    }
+    ck(cudaMemcpyAsync(base + o_y, yp, ybytes, cudaMemcpyHostToDevice, stream), "signal upload");
     h2d_sig += 8 * n;
   }
   // lockstep engine (batched.cu): dense exact dictionary, GAP rule, cached full L
@@ -1125,6 +1153,7 @@ void solve_clusters(fl1_seq* s, const double* Y, bool y_device, int64_t ldy, con
                           (opts->variant == FL1_SCREENED || opts->variant == FL1_PLAIN) &&
                           opts->full_lipschitz != nullptr && k <= fl1::prefix_max_atoms() &&
                           !(pe && pe[0] == '0');
+  fl1::PrefixParams pp{};
   if (use_prefix) {
     const int64_t bcap = (B + 63) / 64 * 64, kt = (k + 63) / 64;
     size_t ptop = 0;
@@ -1146,7 +1175,6 @@ void solve_clusters(fl1_seq* s, const double* Y, bool y_device, int64_t ldy, con
     const size_t q_n = preg(sizeof(int32_t));
     (void)kt;
     char* pb = ctx->batch_scratch(1, ptop + 256).as<char>();
-    fl1::PrefixParams pp{};
     pp.n = n;
     pp.k = k;
     pp.ld = ld;
@@ -1200,32 +1228,27 @@ void solve_clusters(fl1_seq* s, const double* Y, bool y_device, int64_t ldy, con
       pp.step_log = step_log->as<double>();
     }
     bd.handoff = pp.hand;
-    ck(cudaMemcpyAsync(base + o_desc, &bd, sizeof(bd), cudaMemcpyHostToDevice, stream), "desc upload");
     d_steps = pp.steps_out;
-    ck(fl1::prefix_launch(pp, ctx->device, stream), "prefix launch");
   }
+  *reinterpret_cast<fl1::BatchDesc*>(at(o_desc)) = bd;
+  ck(cudaMemcpyAsync(base + o_params, pin, up_end - o_params, cudaMemcpyHostToDevice, stream), "upload");
+  if (use_prefix) ck(fl1::prefix_launch(pp, ctx->device, stream), "prefix launch");
   if (batch > 0) ck(fl1::engine_launch_clusters(p0, n_clusters, csize, pl.sk_m, stream), "cluster launch");
   ck(cudaEventRecord(ev1, stream), "event");
-  ck(cudaMemcpyAsync(hst.data(), base + o_st, sizeof(EngineState) * batch, cudaMemcpyDeviceToHost, stream),
-     "state download");
-  int64_t used = 0;
-  ck(cudaMemcpyAsync(&used, counters + 1, sizeof(int64_t), cudaMemcpyDeviceToHost, stream), "count download");
+  ck(cudaMemcpyAsync(at(o_st), base + o_st, down_end - o_st, cudaMemcpyDeviceToHost, stream), "state download");
   ck(cudaStreamSynchronize(stream), "batched sync");
-  std::vector<int64_t> offs(static_cast<size_t>(B));
-  std::vector<int32_t> all_idx(static_cast<size_t>(std::max<int64_t>(used, 1)));
-  std::vector<double> all_x(static_cast<size_t>(std::max<int64_t>(used, 1)));
-  std::vector<fl1_switch_event> all_sw(static_cast<size_t>(fl1::kMaxLevels * B));
-  ck(cudaMemcpyAsync(offs.data(), base + o_off, sizeof(int64_t) * batch, cudaMemcpyDeviceToHost, stream), "offsets");
+  const int64_t used = reinterpret_cast<const int64_t*>(at(o_cnt))[1];
+  const int64_t* offs = reinterpret_cast<const int64_t*>(at(o_off));
+  const fl1_switch_event* all_sw = reinterpret_cast<const fl1_switch_event*>(at(o_sw));
+  int32_t* all_idx = reinterpret_cast<int32_t*>(pin + img + ybytes);
+  double* all_x = reinterpret_cast<double*>(pin + img + ybytes + ((4 * kb * ub + 15) / 16) * 16);
   if (used > 0) {
-    ck(cudaMemcpyAsync(all_idx.data(), base + o_idx, sizeof(int32_t) * used, cudaMemcpyDeviceToHost, stream), "idx");
-    ck(cudaMemcpyAsync(all_x.data(), base + o_x, sizeof(double) * used, cudaMemcpyDeviceToHost, stream), "x");
+    ck(cudaMemcpyAsync(all_idx, base + o_idx, sizeof(int32_t) * used, cudaMemcpyDeviceToHost, stream), "idx");
+    ck(cudaMemcpyAsync(all_x, base + o_x, sizeof(double) * used, cudaMemcpyDeviceToHost, stream), "x");
   }
-  ck(cudaMemcpyAsync(all_sw.data(), base + o_sw, sizeof(fl1_switch_event) * fl1::kMaxLevels * batch,
-                     cudaMemcpyDeviceToHost, stream),
-     "switches");
   std::vector<std::vector<fl1_trace_row>> traces(static_cast<size_t>(B));
   for (int32_t b = 0; b < batch && opts->collect_trace; ++b) {
-    const int64_t rows = hst[static_cast<size_t>(b)].n_trace;
+    const int64_t rows = hst[b].n_trace;
     traces[static_cast<size_t>(b)].resize(static_cast<size_t>(rows));
     if (rows > 0)
       ck(cudaMemcpyAsync(traces[static_cast<size_t>(b)].data(),
@@ -1248,12 +1271,12 @@ void solve_clusters(fl1_seq* s, const double* Y, bool y_device, int64_t ldy, con
     }
   }
   for (int32_t b = 0; b < batch; ++b) {
-    const EngineState& st = hst[static_cast<size_t>(b)];
+    const EngineState& st = hst[b];
     if (!st.done) throw std::runtime_error("batched solve did not finish");
-    const int32_t* ib = all_idx.data() + offs[static_cast<size_t>(b)];
-    const double* xb = all_x.data() + offs[static_cast<size_t>(b)];
+    const int32_t* ib = all_idx + offs[b];
+    const double* xb = all_x + offs[b];
     auto res = std::make_unique<fl1_result>();
-    const fl1_switch_event* sb = all_sw.data() + static_cast<size_t>(b) * fl1::kMaxLevels;
+    const fl1_switch_event* sb = all_sw + static_cast<size_t>(b) * fl1::kMaxLevels;
     fill_result(*res, st, cfg, k, std::vector<int32_t>(ib, ib + st.S), xb,
                 std::vector<fl1_switch_event>(sb, sb + st.n_switches));
     res->trace = std::move(traces[static_cast<size_t>(b)]);
