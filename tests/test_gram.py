@@ -80,3 +80,29 @@ def test_gram_rejects_wrong_shape(cuda):
     wrong = F.DenseDictionary(np.eye(7), backend=cuda)
     with pytest.raises(F.InvalidArgument):
         F.run_lasso(seq, y, lam, F.SwitchConfig(), F.RunOptions(exact_gram=wrong))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("prefix", ["0", "1"])
+def test_gram_batched(cuda, oracle, monkeypatch, prefix):
+    """Batched solves with an exact Gram: the cluster engines run their exact phase on
+    G (lockstep or not, the trajectory is the direct one)."""
+    monkeypatch.setenv("FL1_BATCH_PREFIX", prefix)
+    rng = np.random.default_rng(41)
+    n, k, B = 120, 500, 7
+    a = syn.gaussian_dictionary(rng, n, k)
+    Y = np.empty((n, B), order="F")
+    for b in range(B):
+        Y[:, b] = syn.observe(rng, a @ syn.sparse_signal(rng, k, 5), None, 30.0)
+    lams = 0.25 * np.max(np.abs(a.T @ Y), axis=0)
+    cfg = F.SwitchConfig(screening_interval=10, max_iterations=5000, rel_tolerance=1e-7)
+    dg = F.DenseDictionary(a, backend=cuda)
+    L = F.lipschitz_bound(dg)
+    seq_g = F.ApproxSequence([F.make_exact_approx(dg)])
+    opts_g = F.RunOptions(variant=F.VARIANT_SCREENED, full_lipschitz=[L], exact_gram=F.gram_matrix(dg))
+    res = F.run_lasso_batched(seq_g, Y, lams, cfg, opts_g, concurrency=-2)
+    do = F.DenseDictionary(a, backend=oracle)
+    seq_o = F.ApproxSequence([F.make_exact_approx(do)])
+    opts_o = F.RunOptions(variant=F.VARIANT_SCREENED, full_lipschitz=[L], exact_gram=F.gram_matrix(do))
+    for b in range(B):
+        assert_parity(res[b], F.run_lasso(seq_o, Y[:, b], lams[b], cfg, opts_o), a, Y[:, b], lams[b])

@@ -266,3 +266,19 @@ def test_sukro_construction_on_gpu_matches_restatement(cuda, oracle):
     for o, r in zip(ours, ref):
         assert np.allclose(o.eps, r["eps"], rtol=1e-9, atol=1e-12)
         assert o.op_err == pytest.approx(r["op_err"], rel=1e-9)
+
+
+@pytest.mark.gpu
+def test_run_single_and_gram_sweep(cuda, tmp_path):
+    """run_single (bench.cpp:240-249) equals the matching sweep run; a use_gram sweep
+    gives the same iterations and ledgers as a direct one."""
+    cfg = small_config(tmp_path / "g")
+    cfg.trials = 1
+    out_g = H.run_sweep(cfg)
+    cfg2 = small_config(tmp_path / "d")
+    cfg2.trials, cfg2.use_gram = 1, False
+    out_d = H.run_sweep(cfg2)
+    for rg, rd in zip(out_g.runs, out_d.runs):
+        assert rg.iterations == rd.iterations and rg.flops == rd.flops and rg.converged == rd.converged
+    single = H.run_single(cfg2, cfg2.lambda_ratios[0], 0, F.VARIANT_SCREENED)
+    assert single.iterations == out_d.runs[1].iterations and single.flops == out_d.runs[1].flops
