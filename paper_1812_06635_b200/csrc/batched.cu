@@ -32,12 +32,17 @@ namespace cg = cooperative_groups;
 namespace fl1 {
 namespace {
 
-constexpr int kPT = 256;            // threads per CTA
+#ifndef FL1_PREFIX_THREADS
+#define FL1_PREFIX_THREADS 512
+#endif
+constexpr int kPT = FL1_PREFIX_THREADS;  // threads per CTA
 constexpr int kPW = kPT / 32;
 constexpr int kTM = 128, kTN = 64;  // output tile: 128 rows (atoms / samples) x 64 signals
+constexpr int kRT = kTM / 8 / (kPT / 32);  // 8-row DMMA tiles per warp
 constexpr int kTK = 32;             // K chunk (rows of A / rho)
 constexpr int kSS = kTK + 4;        // padded smem row stride (doubles)
 constexpr int kStage = (kTM + kTN) * kSS;  // doubles per pipeline stage
+constexpr int kStages = 2;                 // cp.async pipeline depth (3 measured no faster)
 constexpr unsigned kAll = 0xffffffffu;
 constexpr int kSplitMax = 16;      // split-K parts of the contractions (load balance)
 
@@ -54,6 +59,7 @@ __device__ __forceinline__ void cp16(double* dst, const double* src, bool valid)
 }
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 __device__ __forceinline__ void cp_wait1() { asm volatile("cp.async.wait_group 1;\n" ::); }
+__device__ __forceinline__ void cp_wait_pipe() { asm volatile("cp.async.wait_group %0;\n" ::"n"(kStages - 2)); }
 __device__ __forceinline__ void cp_wait0() { asm volatile("cp.async.wait_group 0;\n" ::); }
 
 __device__ __forceinline__ double gtimer() {
@@ -136,9 +142,9 @@ __device__ __noinline__ void gemm_tile(const PrefixParams& p, int rt, int ct, in
   const int64_t K = p.k, ld = p.ld;
   const int nch = static_cast<int>((ld + kTK - 1) / kTK);
   const int c_lo = nch * kp / sk, c_hi = nch * (kp + 1) / sk;
-  double acc[2][8][2];
+  double acc[kRT][8][2];
 #pragma unroll
-  for (int h = 0; h < 2; ++h)
+  for (int h = 0; h < kRT; ++h)
 #pragma unroll
     for (int c = 0; c < 8; ++c) acc[h][c][0] = acc[h][c][1] = 0.0;
   auto issue = [&](int s, int kc) {
@@ -163,33 +169,36 @@ __device__ __noinline__ void gemm_tile(const PrefixParams& p, int rt, int ct, in
       cp16(Rs + c * kSS + kk, ok ? p.R + b * ld + kg : p.R, ok);
     }
   };
-  if (c_lo < c_hi) issue(0, c_lo);
-  cp_commit();
-  for (int kc = c_lo; kc < c_hi; ++kc) {
-    if (kc + 1 < c_hi) issue((kc + 1 - c_lo) & 1, kc + 1);
+  for (int st = 0; st < kStages - 1; ++st) {
+    if (c_lo + st < c_hi) issue(st, c_lo + st);
     cp_commit();
-    cp_wait1();
-    __syncthreads();
-    const double* As = stage + ((kc - c_lo) & 1) * kStage;
+  }
+  for (int kc = c_lo; kc < c_hi; ++kc) {
+    cp_wait_pipe();
+    __syncthreads();  // chunk kc landed; every thread is done with chunk kc-1's stage
+    if (kc + kStages - 1 < c_hi) issue((kc + kStages - 1 - c_lo) % kStages, kc + kStages - 1);
+    cp_commit();
+    const double* As = stage + ((kc - c_lo) % kStages) * kStage;
     const double* Rs = As + kTM * kSS;
 #pragma unroll
     for (int ks = 0; ks < kTK / 4; ++ks) {
-      const double a0v = As[(w * 8 + g) * kSS + ks * 4 + tg];
-      const double a1v = As[(64 + w * 8 + g) * kSS + ks * 4 + tg];
+      double av[kRT];
+#pragma unroll
+      for (int h = 0; h < kRT; ++h) av[h] = As[(h * kPW * 8 + w * 8 + g) * kSS + ks * 4 + tg];
 #pragma unroll
       for (int c = 0; c < 8; ++c) {
         const double bv = Rs[(c * 8 + g) * kSS + ks * 4 + tg];
-        dmma(acc[0][c], a0v, bv);
-        dmma(acc[1][c], a1v, bv);
+#pragma unroll
+        for (int h = 0; h < kRT; ++h) dmma(acc[h][c], av[h], bv);
       }
     }
-    __syncthreads();
   }
   cp_wait0();
+  __syncthreads();  // the staging area is reused by the next tile / the per-signal steps
   double* __restrict__ out = p.corr + static_cast<int64_t>(kp) * K * p.bcap;
 #pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    const int64_t j = j0 + h * 64 + w * 8 + g;
+  for (int h = 0; h < kRT; ++h) {
+    const int64_t j = j0 + h * kPW * 8 + w * 8 + g;
 #pragma unroll
     for (int c = 0; c < 8; ++c) {
 #pragma unroll
@@ -220,9 +229,9 @@ __device__ __noinline__ void gemm_n_tile(const PrefixParams& p, int rt, int ct, 
   constexpr int kAS = kTM + 4;  // As[kk][i] row stride
   const int nch = static_cast<int>((K + kTK - 1) / kTK);
   const int c_lo = nch * kp / sk, c_hi = nch * (kp + 1) / sk;
-  double acc[2][8][2];
+  double acc[kRT][8][2];
 #pragma unroll
-  for (int h = 0; h < 2; ++h)
+  for (int h = 0; h < kRT; ++h)
 #pragma unroll
     for (int c = 0; c < 8; ++c) acc[h][c][0] = acc[h][c][1] = 0.0;
   auto issue = [&](int s, int kc) {
@@ -247,32 +256,35 @@ __device__ __noinline__ void gemm_n_tile(const PrefixParams& p, int rt, int ct, 
       cp16(Bs + c * kSS + kk, ok ? p.vp + b * K + kg : p.vp, ok);
     }
   };
-  if (c_lo < c_hi) issue(0, c_lo);
-  cp_commit();
-  for (int kc = c_lo; kc < c_hi; ++kc) {
-    if (kc + 1 < c_hi) issue((kc + 1 - c_lo) & 1, kc + 1);
+  for (int st = 0; st < kStages - 1; ++st) {
+    if (c_lo + st < c_hi) issue(st, c_lo + st);
     cp_commit();
-    cp_wait1();
+  }
+  for (int kc = c_lo; kc < c_hi; ++kc) {
+    cp_wait_pipe();
     __syncthreads();
-    const double* As = stage + ((kc - c_lo) & 1) * kStage;
+    if (kc + kStages - 1 < c_hi) issue((kc + kStages - 1 - c_lo) % kStages, kc + kStages - 1);
+    cp_commit();
+    const double* As = stage + ((kc - c_lo) % kStages) * kStage;
     const double* Bs = As + kTK * kAS;
 #pragma unroll
     for (int ks = 0; ks < kTK / 4; ++ks) {
-      const double a0v = As[(ks * 4 + tg) * kAS + w * 8 + g];
-      const double a1v = As[(ks * 4 + tg) * kAS + 64 + w * 8 + g];
+      double av[kRT];
+#pragma unroll
+      for (int h = 0; h < kRT; ++h) av[h] = As[(ks * 4 + tg) * kAS + h * kPW * 8 + w * 8 + g];
 #pragma unroll
       for (int c = 0; c < 8; ++c) {
         const double bv = Bs[(c * 8 + g) * kSS + ks * 4 + tg];
-        dmma(acc[0][c], a0v, bv);
-        dmma(acc[1][c], a1v, bv);
+#pragma unroll
+        for (int h = 0; h < kRT; ++h) dmma(acc[h][c], av[h], bv);
       }
     }
-    __syncthreads();
   }
   cp_wait0();
+  __syncthreads();
 #pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    const int64_t i = i0 + h * 64 + w * 8 + g;
+  for (int h = 0; h < kRT; ++h) {
+    const int64_t i = i0 + h * kPW * 8 + w * 8 + g;
 #pragma unroll
     for (int c = 0; c < 8; ++c) {
 #pragma unroll
@@ -888,9 +900,9 @@ __global__ void __launch_bounds__(kPT, 1) prefix_kernel(const __grid_constant__ 
   __shared__ PSh sh;
   const int64_t B = p.batch, K = p.k, N = p.n, ld = p.ld;
   const double t0 = gtimer();
-  // dynamic smem: [staging x2 (contraction tiles; lists in the per-signal steps) | u | act | pact]
+  // dynamic smem: [staging (contraction tiles; lists in the per-signal steps) | u | act | pact]
   double* stage = dsm;
-  double* us = stage + 2 * kStage;
+  double* us = stage + kStages * kStage;
   int32_t* act = reinterpret_cast<int32_t*>(us + ld);
   int32_t* pact = act + B;
   // ---- Engine ctor (254-276) with x = 0, S = K, cached full L: u = 0, momentum off
@@ -1005,9 +1017,9 @@ __global__ void __launch_bounds__(kPT, 1) gram_kernel(const double* __restrict__
   const int nch = static_cast<int>((ld + kTK - 1) / kTK);
   for (int tile = blockIdx.x; tile < n_rt * n_ct; tile += gridDim.x) {
     const int64_t j0 = static_cast<int64_t>(tile % n_rt) * kTM, c0 = static_cast<int64_t>(tile / n_rt) * kTN;
-    double acc[2][8][2];
+    double acc[kRT][8][2];
 #pragma unroll
-    for (int h = 0; h < 2; ++h)
+    for (int h = 0; h < kRT; ++h)
 #pragma unroll
       for (int c = 0; c < 8; ++c) acc[h][c][0] = acc[h][c][1] = 0.0;
     auto issue = [&](int s, int kc) {
@@ -1037,21 +1049,22 @@ __global__ void __launch_bounds__(kPT, 1) gram_kernel(const double* __restrict__
       const double* Bs = As + kTM * kSS;
 #pragma unroll
       for (int ks = 0; ks < kTK / 4; ++ks) {
-        const double a0v = As[(w * 8 + gi) * kSS + ks * 4 + tg];
-        const double a1v = As[(64 + w * 8 + gi) * kSS + ks * 4 + tg];
+        double av[kRT];
+#pragma unroll
+        for (int h = 0; h < kRT; ++h) av[h] = As[(h * kPW * 8 + w * 8 + gi) * kSS + ks * 4 + tg];
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
           const double bv = Bs[(c * 8 + gi) * kSS + ks * 4 + tg];
-          dmma(acc[0][c], a0v, bv);
-          dmma(acc[1][c], a1v, bv);
+#pragma unroll
+          for (int h = 0; h < kRT; ++h) dmma(acc[h][c], av[h], bv);
         }
       }
       __syncthreads();
     }
     cp_wait0();
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int64_t i = j0 + h * 64 + w * 8 + gi;
+    for (int h = 0; h < kRT; ++h) {
+      const int64_t i = j0 + h * kPW * 8 + w * 8 + gi;
 #pragma unroll
       for (int c = 0; c < 8; ++c)
 #pragma unroll
@@ -1098,7 +1111,7 @@ cudaError_t gram_launch(const double* a, int64_t ld, int64_t k, double* g, int64
 }
 
 size_t prefix_smem_bytes(int64_t ld, int64_t batch) {
-  return static_cast<size_t>(2 * kStage + ld) * sizeof(double) + static_cast<size_t>(2 * batch) * sizeof(int32_t);
+  return static_cast<size_t>(kStages * kStage + ld) * sizeof(double) + static_cast<size_t>(2 * batch) * sizeof(int32_t);
 }
 int prefix_split_max() { return kSplitMax; }
 // two per-signal atom lists (12 bytes per entry each) live in the staging area
