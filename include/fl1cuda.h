@@ -220,7 +220,8 @@ int fl1_result_final_active(const fl1_result* r, int32_t* out);
  * sparse apply + ledger, [3] restricted power iterations, [4] switch setups,
  * [5] bytes streamed by the A^T r passes, [6] bytes streamed by the sparse applies
  * (8 N nnz), [7] bytes streamed by power iterations (16 N |S| per step), [8..11] power-iteration
- * sub-phases (apply, combine, adjoint + norms, reduce; ns). out has 12 entries. */
+ * sub-phases (apply, combine, adjoint + norms, reduce; ns), [12] ns and [13] bytes of the
+ * A^T r passes over the full dictionary (|S| = K). out has 14 entries. */
 int fl1_result_profile(const fl1_result* r, double* out);
 void fl1_result_free(fl1_result* r);
 

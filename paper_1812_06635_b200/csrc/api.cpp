@@ -283,7 +283,7 @@ struct fl1_result {
   bool gap_warning = false;
   double device_ms = 0.0, setup_ms = 0.0, batch_ms = -1.0;
   int64_t launches = 0, power_steps = 0;
-  double prof[12] = {0};
+  double prof[14] = {0};
   int64_t h2d = 0, d2h = 0;
 };
 
@@ -653,6 +653,8 @@ void fill_result(fl1_result& r, const EngineState& st, const fl1_switch_config* 
   r.prof[6] = st.prof_apply_bytes;
   r.prof[7] = st.prof_power_bytes;
   for (int i = 0; i < 4; ++i) r.prof[8 + i] = st.prof_pw[i];
+  r.prof[12] = st.prof_full_ns;
+  r.prof[13] = st.prof_full_bytes;
 }
 
 void do_solve(fl1_seq* s, const double* y, bool y_device, double lambda, const fl1_switch_config* cfg,
@@ -1437,7 +1439,7 @@ int fl1_result_final_active(const fl1_result* r, int32_t* out) {
   return guard([&] { std::copy(r->final_active.begin(), r->final_active.end(), out); });
 }
 int fl1_result_profile(const fl1_result* r, double* out) {
-  return guard([&] { std::copy(r->prof, r->prof + 12, out); });
+  return guard([&] { std::copy(r->prof, r->prof + 14, out); });
 }
 void fl1_result_free(fl1_result* r) { delete r; }
 

@@ -1612,7 +1612,13 @@ __device__ __noinline__ void engine_body(const EngineParams& p, Sh& sh, double* 
     if (threadIdx.x == 0) {
       tp1 = globaltimer_ns();
       s.prof_ns[0] += tp1 - tp0;
-      if (lv.kind == kDense) s.prof_bytes += 8.0 * static_cast<double>(p.n) * static_cast<double>(S);
+      if (lv.kind == kDense && !gram) {
+        s.prof_bytes += 8.0 * static_cast<double>(p.n) * static_cast<double>(S);
+        if (S == p.k) {
+          s.prof_full_ns += tp1 - tp0;
+          s.prof_full_bytes += 8.0 * static_cast<double>(p.n) * static_cast<double>(S);
+        }
+      }
     }
 
     // ---------------------------------------------------------- phase B

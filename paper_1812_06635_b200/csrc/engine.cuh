@@ -121,6 +121,8 @@ struct EngineState {
   double prof_bytes;
   double prof_apply_bytes;
   double prof_power_bytes;
+  double prof_full_ns;     // A-phase time of full-dictionary passes (|S| = K)
+  double prof_full_bytes;
   double prof_pw[4];  // power-iteration sub-phases: apply, combine, adjoint+norms, reduce
 };
 

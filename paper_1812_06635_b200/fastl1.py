@@ -387,7 +387,7 @@ def _collect_result(lib: Library, h) -> SolveResult:
         lib.check(lib.result_final_active(h, fa.ctypes.data_as(C.POINTER(C.c_int32))))
     prof = None
     if hasattr(lib, "result_profile"):
-        prof = np.zeros(12)
+        prof = np.zeros(14)
         lib.check(lib.result_profile(h, _dptr(prof)))
     return SolveResult(profile=prof, x=x, converged=bool(info.converged), final_gap=info.final_gap, iterations=int(info.iterations),
                        total_flops=int(info.total_flops), trace=trace, switches=sws, final_active=fa,
