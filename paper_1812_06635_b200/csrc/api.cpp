@@ -1312,7 +1312,9 @@ void solve_single(fl1_seq* s, const double* y, bool y_device, double lambda, con
       bytes += d.kind == fl1::kDense ? 8 * d.ld * d.k : 8 * 2 * static_cast<int64_t>(d.nterms) * d.m * d.q;
     }
     if (opts->exact_gram) bytes += 8 * s->lv.back()->dict->k * s->lv.back()->dict->k;
-    if (!(e && e[0] == '0') && bytes <= kSingleClusterBytes) {
+    int64_t limit = kSingleClusterBytes;
+    if (const char* mb = std::getenv("FL1_SINGLE_CLUSTER_MB")) limit = std::atoll(mb) << 20;
+    if (!(e && e[0] == '0') && bytes <= limit) {
       solve_clusters(s, y, y_device, s->lv.back()->dict->n, &lambda, 1, cfg, opts, kSingleClusterSize, out, false);
       return;
     }
