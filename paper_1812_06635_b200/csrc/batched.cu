@@ -320,18 +320,6 @@ __device__ __forceinline__ uint64_t row_flops_dense(const PrefixParams& p, int64
   return (ua + uz) * un + 6 * ua + 5 * un;
 }
 
-// u (or v) += sum over listed atoms of coef * a_j, rows over threads, list order
-__device__ __forceinline__ void apply_list(const PrefixParams& p, double* us, const double* ent_v,
-                                           const int32_t* ent_j, int n) {
-  for (int64_t i = threadIdx.x; i < p.ld; i += kPT) {
-    double acc = us[i];
-#pragma unroll 4
-    for (int e = 0; e < n; ++e) acc = fma(ent_v[e], __ldg(p.a + static_cast<int64_t>(ent_j[e]) * p.ld + i), acc);
-    us[i] = acc;
-  }
-  __syncthreads();
-}
-
 // Signal b finished in the lockstep: final state + packed (final_active, x) outputs
 // in the cluster engine's format (finish, fastl1.cpp:741-748).
 __device__ void finish_signal(const PrefixParams& p, PSh& sh, int64_t b, bool converged, double gap, double t0) {
@@ -439,22 +427,6 @@ __device__ void handoff_signal(const PrefixParams& p, PSh& sh, int64_t b, double
     sg.mode = 3;
   }
   __syncthreads();
-}
-
-// corr column of slot a: sum of the split-K parts (fixed order) written back to part
-// 0; returns the block max of |corr| over the preserved atoms
-__device__ double combine_corr(const PrefixParams& p, PSh& sh, int64_t a, int64_t b, int sk) {
-  const int64_t K = p.k, part = K * p.bcap;
-  double* cr = p.corr + a * K;
-  const int8_t* mk = p.mask + b * K;
-  double dp = 0.0;
-  for (int64_t j = threadIdx.x; j < K; j += kPT) {
-    double c = __ldcg(cr + j);
-    for (int kp = 1; kp < sk; ++kp) c += __ldcg(cr + kp * part + j);
-    if (sk > 1) __stcg(cr + j, c);
-    if (mk[j]) dp = fmax(dp, fabs(c));
-  }
-  return block_max(dp, sh);
 }
 
 // compute_products (fastl1.cpp:359-369) for signal b's NEXT iteration: rho_g =

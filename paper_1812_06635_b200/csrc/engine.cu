@@ -234,18 +234,14 @@ __device__ __forceinline__ double2 ldg_stream2(const double2* ptr) {
   return r;
 }
 
+#if FL1_V4
 // 256-bit streaming load (sm_100: LDG.E.NA.ENL2.256); p must be 32-byte aligned.
 __device__ __forceinline__ void ldg_stream4(const double* ptr, double2& lo, double2& hi) {
   asm volatile("ld.global.nc.L1::no_allocate.v4.f64 {%0, %1, %2, %3}, [%4];"
                : "=d"(lo.x), "=d"(lo.y), "=d"(hi.x), "=d"(hi.y)
                : "l"(ptr));
 }
-
-__device__ __forceinline__ double soft_threshold(double z, double u) {  // solver.cpp:9-13
-  const double mag = fabs(z) - u;
-  if (mag <= 0.0) return 0.0;
-  return z > 0.0 ? mag : -mag;
-}
+#endif
 
 // CTA slice [lo, hi) of n items (balanced, contiguous).
 __device__ __forceinline__ void slice(int64_t n, int64_t& lo, int64_t& hi) {
@@ -276,11 +272,6 @@ __device__ __forceinline__ double thread_sum_partials(const double* __restrict__
   return acc;
 }
 
-__device__ __forceinline__ double warp_sum_partials(const double* __restrict__ part, int C, int64_t ld, int64_t i) {
-  double acc = 0.0;
-  for (int c = threadIdx.x & 31; c < C; c += 32) acc += __ldcg(part + static_cast<int64_t>(c) * ld + i);
-  return warp_sum(acc);
-}
 
 // Calls f(i, value) for rows i in [lo, hi) (by one thread per row).
 // Few chunks: one thread per row with every load in flight. More: 8 lanes per
@@ -350,18 +341,6 @@ struct PassAcc {
     if (po.vdot) {
       w2 = fma(total, total, w2);
       vw = fma(po.vdot[pos], total, vw);
-    }
-  }
-  // same statistics with the per-atom operand (eps or vdot) already in a register
-  __device__ __forceinline__ void add_v(const EngineParams& p, const PassOut& po, double total, double aux) {
-    if (po.track) {
-      const double ac = po.div_lambda ? fabs(total) / p.lambda : fabs(total);
-      mp = fmax(mp, ac);
-      ms = fmax(ms, ac + aux * po.eps_scale);
-    }
-    if (po.vdot) {
-      w2 = fma(total, total, w2);
-      vw = fma(aux, total, vw);
     }
   }
 };
