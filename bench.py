@@ -20,7 +20,9 @@ run_lasso's run() plus its setup.
 config (rank 0 only under torchrun).
 
 Multi-GPU: replicas only (the reference has no distributed path):
-every rank solves its own seeded instance, no collective on the data path.
+every rank solves the same seeded instance on its own GPU (identical work per rank,
+so the max-over-ranks time measures the hardware, not instance variance); no
+collective on the data path.
 """
 from __future__ import annotations
 
@@ -149,7 +151,7 @@ def run_gpu(args) -> None:
 
     from paper_1812_06635_b200 import fastl1 as F
 
-    inst, d = make_problem(args.config, rank)
+    inst, d = make_problem(args.config, 0)  # every replica solves the same seeded instance
     n, k = inst.a.shape
     L = F.lipschitz_bound(d)  # reference harness caches this outside run_lasso (bench.cpp:193-195)
     seq = F.ApproxSequence([F.make_exact_approx(d)])
@@ -292,7 +294,7 @@ def run_sukro(args) -> None:
 
         dist_mod.init_process_group("nccl", device_id=torch.device("cuda", local))
         dist = dist_mod
-    inst = syn.sukro_instance(seed=3 + 1000 * rank)
+    inst = syn.sukro_instance(seed=3)  # every replica solves the same seeded instance
     n, k = inst.a.shape
     seq = syn.sukro_sequence(inst)
     # per-level Lipschitz constants cached outside run_lasso, as the reference harness does
@@ -424,7 +426,7 @@ def run_path(args) -> None:
 
         dist_mod.init_process_group("nccl", device_id=torch.device("cuda", local))
         dist = dist_mod
-    seed = 4 + 1000 * rank
+    seed = 4  # every replica solves the same seeded instance
     At, y = make_c4_device(seed, f"cuda:{local}")
     k, n = At.shape
     d = F.DenseDictionaryDevice(At.data_ptr(), n, k)
@@ -571,7 +573,7 @@ def run_batched(args) -> None:
 
         dist_mod.init_process_group("nccl", device_id=torch.device("cuda", local))
         dist = dist_mod
-    a, Y, lams = make_c5(5 + 1000 * rank)
+    a, Y, lams = make_c5(5)  # every replica solves the same seeded batch
     n, k = a.shape
     B = Y.shape[1]
     d = F.DenseDictionary(a)
