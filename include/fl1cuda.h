@@ -223,6 +223,12 @@ int fl1_result_final_active(const fl1_result* r, int32_t* out);
  * sub-phases (apply, combine, adjoint + norms, reduce; ns), [12] ns and [13] bytes of the
  * A^T r passes over the full dictionary (|S| = K). out has 14 entries. */
 int fl1_result_profile(const fl1_result* r, double* out);
+/* Bulk accessors for batched results (one call instead of one per result): infos
+ * (count), x (count x K), profiles (count x 14), and the traces / switch events /
+ * final active sets of all results concatenated in result order (sizes from infos). */
+int fl1_results_collect(fl1_result* const* rs, int32_t count, fl1_result_info* infos, double* x, double* profiles);
+int fl1_results_tables(fl1_result* const* rs, int32_t count, fl1_trace_row* traces, fl1_switch_event* switches,
+                       int32_t* final_active);
 void fl1_result_free(fl1_result* r);
 
 /* ---- setup-side primitives on the path ---- */

@@ -167,6 +167,8 @@ PRODUCT_ONLY = {
                                        C.POINTER(RunOptionsC), C.c_int32, _PP]),
     "solve_device": (C.c_int, [_P, C.c_void_p, C.c_double, C.POINTER(SwitchConfigC), C.POINTER(RunOptionsC), _PP]),
     "rng_normals": (C.c_int, [C.c_uint64, C.c_int64, _PD]),
+    "results_collect": (C.c_int, [_PP, C.c_int32, C.POINTER(ResultInfoC), _PD, _PD]),
+    "results_tables": (C.c_int, [_PP, C.c_int32, C.POINTER(TraceRowC), C.POINTER(SwitchEventC), _PI32]),
     "draw_signal": (C.c_int, [_P, C.c_double, C.c_uint64, C.c_int32, _PD, _PD]),
 }
 

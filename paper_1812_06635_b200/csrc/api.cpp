@@ -1443,6 +1443,30 @@ int fl1_result_final_active(const fl1_result* r, int32_t* out) {
 int fl1_result_profile(const fl1_result* r, double* out) {
   return guard([&] { std::copy(r->prof, r->prof + 14, out); });
 }
+int fl1_results_collect(fl1_result* const* rs, int32_t count, fl1_result_info* infos, double* x, double* profiles) {
+  for (int32_t i = 0; i < count; ++i) {
+    const int st = fl1_result_info_get(rs[i], infos + i);
+    if (st != FL1_OK) return st;
+  }
+  return guard([&] {
+    for (int32_t i = 0; i < count; ++i) {
+      const fl1_result& r = *rs[i];
+      if (x) std::copy(r.x.begin(), r.x.end(), x + static_cast<int64_t>(i) * r.k);
+      if (profiles) std::copy(r.prof, r.prof + 14, profiles + static_cast<int64_t>(i) * 14);
+    }
+  });
+}
+int fl1_results_tables(fl1_result* const* rs, int32_t count, fl1_trace_row* traces, fl1_switch_event* switches,
+                       int32_t* final_active) {
+  return guard([&] {
+    for (int32_t i = 0; i < count; ++i) {
+      const fl1_result& r = *rs[i];
+      if (traces) traces = std::copy(r.trace.begin(), r.trace.end(), traces);
+      if (switches) switches = std::copy(r.switches.begin(), r.switches.end(), switches);
+      if (final_active) final_active = std::copy(r.final_active.begin(), r.final_active.end(), final_active);
+    }
+  });
+}
 void fl1_result_free(fl1_result* r) { delete r; }
 
 int fl1_lambda_max(fl1_dict* d, const double* y, double* out) {  // screening.cpp:9-11

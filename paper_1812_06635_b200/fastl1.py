@@ -496,13 +496,47 @@ def run_lasso_batched(seq: ApproxSequence, Y, lambdas, cfg: SwitchConfig, opts: 
     else:
         lib.check(lib.solve_batched_device(seq._h, C.c_void_p(y_dev_ptr), n, _dptr(lam), B, C.byref(c), C.byref(o),
                                            concurrency, hs))
-    out = []
     try:
-        for b in range(B):
-            out.append(_collect_result(lib, hs[b]))
+        return _collect_results(lib, hs, B)
     finally:
         for b in range(B):
             lib.result_free(hs[b])
+
+
+def _collect_results(lib: Library, hs, B: int) -> list:
+    """All results of a batched call through the bulk accessors (4 library calls)."""
+    if B == 0:
+        return []
+    infos = (_abi.ResultInfoC * B)()
+    k = None
+    lib.check(lib.results_collect(hs, B, infos, None, None))
+    k = infos[0].k
+    xs = np.empty((B, k))
+    profs = np.zeros((B, 14))
+    lib.check(lib.results_collect(hs, B, infos, _dptr(xs), _dptr(profs)))
+    nt = [infos[b].n_trace for b in range(B)]
+    ns = [infos[b].n_switches for b in range(B)]
+    na = [infos[b].n_final_active for b in range(B)]
+    traces = np.zeros(max(sum(nt), 1), dtype=TRACE_DTYPE)
+    sws = np.zeros(max(sum(ns), 1), dtype=SWITCH_DTYPE)
+    fas = np.empty(max(sum(na), 1), dtype=np.int32)
+    lib.check(lib.results_tables(hs, B, traces.ctypes.data_as(C.POINTER(_abi.TraceRowC)),
+                                 sws.ctypes.data_as(C.POINTER(_abi.SwitchEventC)),
+                                 fas.ctypes.data_as(C.POINTER(C.c_int32))))
+    out = []
+    ot = os_ = oa = 0
+    for b in range(B):
+        info = infos[b]
+        out.append(SolveResult(profile=profs[b], x=xs[b], converged=bool(info.converged), final_gap=info.final_gap,
+                               iterations=int(info.iterations), total_flops=int(info.total_flops),
+                               trace=traces[ot:ot + nt[b]], switches=sws[os_:os_ + ns[b]], final_active=fas[oa:oa + na[b]],
+                               gap_warning=bool(info.gap_warning), device_ms=info.device_ms, setup_ms=info.setup_ms,
+                               kernel_launches=int(info.kernel_launches), power_iterations=int(info.power_iterations),
+                               h2d_bytes=int(info.h2d_bytes), d2h_bytes=int(info.d2h_bytes),
+                               batch_device_ms=float(info.batch_device_ms)))
+        ot += nt[b]
+        os_ += ns[b]
+        oa += na[b]
     return out
 
 
