@@ -400,3 +400,42 @@ def test_single_cluster_route_matches_grid(cuda, oracle16, monkeypatch):
     o = F.run_lasso(seq_o, inst.y, inst.lam, cfg, opts)
     assert_parity(cl, o, inst.a, inst.y, inst.lam)
     assert_parity(gr, o, inst.a, inst.y, inst.lam)
+
+
+def test_large_path_first_lambdas_match_oracle(cuda, oracle16):
+    """BASELINE configs[3] at full size (8192 x 65536, 4 GiB): the first three lambdas of
+    the warm-started path against the oracle on the same matrix (host copy), with the
+    oracle's own warm start -- identical trajectories (sets, ledger, support) and 1e-9
+    objectives at the reference's full size."""
+    import torch
+
+    n, k = 8192, 65536
+    gen = torch.Generator(device="cuda").manual_seed(4)
+    At = torch.randn(k, n, device="cuda", dtype=torch.float64, generator=gen)
+    At /= At.norm(dim=1, keepdim=True)
+    rng = np.random.default_rng(4)
+    x0 = np.zeros(k)
+    pos = rng.choice(k, 800, replace=False)
+    x0[pos] = rng.standard_normal(800)
+    clean = At.T @ torch.from_numpy(x0).cuda()
+    sigma = float(clean.norm()) / np.sqrt(n) * 10 ** (-20 / 20)
+    y = (clean + sigma * torch.from_numpy(rng.standard_normal(n)).cuda()).cpu().numpy()
+    a = At.cpu().numpy().T  # column-major N x K view of the same bytes
+    del clean
+    d = F.DenseDictionaryDevice(At.data_ptr(), n, k, backend=cuda)
+    L = F.lipschitz_bound(d)
+    lmax = F.lambda_max(d, y)
+    seq_g = F.ApproxSequence([F.make_exact_approx(d)])
+    seq_o = F.ApproxSequence([F.make_exact_approx(F.DenseDictionary(a, backend=oracle16))])
+    cfg = F.SwitchConfig(screening_interval=10, max_iterations=5000, rel_tolerance=1e-6)
+    xg = xo = None
+    for ratio in syn.CONFIGS["c4"]["lam_ratios"][:3]:
+        lam = ratio * lmax
+        g = F.run_lasso(seq_g, y, lam, cfg, F.RunOptions(variant=F.VARIANT_SCREENED, full_lipschitz=[L], x_init=xg))
+        o = F.run_lasso(seq_o, y, lam, cfg, F.RunOptions(variant=F.VARIANT_SCREENED, full_lipschitz=[L], x_init=xo))
+        assert g.converged and o.converged
+        assert g.iterations == o.iterations and g.total_flops == o.total_flops
+        assert np.array_equal(g.final_active, o.final_active)
+        assert np.array_equal(g.x != 0, o.x != 0)
+        assert np.max(np.abs(g.x - o.x)) <= 1e-9 * max(1.0, np.max(np.abs(o.x)))
+        xg, xo = g.x, o.x
