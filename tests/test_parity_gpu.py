@@ -439,3 +439,21 @@ def test_large_path_first_lambdas_match_oracle(cuda, oracle16):
         assert np.array_equal(g.x != 0, o.x != 0)
         assert np.max(np.abs(g.x - o.x)) <= 1e-9 * max(1.0, np.max(np.abs(o.x)))
         xg, xo = g.x, o.x
+
+
+def test_batched_full_size_config5_sample(cuda, oracle16):
+    """BASELINE configs[4] at full size (512 signals on 1024 x 4096) through the default
+    batched route (lockstep engine + cluster engines): a sample of 24 signals equals
+    the oracle's own per-signal solves (trajectory, ledger, support, 1e-9 objective)."""
+    import bench
+
+    a, Y, lams = bench.make_c5(5)
+    dg = F.DenseDictionary(a, backend=cuda)
+    L = F.lipschitz_bound(dg)
+    cfg = F.SwitchConfig(screening_interval=10, max_iterations=5000, rel_tolerance=1e-6)
+    opts = F.RunOptions(variant=F.VARIANT_SCREENED, full_lipschitz=[L])
+    res = F.run_lasso_batched(F.ApproxSequence([F.make_exact_approx(dg)]), Y, lams, cfg, opts)
+    assert len(res) == Y.shape[1] and all(r.converged for r in res)
+    seq_o = F.ApproxSequence([F.make_exact_approx(F.DenseDictionary(a, backend=oracle16))])
+    for b in range(0, Y.shape[1], 22):
+        assert_parity(res[b], F.run_lasso(seq_o, Y[:, b], lams[b], cfg, opts), a, Y[:, b], lams[b])
