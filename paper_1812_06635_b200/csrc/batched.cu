@@ -38,7 +38,9 @@ namespace {
 constexpr int kPT = FL1_PREFIX_THREADS;  // threads per CTA
 constexpr int kPW = kPT / 32;
 constexpr int kTM = 128, kTN = 64;  // output tile: 128 rows (atoms / samples) x 64 signals
-constexpr int kRT = kTM / 8 / (kPT / 32);  // 8-row DMMA tiles per warp
+// warp grid over a 128 x 64 output tile: kWR x kWC warps, each kRT x kCT 8x8 DMMA tiles
+constexpr int kWR = 8, kWC = (kPT / 32) / kWR;
+constexpr int kRT = kTM / 8 / kWR, kCT = kTN / 8 / kWC;
 constexpr int kTK = 32;             // K chunk (rows of A / rho)
 constexpr int kSS = kTK + 4;        // padded smem row stride (doubles)
 constexpr int kStage = (kTM + kTN) * kSS;  // doubles per pipeline stage
@@ -142,11 +144,12 @@ __device__ __noinline__ void gemm_tile(const PrefixParams& p, int rt, int ct, in
   const int64_t K = p.k, ld = p.ld;
   const int nch = static_cast<int>((ld + kTK - 1) / kTK);
   const int c_lo = nch * kp / sk, c_hi = nch * (kp + 1) / sk;
-  double acc[kRT][8][2];
+  const int wr = w % kWR, wc = w / kWR;
+  double acc[kRT][kCT][2];
 #pragma unroll
   for (int h = 0; h < kRT; ++h)
 #pragma unroll
-    for (int c = 0; c < 8; ++c) acc[h][c][0] = acc[h][c][1] = 0.0;
+    for (int c = 0; c < kCT; ++c) acc[h][c][0] = acc[h][c][1] = 0.0;
   auto issue = [&](int s, int kc) {
     double* As = stage + s * kStage;
     double* Rs = As + kTM * kSS;
@@ -182,15 +185,15 @@ __device__ __noinline__ void gemm_tile(const PrefixParams& p, int rt, int ct, in
     const double* Rs = As + kTM * kSS;
 #pragma unroll
     for (int ks = 0; ks < kTK / 4; ++ks) {
-      double av[kRT];
+      double av[kRT], bv[kCT];
 #pragma unroll
-      for (int h = 0; h < kRT; ++h) av[h] = As[(h * kPW * 8 + w * 8 + g) * kSS + ks * 4 + tg];
+      for (int h = 0; h < kRT; ++h) av[h] = As[((h * kWR + wr) * 8 + g) * kSS + ks * 4 + tg];
 #pragma unroll
-      for (int c = 0; c < 8; ++c) {
-        const double bv = Rs[(c * 8 + g) * kSS + ks * 4 + tg];
+      for (int c = 0; c < kCT; ++c) bv[c] = Rs[((wc * kCT + c) * 8 + g) * kSS + ks * 4 + tg];
 #pragma unroll
-        for (int h = 0; h < kRT; ++h) dmma(acc[h][c], av[h], bv);
-      }
+      for (int h = 0; h < kRT; ++h)
+#pragma unroll
+        for (int c = 0; c < kCT; ++c) dmma(acc[h][c], av[h], bv[c]);
     }
   }
   cp_wait0();
@@ -198,12 +201,12 @@ __device__ __noinline__ void gemm_tile(const PrefixParams& p, int rt, int ct, in
   double* __restrict__ out = p.corr + static_cast<int64_t>(kp) * K * p.bcap;
 #pragma unroll
   for (int h = 0; h < kRT; ++h) {
-    const int64_t j = j0 + h * kPW * 8 + w * 8 + g;
+    const int64_t j = j0 + (h * kWR + wr) * 8 + g;
 #pragma unroll
-    for (int c = 0; c < 8; ++c) {
+    for (int c = 0; c < kCT; ++c) {
 #pragma unroll
       for (int i = 0; i < 2; ++i) {
-        const int64_t a = a0 + c * 8 + 2 * tg + i;
+        const int64_t a = a0 + (wc * kCT + c) * 8 + 2 * tg + i;
         if (j < K && a < n_act) __stcg(out + a * K + j, acc[h][c][i]);
       }
     }
@@ -229,11 +232,12 @@ __device__ __noinline__ void gemm_n_tile(const PrefixParams& p, int rt, int ct, 
   constexpr int kAS = kTM + 4;  // As[kk][i] row stride
   const int nch = static_cast<int>((K + kTK - 1) / kTK);
   const int c_lo = nch * kp / sk, c_hi = nch * (kp + 1) / sk;
-  double acc[kRT][8][2];
+  const int wr = w % kWR, wc = w / kWR;
+  double acc[kRT][kCT][2];
 #pragma unroll
   for (int h = 0; h < kRT; ++h)
 #pragma unroll
-    for (int c = 0; c < 8; ++c) acc[h][c][0] = acc[h][c][1] = 0.0;
+    for (int c = 0; c < kCT; ++c) acc[h][c][0] = acc[h][c][1] = 0.0;
   auto issue = [&](int s, int kc) {
     double* As = stage + s * kStage;
     double* Bs = As + kTK * kAS;
@@ -269,27 +273,27 @@ __device__ __noinline__ void gemm_n_tile(const PrefixParams& p, int rt, int ct, 
     const double* Bs = As + kTK * kAS;
 #pragma unroll
     for (int ks = 0; ks < kTK / 4; ++ks) {
-      double av[kRT];
+      double av[kRT], bv[kCT];
 #pragma unroll
-      for (int h = 0; h < kRT; ++h) av[h] = As[(ks * 4 + tg) * kAS + h * kPW * 8 + w * 8 + g];
+      for (int h = 0; h < kRT; ++h) av[h] = As[(ks * 4 + tg) * kAS + (h * kWR + wr) * 8 + g];
 #pragma unroll
-      for (int c = 0; c < 8; ++c) {
-        const double bv = Bs[(c * 8 + g) * kSS + ks * 4 + tg];
+      for (int c = 0; c < kCT; ++c) bv[c] = Bs[((wc * kCT + c) * 8 + g) * kSS + ks * 4 + tg];
 #pragma unroll
-        for (int h = 0; h < kRT; ++h) dmma(acc[h][c], av[h], bv);
-      }
+      for (int h = 0; h < kRT; ++h)
+#pragma unroll
+        for (int c = 0; c < kCT; ++c) dmma(acc[h][c], av[h], bv[c]);
     }
   }
   cp_wait0();
   __syncthreads();
 #pragma unroll
   for (int h = 0; h < kRT; ++h) {
-    const int64_t i = i0 + h * kPW * 8 + w * 8 + g;
+    const int64_t i = i0 + (h * kWR + wr) * 8 + g;
 #pragma unroll
-    for (int c = 0; c < 8; ++c) {
+    for (int c = 0; c < kCT; ++c) {
 #pragma unroll
       for (int q = 0; q < 2; ++q) {
-        const int64_t pc = c0 + c * 8 + 2 * tg + q;
+        const int64_t pc = c0 + (wc * kCT + c) * 8 + 2 * tg + q;
         if (i < ld && pc < n_pow) __stcg(p.np + (static_cast<int64_t>(kp) * p.bcap + pc) * ld + i, acc[h][c][q]);
       }
     }
@@ -985,15 +989,16 @@ __global__ void __launch_bounds__(kPT, 1) gram_kernel(const double* __restrict__
                                                       double* __restrict__ g, int64_t ldg) {
   extern __shared__ __align__(16) double dsm[];
   const int w = threadIdx.x >> 5, l = threadIdx.x & 31, gi = l >> 2, tg = l & 3;
+  const int wr = w % kWR, wc = w / kWR;
   const int n_rt = static_cast<int>((k + kTM - 1) / kTM), n_ct = static_cast<int>((k + kTN - 1) / kTN);
   const int nch = static_cast<int>((ld + kTK - 1) / kTK);
   for (int tile = blockIdx.x; tile < n_rt * n_ct; tile += gridDim.x) {
     const int64_t j0 = static_cast<int64_t>(tile % n_rt) * kTM, c0 = static_cast<int64_t>(tile / n_rt) * kTN;
-    double acc[kRT][8][2];
+    double acc[kRT][kCT][2];
 #pragma unroll
     for (int h = 0; h < kRT; ++h)
 #pragma unroll
-      for (int c = 0; c < 8; ++c) acc[h][c][0] = acc[h][c][1] = 0.0;
+      for (int c = 0; c < kCT; ++c) acc[h][c][0] = acc[h][c][1] = 0.0;
     auto issue = [&](int s, int kc) {
       double* As = dsm + s * kStage;
       double* Bs = As + kTM * kSS;
@@ -1021,27 +1026,27 @@ __global__ void __launch_bounds__(kPT, 1) gram_kernel(const double* __restrict__
       const double* Bs = As + kTM * kSS;
 #pragma unroll
       for (int ks = 0; ks < kTK / 4; ++ks) {
-        double av[kRT];
+        double av[kRT], bv[kCT];
 #pragma unroll
-        for (int h = 0; h < kRT; ++h) av[h] = As[(h * kPW * 8 + w * 8 + gi) * kSS + ks * 4 + tg];
+        for (int h = 0; h < kRT; ++h) av[h] = As[((h * kWR + wr) * 8 + gi) * kSS + ks * 4 + tg];
 #pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          const double bv = Bs[(c * 8 + gi) * kSS + ks * 4 + tg];
+        for (int c = 0; c < kCT; ++c) bv[c] = Bs[((wc * kCT + c) * 8 + gi) * kSS + ks * 4 + tg];
 #pragma unroll
-          for (int h = 0; h < kRT; ++h) dmma(acc[h][c], av[h], bv);
-        }
+        for (int h = 0; h < kRT; ++h)
+#pragma unroll
+          for (int c = 0; c < kCT; ++c) dmma(acc[h][c], av[h], bv[c]);
       }
       __syncthreads();
     }
     cp_wait0();
 #pragma unroll
     for (int h = 0; h < kRT; ++h) {
-      const int64_t i = j0 + h * kPW * 8 + w * 8 + gi;
+      const int64_t i = j0 + (h * kWR + wr) * 8 + gi;
 #pragma unroll
-      for (int c = 0; c < 8; ++c)
+      for (int c = 0; c < kCT; ++c)
 #pragma unroll
         for (int q = 0; q < 2; ++q) {
-          const int64_t j = c0 + c * 8 + 2 * tg + q;
+          const int64_t j = c0 + (wc * kCT + c) * 8 + 2 * tg + q;
           if (i < k && j < k) g[j * ldg + i] = acc[h][c][q];
         }
     }
