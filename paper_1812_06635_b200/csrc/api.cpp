@@ -512,6 +512,10 @@ EngineState run_utility(DictImpl& d, int mode, const double* in_host, double* ou
        "output download");
   ck(cudaMemcpyAsync(&st, p.st, sizeof(st), cudaMemcpyDeviceToHost, w.stream), "state download");
   ck(cudaStreamSynchronize(w.stream), "sync");
+  if (std::getenv("FL1_UTIL_LOG"))  // diagnostics: power-step count and sub-phase times (ns)
+    std::fprintf(stderr, "fl1 utility mode %d: %lld power steps, apply %.0f combine %.0f adjoint %.0f reduce %.0f ns\n",
+                 mode, static_cast<long long>(st.power_steps), st.prof_pw[0], st.prof_pw[1], st.prof_pw[2],
+                 st.prof_pw[3]);
   return st;
 }
 

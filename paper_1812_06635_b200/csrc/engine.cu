@@ -214,9 +214,16 @@ __device__ void grid_reduce(const EngineParams& p, Sh& sh, unsigned mask_sum, un
     if (!(((mask_sum | mask_max) >> slot) & 1u)) continue;
     const bool mx = (mask_max >> slot) & 1u;
     double acc = mx ? -DBL_MAX : 0.0;
-    for (int b = l; b < p.grid; b += 32) {
-      const double e = __ldcg(p.bred + static_cast<int64_t>(b) * kBred + slot);
-      acc = mx ? fmax(acc, e) : acc + e;
+    for (int b0 = l; b0 < p.grid; b0 += 256) {  // 8 loads in flight per lane, added in b order
+      double e[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int b = b0 + 32 * q;
+        e[q] = b < p.grid ? __ldcg(p.bred + static_cast<int64_t>(b) * kBred + slot) : 0.0;
+      }
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        if (b0 + 32 * q < p.grid) acc = mx ? fmax(acc, e[q]) : acc + e[q];
     }
     acc = mx ? warp_max(acc) : warp_sum(acc);
     if (l == 0) sh.res[slot] = acc;
@@ -272,6 +279,24 @@ __device__ __forceinline__ double thread_sum_partials(const double* __restrict__
   return acc;
 }
 
+// Lane g of an 8-lane row group: sum of part[c * ld + i] over c = g, g + 8, ... < C
+// in that order, with up to 8 loads in flight (not one L2 round trip per chunk).
+__device__ __forceinline__ double lane_sum_partials(const double* __restrict__ part, int C, int64_t ld, int64_t i,
+                                                    int g) {
+  double acc = 0.0;
+  for (int c0 = g; c0 < C; c0 += 64) {
+    double v[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int c = c0 + 8 * q;
+      v[q] = c < C ? __ldcg(part + static_cast<int64_t>(c) * ld + i) : 0.0;
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      if (c0 + 8 * q < C) acc += v[q];
+  }
+  return acc;
+}
 
 // Calls f(i, value) for rows i in [lo, hi) (by one thread per row).
 // Few chunks: one thread per row with every load in flight. More: 8 lanes per
@@ -287,8 +312,7 @@ __device__ __forceinline__ void combine_rows(const double* __restrict__ part, in
     for (int64_t i0 = lo; i0 < hi; i0 += kThreads / 8) {  // uniform trip count (shuffles below)
       const int64_t i = i0 + (threadIdx.x >> 3);
       double acc = 0.0;
-      if (i < hi)
-        for (int c = g; c < C; c += 8) acc += __ldcg(part + static_cast<int64_t>(c) * ld + i);
+      if (i < hi) acc = lane_sum_partials(part, C, ld, i, g);
       acc += __shfl_xor_sync(kFull, acc, 4);
       acc += __shfl_xor_sync(kFull, acc, 2);
       acc += __shfl_xor_sync(kFull, acc, 1);
@@ -326,6 +350,7 @@ struct PassOut {
   bool div_lambda;       // maxima of |out|/lambda (exact-fit branch, fastl1.cpp:440-446)
   int slot_plain, slot_stable;
   const double* vdot;    // non-null: per-CTA sums of out^2 and vdot*out (power iteration)
+  int bulk;              // stream through the bulk-copy ring (p.bulk_stages > 0; power iterations)
 };
 
 struct PassAcc {
@@ -476,7 +501,7 @@ __device__ __noinline__ void dense_adjoint(const EngineParams& p, Sh& sh, const 
       ++cc;                                                                                           \
     }                                                                                                 \
   } while (0)
-  if (u_lo < u_hi && p.bulk_stages >= 2) {
+  if (u_lo < u_hi && po.bulk && !s_vcluster && p.bulk_stages >= 2) {
     // bulk-copy ring: lane 0 streams whole units into shared memory (one mbarrier per
     // stage), so R units per warp are in flight instead of two register units
     const int R = p.bulk_stages;
@@ -1099,7 +1124,7 @@ __device__ __noinline__ double power_iteration(const EngineParams& p, Sh& sh, co
       tq2 = globaltimer_ns();
       sh.s.prof_pw[1] += tq2 - tq1;
     }
-    PassOut po{p.pw, 0, 0.0, false, 0, 0, p.pv};
+    PassOut po{p.pw, 0, 0.0, false, 0, 0, p.pv, 1};
     op_adjoint(p, sh, lv, bk.idx, bk.eps, S, sc.vec, sc.rt, po);
     vsync();
     double tq3 = 0.0;
@@ -1177,9 +1202,8 @@ __device__ void combine_u(const EngineParams& p, Sh& sh, int C, bool shift, bool
         u = thread_sum_partials(p.up, C, p.ld, i);
         if (fix) f = thread_sum_partials(p.dvp, C, p.ld, i);
       } else {
-        for (int c = g; c < C; c += 8) u += __ldcg(p.up + static_cast<int64_t>(c) * p.ld + i);
-        if (fix)
-          for (int c = g; c < C; c += 8) f += __ldcg(p.dvp + static_cast<int64_t>(c) * p.ld + i);
+        u = lane_sum_partials(p.up, C, p.ld, i, g);
+        if (fix) f = lane_sum_partials(p.dvp, C, p.ld, i, g);
       }
     }
     if (G == 8) {
@@ -1532,7 +1556,17 @@ __device__ __noinline__ void engine_body(const EngineParams& p, Sh& sh, double* 
         double sacc = 0.0;
         if (w < 3) {
           const int slot = kSlRhoSq + w;
-          for (int b = l; b < p.grid; b += 32) sacc += __ldcg(p.bred + static_cast<int64_t>(b) * kBred + slot);
+          for (int b0 = l; b0 < p.grid; b0 += 256) {
+            double e[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              const int b = b0 + 32 * q;
+              e[q] = b < p.grid ? __ldcg(p.bred + static_cast<int64_t>(b) * kBred + slot) : 0.0;
+            }
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+              if (b0 + 32 * q < p.grid) sacc += e[q];
+          }
         }
         load_vec_smem(p, p.rho, sc.vec);  // ends with __syncthreads
         if (w < 3) {
@@ -1770,6 +1804,7 @@ __device__ __noinline__ void engine_body(const EngineParams& p, Sh& sh, double* 
     // u = A_S x_next over the kept nonzeros (131-146) and the v history fix for atoms
     // dropped by this screening pass (FISTA, 673-684), in the same phase: dense work
     // items re-derive the coefficients with ProxCtx; the SuKro scatter is slice-owned.
+    FL1_MARK(7);
     int C_apply = 0;
     const bool fix_pass = !stop_now && fista && sh.screen_now;
     if (!stop_now) {
@@ -2110,8 +2145,10 @@ cudaError_t screen_kernel_launch(int64_t n, const double* dots, const double* ep
 // roofline (measured: 2-4 stages change the c2 pass by < 3%), while the larger
 // shared-memory carve-out shrinks L1 for the other phases. FL1_BULK_STAGES=R enables it.
 int engine_bulk_stages(int64_t ld) {
+  // power-iteration adjoints stream through a 3-stage bulk-copy ring by default
+  // (FL1_BULK_STAGES: 0 = register ring everywhere)
   const char* e = std::getenv("FL1_BULK_STAGES");
-  if (!e) return 0;
+  if (!e) e = "3";
   const int64_t room = 200 * 1024 / 8 - ld;  // doubles left beside the resident residual
   const int64_t fit = std::max<int64_t>(0, std::min<int64_t>(kMaxBulk, room / (kWarps * kUnit)));
   const int64_t r = std::min<int64_t>(fit, std::atoi(e));
