@@ -1635,21 +1635,6 @@ __device__ __noinline__ void engine_body(const EngineParams& p, Sh& sh, double* 
     }
 
     // ---------------------------------------------------------- phase B
-    // prefetch this thread's first atom (independent of the scalar reduction below)
-    ProxCtx::Atom pre{};
-    {
-      const int64_t q = lo + threadIdx.x;
-      if (q < hi) {
-        pre.c = p.corr[q];
-        pre.xo = bk.x[q];
-        pre.xpv = bk.xp[q];
-        pre.cy = (exact_fit || gram) ? p.corr_y[q] : 0.0;
-        pre.eps = bk.eps[q];
-        pre.en = bk.en[q];
-        pre.an = bk.an[q];
-        pre.aty = p.rule == FL1_RULE_DYNAMIC ? ((p.precompute_aty && s.atye_valid) ? bk.atye[q] : bk.aty[q]) : 0.0;
-      }
-    }
     const int l1s = l1_slot(s.t);
     if (gram) {
       grid_reduce(p, sh, (1u << l1s) | (1u << kSlGwa) | (1u << kSlGwg) | (1u << kSlGxa) | (1u << kSlGxg),
@@ -1670,6 +1655,21 @@ __device__ __noinline__ void engine_body(const EngineParams& p, Sh& sh, double* 
       grid_reduce(p, sh, 1u << l1s,
                   exact_fit ? ((1u << kSlMaxPlainY) | (1u << kSlMaxStableY))
                             : ((1u << kSlMaxPlain) | (1u << kSlMaxStable)));
+    }
+    // prefetch this thread's first atom (overlaps the scalar block below)
+    ProxCtx::Atom pre{};
+    {
+      const int64_t q = lo + threadIdx.x;
+      if (q < hi) {
+        pre.c = p.corr[q];
+        pre.xo = bk.x[q];
+        pre.xpv = bk.xp[q];
+        pre.cy = (exact_fit || gram) ? p.corr_y[q] : 0.0;
+        pre.eps = bk.eps[q];
+        pre.en = bk.en[q];
+        pre.an = bk.an[q];
+        pre.aty = p.rule == FL1_RULE_DYNAMIC ? ((p.precompute_aty && s.atye_valid) ? bk.atye[q] : bk.aty[q]) : 0.0;
+      }
     }
     if (threadIdx.x == 0) {
       const double x_l1 = sh.res[l1s];
