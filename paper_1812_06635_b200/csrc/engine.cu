@@ -214,6 +214,9 @@ __device__ void grid_reduce(const EngineParams& p, Sh& sh, unsigned mask_sum, un
     if (!(((mask_sum | mask_max) >> slot) & 1u)) continue;
     const bool mx = (mask_max >> slot) & 1u;
     double acc = mx ? -DBL_MAX : 0.0;
+    if (p.grid <= 32) {  // one partial per lane (cluster mode)
+      if (l < p.grid) acc = __ldcg(p.bred + static_cast<int64_t>(l) * kBred + slot);
+    } else
     for (int b0 = l; b0 < p.grid; b0 += 256) {  // 8 loads in flight per lane, added in b order
       double e[8];
 #pragma unroll
@@ -1556,6 +1559,9 @@ __device__ __noinline__ void engine_body(const EngineParams& p, Sh& sh, double* 
         double sacc = 0.0;
         if (w < 3) {
           const int slot = kSlRhoSq + w;
+          if (p.grid <= 32) {
+            if (l < p.grid) sacc = __ldcg(p.bred + static_cast<int64_t>(l) * kBred + slot);
+          } else
           for (int b0 = l; b0 < p.grid; b0 += 256) {
             double e[8];
 #pragma unroll
