@@ -582,8 +582,9 @@ def run_batched(args) -> None:
     cfg = F.SwitchConfig(screening_interval=10, max_iterations=5000, rel_tolerance=1e-6)
     opts = F.RunOptions(variant=F.VARIANT_SCREENED, full_lipschitz=[L])
     Yd = torch.from_numpy(np.ascontiguousarray(Y.T)).to(f"cuda:{local}")  # row b = signal b = column-major N x B
-    for _ in range(args.warmup):
+    for _ in range(args.warmup):  # both entry points (host-Y staging buffers are sized on first use)
         F.run_lasso_batched(seq, (n, B), lams, cfg, opts, args.concurrency, y_dev_ptr=Yd.data_ptr())
+        F.run_lasso_batched(seq, Y, lams, cfg, opts, args.concurrency)
     if dist:
         dist.barrier()
     torch.cuda.synchronize()

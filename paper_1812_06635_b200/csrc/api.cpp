@@ -36,6 +36,8 @@ cudaError_t engine_configure(int64_t ld, int64_t sukro_m, int device, int* grid_
 cudaError_t engine_launch(const EngineParams& p, int64_t sukro_m, cudaStream_t stream);
 size_t prefix_smem_bytes(int64_t ld, int64_t batch);
 cudaError_t prefix_launch(const PrefixParams& p, int device, cudaStream_t stream);
+cudaError_t trace_pack_launch(const fl1_trace_row* src, int64_t cap, const int64_t* off, int32_t batch,
+                              fl1_trace_row* dst, cudaStream_t stream);
 int prefix_split_max();
 cudaError_t gram_launch(const double* a, int64_t ld, int64_t k, double* g, int64_t ldg, int device,
                         cudaStream_t stream);
@@ -173,11 +175,23 @@ struct fl1_ctx {
                                      int grid_cap = 0);
   // device scratch of the batched entry, kept between calls (one batched call at a time)
   std::mutex batch_mu;
-  std::unique_ptr<DevBuf> batch_buf[2];
+  std::unique_ptr<DevBuf> batch_buf[3];
   cudaStream_t batch_stream = nullptr;
   cudaEvent_t batch_ev[2] = {nullptr, nullptr};
   void* batch_pinned = nullptr;
   size_t batch_pinned_bytes = 0;
+  void* trace_pinned = nullptr;  // packed trace rows of a batched call
+  size_t trace_pinned_bytes = 0;
+  char* pinned_traces(size_t bytes) {
+    if (trace_pinned_bytes < bytes) {
+      if (trace_pinned) cudaFreeHost(trace_pinned);
+      trace_pinned = nullptr;
+      trace_pinned_bytes = 0;
+      ck(cudaHostAlloc(&trace_pinned, bytes + bytes / 8, cudaHostAllocDefault), "cudaHostAlloc");
+      trace_pinned_bytes = bytes + bytes / 8;
+    }
+    return static_cast<char*>(trace_pinned);
+  }
   std::map<std::tuple<int64_t, int64_t, int>, std::pair<int, int>> cluster_cfg;  // (ld, sk_m, csize) -> (grid, clusters)
   char* pinned_scratch(size_t bytes) {
     if (batch_pinned_bytes < bytes) {
@@ -196,6 +210,7 @@ struct fl1_ctx {
   }
   ~fl1_ctx() {
     if (batch_pinned) cudaFreeHost(batch_pinned);
+    if (trace_pinned) cudaFreeHost(trace_pinned);
     for (auto e : batch_ev)
       if (e) cudaEventDestroy(e);
     if (batch_stream) cudaStreamDestroy(batch_stream);
@@ -272,7 +287,7 @@ struct fl1_seq {
 
 struct fl1_result {
   int64_t k = 0;
-  std::vector<double> x;
+  std::vector<double> xv;  // x at final_active (x is zero elsewhere; expanded by the accessors)
   bool converged = false;
   double final_gap = std::numeric_limits<double>::quiet_NaN();
   uint64_t iterations = 0;
@@ -641,8 +656,7 @@ void fill_params(EngineParams& p, const SolvePlan& pl, fl1_seq* s, double lambda
 void fill_result(fl1_result& r, const EngineState& st, const fl1_switch_config* cfg, int64_t k,
                  std::vector<int32_t> idx, const double* xs, std::vector<fl1_switch_event> sws) {
   r.k = k;
-  r.x.assign(static_cast<size_t>(k), 0.0);
-  for (size_t q = 0; q < idx.size(); ++q) r.x[static_cast<size_t>(idx[q])] = xs[q];
+  r.xv.assign(xs, xs + idx.size());
   r.final_active = std::move(idx);
   r.converged = st.converged != 0;
   r.iterations = st.converged ? st.t : cfg->max_iterations;
@@ -1033,6 +1047,13 @@ namespace {
 void solve_clusters(fl1_seq* s, const double* Y, bool y_device, int64_t ldy, const double* lambdas, int32_t batch,
                     const fl1_switch_config* cfg, const fl1_run_options* opts, int csize, fl1_result** out,
                     bool allow_prefix = true) {
+  const auto hl0 = std::chrono::steady_clock::now();
+  const bool host_log = std::getenv("FL1_HOST_LOG") != nullptr;  // diagnostics: host-side stage times
+  auto hlog = [&](const char* what) {
+    if (host_log)
+      std::fprintf(stderr, "fl1 batched host: %-12s %.3f ms\n", what,
+                   std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - hl0).count());
+  };
   const SolvePlan pl = plan_solve(s, cfg, opts);
   for (int32_t b = 0; b < batch; ++b)
     if (!(lambdas[b] > 0)) throw std::invalid_argument("lambda must be positive");
@@ -1136,6 +1157,7 @@ void solve_clusters(fl1_seq* s, const double* Y, bool y_device, int64_t ldy, con
     hst[b].t_k = 1.0;
   }
   std::copy(lambdas, lambdas + batch, reinterpret_cast<double*>(at(o_lam)));
+  hlog("prepared");
   ck(cudaEventRecord(ev0, stream), "event");
   ck(cudaMemsetAsync(base, 0, ws_bytes * static_cast<size_t>(n_clusters), stream), "workspace memset");
   ck(cudaMemsetAsync(counters, 0, sizeof(int64_t) * (2 + n_clusters), stream), "counter memset");
@@ -1242,27 +1264,44 @@ void solve_clusters(fl1_seq* s, const double* Y, bool y_device, int64_t ldy, con
   if (batch > 0) ck(fl1::engine_launch_clusters(p0, n_clusters, csize, pl.sk_m, stream), "cluster launch");
   ck(cudaEventRecord(ev1, stream), "event");
   ck(cudaMemcpyAsync(at(o_st), base + o_st, down_end - o_st, cudaMemcpyDeviceToHost, stream), "state download");
+  hlog("launched");
   ck(cudaStreamSynchronize(stream), "batched sync");
+  hlog("synced");
   const int64_t used = reinterpret_cast<const int64_t*>(at(o_cnt))[1];
   const int64_t* offs = reinterpret_cast<const int64_t*>(at(o_off));
   const fl1_switch_event* all_sw = reinterpret_cast<const fl1_switch_event*>(at(o_sw));
   int32_t* all_idx = reinterpret_cast<int32_t*>(pin + img + ybytes);
   double* all_x = reinterpret_cast<double*>(pin + img + ybytes + ((4 * kb * ub + 15) / 16) * 16);
+  if (host_log) std::fprintf(stderr, "fl1 batched host: packed outputs %lld\n", static_cast<long long>(used));
   if (used > 0) {
     ck(cudaMemcpyAsync(all_idx, base + o_idx, sizeof(int32_t) * used, cudaMemcpyDeviceToHost, stream), "idx");
     ck(cudaMemcpyAsync(all_x, base + o_x, sizeof(double) * used, cudaMemcpyDeviceToHost, stream), "x");
   }
-  std::vector<std::vector<fl1_trace_row>> traces(static_cast<size_t>(B));
-  for (int32_t b = 0; b < batch && opts->collect_trace; ++b) {
-    const int64_t rows = hst[b].n_trace;
-    traces[static_cast<size_t>(b)].resize(static_cast<size_t>(rows));
-    if (rows > 0)
-      ck(cudaMemcpyAsync(traces[static_cast<size_t>(b)].data(),
-                         base + o_tr + sizeof(fl1_trace_row) * static_cast<size_t>(b * cap),
-                         sizeof(fl1_trace_row) * rows, cudaMemcpyDeviceToHost, stream),
-         "trace download");
+  // traces: rows [b * cap, b * cap + n_trace_b) of every signal, packed on the device
+  // and downloaded in one copy (not one pageable copy per signal)
+  std::vector<int64_t> toff(static_cast<size_t>(B) + 1, 0);
+  for (int32_t b = 0; b < batch; ++b)
+    toff[static_cast<size_t>(b) + 1] = toff[static_cast<size_t>(b)] + (opts->collect_trace ? hst[b].n_trace : 0);
+  const int64_t trows = toff[static_cast<size_t>(batch)];
+  const fl1_trace_row* all_tr = nullptr;
+  if (trows > 0) {
+    const size_t off_bytes = (sizeof(int64_t) * (static_cast<size_t>(B) + 1) + 255) / 256 * 256;
+    char* tp = ctx->pinned_traces(off_bytes + sizeof(fl1_trace_row) * static_cast<size_t>(trows));
+    std::copy(toff.begin(), toff.end(), reinterpret_cast<int64_t*>(tp));
+    char* tb = ctx->batch_scratch(2, off_bytes + sizeof(fl1_trace_row) * static_cast<size_t>(trows)).as<char>();
+    ck(cudaMemcpyAsync(tb, tp, sizeof(int64_t) * (static_cast<size_t>(B) + 1), cudaMemcpyHostToDevice, stream),
+       "trace offsets");
+    ck(fl1::trace_pack_launch(reinterpret_cast<const fl1_trace_row*>(base + o_tr), cap,
+                              reinterpret_cast<const int64_t*>(tb), batch,
+                              reinterpret_cast<fl1_trace_row*>(tb + off_bytes), stream),
+       "trace pack");
+    ck(cudaMemcpyAsync(tp + off_bytes, tb + off_bytes, sizeof(fl1_trace_row) * static_cast<size_t>(trows),
+                       cudaMemcpyDeviceToHost, stream),
+       "trace download");
+    all_tr = reinterpret_cast<const fl1_trace_row*>(tp + off_bytes);
   }
   ck(cudaStreamSynchronize(stream), "download sync");
+  hlog("downloaded");
   float batch_ms = 0.f;
   ck(cudaEventElapsedTime(&batch_ms, ev0, ev1), "elapsed");
   if (step_log && d_steps) {
@@ -1285,17 +1324,20 @@ void solve_clusters(fl1_seq* s, const double* Y, bool y_device, int64_t ldy, con
     const fl1_switch_event* sb = all_sw + static_cast<size_t>(b) * fl1::kMaxLevels;
     fill_result(*res, st, cfg, k, std::vector<int32_t>(ib, ib + st.S), xb,
                 std::vector<fl1_switch_event>(sb, sb + st.n_switches));
-    res->trace = std::move(traces[static_cast<size_t>(b)]);
+    if (all_tr)
+      res->trace.assign(all_tr + toff[static_cast<size_t>(b)], all_tr + toff[static_cast<size_t>(b) + 1]);
     res->device_ms = (st.end_ns - st.start_ns) * 1e-6;
+    if (res->setup_ms < 0.0) res->setup_ms = 0.0;  // hand-off signals ran their setup in the lockstep launch
     res->batch_ms = batch_ms;
     res->launches = 0;  // one launch for the whole batch (fl1_result_info.kernel_launches of signal 0 = 1)
-    if (b == 0) res->launches = use_prefix ? 2 : 1;
+    if (b == 0) res->launches = (use_prefix ? 2 : 1) + (all_tr ? 1 : 0);  // + the trace packing kernel
     res->h2d = h2d_sig;
     res->d2h = static_cast<int64_t>(sizeof(EngineState)) + 12 * st.S +
                st.n_switches * static_cast<int64_t>(sizeof(fl1_switch_event)) +
                st.n_trace * static_cast<int64_t>(sizeof(fl1_trace_row));
     out[b] = res.release();
   }
+  hlog("results");
 }
 
 // A single solve on a small, L2-resident dictionary is latency-bound: one
@@ -1432,8 +1474,14 @@ int fl1_result_info_get(const fl1_result* r, fl1_result_info* o) {
     o->batch_device_ms = r->batch_ms >= 0.0 ? r->batch_ms : r->device_ms;
   });
 }
+namespace {
+void expand_x(const fl1_result& r, double* out) {  // finish (741-748): scatter to length K
+  std::fill(out, out + r.k, 0.0);
+  for (size_t q = 0; q < r.xv.size(); ++q) out[r.final_active[q]] = r.xv[q];
+}
+}  // namespace
 int fl1_result_x(const fl1_result* r, double* out) {
-  return guard([&] { std::copy(r->x.begin(), r->x.end(), out); });
+  return guard([&] { expand_x(*r, out); });
 }
 int fl1_result_trace(const fl1_result* r, fl1_trace_row* out) {
   return guard([&] { std::copy(r->trace.begin(), r->trace.end(), out); });
@@ -1455,7 +1503,7 @@ int fl1_results_collect(fl1_result* const* rs, int32_t count, fl1_result_info* i
   return guard([&] {
     for (int32_t i = 0; i < count; ++i) {
       const fl1_result& r = *rs[i];
-      if (x) std::copy(r.x.begin(), r.x.end(), x + static_cast<int64_t>(i) * r.k);
+      if (x) expand_x(r, x + static_cast<int64_t>(i) * r.k);
       if (profiles) std::copy(r.prof, r.prof + 14, profiles + static_cast<int64_t>(i) * 14);
     }
   });

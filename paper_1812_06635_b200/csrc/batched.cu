@@ -1117,4 +1117,21 @@ cudaError_t prefix_launch(const PrefixParams& p, int device, cudaStream_t stream
                                      stream);
 }
 
+// Batched traces: signal b's rows [b * cap, b * cap + n_b) packed to [off[b], off[b+1]).
+__global__ void trace_pack_kernel(const fl1_trace_row* __restrict__ src, int64_t cap, const int64_t* __restrict__ off,
+                                  int32_t batch, fl1_trace_row* __restrict__ dst) {
+  for (int32_t b = blockIdx.x; b < batch; b += gridDim.x) {
+    const int64_t o = off[b], n = off[b + 1] - o;
+    const fl1_trace_row* s = src + static_cast<int64_t>(b) * cap;
+    for (int64_t r = threadIdx.x; r < n; r += blockDim.x) dst[o + r] = s[r];
+  }
+}
+
+cudaError_t trace_pack_launch(const fl1_trace_row* src, int64_t cap, const int64_t* off, int32_t batch,
+                              fl1_trace_row* dst, cudaStream_t stream) {
+  if (batch <= 0) return cudaSuccess;
+  trace_pack_kernel<<<std::min<int32_t>(batch, 1024), 128, 0, stream>>>(src, cap, off, batch, dst);
+  return cudaGetLastError();
+}
+
 }  // namespace fl1

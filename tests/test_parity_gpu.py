@@ -322,7 +322,7 @@ def test_batched_lockstep_prefix(cuda, oracle16, variant, solver):
     seq_g = F.ApproxSequence([F.make_exact_approx(F.DenseDictionary(a, backend=cuda))])
     seq_o = F.ApproxSequence([F.make_exact_approx(F.DenseDictionary(a, backend=oracle16))])
     res = F.run_lasso_batched(seq_g, Y, lams, cfg, opts, concurrency=-2)
-    assert res[0].kernel_launches == 2  # prefix + cluster engine
+    assert res[0].kernel_launches == 3  # prefix + cluster engine + trace packing
     for b in range(0, B, 3 if variant == F.VARIANT_PLAIN else 1):
         o = F.run_lasso(seq_o, Y[:, b], lams[b], cfg, opts)
         assert_parity(res[b], o, a, Y[:, b], lams[b])
