@@ -1284,20 +1284,33 @@ void solve_clusters(fl1_seq* s, const double* Y, bool y_device, int64_t ldy, con
     toff[static_cast<size_t>(b) + 1] = toff[static_cast<size_t>(b)] + (opts->collect_trace ? hst[b].n_trace : 0);
   const int64_t trows = toff[static_cast<size_t>(batch)];
   const fl1_trace_row* all_tr = nullptr;
+  bool packed_launch = false;
   if (trows > 0) {
     const size_t off_bytes = (sizeof(int64_t) * (static_cast<size_t>(B) + 1) + 255) / 256 * 256;
     char* tp = ctx->pinned_traces(off_bytes + sizeof(fl1_trace_row) * static_cast<size_t>(trows));
     std::copy(toff.begin(), toff.end(), reinterpret_cast<int64_t*>(tp));
-    char* tb = ctx->batch_scratch(2, off_bytes + sizeof(fl1_trace_row) * static_cast<size_t>(trows)).as<char>();
-    ck(cudaMemcpyAsync(tb, tp, sizeof(int64_t) * (static_cast<size_t>(B) + 1), cudaMemcpyHostToDevice, stream),
-       "trace offsets");
-    ck(fl1::trace_pack_launch(reinterpret_cast<const fl1_trace_row*>(base + o_tr), cap,
-                              reinterpret_cast<const int64_t*>(tb), batch,
-                              reinterpret_cast<fl1_trace_row*>(tb + off_bytes), stream),
-       "trace pack");
-    ck(cudaMemcpyAsync(tp + off_bytes, tb + off_bytes, sizeof(fl1_trace_row) * static_cast<size_t>(trows),
-                       cudaMemcpyDeviceToHost, stream),
-       "trace download");
+    if (batch <= 4) {  // few signals: one async copy each straight into pinned memory
+      for (int32_t b = 0; b < batch; ++b) {
+        const int64_t rows = toff[static_cast<size_t>(b) + 1] - toff[static_cast<size_t>(b)];
+        if (rows > 0)
+          ck(cudaMemcpyAsync(tp + off_bytes + sizeof(fl1_trace_row) * static_cast<size_t>(toff[static_cast<size_t>(b)]),
+                             base + o_tr + sizeof(fl1_trace_row) * static_cast<size_t>(b * cap),
+                             sizeof(fl1_trace_row) * static_cast<size_t>(rows), cudaMemcpyDeviceToHost, stream),
+             "trace download");
+      }
+    } else {
+      char* tb = ctx->batch_scratch(2, off_bytes + sizeof(fl1_trace_row) * static_cast<size_t>(trows)).as<char>();
+      ck(cudaMemcpyAsync(tb, tp, sizeof(int64_t) * (static_cast<size_t>(B) + 1), cudaMemcpyHostToDevice, stream),
+         "trace offsets");
+      ck(fl1::trace_pack_launch(reinterpret_cast<const fl1_trace_row*>(base + o_tr), cap,
+                                reinterpret_cast<const int64_t*>(tb), batch,
+                                reinterpret_cast<fl1_trace_row*>(tb + off_bytes), stream),
+         "trace pack");
+      ck(cudaMemcpyAsync(tp + off_bytes, tb + off_bytes, sizeof(fl1_trace_row) * static_cast<size_t>(trows),
+                         cudaMemcpyDeviceToHost, stream),
+         "trace download");
+      packed_launch = true;
+    }
     all_tr = reinterpret_cast<const fl1_trace_row*>(tp + off_bytes);
   }
   ck(cudaStreamSynchronize(stream), "download sync");
@@ -1330,7 +1343,7 @@ void solve_clusters(fl1_seq* s, const double* Y, bool y_device, int64_t ldy, con
     if (res->setup_ms < 0.0) res->setup_ms = 0.0;  // hand-off signals ran their setup in the lockstep launch
     res->batch_ms = batch_ms;
     res->launches = 0;  // one launch for the whole batch (fl1_result_info.kernel_launches of signal 0 = 1)
-    if (b == 0) res->launches = (use_prefix ? 2 : 1) + (all_tr ? 1 : 0);  // + the trace packing kernel
+    if (b == 0) res->launches = (use_prefix ? 2 : 1) + (packed_launch ? 1 : 0);  // + the trace packing kernel
     res->h2d = h2d_sig;
     res->d2h = static_cast<int64_t>(sizeof(EngineState)) + 12 * st.S +
                st.n_switches * static_cast<int64_t>(sizeof(fl1_switch_event)) +
