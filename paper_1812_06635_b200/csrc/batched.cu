@@ -37,6 +37,8 @@ namespace {
 #endif
 constexpr int kPT = FL1_PREFIX_THREADS;  // threads per CTA
 constexpr int kPW = kPT / 32;
+constexpr int kIt = 9;  // atoms per lane of a warp range: K <= prefix_max_atoms() = 4608 -> 288 per warp
+constexpr int kItB = 3; // atoms per lane loaded together in the prox pass
 constexpr int kTM = 128, kTN = 64;  // output tile: 128 rows (atoms / samples) x 64 signals
 // warp grid over a 128 x 64 output tile: kWR x kWC warps, each kRT x kCT 8x8 DMMA tiles
 constexpr int kWR = 8, kWC = (kPT / 32) / kWR;
@@ -494,50 +496,61 @@ __device__ __forceinline__ int warp_append(bool flag, double v, int32_t j, doubl
   return cnt + __popc(bal);
 }
 
-// rows over threads: acc_i += sum over the warp segments (in warp = atom order);
-// four rows per thread and four entries per round keep 16 loads in flight
+// rows over threads: acc_i += sum over the warp segments (in warp = atom order).
+// The entries are walked as one list across the segments (a uniform cursor), eight
+// per round, two rows per thread: 16 loads in flight and ~nnz/8 L2 round trips
+// instead of one per entry at every segment's tail.
+constexpr int kApE = 8, kApR = 2;
 __device__ __forceinline__ void apply_segments(const PrefixParams& p, double* us, const double* ev, const int32_t* ej,
                                                int64_t seg, const int32_t* cnt, double sign) {
   const int64_t ld = p.ld;
   const double* __restrict__ A = p.a;
-  for (int64_t i0 = threadIdx.x; i0 < ld; i0 += 4 * kPT) {
-    double acc[4];
-    bool ok[4];
+  for (int64_t i0 = threadIdx.x; i0 < ld; i0 += kApR * kPT) {
+    double acc[kApR];
+    bool ok[kApR];
 #pragma unroll
-    for (int r = 0; r < 4; ++r) {
+    for (int r = 0; r < kApR; ++r) {
       ok[r] = i0 + r * kPT < ld;
       acc[r] = ok[r] ? us[i0 + r * kPT] : 0.0;
     }
-    for (int w = 0; w < kPW; ++w) {
-      const double* v = ev + w * seg;
-      const int32_t* jj = ej + w * seg;
-      const int n = cnt[w];
-      int e = 0;
-      for (; e + 4 <= n; e += 4) {
-        double a[4][4];
+    int cw = 0, ce = 0;  // cursor: segment, entry
+    while (true) {
+      int32_t jq[kApE];
+      double vq[kApE];
+      int got = 0;
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const double* col = A + static_cast<int64_t>(jj[e + q]) * ld + i0;
-#pragma unroll
-          for (int r = 0; r < 4; ++r) a[q][r] = ok[r] ? __ldg(col + r * kPT) : 0.0;
+      for (int q = 0; q < kApE; ++q) {
+        while (cw < kPW && ce >= cnt[cw]) {
+          ++cw;
+          ce = 0;
         }
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const double c = sign * v[e + q];
-#pragma unroll
-          for (int r = 0; r < 4; ++r) acc[r] = fma(c, a[q][r], acc[r]);
+        jq[q] = -1;
+        vq[q] = 0.0;
+        if (cw < kPW) {
+          jq[q] = ej[cw * seg + ce];
+          vq[q] = sign * ev[cw * seg + ce];
+          ++ce;
+          ++got;
         }
       }
-      for (; e < n; ++e) {
-        const double* col = A + static_cast<int64_t>(jj[e]) * ld + i0;
-        const double c = sign * v[e];
+      if (got == 0) break;
+      double a[kApE][kApR];
 #pragma unroll
-        for (int r = 0; r < 4; ++r)
-          if (ok[r]) acc[r] = fma(c, __ldg(col + r * kPT), acc[r]);
+      for (int q = 0; q < kApE; ++q) {
+        const double* col = A + static_cast<int64_t>(jq[q] < 0 ? 0 : jq[q]) * ld + i0;
+#pragma unroll
+        for (int r = 0; r < kApR; ++r) a[q][r] = (ok[r] && jq[q] >= 0) ? __ldg(col + r * kPT) : 0.0;
       }
+#pragma unroll
+      for (int q = 0; q < kApE; ++q) {
+        if (jq[q] < 0) continue;
+#pragma unroll
+        for (int r = 0; r < kApR; ++r) acc[r] = fma(vq[q], a[q][r], acc[r]);
+      }
+      if (got < kApE) break;
     }
 #pragma unroll
-    for (int r = 0; r < 4; ++r)
+    for (int r = 0; r < kApR; ++r)
       if (ok[r]) us[i0 + r * kPT] = acc[r];
   }
   __syncthreads();
@@ -680,12 +693,33 @@ __device__ __noinline__ void fista_step(const PrefixParams& p, PSh& sh, int64_t 
   double* cr = p.corr + a * K;
   int8_t* mk = p.mask + b * K;
   // corr = sum of the split-K parts, written back to part 0; max |corr| over the set
+  // (all kIt atoms of a lane loaded together: one L2 round trip per split part)
   double dp = 0.0;
-  for (int64_t j = wr.lo + l; j < wr.hi; j += 32) {
-    double c = __ldcg(cr + j);
-    for (int kp = 1; kp < sk; ++kp) c += __ldcg(cr + kp * part + j);
-    if (sk > 1) __stcg(cr + j, c);
-    if (mk[j]) dp = fmax(dp, fabs(c));
+  {
+    double cv[kIt];
+#pragma unroll
+    for (int i = 0; i < kIt; ++i) {
+      const int64_t j = wr.lo + l + 32 * i;
+      cv[i] = j < wr.hi ? __ldcg(cr + j) : 0.0;
+    }
+    for (int kp = 1; kp < sk; ++kp) {
+      double pv[kIt];
+#pragma unroll
+      for (int i = 0; i < kIt; ++i) {
+        const int64_t j = wr.lo + l + 32 * i;
+        pv[i] = j < wr.hi ? __ldcg(cr + kp * part + j) : 0.0;
+      }
+#pragma unroll
+      for (int i = 0; i < kIt; ++i) cv[i] += pv[i];
+    }
+#pragma unroll
+    for (int i = 0; i < kIt; ++i) {
+      const int64_t j = wr.lo + l + 32 * i;
+      if (j < wr.hi) {
+        if (sk > 1) __stcg(cr + j, cv[i]);
+        if (mk[j]) dp = fmax(dp, fabs(cv[i]));
+      }
+    }
   }
   dp = block_max(dp, sh);
   if (threadIdx.x == 0) {
@@ -781,18 +815,34 @@ __device__ __noinline__ void fista_step(const PrefixParams& p, PSh& sh, int64_t 
   int32_t* fx_j = nz_j + seg * kPW;
   int nz_c = 0, fx_c = 0;
   double red3[3] = {0.0, 0.0, 0.0};  // kept, nnz(x_new), |x_new|_1
-  for (int64_t base = wr.lo; base < wr.hi; base += 32) {
+  for (int64_t b0 = wr.lo; b0 < wr.hi; b0 += 32 * kItB) {
+    // the next kItB groups of 32 atoms: every load issued before the first is used
+    bool onv[kItB];
+    double cq[kItB], xq[kItB], xpq[kItB], eq[kItB];
+#pragma unroll
+    for (int i = 0; i < kItB; ++i) {
+      const int64_t j = b0 + 32 * i + l;
+      onv[i] = j < wr.hi && mk[j];
+      cq[i] = onv[i] ? __ldcg(cr + j) : 0.0;
+      xq[i] = onv[i] ? xc[j] : 0.0;
+      xpq[i] = (onv[i] && m != 0.0) ? xpc[j] : 0.0;
+      eq[i] = (onv[i] && screen) ? p.en[j] : 0.0;
+    }
+#pragma unroll
+  for (int i = 0; i < kItB; ++i) {
+    const int64_t base = b0 + 32 * i;
+    if (base >= wr.hi) break;  // warp-uniform
     const int64_t j = base + l;
     double v = 0.0, fixv = 0.0;
-    if (j < wr.hi && mk[j]) {
-      const double c = __ldcg(cr + j);
-      const double xo = xc[j];
-      const double xpv = m != 0.0 ? xpc[j] : 0.0;
+    if (onv[i]) {
+      const double c = cq[i];
+      const double xo = xq[i];
+      const double xpv = xpq[i];
       const double gg = m != 0.0 ? __fma_rn(1.0 + m, xo, -__dmul_rn(m, xpv)) : xo;
       const double z = __fma_rn(inv_l, c, gg);
       const double mag = fabs(z) - thresh;
       v = mag <= 0.0 ? 0.0 : (z > 0.0 ? mag : -mag);
-      const bool keep = !screen || __fma_rn(rad, p.en[j], fabs(__dmul_rn(spv, c))) >= 1.0;
+      const bool keep = !screen || __fma_rn(rad, eq[i], fabs(__dmul_rn(spv, c))) >= 1.0;
       if (keep) {
         red3[0] += 1.0;
       } else {  // dropped: x_prev of the shifted history is the old x
@@ -808,6 +858,7 @@ __device__ __noinline__ void fista_step(const PrefixParams& p, PSh& sh, int64_t 
     if (j < wr.hi) xn[j] = v;
     nz_c = warp_append(v != 0.0, v, static_cast<int32_t>(j), nz_v + w * seg, nz_j + w * seg, nz_c);
     fx_c = warp_append(fixv != 0.0, fixv, static_cast<int32_t>(j), fx_v + w * seg, fx_j + w * seg, fx_c);
+  }
   }
   if (l == 0) {
     sh.nzc[w] = nz_c;
