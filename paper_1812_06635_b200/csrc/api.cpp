@@ -346,6 +346,15 @@ size_t carve(EngineParams& p, char* base, int64_t n, int64_t k, int64_t ld, int 
   p.corr_y = c.take<double>(kk);
   p.part = c.take<double>(kk * units);
   p.cnt = c.take<int32_t>(kk);
+  p.nzv = c.take<double>(kk);
+  p.nzj = c.take<int32_t>(kk);
+  p.fxv = c.take<double>(kk);
+  p.fxj = c.take<int32_t>(kk);
+  p.lcnt = c.take<int32_t>(2 * static_cast<int64_t>(grid));
+  {
+    const char* e = std::getenv("FL1_LIST_APPLY");
+    p.list_apply = e ? std::atoi(e) : 1;
+  }
   p.pv = c.take<double>(kk);
   p.pw = c.take<double>(kk);
   p.PU = c.take<double>(ld);

@@ -1247,6 +1247,152 @@ __device__ void combine_u(const EngineParams& p, Sh& sh, int C, bool shift, bool
   }
 }
 
+// Phase E of dense levels with phase-B lists: u_i = sum over the kept nonzeros of
+// x_next (the CTAs' lists in CTA = position order) of x_j A(i, j) for this CTA's rows,
+// the v-fix sum over the dropped atoms' previous iterate likewise, then the same
+// per-row epilogue as combine_u. Replaces the chunked apply partials (and their
+// ProxCtx re-derivation) with one gather of the nonzero columns' row segments.
+constexpr int kLRB = 64;  // rows per block (at most 2 per lane)
+
+// This warp's share of one list for rows [rb, rb + 32 RL): lane l accumulates rows
+// rb + l + 32 r in entry order; 32 / RL entries' column segments in flight per lane.
+template <int RL>
+__device__ __forceinline__ void list_rows(const double* __restrict__ A, int64_t ld, int64_t S, int G, const int32_t* pp,
+                                          const double* lv_v, const int32_t* lv_j, int e0, int e1, int64_t rb,
+                                          int64_t ihi, double (&acc)[2]) {
+  constexpr int kE = 32 / RL;
+  const int l = threadIdx.x & 31;
+  for (int eb = e0; eb < e1; eb += 32) {
+    // lane q fetches entry eb + q (its CTA by binary search over the prefix)
+    int32_t cj = 0;
+    double cv = 0.0;
+    if (eb + l < e1) {
+      const int e = eb + l;
+      int a = 0, b = G;  // largest c with pp[c] <= e
+      while (b - a > 1) {
+        const int mid = (a + b) >> 1;
+        if (pp[mid] <= e) a = mid;
+        else b = mid;
+      }
+      const int64_t at = S * a / G + (e - pp[a]);
+      cj = lv_j[at];
+      cv = lv_v[at];
+    }
+    const int ne = min(32, e1 - eb);
+    for (int q0 = 0; q0 < ne; q0 += kE) {
+      double av[kE][RL];
+#pragma unroll
+      for (int q = 0; q < kE; ++q) {
+        const int32_t j = __shfl_sync(kFull, cj, (q0 + q) & 31);
+        const double* col = A + static_cast<int64_t>(j) * ld + rb + l;
+#pragma unroll
+        for (int r = 0; r < RL; ++r)
+          av[q][r] = (q0 + q < ne && rb + l + 32 * r < ihi) ? __ldcg(col + 32 * r) : 0.0;
+      }
+#pragma unroll
+      for (int q = 0; q < kE; ++q) {
+        const double v = __shfl_sync(kFull, cv, (q0 + q) & 31);
+        if (q0 + q < ne) {
+#pragma unroll
+          for (int r = 0; r < RL; ++r) acc[r] = fma(v, av[q][r], acc[r]);
+        }
+      }
+    }
+  }
+}
+
+__device__ __noinline__ void combine_u_lists(const EngineParams& p, Sh& sh, const DevLevel& lv, int64_t S, bool shift,
+                                             bool fix, double m, double* scratch) {
+  const int G = vsize();
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  int64_t ilo, ihi;
+  slice(p.ld, ilo, ihi);
+  const bool mom = m != 0.0;
+  // the first block's per-row operands, loaded while the list lengths are scanned
+  double pre_u = 0.0, pre_v = 0.0, pre_y = 0.0;
+  if (threadIdx.x < kLRB && ilo + threadIdx.x < ihi) {
+    const int64_t i = ilo + threadIdx.x;
+    pre_y = p.y[i];
+    if (shift) pre_u = __ldcg(p.U + i);
+    else if (mom) pre_v = __ldcg(p.V + i);
+  }
+  int32_t* pre = reinterpret_cast<int32_t*>(scratch);  // [2][G + 1] exclusive prefix of the list lengths
+  double* wpart = scratch + (G + 2);                    // [2][kWarps][kLRB]
+  for (int t = threadIdx.x; t < 2 * G; t += kThreads) pre[(t / G) * (G + 1) + 1 + t % G] = __ldcg(p.lcnt + t);
+  if (threadIdx.x < 2) pre[threadIdx.x * (G + 1)] = 0;
+  __syncthreads();
+  if (w < 2) {  // warp 0: apply lists, warp 1: fix lists
+    int32_t* pp = pre + w * (G + 1);
+    int carry = 0;
+    for (int c0 = 0; c0 < G; c0 += 32) {
+      int v = c0 + l < G ? pp[1 + c0 + l] : 0;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(kFull, v, o);
+        if (l >= o) v += t;
+      }
+      if (c0 + l < G) pp[1 + c0 + l] = v + carry;
+      carry += __shfl_sync(kFull, v, 31);
+    }
+  }
+  __syncthreads();
+  const double* __restrict__ A = lv.a;
+  const int64_t ld = p.ld;
+  double arr = 0.0, ary = 0.0, aee = 0.0;
+  for (int64_t rb = ilo; rb < ihi; rb += kLRB) {
+    const bool one = ihi - rb <= 32;  // block-uniform
+    for (int src = 0; src < (fix ? 2 : 1); ++src) {
+      const int32_t* pp = pre + src * (G + 1);
+      const int E = pp[G];
+      const int e0 = static_cast<int>(static_cast<int64_t>(E) * w / kWarps);
+      const int e1 = static_cast<int>(static_cast<int64_t>(E) * (w + 1) / kWarps);
+      double acc[2] = {0.0, 0.0};
+      if (one)
+        list_rows<1>(A, ld, S, G, pp, src == 0 ? p.nzv : p.fxv, src == 0 ? p.nzj : p.fxj, e0, e1, rb, ihi, acc);
+      else
+        list_rows<2>(A, ld, S, G, pp, src == 0 ? p.nzv : p.fxv, src == 0 ? p.nzj : p.fxj, e0, e1, rb, ihi, acc);
+#pragma unroll
+      for (int r = 0; r < 2; ++r) wpart[(src * kWarps + w) * kLRB + l + 32 * r] = acc[r];
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < kLRB && rb + t < ihi; t += kThreads) {
+      const int64_t i = rb + t;
+      double u = 0.0, f = 0.0;
+      for (int ww = 0; ww < kWarps; ++ww) u += wpart[ww * kLRB + t];
+      if (fix)
+        for (int ww = 0; ww < kWarps; ++ww) f += wpart[(kWarps + ww) * kLRB + t];
+      const bool first = rb == ilo;
+      const double yi = first ? pre_y : p.y[i];  // zero on padded rows
+      double v = 0.0;
+      if (shift) {
+        v = (first ? pre_u : __ldcg(p.U + i)) - f;  // v = u_old with the history fix (581-590, 673-684)
+        __stcg(p.V + i, v);
+      } else if (mom) {
+        v = first ? pre_v : __ldcg(p.V + i);
+      }
+      __stcg(p.U + i, u);
+      const double uw = mom ? (1.0 + m) * u - m * v : u;
+      const double r = i < p.n ? yi - uw : 0.0;
+      __stcg(p.rho + i, r);
+      arr = fma(r, r, arr);
+      ary = fma(yi, r, ary);
+      if (mom && i < p.n) {
+        const double e = yi - u;
+        aee = fma(e, e, aee);
+      }
+    }
+    __syncthreads();  // wpart is reused by the next row block
+  }
+  double v[3] = {arr, ary, aee};
+  const bool mx[3] = {false, false, false};
+  block_reduce<3>(v, mx, sh);
+  if (threadIdx.x == 0) {
+    put_slot(p, kSlRhoSq, v[0]);
+    put_slot(p, kSlRhoY, v[1]);
+    put_slot(p, kSlRhoE, v[2]);
+  }
+}
+
 // momentum of the next iteration from the FISTA state (fastl1.cpp:465-470)
 __device__ __forceinline__ double next_momentum(const EngineParams& p, double t_k, bool ready) {
   if (p.solver != FL1_FISTA || !ready) return 0.0;
@@ -1771,31 +1917,83 @@ __device__ __noinline__ void engine_body(const EngineParams& p, Sh& sh, double* 
     px.rule_gap = p.rule == FL1_RULE_GAP;
     px.ray_is_y = sh.ray_is_y;
     px.use_atye = p.precompute_aty && s.atye_valid;
+    const bool fix_pass = !stop_now && fista && sh.screen_now;
+    // dense (not Gram): phase B lists this CTA's kept nonzeros and v-fix entries, and
+    // phase E forms u (and the fix) by row slices straight from the lists
+    const bool lists = p.list_apply && lv.kind == kDense && !gram && !stop_now &&
+                       (ld + vsize() - 1) / vsize() <= kLRB;  // one row block per CTA
     {  // per-atom sphere test + prox on this CTA's slice (results to xnew / keep)
       double kept = 0.0, look = 0.0, nnz = 0.0, l1n = 0.0;
-      for (int64_t q = lo + threadIdx.x; q < hi; q += kThreads) {
-        ProxCtx::Atom a;
-        if (q == lo + threadIdx.x) {
-          a = pre;
-          if (px.m == 0.0) a.xpv = 0.0;
-        } else {
-          a = px.load(q);
+      int32_t na = 0, nf = 0;  // list lengths (lists only)
+      const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+      for (int64_t q0 = lo; q0 < hi; q0 += kThreads) {  // uniform trip count (list appends)
+        const int64_t q = q0 + threadIdx.x;
+        bool fa = false, ff = false;
+        double va = 0.0, vf = 0.0;
+        if (q < hi) {
+          ProxCtx::Atom a;
+          if (q == lo + threadIdx.x) {
+            a = pre;
+            if (px.m == 0.0) a.xpv = 0.0;
+          } else {
+            a = px.load(q);
+          }
+          if (stop_now) {
+            nnz += a.xo != 0.0 ? 1.0 : 0.0;
+          } else {
+            const double d = px.screen_now ? px.dot(a) : 0.0;
+            const bool kp = px.keep(a, d);
+            look += px.look(a, d, kp) ? 1.0 : 0.0;
+            const double xn = px.xnew(a);
+            p.xnew[q] = xn;
+            bk.keep[q] = static_cast<int8_t>(kp);
+            if (kp) {
+              kept += 1.0;
+              nnz += xn != 0.0 ? 1.0 : 0.0;
+              l1n += fabs(xn);  // ||x_{t+1}||_1 over the preserved set (next iteration's 473)
+            }
+            fa = kp && xn != 0.0;
+            ff = fix_pass && !kp && a.xo != 0.0;
+            va = xn;
+            vf = a.xo;
+          }
         }
-        if (stop_now) {
-          nnz += a.xo != 0.0 ? 1.0 : 0.0;
-          continue;
+        if (lists) {  // ordered appends (position order) at this CTA's slice offset
+          const int32_t col = (fa || ff) ? bk.idx[q] : 0;
+          const unsigned ba = __ballot_sync(kFull, fa), bf = __ballot_sync(kFull, ff);
+          if (l == 0) {
+            sh.wcount[0][w] = __popc(ba);
+            sh.wcount[1][w] = __popc(bf);
+          }
+          __syncthreads();
+          int oa = na, of = nf, ta = 0, tf = 0;
+          for (int ww = 0; ww < kWarps; ++ww) {
+            if (ww < w) {
+              oa += sh.wcount[0][ww];
+              of += sh.wcount[1][ww];
+            }
+            ta += sh.wcount[0][ww];
+            tf += sh.wcount[1][ww];
+          }
+          const unsigned below = (1u << l) - 1u;
+          if (fa) {
+            const int64_t at = lo + oa + __popc(ba & below);
+            p.nzj[at] = col;
+            p.nzv[at] = va;
+          }
+          if (ff) {
+            const int64_t at = lo + of + __popc(bf & below);
+            p.fxj[at] = col;
+            p.fxv[at] = vf;
+          }
+          na += ta;
+          nf += tf;
+          __syncthreads();  // wcount is reused by the next round
         }
-        const double d = px.screen_now ? px.dot(a) : 0.0;
-        const bool kp = px.keep(a, d);
-        look += px.look(a, d, kp) ? 1.0 : 0.0;
-        const double xn = px.xnew(a);
-        p.xnew[q] = xn;
-        bk.keep[q] = static_cast<int8_t>(kp);
-        if (kp) {
-          kept += 1.0;
-          nnz += xn != 0.0 ? 1.0 : 0.0;
-          l1n += fabs(xn);  // ||x_{t+1}||_1 over the preserved set (next iteration's 473)
-        }
+      }
+      if (lists && threadIdx.x == 0) {
+        p.lcnt[vrank()] = na;
+        p.lcnt[vsize() + vrank()] = nf;
       }
       double v[4] = {kept, look, nnz, l1n};
       const bool mx[4] = {false, false, false, false};
@@ -1812,8 +2010,7 @@ __device__ __noinline__ void engine_body(const EngineParams& p, Sh& sh, double* 
     // items re-derive the coefficients with ProxCtx; the SuKro scatter is slice-owned.
     FL1_MARK(7);
     int C_apply = 0;
-    const bool fix_pass = !stop_now && fista && sh.screen_now;
-    if (!stop_now) {
+    if (!stop_now && !lists) {
       if (lv.kind == kDense) {
         ApplySrc as{bk.idx, nullptr, nullptr, 1.0, nullptr, nullptr, &px};
         const DevLevel glv = gram_level(p);  // Gram mode: gx = G x, gv fix over G columns (596-600, 678-679)
@@ -1962,6 +2159,7 @@ __device__ __noinline__ void engine_body(const EngineParams& p, Sh& sh, double* 
     {  // combine u (and v <- u_old - fix), then the next iteration's rho_g
       const double tk_next = fista ? (s.momentum_ready ? sh.t_next : s.t_k) : s.t_k;
       if (gram) combine_g(p, C_apply, fista, fix_pass);
+      else if (lists) combine_u_lists(p, sh, lv, S, fista, fix_pass, next_momentum(p, tk_next, fista), sc.red);
       else combine_u(p, sh, C_apply, fista, fix_pass, next_momentum(p, tk_next, fista));
     }
     if (threadIdx.x == 0) {

@@ -271,6 +271,14 @@ struct alignas(16) EngineParams {
   double* corr_y;   // K (exact-fit fallback)
   double* part;     // K * units-per-column
   int32_t* cnt;     // K column-completion counters
+  // dense phase B -> E: each CTA's kept nonzeros of x_next and the v-fix entries of its
+  // dropped atoms, in position order at the CTA's slice offset, counts per CTA
+  double* nzv;
+  int32_t* nzj;
+  double* fxv;
+  int32_t* fxj;
+  int32_t* lcnt;    // [grid] apply counts, [grid] fix counts
+  int32_t list_apply;  // 1: dense u = A x from the lists in phase E (FL1_LIST_APPLY)
   double* pv;       // K
   double* pw;       // K
   double* PU;       // ld: power-iteration A v (combined)
