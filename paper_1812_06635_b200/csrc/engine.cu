@@ -1301,24 +1301,47 @@ __device__ __forceinline__ void list_rows(const double* __restrict__ A, int64_t 
   }
 }
 
+// Loads of combine_u_lists that depend on nothing decided in phase E (the list
+// lengths, the first row block's u_old / v / y), issued at the start of the phase so
+// they overlap its slot reduction.
+struct ListPre {
+  int32_t c[2];
+  double u, v, y;
+};
+__device__ __forceinline__ ListPre lists_issue(const EngineParams& p, bool shift, bool mom) {
+  ListPre lp{{0, 0}, 0.0, 0.0, 0.0};
+  const int G = vsize();
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    const int t = threadIdx.x + q * kThreads;
+    if (t < 2 * G) lp.c[q] = __ldcg(p.lcnt + t);
+  }
+  int64_t ilo, ihi;
+  slice(p.ld, ilo, ihi);
+  if (threadIdx.x < kLRB && ilo + threadIdx.x < ihi) {
+    const int64_t i = ilo + threadIdx.x;
+    lp.y = p.y[i];
+    if (shift) lp.u = __ldcg(p.U + i);
+    else if (mom) lp.v = __ldcg(p.V + i);
+  }
+  return lp;
+}
+
 __device__ __noinline__ void combine_u_lists(const EngineParams& p, Sh& sh, const DevLevel& lv, int64_t S, bool shift,
-                                             bool fix, double m, double* scratch) {
+                                             bool fix, double m, double* scratch, const ListPre& lp) {
   const int G = vsize();
   const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
   int64_t ilo, ihi;
   slice(p.ld, ilo, ihi);
   const bool mom = m != 0.0;
-  // the first block's per-row operands, loaded while the list lengths are scanned
-  double pre_u = 0.0, pre_v = 0.0, pre_y = 0.0;
-  if (threadIdx.x < kLRB && ilo + threadIdx.x < ihi) {
-    const int64_t i = ilo + threadIdx.x;
-    pre_y = p.y[i];
-    if (shift) pre_u = __ldcg(p.U + i);
-    else if (mom) pre_v = __ldcg(p.V + i);
-  }
+  const double pre_u = lp.u, pre_v = lp.v, pre_y = lp.y;
   int32_t* pre = reinterpret_cast<int32_t*>(scratch);  // [2][G + 1] exclusive prefix of the list lengths
   double* wpart = scratch + (G + 2);                    // [2][kWarps][kLRB]
-  for (int t = threadIdx.x; t < 2 * G; t += kThreads) pre[(t / G) * (G + 1) + 1 + t % G] = __ldcg(p.lcnt + t);
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    const int t = threadIdx.x + q * kThreads;
+    if (t < 2 * G) pre[(t / G) * (G + 1) + 1 + t % G] = lp.c[q];
+  }
   if (threadIdx.x < 2) pre[threadIdx.x * (G + 1)] = 0;
   __syncthreads();
   if (w < 2) {  // warp 0: apply lists, warp 1: fix lists
@@ -2031,6 +2054,18 @@ __device__ __noinline__ void engine_body(const EngineParams& p, Sh& sh, double* 
     }
 
     // ---------------------------------------------------------- phase E
+    const bool shift_u = fista;  // combine: v <- u_old - fix (FISTA history)
+    const double tk_next = fista ? (s.momentum_ready ? sh.t_next : s.t_k) : s.t_k;
+    const double m_next = next_momentum(p, tk_next, fista);
+    ListPre lp{};
+    double xo_pre = 0.0, xn_pre = 0.0;  // this thread's first slice position (x_prev <- x, x <- x_next)
+    if (lists) {
+      lp = lists_issue(p, shift_u, m_next != 0.0);
+      if (lo + threadIdx.x < hi) {
+        xo_pre = bk.x[lo + threadIdx.x];
+        xn_pre = p.xnew[lo + threadIdx.x];
+      }
+    }
     grid_reduce(p, sh, (1u << kSlKept) | (1u << kSlLook) | (1u << kSlNnz), 0u);
     if (threadIdx.x == 0) {
       sh.S_new = stop_now ? S : static_cast<int64_t>(sh.res[kSlKept]);
@@ -2152,15 +2187,16 @@ __device__ __noinline__ void engine_body(const EngineParams& p, Sh& sh, double* 
       if (threadIdx.x == 0) put_slot(p, kSlMaxEps, v[0]);
     } else {  // same positions: x_prev = x, x = x_next on this CTA's slice
       for (int64_t q = lo + threadIdx.x; q < hi; q += kThreads) {
-        if (fista) bk.xp[q] = bk.x[q];
-        bk.x[q] = p.xnew[q];
+        const bool first = lists && q == lo + threadIdx.x;
+        const double xo = first ? xo_pre : bk.x[q];
+        if (fista) bk.xp[q] = xo;
+        bk.x[q] = first ? xn_pre : p.xnew[q];
       }
     }
     {  // combine u (and v <- u_old - fix), then the next iteration's rho_g
-      const double tk_next = fista ? (s.momentum_ready ? sh.t_next : s.t_k) : s.t_k;
       if (gram) combine_g(p, C_apply, fista, fix_pass);
-      else if (lists) combine_u_lists(p, sh, lv, S, fista, fix_pass, next_momentum(p, tk_next, fista), sc.red);
-      else combine_u(p, sh, C_apply, fista, fix_pass, next_momentum(p, tk_next, fista));
+      else if (lists) combine_u_lists(p, sh, lv, S, shift_u, fix_pass, m_next, sc.red, lp);
+      else combine_u(p, sh, C_apply, shift_u, fix_pass, m_next);
     }
     if (threadIdx.x == 0) {
       if (fista) {  // 581-590
