@@ -1383,7 +1383,9 @@ void solve_single(fl1_seq* s, const double* y, bool y_device, double lambda, con
     int64_t limit = kSingleClusterBytes;
     if (const char* mb = std::getenv("FL1_SINGLE_CLUSTER_MB")) limit = std::atoll(mb) << 20;
     if (!(e && e[0] == '0') && bytes <= limit) {
-      solve_clusters(s, y, y_device, s->lv.back()->dict->n, &lambda, 1, cfg, opts, kSingleClusterSize, out, false);
+      int csize = kSingleClusterSize;
+      if (const char* cs = std::getenv("FL1_SINGLE_CLUSTER_SIZE")) csize = std::atoi(cs);
+      solve_clusters(s, y, y_device, s->lv.back()->dict->n, &lambda, 1, cfg, opts, csize, out, false);
       return;
     }
   }
