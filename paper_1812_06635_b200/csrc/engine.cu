@@ -1066,6 +1066,106 @@ struct Scratch {
   double* red;     // kWarps * kUnit doubles: apply warp partials (aliases rt)
 };
 
+// Cluster mode, dense level, this CTA's preserved columns fit in shared memory: the
+// whole restricted power iteration runs on chip. Each CTA keeps its slice's columns
+// resident, writes its apply partial to shared memory, and every CTA reads all of
+// them through distributed shared memory (and the step statistics likewise): two
+// cluster barriers per step and no global-memory round trip. Same fixed-order sums
+// on every CTA, so the estimate and the leading vector are identical everywhere.
+__device__ __forceinline__ bool power_onchip_fits(const EngineParams& p, const DevLevel& lv, int64_t S) {
+  if (!s_vcluster || vsize() > 16 || lv.kind != kDense || lv.rows != 0) return false;
+  const int64_t nc = (S + vsize() - 1) / vsize();
+  return nc * p.ld + p.ld + 4 + 2 * nc <= p.scratch_len;
+}
+
+__device__ __noinline__ double power_iteration_onchip(const EngineParams& p, Sh& sh, const DevLevel& lv, const Bank& bk,
+                                                      int64_t S, const double* cur_src, double cur_div, int max_iter,
+                                                      double rel_tol, int min_iter, const Scratch& sc) {
+  cg::cluster_group cl = cg::this_cluster();
+  const int G = vsize();
+  const int64_t ld = p.ld;
+  int64_t lo, hi;
+  slice(S, lo, hi);
+  const int nc = static_cast<int>(hi - lo), ncmax = static_cast<int>((S + G - 1) / G);
+  double* cache = sc.red;                                 // [ncmax][ld] this CTA's columns
+  double* P = cache + static_cast<int64_t>(ncmax) * ld;   // [ld] apply partial (read by the cluster)
+  double* stats = P + ld;                                 // [4] step statistics (read by the cluster)
+  double* vloc = stats + 4;                               // [ncmax] v on this CTA's positions
+  double* zbuf = vloc + ncmax;                            // [ncmax] z on this CTA's positions
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  const int64_t n2 = ld >> 1;
+  for (int c = 0; c < nc; ++c) {
+    const double2* col = reinterpret_cast<const double2*>(lv.a + static_cast<int64_t>(bk.idx[lo + c]) * ld);
+    double2* dst = reinterpret_cast<double2*>(cache + static_cast<int64_t>(c) * ld);
+    for (int64_t e = threadIdx.x; e < n2; e += kThreads) dst[e] = ldg_stream2(col + e);
+  }
+  for (int c = threadIdx.x; c < nc; c += kThreads) vloc[c] = cur_src[lo + c] / cur_div;
+  __syncthreads();
+  double estimate = 0.0;
+  bool have_w = false;
+  for (int it = 0; it < max_iter; ++it) {
+    double tq0 = 0.0;
+    if (threadIdx.x == 0) {
+      sh.s.power_steps += 1;
+      sh.s.prof_power_bytes += 16.0 * static_cast<double>(p.n) * static_cast<double>(S);
+      tq0 = globaltimer_ns();
+    }
+    for (int64_t i = threadIdx.x; i < ld; i += kThreads) {  // apply: this CTA's partial of A v
+      double acc = 0.0;
+      for (int c = 0; c < nc; ++c) acc = fma(vloc[c], cache[static_cast<int64_t>(c) * ld + i], acc);
+      P[i] = acc;
+    }
+    cl.sync();
+    for (int64_t i = threadIdx.x; i < ld; i += kThreads) {  // w = sum of the partials, rank order
+      double acc = 0.0;
+      for (int r = 0; r < G; ++r) acc += cl.map_shared_rank(P, r)[i];
+      sc.vec[i] = acc;
+    }
+    __syncthreads();
+    for (int c = w; c < nc; c += kWarps) {  // adjoint on this CTA's columns
+      const double* col = cache + static_cast<int64_t>(c) * ld;
+      double sd = 0.0;
+      for (int64_t i = l; i < ld; i += 32) sd = fma(col[i], sc.vec[i], sd);
+      sd = warp_sum(sd);
+      if (l == 0) zbuf[c] = sd;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double s2 = 0.0, svw = 0.0;
+      for (int c = 0; c < nc; ++c) {
+        s2 = fma(zbuf[c], zbuf[c], s2);
+        svw = fma(vloc[c], zbuf[c], svw);
+      }
+      stats[0] = s2;
+      stats[1] = svw;
+    }
+    cl.sync();
+    double tot2 = 0.0, totvw = 0.0;
+    for (int r = 0; r < G; ++r) {
+      const double* st = cl.map_shared_rank(stats, r);
+      tot2 += st[0];
+      totvw += st[1];
+    }
+    if (threadIdx.x == 0) sh.s.prof_pw[2] += globaltimer_ns() - tq0;
+    const double nrm = sqrt(tot2);
+    if (nrm == 0.0) {
+      estimate = 0.0;
+      break;
+    }
+    const double prev = estimate;
+    estimate = totvw;
+    __syncthreads();  // every thread has read vloc (statistics) before it changes
+    for (int c = threadIdx.x; c < nc; c += kThreads) vloc[c] = zbuf[c] / nrm;
+    have_w = true;
+    __syncthreads();
+    if (it > min_iter && fabs(estimate - prev) <= rel_tol * estimate) break;
+  }
+  (void)have_w;  // vloc is v after the last update either way (fastl1 lead_vector)
+  for (int c = threadIdx.x; c < nc; c += kThreads) bk.lead[lo + c] = vloc[c];
+  cl.sync();  // no CTA reuses its scratch while another may still read its partial / statistics
+  return estimate;
+}
+
 __device__ __noinline__ double power_iteration(const EngineParams& p, Sh& sh, const DevLevel& lv, const Bank& bk, int64_t S,
                                   bool try_warm, const Scratch& sc) {
   int64_t lo, hi;
@@ -1093,6 +1193,8 @@ __device__ __noinline__ double power_iteration(const EngineParams& p, Sh& sh, co
   const int max_iter = warm ? 12 : 200;
   const double rel_tol = warm ? 1e-5 : 1e-9;
   const int min_iter = warm ? 2 : 4;
+  if (p.power_onchip && power_onchip_fits(p, lv, S))
+    return power_iteration_onchip(p, sh, lv, bk, S, cur_src, cur_div, max_iter, rel_tol, min_iter, sc);
   bool have_w = false;  // pw holds the last w (v = pw / cur_div)
   for (int it = 0; it < max_iter; ++it) {
     if (threadIdx.x == 0) {
