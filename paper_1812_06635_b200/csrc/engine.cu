@@ -137,6 +137,10 @@ __device__ __forceinline__ void bulk_wait(uint64_t* bar, uint32_t parity) {
         : "memory");
   }
 }
+// Per-CTA column results of a dense adjoint pass (merge + statistics stay on chip
+// when the CTA's slice has at most kColBuf columns).
+constexpr int kColBuf = 1024;
+__shared__ double s_colsum[kColBuf];
 __device__ __forceinline__ int vsize() { return s_vsize; }
 __device__ __forceinline__ int vrank() { return s_vrank; }
 __device__ __forceinline__ void vsync() {
@@ -417,6 +421,8 @@ __device__ __noinline__ void dense_adjoint(const EngineParams& p, Sh& sh, const 
   const double2* __restrict__ A2 = reinterpret_cast<const double2*>(lv.a) + l;
   const double2* __restrict__ r2 = reinterpret_cast<const double2*>(r) + l;
   double* __restrict__ out = po.out;
+  const bool on_chip = c1 - c0 <= kColBuf;
+  double* __restrict__ dst = on_chip ? s_colsum : out + c0;  // column results, relative to c0
   PassAcc acc;
   int nf = 0;
   // Units are visited in order; three register buffers form a ring so two
@@ -489,7 +495,7 @@ __device__ __noinline__ void dense_adjoint(const EngineParams& p, Sh& sh, const 
       const bool whole_ = col_end_ && began_here;                                                     \
       if (l == 0) {                                                                                   \
         if (whole_) {                                                                                 \
-          out[c0 + cc] = t_;                                                                          \
+          dst[cc] = t_;                                                                               \
         } else {                                                                                      \
           sh.frag[w][nf].pos = c0 + cc;                                                               \
           sh.frag[w][nf].sum = t_;                                                                    \
@@ -580,27 +586,41 @@ __device__ __noinline__ void dense_adjoint(const EngineParams& p, Sh& sh, const 
 #undef FL1_RV
   if (l == 0) sh.nfrag[w] = nf;
   __syncthreads();
-  // merge columns split between warps, in warp (= unit) order
-  if (threadIdx.x == 0) {
-    int64_t cp = -1;
-    double cs = 0.0;
-    for (int ww = 0; ww < kWarps; ++ww)
-      for (int f = 0; f < sh.nfrag[ww]; ++f) {
-        const Frag fr = sh.frag[ww][f];
-        if (fr.pos != cp) {
-          if (cp >= 0) out[cp] = cs;
-          cp = fr.pos;
-          cs = fr.sum;
-        } else {
-          cs += fr.sum;
+  // merge columns split between warps, in warp (= unit) order: the fragments, in
+  // (warp, slot) order, are sorted by column; the first fragment of each column sums
+  // its run left to right (the order of a serial merge), one thread per fragment
+  if (threadIdx.x < 2 * kWarps) {
+    const int ww = threadIdx.x >> 1, f = threadIdx.x & 1;
+    if (f < sh.nfrag[ww]) {
+      const Frag fr = sh.frag[ww][f];
+      bool head = true;
+      for (int k = 2 * ww + f - 1; k >= 0; --k)
+        if ((k & 1) < sh.nfrag[k >> 1]) {
+          head = sh.frag[k >> 1][k & 1].pos != fr.pos;
+          break;
         }
+      if (head) {
+        double cs = fr.sum;
+        for (int k = 2 * ww + f + 1; k < 2 * kWarps; ++k) {
+          if ((k & 1) >= sh.nfrag[k >> 1]) continue;
+          const Frag nx = sh.frag[k >> 1][k & 1];
+          if (nx.pos != fr.pos) break;
+          cs += nx.sum;
+        }
+        dst[fr.pos - c0] = cs;
       }
-    if (cp >= 0) out[cp] = cs;
+    }
   }
   __syncthreads();
   // per-CTA statistics over this CTA's columns (fixed thread -> position map); a
   // separate short pass is cheaper than statistics inside the streaming loop
-  if (po.track || po.vdot) {
+  if (on_chip) {
+    for (int64_t pos = c0 + threadIdx.x; pos < c1; pos += kThreads) {
+      const double v = s_colsum[pos - c0];
+      out[pos] = v;
+      if (po.track || po.vdot) acc.add(p, po, eps, pos, v);
+    }
+  } else if (po.track || po.vdot) {
     for (int64_t pos = c0 + threadIdx.x; pos < c1; pos += kThreads) acc.add(p, po, eps, pos, out[pos]);
   }
   finish_pass(p, sh, po, acc);
