@@ -1238,6 +1238,8 @@ void solve_clusters(fl1_seq* s, const double* Y, bool y_device, int64_t ldy, con
     // short, small-set tail (measured best on B200; 0 and 1 are the other policies)
     pp.policy = 2;
     if (const char* pol = std::getenv("FL1_LOCKSTEP_POLICY")) pp.policy = std::atoi(pol);
+    const char* smode = std::getenv("FL1_SPLIT_MODE");
+    pp.split_mode = smode ? std::atoi(smode) : 1;
     pp.X3[0] = reinterpret_cast<double*>(pb + q_x0);
     pp.X3[1] = reinterpret_cast<double*>(pb + q_x1);
     pp.X3[2] = reinterpret_cast<double*>(pb + q_x2);

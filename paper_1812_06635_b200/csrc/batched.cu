@@ -215,9 +215,23 @@ __device__ __noinline__ void gemm_tile(const PrefixParams& p, int rt, int ct, in
   }
 }
 
-// split-K factor for T output tiles on G CTAs: split only while the tiles alone
-// leave more than a third of the CTAs idle (partials cost a write + read each)
-__device__ __forceinline__ int split_for(int T, int G) {
+// split-K factor for T output tiles of nch K-chunks on G CTAs: the fewest-waves choice,
+// cost ceil(T s / G) / s (tile waves in units of a whole tile) plus ~2% per extra part
+// (partial write + read, per-item prologue), each part at least 4 chunks deep
+__device__ __forceinline__ int split_for(int T, int G, int nch) {
+  int best = 1;
+  float best_cost = static_cast<float>((T + G - 1) / G) * 1.02f;
+  for (int s = 2; s <= kSplitMax && nch / s >= 4; ++s) {
+    const float cost = static_cast<float>((T * s + G - 1) / G) / static_cast<float>(s) * (1.0f + 0.02f * s);
+    if (cost < best_cost) {
+      best = s;
+      best_cost = cost;
+    }
+  }
+  return best;
+}
+
+__device__ __forceinline__ int split_old(int T, int G) {
   int s = 1;
   while (s < kSplitMax && 3 * T * s < 2 * G) s *= 2;
   return s;
@@ -611,6 +625,33 @@ __device__ void enter_power(const PrefixParams& p, PSh& sh, int64_t b) {
   __syncthreads();
 }
 
+// corr of this lane's atoms (wr.lo + l + 32 i) summed over the split-K parts in part
+// order, two parts' loads in flight together
+__device__ __forceinline__ void sum_parts(const double* __restrict__ cr, int64_t part, int sk, const WarpRange& wr,
+                                          double (&cv)[kIt]) {
+  const int l = threadIdx.x & 31;
+#pragma unroll
+  for (int i = 0; i < kIt; ++i) {
+    const int64_t j = wr.lo + l + 32 * i;
+    cv[i] = j < wr.hi ? __ldcg(cr + j) : 0.0;
+  }
+  for (int kp0 = 1; kp0 < sk; kp0 += 2) {
+    double pv[2][kIt];
+#pragma unroll
+    for (int q = 0; q < 2; ++q)
+#pragma unroll
+      for (int i = 0; i < kIt; ++i) {
+        const int64_t j = wr.lo + l + 32 * i;
+        pv[q][i] = (kp0 + q < sk && j < wr.hi) ? __ldcg(cr + (kp0 + q) * part + j) : 0.0;
+      }
+#pragma unroll
+    for (int q = 0; q < 2; ++q)
+      if (kp0 + q < sk)
+#pragma unroll
+        for (int i = 0; i < kIt; ++i) cv[i] += pv[q][i];
+  }
+}
+
 // One power step's update after v_new = A_S^T A_S v (slot a's corr column parts).
 __device__ __noinline__ void power_step(const PrefixParams& p, PSh& sh, int64_t a, int64_t b, int sk, double t0) {
   PrefixSig& sg = p.sig[b];
@@ -622,13 +663,17 @@ __device__ __noinline__ void power_step(const PrefixParams& p, PSh& sh, int64_t 
   const WarpRange wr(K);
   const int l = threadIdx.x & 31;
   double v[3] = {0.0, 0.0, 0.0};  // |v_new|^2, v.v_new
-  for (int64_t j = wr.lo + l; j < wr.hi; j += 32) {
-    if (!mk[j]) continue;
-    double c = __ldcg(cr + j);
-    for (int kp = 1; kp < sk; ++kp) c += __ldcg(cr + kp * part + j);
-    src[j] = c;  // v_new (unnormalised) = the next cur_src
-    v[0] = fma(c, c, v[0]);
-    v[1] = fma(vp[j], c, v[1]);
+  double cv[kIt];
+  sum_parts(cr, part, sk, wr, cv);
+#pragma unroll
+  for (int i = 0; i < kIt; ++i) {
+    const int64_t j = wr.lo + l + 32 * i;
+    if (j < wr.hi && mk[j]) {
+      const double c = cv[i];
+      src[j] = c;  // v_new (unnormalised) = the next cur_src
+      v[0] = fma(c, c, v[0]);
+      v[1] = fma(vp[j], c, v[1]);
+    }
   }
   block_sum3(v, sh);
   if (threadIdx.x == 0) {
@@ -697,21 +742,7 @@ __device__ __noinline__ void fista_step(const PrefixParams& p, PSh& sh, int64_t 
   double dp = 0.0;
   {
     double cv[kIt];
-#pragma unroll
-    for (int i = 0; i < kIt; ++i) {
-      const int64_t j = wr.lo + l + 32 * i;
-      cv[i] = j < wr.hi ? __ldcg(cr + j) : 0.0;
-    }
-    for (int kp = 1; kp < sk; ++kp) {
-      double pv[kIt];
-#pragma unroll
-      for (int i = 0; i < kIt; ++i) {
-        const int64_t j = wr.lo + l + 32 * i;
-        pv[i] = j < wr.hi ? __ldcg(cr + kp * part + j) : 0.0;
-      }
-#pragma unroll
-      for (int i = 0; i < kIt; ++i) cv[i] += pv[i];
-    }
+    sum_parts(cr, part, sk, wr, cv);
 #pragma unroll
     for (int i = 0; i < kIt; ++i) {
       const int64_t j = wr.lo + l + 32 * i;
@@ -993,7 +1024,8 @@ __global__ void __launch_bounds__(kPT, 1) prefix_kernel(const __grid_constant__ 
     if (n_pow > 0) {
       const int n_rt = static_cast<int>((ld + kTM - 1) / kTM);
       const int n_ct = (n_pow + kTN - 1) / kTN;
-      const int sk = split_for(n_rt * n_ct, gridDim.x);
+      const int sk = p.split_mode ? split_for(n_rt * n_ct, gridDim.x, static_cast<int>((K + kTK - 1) / kTK))
+                                  : split_old(n_rt * n_ct, gridDim.x);
       for (int item = blockIdx.x; item < n_rt * n_ct * sk; item += gridDim.x) {
         const int tile = item % (n_rt * n_ct), kp = item / (n_rt * n_ct);
         gemm_n_tile(p, tile % n_rt, tile / n_rt, kp, sk, n_pow, pact, act, stage);
@@ -1012,7 +1044,8 @@ __global__ void __launch_bounds__(kPT, 1) prefix_kernel(const __grid_constant__ 
     // ---- Corr = A^T [rho | w] for every unfinished signal (fp64 tensor cores)
     const int n_rt = static_cast<int>((K + kTM - 1) / kTM);
     const int n_ct = (n_act + kTN - 1) / kTN;
-    const int sk = split_for(n_rt * n_ct, gridDim.x);
+    const int sk = p.split_mode ? split_for(n_rt * n_ct, gridDim.x, static_cast<int>((ld + kTK - 1) / kTK))
+                                : split_old(n_rt * n_ct, gridDim.x);
     for (int item = blockIdx.x; item < n_rt * n_ct * sk; item += gridDim.x) {
       const int tile = item % (n_rt * n_ct), kp = item / (n_rt * n_ct);
       gemm_tile(p, tile % n_rt, tile / n_rt, kp, sk, n_act, act, stage);

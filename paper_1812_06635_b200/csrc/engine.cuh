@@ -187,6 +187,7 @@ struct PrefixParams {
   uint64_t max_it;
   int32_t interval, solver, variant, collect_trace;
   int32_t policy;             // hand-off: 0 never, 1 at the first shrink, 2 after the first power iteration
+  int32_t split_mode;         // split-K choice of the contractions: 1 fewest waves, 0 fill-only (FL1_SPLIT_MODE)
   double* X3[3];              // three k x B iterate buffers (roles rotate, PrefixSig::rot)
   double* U2[2];              // two ld x B buffers for u and v (PrefixSig::uswap)
   int8_t* mask;               // k x B preserved-set masks
