@@ -63,8 +63,8 @@ if __name__ == "__main__":
     if "--timeline" in sys.argv:  # instrumented build: per-CTA phase timeline (FL1_TIMELINE_OUT=path)
         print(build(force=True, defines={"FL1_TIMELINE": 1}, out=PKG / "_build" / "libfl1cuda_timeline.so"))
     elif "--variants" in sys.argv:  # tuning sweep: libfl1cuda_t{threads}_u{unit}.so
-        for t, u, rg, v4 in ((256, 512, 2, 0), (256, 512, 2, 1), (256, 1024, 2, 1), (256, 512, 3, 1)):
-            print(build(force=True, defines={"FL1_THREADS": t, "FL1_UNIT": u, "FL1_RING": rg, "FL1_V4": v4},
-                        out=PKG / "_build" / f"libfl1cuda_t{t}_u{u}_r{rg}_v{v4}.so"))
+        for t, u, rg in ((256, 512, 2), (256, 1024, 2), (256, 512, 3)):
+            print(build(force=True, defines={"FL1_THREADS": t, "FL1_UNIT": u, "FL1_RING": rg},
+                        out=PKG / "_build" / f"libfl1cuda_t{t}_u{u}_r{rg}.so"))
     else:
         print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))

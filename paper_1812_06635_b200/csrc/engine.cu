@@ -248,15 +248,6 @@ __device__ __forceinline__ double2 ldg_stream2(const double2* ptr) {
   return r;
 }
 
-#if FL1_V4
-// 256-bit streaming load (sm_100: LDG.E.NA.ENL2.256); p must be 32-byte aligned.
-__device__ __forceinline__ void ldg_stream4(const double* ptr, double2& lo, double2& hi) {
-  asm volatile("ld.global.nc.L1::no_allocate.v4.f64 {%0, %1, %2, %3}, [%4];"
-               : "=d"(lo.x), "=d"(lo.y), "=d"(hi.x), "=d"(hi.y)
-               : "l"(ptr));
-}
-#endif
-
 // CTA slice [lo, hi) of n items (balanced, contiguous).
 __device__ __forceinline__ void slice(int64_t n, int64_t& lo, int64_t& hi) {
   lo = n * vrank() / vsize();
@@ -409,8 +400,6 @@ __device__ __noinline__ void dense_adjoint(const EngineParams& p, Sh& sh, const 
   const int64_t n = p.n;
   const int U = static_cast<int>((n + kUnit - 1) / kUnit);
   const int last_nd2 = static_cast<int>(((n - static_cast<int64_t>(U - 1) * kUnit) + 1) >> 1);
-  const int last_nd = static_cast<int>(n - static_cast<int64_t>(U - 1) * kUnit);
-  (void)last_nd;
   const int64_t ld2 = p.ld >> 1;
   int64_t c0, c1;
   slice(S, c0, c1);
@@ -436,30 +425,6 @@ __device__ __noinline__ void dense_adjoint(const EngineParams& p, Sh& sh, const 
   int cc = ic, ch = ih;
   const double2* colp = nullptr;
   int colp_c = -1;
-#if FL1_V4
-  // 256-bit loads: lane l owns doubles [4(l + 32 q), 4(l + 32 q) + 4) of the unit
-#define FL1_ISSUE(B)                                                                                  \
-  do {                                                                                                \
-    if (ic != colp_c) {                                                                               \
-      colp = A2 + static_cast<int64_t>(__ldg(idx + c0 + ic)) * ld2;                                   \
-      colp_c = ic;                                                                                    \
-    }                                                                                                 \
-    const double* src_ = reinterpret_cast<const double*>(colp - l) + ih * kUnit + 4 * l;              \
-    const int lim_ = (ih == U - 1 ? last_nd : kUnit) - 4 * l;                                         \
-    _Pragma("unroll") for (int q = 0; q < kV / 2; ++q) {                                              \
-      if (128 * q < lim_) {                                                                           \
-        ldg_stream4(src_ + 128 * q, B[2 * q], B[2 * q + 1]);                                          \
-      } else {                                                                                        \
-        B[2 * q] = make_double2(0.0, 0.0);                                                            \
-        B[2 * q + 1] = make_double2(0.0, 0.0);                                                        \
-      }                                                                                               \
-    }                                                                                                 \
-    if (++ih == U) {                                                                                  \
-      ih = 0;                                                                                         \
-      ++ic;                                                                                           \
-    }                                                                                                 \
-  } while (0)
-#else
 #define FL1_ISSUE(B)                                                                                  \
   do {                                                                                                \
     if (ic != colp_c) {                                                                               \
@@ -475,15 +440,10 @@ __device__ __noinline__ void dense_adjoint(const EngineParams& p, Sh& sh, const 
       ++ic;                                                                                           \
     }                                                                                                 \
   } while (0)
-#endif
-#if FL1_V4
-#define FL1_RV(q) rr_[(q & 1) + 64 * (q >> 1) + 2 * l]  /* double2 index of element pair q */
-#else
 #define FL1_RV(q) rr_[32 * q]
-#endif
 #define FL1_CONSUME(B, U_)                                                                            \
   do {                                                                                                \
-    const double2* rr_ = r2 + ch * (kUnit / 2) - (FL1_V4 ? l : 0);                                    \
+    const double2* rr_ = r2 + ch * (kUnit / 2);                                                       \
     _Pragma("unroll") for (int q = 0; q < kV; ++q) {                                                  \
       const double2 rv_ = FL1_RV(q);                                                                  \
       s = fma(B[q].x, rv_.x, s);                                                                      \

@@ -18,9 +18,6 @@ constexpr int kMaxLevels = 8;
 #ifndef FL1_RING
 #define FL1_RING 2  // register ring depth of the streaming passes (2: no spills at 255 regs)
 #endif
-#ifndef FL1_V4
-#define FL1_V4 0  // 256-bit loads in the A^T r pass (needs ld % 4 == 0)
-#endif
 #ifndef FL1_UNIT
 #define FL1_UNIT 512
 #endif
