@@ -356,6 +356,8 @@ size_t carve(EngineParams& p, char* base, int64_t n, int64_t k, int64_t ld, int 
     p.list_apply = e ? std::atoi(e) : 1;
     const char* o = std::getenv("FL1_POWER_ONCHIP");
     p.power_onchip = o ? std::atoi(o) : 1;
+    const char* ep = std::getenv("FL1_EARLY_PROX");
+    p.early_prox = ep ? std::atoi(ep) : 1;
   }
   p.pv = c.take<double>(kk);
   p.pw = c.take<double>(kk);

@@ -94,6 +94,7 @@ constexpr int kSlGwa = 17;   // Gram mode: w . A^T y   (w = extrapolated x)
 constexpr int kSlGwg = 18;   //            w . G w
 constexpr int kSlGxa = 19;   //            x . A^T y
 constexpr int kSlGxg = 20;   //            x . G x
+constexpr int kSlNnzX = 21;  // early prox: nnz of the current x (the ledger row if the iteration stops)
 
 // Virtual grid: the engine runs either on the whole GPU (one cooperative launch,
 // grid-wide barrier) or inside one thread-block cluster per solve (batched mode,
@@ -157,7 +158,7 @@ struct Frag {
 
 struct Sh {
   EngineState s;
-  double red[kWarps * 4];
+  double red[kWarps * 8];
   double res[kBred];
   // per-iteration scalars (identical in every CTA)
   double t_next;
@@ -1498,6 +1499,102 @@ __device__ __noinline__ void combine_u_lists(const EngineParams& p, Sh& sh, cons
   }
 }
 
+// ||x||_1 partial of this CTA's slice into the slot of iteration t
+__device__ __forceinline__ int l1_slot(uint64_t t) { return (t & 1) ? kSlL1b : kSlL1; }
+
+// Per-atom sphere test + prox on the CTA slice [lo, hi) (results to xnew / keep), the
+// CTA's ordered apply / v-fix lists, and its kept / look / nnz / ||x_next||_1 slots.
+// `early`: called before the first barrier of a non-screening dense iteration, where
+// the stop decision is not known yet; the nnz of the current x (the ledger row of a
+// stopping iteration) goes to kSlNnzX.
+__device__ __forceinline__ void slice_prox(const EngineParams& p, Sh& sh, const Bank& bk, const ProxCtx& px, int64_t lo,
+                                        int64_t hi, bool stop_now, bool fix_pass, bool lists,
+                                        const ProxCtx::Atom* pre, bool early, uint64_t t) {
+  double kept = 0.0, look = 0.0, nnz = 0.0, l1n = 0.0, nnzx = 0.0;
+  int32_t na = 0, nf = 0;  // list lengths (lists only)
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  for (int64_t q0 = lo; q0 < hi; q0 += kThreads) {  // uniform trip count (list appends)
+    const int64_t q = q0 + threadIdx.x;
+    bool fa = false, ff = false;
+    double va = 0.0, vf = 0.0;
+    if (q < hi) {
+      ProxCtx::Atom a;
+      if (pre && q == lo + threadIdx.x) {
+        a = *pre;
+        if (px.m == 0.0) a.xpv = 0.0;
+      } else {
+        a = px.load(q);
+      }
+      if (early) nnzx += a.xo != 0.0 ? 1.0 : 0.0;
+      if (stop_now) {
+        nnz += a.xo != 0.0 ? 1.0 : 0.0;
+      } else {
+        const double d = px.screen_now ? px.dot(a) : 0.0;
+        const bool kp = px.keep(a, d);
+        look += px.look(a, d, kp) ? 1.0 : 0.0;
+        const double xn = px.xnew(a);
+        p.xnew[q] = xn;
+        bk.keep[q] = static_cast<int8_t>(kp);
+        if (kp) {
+          kept += 1.0;
+          nnz += xn != 0.0 ? 1.0 : 0.0;
+          l1n += fabs(xn);  // ||x_{t+1}||_1 over the preserved set (next iteration's 473)
+        }
+        fa = kp && xn != 0.0;
+        ff = fix_pass && !kp && a.xo != 0.0;
+        va = xn;
+        vf = a.xo;
+      }
+    }
+    if (lists) {  // ordered appends (position order) at this CTA's slice offset
+      const int32_t col = (fa || ff) ? bk.idx[q] : 0;
+      const unsigned ba = __ballot_sync(kFull, fa), bf = __ballot_sync(kFull, ff);
+      if (l == 0) {
+        sh.wcount[0][w] = __popc(ba);
+        sh.wcount[1][w] = __popc(bf);
+      }
+      __syncthreads();
+      int oa = na, of = nf, ta = 0, tf = 0;
+      for (int ww = 0; ww < kWarps; ++ww) {
+        if (ww < w) {
+          oa += sh.wcount[0][ww];
+          of += sh.wcount[1][ww];
+        }
+        ta += sh.wcount[0][ww];
+        tf += sh.wcount[1][ww];
+      }
+      const unsigned below = (1u << l) - 1u;
+      if (fa) {
+        const int64_t at = lo + oa + __popc(ba & below);
+        p.nzj[at] = col;
+        p.nzv[at] = va;
+      }
+      if (ff) {
+        const int64_t at = lo + of + __popc(bf & below);
+        p.fxj[at] = col;
+        p.fxv[at] = vf;
+      }
+      na += ta;
+      nf += tf;
+      __syncthreads();  // wcount is reused by the next round
+    }
+  }
+  if (lists && threadIdx.x == 0) {
+    p.lcnt[vrank()] = na;
+    p.lcnt[vsize() + vrank()] = nf;
+  }
+  double v[5] = {kept, look, nnz, l1n, nnzx};
+  const bool mx[5] = {false, false, false, false, false};
+  block_reduce<5>(v, mx, sh);
+  if (threadIdx.x == 0) {
+    put_slot(p, kSlKept, v[0]);
+    put_slot(p, kSlLook, v[1]);
+    put_slot(p, kSlNnz, v[2]);
+    if (!stop_now) put_slot(p, l1_slot(t + 1), v[3]);
+    if (early) put_slot(p, kSlNnzX, v[4]);
+  }
+}
+
 // momentum of the next iteration from the FISTA state (fastl1.cpp:465-470)
 __device__ __forceinline__ double next_momentum(const EngineParams& p, double t_k, bool ready) {
   if (p.solver != FL1_FISTA || !ready) return 0.0;
@@ -1505,8 +1602,6 @@ __device__ __forceinline__ double next_momentum(const EngineParams& p, double t_
   return (t_k - 1.0) / t_next;
 }
 
-// ||x||_1 partial of this CTA's slice into the slot of iteration t
-__device__ __forceinline__ int l1_slot(uint64_t t) { return (t & 1) ? kSlL1b : kSlL1; }
 
 // Gram-mode compute_products (fastl1.cpp:373-393) on this CTA's slice: corr_j =
 // aty_j - gw_j with gw = (1+m) gx - m gv, the y-ray correlations aty_j, both pairs of
@@ -1875,6 +1970,24 @@ __device__ __noinline__ void engine_body(const EngineParams& p, Sh& sh, double* 
         op_adjoint(p, sh, lv, bk.idx, bk.eps, S, sc.vec, sc.rt, po);
       }
     }
+    // Non-screening dense iterations: the prox and the apply lists need only this CTA's
+    // corr, so they run before the barrier, and the phase-B and phase-E reductions
+    // become one (the stop decision, unknown here, only selects the ledger's nnz).
+    const bool early = p.early_prox && !gram && !exact_fit && lv.kind == kDense && p.list_apply && !p.observe &&
+                       (ld + vsize() - 1) / vsize() <= kLRB &&
+                       (p.variant == FL1_PLAIN || s.t % static_cast<uint64_t>(p.interval) != 0);
+    if (early) {
+      ProxCtx px{};
+      px.corr = p.corr;
+      px.x = bk.x;
+      px.xp = bk.xp;
+      px.m = momentum;
+      px.inv_l = s.inv_l;
+      px.thresh = lambda * s.inv_l;
+      px.lambda = lambda;
+      px.rule_gap = p.rule == FL1_RULE_GAP;
+      slice_prox(p, sh, bk, px, lo, hi, false, false, true, nullptr, true, s.t);
+    }
     FL1_MARK(1);
     vsync();  // ------------------------------------------------ sync 1
     FL1_MARK(2);
@@ -1909,13 +2022,14 @@ __device__ __noinline__ void engine_body(const EngineParams& p, Sh& sh, double* 
       }
       __syncthreads();
     } else {
-      grid_reduce(p, sh, 1u << l1s,
+      grid_reduce(p, sh,
+                  (1u << l1s) | (early ? (1u << kSlKept) | (1u << kSlLook) | (1u << kSlNnz) | (1u << kSlNnzX) : 0u),
                   exact_fit ? ((1u << kSlMaxPlainY) | (1u << kSlMaxStableY))
                             : ((1u << kSlMaxPlain) | (1u << kSlMaxStable)));
     }
     // prefetch this thread's first atom (overlaps the scalar block below)
     ProxCtx::Atom pre{};
-    {
+    if (!early) {
       const int64_t q = lo + threadIdx.x;
       if (q < hi) {
         pre.c = p.corr[q];
@@ -2027,89 +2141,7 @@ __device__ __noinline__ void engine_body(const EngineParams& p, Sh& sh, double* 
     // phase E forms u (and the fix) by row slices straight from the lists
     const bool lists = p.list_apply && lv.kind == kDense && !gram && !stop_now &&
                        (ld + vsize() - 1) / vsize() <= kLRB;  // one row block per CTA
-    {  // per-atom sphere test + prox on this CTA's slice (results to xnew / keep)
-      double kept = 0.0, look = 0.0, nnz = 0.0, l1n = 0.0;
-      int32_t na = 0, nf = 0;  // list lengths (lists only)
-      const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-      for (int64_t q0 = lo; q0 < hi; q0 += kThreads) {  // uniform trip count (list appends)
-        const int64_t q = q0 + threadIdx.x;
-        bool fa = false, ff = false;
-        double va = 0.0, vf = 0.0;
-        if (q < hi) {
-          ProxCtx::Atom a;
-          if (q == lo + threadIdx.x) {
-            a = pre;
-            if (px.m == 0.0) a.xpv = 0.0;
-          } else {
-            a = px.load(q);
-          }
-          if (stop_now) {
-            nnz += a.xo != 0.0 ? 1.0 : 0.0;
-          } else {
-            const double d = px.screen_now ? px.dot(a) : 0.0;
-            const bool kp = px.keep(a, d);
-            look += px.look(a, d, kp) ? 1.0 : 0.0;
-            const double xn = px.xnew(a);
-            p.xnew[q] = xn;
-            bk.keep[q] = static_cast<int8_t>(kp);
-            if (kp) {
-              kept += 1.0;
-              nnz += xn != 0.0 ? 1.0 : 0.0;
-              l1n += fabs(xn);  // ||x_{t+1}||_1 over the preserved set (next iteration's 473)
-            }
-            fa = kp && xn != 0.0;
-            ff = fix_pass && !kp && a.xo != 0.0;
-            va = xn;
-            vf = a.xo;
-          }
-        }
-        if (lists) {  // ordered appends (position order) at this CTA's slice offset
-          const int32_t col = (fa || ff) ? bk.idx[q] : 0;
-          const unsigned ba = __ballot_sync(kFull, fa), bf = __ballot_sync(kFull, ff);
-          if (l == 0) {
-            sh.wcount[0][w] = __popc(ba);
-            sh.wcount[1][w] = __popc(bf);
-          }
-          __syncthreads();
-          int oa = na, of = nf, ta = 0, tf = 0;
-          for (int ww = 0; ww < kWarps; ++ww) {
-            if (ww < w) {
-              oa += sh.wcount[0][ww];
-              of += sh.wcount[1][ww];
-            }
-            ta += sh.wcount[0][ww];
-            tf += sh.wcount[1][ww];
-          }
-          const unsigned below = (1u << l) - 1u;
-          if (fa) {
-            const int64_t at = lo + oa + __popc(ba & below);
-            p.nzj[at] = col;
-            p.nzv[at] = va;
-          }
-          if (ff) {
-            const int64_t at = lo + of + __popc(bf & below);
-            p.fxj[at] = col;
-            p.fxv[at] = vf;
-          }
-          na += ta;
-          nf += tf;
-          __syncthreads();  // wcount is reused by the next round
-        }
-      }
-      if (lists && threadIdx.x == 0) {
-        p.lcnt[vrank()] = na;
-        p.lcnt[vsize() + vrank()] = nf;
-      }
-      double v[4] = {kept, look, nnz, l1n};
-      const bool mx[4] = {false, false, false, false};
-      block_reduce<4>(v, mx, sh);
-      if (threadIdx.x == 0) {
-        put_slot(p, kSlKept, v[0]);
-        put_slot(p, kSlLook, v[1]);
-        put_slot(p, kSlNnz, v[2]);
-        if (!stop_now) put_slot(p, l1_slot(s.t + 1), v[3]);
-      }
-    }
+    if (!early) slice_prox(p, sh, bk, px, lo, hi, stop_now, fix_pass, lists, &pre, false, s.t);
     // u = A_S x_next over the kept nonzeros (131-146) and the v history fix for atoms
     // dropped by this screening pass (FISTA, 673-684), in the same phase: dense work
     // items re-derive the coefficients with ProxCtx; the SuKro scatter is slice-owned.
@@ -2127,7 +2159,7 @@ __device__ __noinline__ void engine_body(const EngineParams& p, Sh& sh, double* 
       }
     }
     FL1_MARK(3);
-    vsync();  // ------------------------------------------------ sync 2
+    if (!early) vsync();  // -------------------------------------- sync 2
     FL1_MARK(4);
     double tp2 = 0.0;
     if (threadIdx.x == 0) {
@@ -2148,11 +2180,11 @@ __device__ __noinline__ void engine_body(const EngineParams& p, Sh& sh, double* 
         xn_pre = p.xnew[lo + threadIdx.x];
       }
     }
-    grid_reduce(p, sh, (1u << kSlKept) | (1u << kSlLook) | (1u << kSlNnz), 0u);
+    if (!early) grid_reduce(p, sh, (1u << kSlKept) | (1u << kSlLook) | (1u << kSlNnz), 0u);  // (early: in phase B)
     if (threadIdx.x == 0) {
       sh.S_new = stop_now ? S : static_cast<int64_t>(sh.res[kSlKept]);
       sh.look = static_cast<int64_t>(sh.res[kSlLook]);
-      sh.nnz = static_cast<int64_t>(sh.res[kSlNnz]);
+      sh.nnz = static_cast<int64_t>(sh.res[(early && stop_now) ? kSlNnzX : kSlNnz]);
       sh.gamma = -1.0;
       sh.next_dict = s.dict_index;
       sh.speed = 0;

@@ -278,6 +278,7 @@ struct alignas(16) EngineParams {
   int32_t* lcnt;    // [grid] apply counts, [grid] fix counts
   int32_t list_apply;  // 1: dense u = A x from the lists in phase E (FL1_LIST_APPLY)
   int32_t power_onchip;  // 1: cluster-mode power iterations on chip when they fit (FL1_POWER_ONCHIP)
+  int32_t early_prox;    // 1: non-screening dense iterations run the prox before the first barrier (FL1_EARLY_PROX)
   double* pv;       // K
   double* pw;       // K
   double* PU;       // ld: power-iteration A v (combined)
