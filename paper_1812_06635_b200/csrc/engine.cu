@@ -142,6 +142,22 @@ __device__ __forceinline__ void bulk_wait(uint64_t* bar, uint32_t parity) {
 // when the CTA's slice has at most kColBuf columns).
 constexpr int kColBuf = 1024;
 __shared__ double s_colsum[kColBuf];
+// early prox: each thread's first atom of the slice, staged during the pass
+__shared__ double s_ex[FL1_THREADS];
+__shared__ double s_exp[FL1_THREADS];
+__shared__ int32_t s_eidx[FL1_THREADS];
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
+               "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
+               "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 __device__ __forceinline__ int vsize() { return s_vsize; }
 __device__ __forceinline__ int vrank() { return s_vrank; }
 __device__ __forceinline__ void vsync() {
@@ -1509,7 +1525,8 @@ __device__ __forceinline__ int l1_slot(uint64_t t) { return (t & 1) ? kSlL1b : k
 // stopping iteration) goes to kSlNnzX.
 __device__ __forceinline__ void slice_prox(const EngineParams& p, Sh& sh, const Bank& bk, const ProxCtx& px, int64_t lo,
                                         int64_t hi, bool stop_now, bool fix_pass, bool lists,
-                                        const ProxCtx::Atom* pre, bool early, uint64_t t) {
+                                        const ProxCtx::Atom* pre, const int32_t* pre_idx, bool early,
+                                        uint64_t t) {
   double kept = 0.0, look = 0.0, nnz = 0.0, l1n = 0.0, nnzx = 0.0;
   int32_t na = 0, nf = 0;  // list lengths (lists only)
   const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
@@ -1547,7 +1564,7 @@ __device__ __forceinline__ void slice_prox(const EngineParams& p, Sh& sh, const 
       }
     }
     if (lists) {  // ordered appends (position order) at this CTA's slice offset
-      const int32_t col = (fa || ff) ? bk.idx[q] : 0;
+      const int32_t col = (fa || ff) ? ((pre_idx && q == lo + threadIdx.x) ? pre_idx[threadIdx.x] : bk.idx[q]) : 0;
       const unsigned ba = __ballot_sync(kFull, fa), bf = __ballot_sync(kFull, ff);
       if (l == 0) {
         sh.wcount[0][w] = __popc(ba);
@@ -1939,6 +1956,24 @@ __device__ __noinline__ void engine_body(const EngineParams& p, Sh& sh, double* 
       __syncthreads();
     }
     bool exact_fit = !gram && !(sh.rho_sq > 0.0);  // Gram mode decides after the phase-B reduction
+    // Non-screening dense iterations: the prox and the apply lists need only this CTA's
+    // corr, so they run before the barrier, and the phase-B and phase-E reductions
+    // become one (the stop decision, unknown here, only selects the ledger's nnz).
+    // Each thread's first atom (x, x_prev, column) is staged into shared memory by
+    // cp.async while the pass streams (no registers held across it).
+    const bool early = p.early_prox && !gram && !exact_fit && lv.kind == kDense && p.list_apply && !p.observe &&
+                       (ld + vsize() - 1) / vsize() <= kLRB &&
+                       (p.variant == FL1_PLAIN || s.t % static_cast<uint64_t>(p.interval) != 0);
+    if (early) {
+      const int64_t q = lo + threadIdx.x;
+      if (q < hi) {
+        cp_async8(&s_ex[threadIdx.x], bk.x + q);
+        if (momentum != 0.0) cp_async8(&s_exp[threadIdx.x], bk.xp + q);
+        else s_exp[threadIdx.x] = 0.0;
+        cp_async4(&s_eidx[threadIdx.x], bk.idx + q);
+      }
+      cp_async_commit();
+    }
     if (gram) {
       gram_products(p, sh, bk, S, momentum);
     } else if (!exact_fit) {
@@ -1970,13 +2005,16 @@ __device__ __noinline__ void engine_body(const EngineParams& p, Sh& sh, double* 
         op_adjoint(p, sh, lv, bk.idx, bk.eps, S, sc.vec, sc.rt, po);
       }
     }
-    // Non-screening dense iterations: the prox and the apply lists need only this CTA's
-    // corr, so they run before the barrier, and the phase-B and phase-E reductions
-    // become one (the stop decision, unknown here, only selects the ledger's nnz).
-    const bool early = p.early_prox && !gram && !exact_fit && lv.kind == kDense && p.list_apply && !p.observe &&
-                       (ld + vsize() - 1) / vsize() <= kLRB &&
-                       (p.variant == FL1_PLAIN || s.t % static_cast<uint64_t>(p.interval) != 0);
-    if (early) {
+    if (early) {  // the early prox (see above)
+      cp_async_wait_all();
+      __syncthreads();
+      const int64_t q = lo + threadIdx.x;
+      ProxCtx::Atom pre{};
+      if (q < hi) {
+        pre.c = hi - lo <= kColBuf ? s_colsum[threadIdx.x] : p.corr[q];  // the pass's column results
+        pre.xo = s_ex[threadIdx.x];
+        pre.xpv = s_exp[threadIdx.x];
+      }
       ProxCtx px{};
       px.corr = p.corr;
       px.x = bk.x;
@@ -1986,7 +2024,7 @@ __device__ __noinline__ void engine_body(const EngineParams& p, Sh& sh, double* 
       px.thresh = lambda * s.inv_l;
       px.lambda = lambda;
       px.rule_gap = p.rule == FL1_RULE_GAP;
-      slice_prox(p, sh, bk, px, lo, hi, false, false, true, nullptr, true, s.t);
+      slice_prox(p, sh, bk, px, lo, hi, false, false, true, &pre, s_eidx, true, s.t);
     }
     FL1_MARK(1);
     vsync();  // ------------------------------------------------ sync 1
@@ -2141,7 +2179,7 @@ __device__ __noinline__ void engine_body(const EngineParams& p, Sh& sh, double* 
     // phase E forms u (and the fix) by row slices straight from the lists
     const bool lists = p.list_apply && lv.kind == kDense && !gram && !stop_now &&
                        (ld + vsize() - 1) / vsize() <= kLRB;  // one row block per CTA
-    if (!early) slice_prox(p, sh, bk, px, lo, hi, stop_now, fix_pass, lists, &pre, false, s.t);
+    if (!early) slice_prox(p, sh, bk, px, lo, hi, stop_now, fix_pass, lists, &pre, nullptr, false, s.t);
     // u = A_S x_next over the kept nonzeros (131-146) and the v history fix for atoms
     // dropped by this screening pass (FISTA, 673-684), in the same phase: dense work
     // items re-derive the coefficients with ProxCtx; the SuKro scatter is slice-owned.
