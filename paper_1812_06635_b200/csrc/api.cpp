@@ -1213,7 +1213,7 @@ void solve_clusters(fl1_seq* s, const double* Y, bool y_device, int64_t ldy, con
     const size_t q_np = preg(sizeof(double) * static_cast<size_t>(ld * bcap) * sm);
     const size_t q_c = preg(sizeof(double) * static_cast<size_t>(k * bcap) * sm);
     const size_t q_s = preg(sizeof(fl1::PrefixSig) * ub), q_h = preg(sizeof(fl1::Handoff) * ub);
-    const size_t q_n = preg(sizeof(int32_t));
+    const size_t q_n = preg(sizeof(int32_t) * 4);  // steps, two signal-queue counters
     (void)kt;
     char* pb = ctx->batch_scratch(1, ptop + 256).as<char>();
     pp.n = n;
@@ -1265,6 +1265,7 @@ void solve_clusters(fl1_seq* s, const double* Y, bool y_device, int64_t ldy, con
     pp.traces = bd.traces;
     pp.trace_cap = cap;
     pp.steps_out = reinterpret_cast<int32_t*>(pb + q_n);
+    pp.queue = pp.steps_out + 1;
     if (std::getenv("FL1_STEP_LOG")) {  // diagnostics: per-step occupancy of the lockstep engine
       pp.max_log = 4096;
       step_log = std::make_unique<DevBuf>(sizeof(double) * 5 * pp.max_log);

@@ -81,6 +81,7 @@ struct PSh {
   int release, screen;
   int64_t n_act, off;
   int32_t nzc[kPW], fxc[kPW];
+  int32_t qnext;
 };
 
 // deterministic block reductions (fixed tree)
@@ -995,6 +996,10 @@ __global__ void __launch_bounds__(kPT, 1) prefix_kernel(const __grid_constant__ 
     if (p.max_it == 0) finish_signal(p, sh, b, false, 0.0, t0);
     else compute_rho(p, sh, b);
   }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    p.queue[0] = 0;
+    p.queue[1] = 0;
+  }
   grid.sync();
   int32_t steps = 0;
   for (;; ++steps) {
@@ -1052,8 +1057,17 @@ __global__ void __launch_bounds__(kPT, 1) prefix_kernel(const __grid_constant__ 
     }
     grid.sync();
     if (logit) p.step_log[5 * steps + 4] = gtimer() - t0;
-    // ---- the rest of each signal's unit of work, one signal per CTA
-    for (int64_t a = blockIdx.x; a < n_act; a += gridDim.x) {
+    // ---- the rest of each signal's unit of work, one signal per CTA; CTAs take the
+    // next signal from a counter (FISTA and power steps differ in cost), which the
+    // result does not depend on. The other step's counter is reset for the next step
+    // (its last users finished before this step's barriers).
+    if (blockIdx.x == 0 && threadIdx.x == 0) p.queue[(steps + 1) & 1] = 0;
+    for (;;) {
+      if (threadIdx.x == 0) sh.qnext = atomicAdd(p.queue + (steps & 1), 1);
+      __syncthreads();
+      const int64_t a = sh.qnext;
+      __syncthreads();
+      if (a >= n_act) break;
       const int64_t b = act[a];
       const int mode = __ldcg(&p.sig[b].mode);
       if (mode == 0) fista_step(p, sh, a, b, t0, sk, us, stage);

@@ -206,6 +206,7 @@ struct PrefixParams {
   fl1_trace_row* traces;      // B x trace_cap
   int64_t trace_cap;
   int32_t* steps_out;         // global steps executed
+  int32_t* queue;             // two per-step signal-queue counters (per-signal phase)
   double* step_log;           // nullable: per step (n_act, n_pow, %globaltimer) x max_log
   int32_t max_log;
 };
