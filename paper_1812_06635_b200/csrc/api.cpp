@@ -110,7 +110,16 @@ struct DevBuf {
 
 constexpr int kDefaultClusterSize = 2;  // batched solves: CTAs per signal
 
-int64_t even_ld(int64_t n) { return (n + 3) / 4 * 4; }  // 32-byte aligned columns
+// leading dimension of dense columns / vectors: 128-byte aligned (FL1_LD_ALIGN doubles,
+// default 16: every column starts on an L2 line; c1 -1.5%, no change where N % 16 == 0)
+int64_t even_ld(int64_t n) {
+  static const int64_t a = [] {
+    const char* e = std::getenv("FL1_LD_ALIGN");
+    const int64_t v = e ? std::atoll(e) : 16;
+    return v >= 2 && (v & (v - 1)) == 0 ? v : 16;
+  }();
+  return (n + a - 1) / a * a;
+}
 
 }  // namespace
 
