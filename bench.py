@@ -116,6 +116,16 @@ def reduce_over_ranks(dist, device, per_solve_s: float, e2e_s: float, iters: flo
     return float(mx[0]), float(mx[1]), float(sm[2])
 
 
+def ncu_traffic(config):
+    """DRAM bytes (read + write) per launch of the config's top kernel, from the committed
+    ncu --set full capture (profiles/ncu_summary.json); None without one."""
+    summ = ROOT / "profiles" / "ncu_summary.json"
+    try:
+        return json.loads(summ.read_text()).get(config, {}).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
 def algorithmic_bytes(res, n: int) -> float:
     """sum_t 8 N (|S_t| + nnz(x_{t+1})) + 16 N |S| per power step."""
     tr = res.trace
@@ -203,13 +213,7 @@ def run_gpu(args) -> None:
     achieved = alg / (r0.device_ms / 1e3) / 1e9
     pr = r0.profile
     hot_gbs = pr[5] / pr[0] if pr[0] > 0 else None  # bytes / ns = GB/s
-    traffic = None
-    summ = ROOT / "profiles" / "ncu_summary.json"
-    if summ.exists():
-        try:
-            traffic = json.loads(summ.read_text()).get(args.config, {}).get("dram_bytes_per_launch")
-        except Exception:
-            traffic = None
+    traffic = ncu_traffic(args.config)
     cpu = cpu_baseline(args.config, inst, L) if not args.no_cpu_baseline else None
     e2e_r = e2e_res[-1]
     line = {
@@ -368,7 +372,8 @@ def run_sukro(args) -> None:
                 "d2h_bytes_per_step": int(e2e_r.d2h_bytes)},
         "gpu_launches": int(launches),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": None, "peak_source": peak_src,
+                     "traffic": ncu_traffic("c3"), "traffic_note": "whole solve launch (SuKro + exact phases)",
+                     "peak_source": peak_src,
                      "algorithmic_bytes_per_launch": dense_bytes,
                      "kernel": "fl1::engine_kernel, exact dense phase (after the last switch)",
                      "sukro_phase": {"flops": sk_flops, "ms": sk_ms, "TFLOPs": sk_flops / (sk_ms / 1e3) / 1e12,
@@ -632,7 +637,8 @@ def run_batched(args) -> None:
                 "d2h_bytes_per_step": int(sum(r.d2h_bytes for r in e2e_last))},
         "gpu_launches": int(launches),
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak_t, "unit": "TFLOP/s",
-                     "frac": achieved / peak_t, "traffic": None, "peak_source": peak_src_t,
+                     "frac": achieved / peak_t, "traffic": ncu_traffic("c5"),
+                     "traffic_note": "DRAM bytes of the lockstep launch (prefix_kernel)", "peak_source": peak_src_t,
                      "algorithmic_flops_per_launch": flops,
                      "kernel": "fl1::prefix_kernel (lockstep batched engine, DMMA m8n8k4) + fl1::engine_kernel",
                      "note": "algorithmic FLOPs = 2 N K per signal-iteration (SURVEY 8d); the lockstep also runs "

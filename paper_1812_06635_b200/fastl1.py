@@ -503,6 +503,12 @@ def run_lasso_batched(seq: ApproxSequence, Y, lambdas, cfg: SwitchConfig, opts: 
             lib.result_free(hs[b])
 
 
+def _info_columns(infos) -> dict:
+    """Field -> numpy column of a ctypes array of fl1_result_info (no per-struct attribute access)."""
+    arr = np.ctypeslib.as_array(infos)
+    return {f: arr[f] for f in arr.dtype.names}
+
+
 def _collect_results(lib: Library, hs, B: int) -> list:
     """All results of a batched call through the bulk accessors (4 library calls)."""
     if B == 0:
@@ -514,9 +520,8 @@ def _collect_results(lib: Library, hs, B: int) -> list:
     xs = np.empty((B, k))
     profs = np.zeros((B, 14))
     lib.check(lib.results_collect(hs, B, infos, _dptr(xs), _dptr(profs)))
-    nt = [infos[b].n_trace for b in range(B)]
-    ns = [infos[b].n_switches for b in range(B)]
-    na = [infos[b].n_final_active for b in range(B)]
+    cols = {f: v.tolist() for f, v in _info_columns(infos).items()}  # one pass over the structs
+    nt, ns, na = cols["n_trace"], cols["n_switches"], cols["n_final_active"]
     traces = np.zeros(max(sum(nt), 1), dtype=TRACE_DTYPE)
     sws = np.zeros(max(sum(ns), 1), dtype=SWITCH_DTYPE)
     fas = np.empty(max(sum(na), 1), dtype=np.int32)
@@ -526,14 +531,14 @@ def _collect_results(lib: Library, hs, B: int) -> list:
     out = []
     ot = os_ = oa = 0
     for b in range(B):
-        info = infos[b]
-        out.append(SolveResult(profile=profs[b], x=xs[b], converged=bool(info.converged), final_gap=info.final_gap,
-                               iterations=int(info.iterations), total_flops=int(info.total_flops),
-                               trace=traces[ot:ot + nt[b]], switches=sws[os_:os_ + ns[b]], final_active=fas[oa:oa + na[b]],
-                               gap_warning=bool(info.gap_warning), device_ms=info.device_ms, setup_ms=info.setup_ms,
-                               kernel_launches=int(info.kernel_launches), power_iterations=int(info.power_iterations),
-                               h2d_bytes=int(info.h2d_bytes), d2h_bytes=int(info.d2h_bytes),
-                               batch_device_ms=float(info.batch_device_ms)))
+        out.append(SolveResult(profile=profs[b], x=xs[b], converged=bool(cols["converged"][b]),
+                               final_gap=cols["final_gap"][b], iterations=cols["iterations"][b],
+                               total_flops=cols["total_flops"][b], trace=traces[ot:ot + nt[b]],
+                               switches=sws[os_:os_ + ns[b]], final_active=fas[oa:oa + na[b]],
+                               gap_warning=bool(cols["gap_warning"][b]), device_ms=cols["device_ms"][b],
+                               setup_ms=cols["setup_ms"][b], kernel_launches=cols["kernel_launches"][b],
+                               power_iterations=cols["power_iterations"][b], h2d_bytes=cols["h2d_bytes"][b],
+                               d2h_bytes=cols["d2h_bytes"][b], batch_device_ms=cols["batch_device_ms"][b]))
         ot += nt[b]
         os_ += ns[b]
         oa += na[b]
