@@ -1385,6 +1385,8 @@ void solve_clusters(fl1_seq* s, const double* Y, bool y_device, int64_t ldy, con
 // grid path; FL1_SINGLE_CLUSTER=0 disables the route.
 constexpr int64_t kSingleClusterBytes = 16ll << 20;
 constexpr int kSingleClusterSize = 16;
+constexpr int64_t kSmallClusterBytes = 8ll << 20;
+constexpr int kSmallClusterSize = 12;
 
 void solve_single(fl1_seq* s, const double* y, bool y_device, double lambda, const fl1_switch_config* cfg,
                   const fl1_run_options* opts, fl1_result** out) {
@@ -1399,7 +1401,10 @@ void solve_single(fl1_seq* s, const double* y, bool y_device, double lambda, con
     int64_t limit = kSingleClusterBytes;
     if (const char* mb = std::getenv("FL1_SINGLE_CLUSTER_MB")) limit = std::atoll(mb) << 20;
     if (!(e && e[0] == '0') && bytes <= limit) {
-      int csize = kSingleClusterSize;
+      // up to 8 MiB, 12 CTAs: the on-chip power iteration's distributed-shared-memory
+      // sums get cheaper with fewer ranks faster than the passes slow down (c1: 16 CTAs
+      // 1.070 ms, 12 CTAs 1.039 ms, 8 CTAs 1.066 ms)
+      int csize = bytes <= kSmallClusterBytes ? kSmallClusterSize : kSingleClusterSize;
       if (const char* cs = std::getenv("FL1_SINGLE_CLUSTER_SIZE")) csize = std::atoi(cs);
       solve_clusters(s, y, y_device, s->lv.back()->dict->n, &lambda, 1, cfg, opts, csize, out, false);
       return;

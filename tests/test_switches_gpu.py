@@ -47,6 +47,7 @@ SWITCHES = [
     ("FL1_BULK_STAGES", "0"),      # register ring for the power-iteration adjoints
     ("FL1_SINGLE_CLUSTER", "0"),   # small dictionaries on the full grid
     ("FL1_POWER_ONCHIP", "0"),     # cluster-mode power iterations streamed, not resident
+    ("FL1_SINGLE_CLUSTER_SIZE", "16"),  # the single-cluster route on 16 CTAs (default 12 up to 8 MiB)
 ]
 
 CASES = {  # name, seed, n, k, nnz: c1 (single-cluster route) and a full-grid dense solve
