@@ -2542,10 +2542,12 @@ cudaError_t screen_kernel_launch(int64_t n, const double* dots, const double* ep
 // roofline (measured: 2-4 stages change the c2 pass by < 3%), while the larger
 // shared-memory carve-out shrinks L1 for the other phases. FL1_BULK_STAGES=R enables it.
 int engine_bulk_stages(int64_t ld) {
-  // power-iteration adjoints stream through a 3-stage bulk-copy ring by default
-  // (FL1_BULK_STAGES: 0 = register ring everywhere)
+  // power-iteration adjoints stream through a 2-stage bulk-copy ring by default: the
+  // ring's shared memory is the engine's scratch, and the smaller carve-out leaves
+  // more L1 to the register-ring passes (c2 6.66 -> 6.57 ms, c4 897 -> 890 ms against
+  // 3 stages; FL1_BULK_STAGES: 0 = register ring everywhere)
   const char* e = std::getenv("FL1_BULK_STAGES");
-  if (!e) e = "3";
+  if (!e) e = "2";
   const int64_t room = 200 * 1024 / 8 - ld;  // doubles left beside the resident residual
   const int64_t fit = std::max<int64_t>(0, std::min<int64_t>(kMaxBulk, room / (kWarps * kUnit)));
   const int64_t r = std::min<int64_t>(fit, std::atoi(e));
