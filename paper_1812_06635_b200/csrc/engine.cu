@@ -140,7 +140,7 @@ __device__ __forceinline__ void bulk_wait(uint64_t* bar, uint32_t parity) {
 }
 // Per-CTA column results of a dense adjoint pass (merge + statistics stay on chip
 // when the CTA's slice has at most kColBuf columns).
-constexpr int kColBuf = 1024;
+constexpr int kColBuf = 512;  // 4 KiB: keeps c2's shared memory under the 100 KiB carve-out (more L1)
 __shared__ double s_colsum[kColBuf];
 // early prox: each thread's first atom of the slice, staged during the pass
 __shared__ double s_ex[FL1_THREADS];
