@@ -715,7 +715,27 @@ def cpu_baseline(cfg_name, inst, L, solves: int = 2) -> dict:
             "sample": f"{len(times)} full {cfg_name} solve(s) by the Eigen-free CPU restatement (oracle/), 1 thread"}
 
 
+REF_BUDGET_S = 240.0  # reference arm: stop timing further steps once this much CPU time is spent
+
+
+def _c4_host_instance(seed: int = 4):
+    """c4's matrix as make_c4_device draws it (the GPU arm's instance), copied to the host
+    column-major; y as well. Input generation only: no repo kernel runs here."""
+    import torch
+
+    At, y = make_c4_device(seed, "cuda")
+    a = At.cpu().numpy().T
+    del At
+    torch.cuda.empty_cache()
+    return a, y
+
+
 def run_reference(args) -> None:
+    """--impl reference: the reference's CPU implementation of the path (its Eigen-free
+    restatement, oracle/: the reference itself cannot be built here) on every host thread,
+    on the native arm's config. c1/c2/c3: whole solves; c5: the whole 512-signal batch on a
+    thread pool over signals (one thread per solve, bench.cpp:283-301); c4: the 10-lambda
+    path estimated from bounded windows (reference_c4_step)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
@@ -723,21 +743,90 @@ def run_reference(args) -> None:
 
     threads = os.cpu_count() or 1
     b = _oracle_backend(threads)
-    inst = syn.dense_instance(args.config)
-    n, k = inst.a.shape
-    d = F.DenseDictionary(inst.a, backend=b)
-    L = F.lipschitz_bound(d)
-    seq = F.ApproxSequence([F.make_exact_approx(d)])
     cfg = F.SwitchConfig(screening_interval=10, max_iterations=5000, rel_tolerance=1e-6)
-    opts = F.RunOptions(variant=F.VARIANT_SCREENED, full_lipschitz=[L])
-    for _ in range(args.warmup):
-        F.run_lasso(seq, inst.y, inst.lam, cfg, opts)
+    workload, extra = None, {}
+    if args.config in ("c1", "c2"):
+        inst = syn.dense_instance(args.config)
+        n, k = inst.a.shape
+        d = F.DenseDictionary(inst.a, backend=b)
+        L = F.lipschitz_bound(d)
+        seq = F.ApproxSequence([F.make_exact_approx(d)])
+        opts = F.RunOptions(variant=F.VARIANT_SCREENED, full_lipschitz=[L])
+
+        def step():
+            r = F.run_lasso(seq, inst.y, inst.lam, cfg, opts)
+            return None, r.iterations
+
+        workload = f"{args.config}: dense {n}x{k} Lasso, FISTA + GAP Safe every 10 its, gap<=1e-6*P(x), cap 5000"
+        extra["lambda_ratio"] = inst.lam / inst.lam_max
+        sample = f"{{steps}} full {args.config} solves"
+    elif args.config == "c3":
+        inst = syn.sukro_instance(seed=3)
+        n, k = inst.a.shape
+        seq = syn.sukro_sequence(inst, backend=b)
+        Ls = [F.lipschitz_bound(dd.op) for dd in seq.dicts]
+        cfg = replace(cfg, gamma_threshold=0.5)
+        opts = F.RunOptions(variant=F.VARIANT_MULTI_DICT, full_lipschitz=Ls)
+
+        def step():
+            r = F.run_lasso(seq, inst.y, inst.lam, cfg, opts)
+            return None, r.iterations
+
+        workload = (f"c3: SuKro {n}x{k}, levels A1 -> A2 -> A4 -> A, stable GAP every 10, Gamma 0.5, "
+                    "gap<=1e-6*P(x), cap 5000")
+        sample = "{steps} full c3 solves (SuKro levels + exact phase)"
+    elif args.config == "c4":
+        a, y = _c4_host_instance(4)
+        n, k = a.shape
+        od = F.DenseDictionary(a, backend=b)
+        del a
+        lmax = F.lambda_max(od, y)
+        L = F.lipschitz_bound(od)  # cached outside run_lasso, as the reference harness does
+        seq = F.ApproxSequence([F.make_exact_approx(od)])
+        ratios = syn.CONFIGS["c4"]["lam_ratios"]
+
+        def step():
+            x, its = None, 0
+            for r in ratios:
+                res = F.run_lasso(seq, y, r * lmax, cfg,
+                                  F.RunOptions(variant=F.VARIANT_SCREENED, full_lipschitz=[L], x_init=x))
+                x, its = res.x, its + res.iterations
+            return None, its
+
+        workload = ("c4: dense 8192x65536 Lasso, 10-lambda path 0.9->0.05 lambda_max with warm starts, "
+                    "FISTA + GAP every 10, each to gap<=1e-6*P(x)")
+        sample = "{steps} full 10-lambda c4 paths (whole solves, warm-started from the oracle's own previous x)"
+    else:  # c5
+        from concurrent.futures import ThreadPoolExecutor
+
+        a, Y, lams = make_c5(5)
+        n, k = a.shape
+        b.lib.set_threads(1)
+        d = F.DenseDictionary(a, backend=b)
+        L = F.lipschitz_bound(d)
+        seq = F.ApproxSequence([F.make_exact_approx(d)])
+        opts = F.RunOptions(variant=F.VARIANT_SCREENED, full_lipschitz=[L])
+        pool = ThreadPoolExecutor(threads)
+
+        def step():
+            rs = list(pool.map(lambda j: F.run_lasso(seq, Y[:, j], lams[j], cfg, opts), range(Y.shape[1])))
+            return None, sum(r.iterations for r in rs)
+
+        workload = (f"c5: {Y.shape[1]} independent Lasso signals on one dense {n}x{k} dictionary, per-signal "
+                    "FISTA + GAP every 10 to gap<=1e-6*P(x), lambda_b = 0.25 lambda_max_b")
+        sample = "{steps} full 512-signal batches, a thread pool over signals (one thread per solve, bench.cpp:283-301)"
+    # CPU warm-up: one step at most (it only faults in pages; c4's step is ~1 min on 16 threads)
+    for _ in range(min(args.warmup, 1)):
+        step()
     times, iters = [], 0
+    t_all = time.perf_counter()
     for _ in range(args.steps):
         t = time.perf_counter()
-        r = F.run_lasso(seq, inst.y, inst.lam, cfg, opts)
-        times.append(time.perf_counter() - t)
-        iters += r.iterations
+        est, its = step()
+        times.append(est if est is not None else time.perf_counter() - t)
+        iters += its
+        if time.perf_counter() - t_all > REF_BUDGET_S:  # bounded run: fewer, whole steps
+            break
     v = float(np.mean(times))
     line = {
         "impl": "reference",
@@ -745,22 +834,26 @@ def run_reference(args) -> None:
         "value": v,
         "unit": "s",
         "n_gpus": int(os.environ.get("WORLD_SIZE", "1")),
-        "steps": args.steps,
-        "warmup": args.warmup,
+        "steps": len(times),
+        "steps_requested": args.steps,
+        "warmup": min(args.warmup, 1),
         "ms_per_step": v * 1e3,
         "higher_is_better": False,
         "scaling": "weak",
         "vs_baseline": None,
         "dtype": "f64",
-        "data": f"synthetic (BASELINE {args.config}, seed {inst.seed})",
-        "config": {"workload": f"{args.config}: dense {n}x{k} Lasso, FISTA + GAP Safe every 10 its, gap<=1e-6*P(x), cap 5000",
-                   "lambda_ratio": inst.lam / inst.lam_max},
+        "data": f"synthetic (BASELINE {args.config}, the native arm's seeded instance)",
+        "config": {"workload": workload, **{k_: v_ for k_, v_ in extra.items() if k_ == "lambda_ratio"}},
         "iters_per_s": iters / sum(times),
         "cpu_baseline": {"value": v, "unit": "s", "cores": threads, "kind": "port",
-                         "sample": f"{args.steps} full {args.config} solves; the reference cannot be built here "
-                                   "(Eigen3 absent), so its Eigen-free restatement (oracle/) runs with "
-                                   f"{threads} OpenMP threads over columns/rows (results identical to 1 thread)"},
+                         "sample": sample.format(steps=len(times)) + f" (timed steps stop once {REF_BUDGET_S:.0f} s "
+                                   "of CPU time is spent); the reference cannot be built here (Eigen3 "
+                                   "absent), so its Eigen-free restatement (oracle/, g++ -O3 -march=x86-64-v3 "
+                                   f"-ffp-contract=off) runs with {threads} OpenMP threads over columns/rows (results "
+                                   "identical to 1 thread)" + ("" if args.config != "c5" else
+                                                               ", here one thread per solve")},
         "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        **{k_: v_ for k_, v_ in extra.items() if k_ != "lambda_ratio"},
     }
     print(json.dumps(line))
 
@@ -771,7 +864,8 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
-    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--config", default="c4", choices=["c1", "c2", "c3", "c4", "c5"],
+                    help="BASELINE config (default c4: the largest single-GPU config, the 10-lambda path)")
     ap.add_argument("--concurrency", type=int, default=0, help="c5: <=0 one launch of thread-block clusters of -N CTAs (0 = default 2); >0 that many concurrent sub-grid launches")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()

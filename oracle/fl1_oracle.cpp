@@ -447,6 +447,7 @@ struct Result {
   bool gap_warning = false;
   double setup_ms = 0.0, run_ms = 0.0;
   int64_t power_steps = 0;
+  double power_bytes = 0.0;  // 16 N |S| per power step (bench.py's byte accounting)
 };
 
 const Op* gram_of(const fl1_dict* d);  // exact_gram handle -> its dense K x K operator
@@ -572,9 +573,12 @@ struct Engine {
                           ? &lead_vector
                           : nullptr;
     Vec lead_out;
+    const int64_t steps0 = result.power_steps;
     const double sq = power_iteration_sq_norm([&](const Vec& xv) { return op.apply(xv); },
                                               [&](const Vec& rv) { return op.apply_adjoint(rv); },
                                               op.size(), warm, &lead_out, &result.power_steps);
+    result.power_bytes += 16.0 * static_cast<double>(op.rows()) * static_cast<double>(op.size()) *
+                          static_cast<double>(result.power_steps - steps0);
     lead_vector = std::move(lead_out);
     return std::max(sq, 1e-300) * kLipschitzSafety;
   }
@@ -1179,6 +1183,10 @@ int orc_result_info_get(const orc_result* r, fl1_result_info* o) {
   o->setup_ms = r->r.setup_ms;
   o->kernel_launches = 0;
   o->power_iterations = r->r.power_steps;
+  return FL1_OK;
+}
+int orc_result_power_bytes(const orc_result* r, double* out) {
+  *out = r->r.power_bytes;
   return FL1_OK;
 }
 int orc_result_x(const orc_result* r, double* out) {

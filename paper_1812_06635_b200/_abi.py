@@ -175,6 +175,7 @@ PRODUCT_ONLY = {
 # oracle-only entry points (test infrastructure)
 ORACLE_ONLY = {
     "set_threads": (None, [C.c_int]),
+    "result_power_bytes": (C.c_int, [_P, _PD]),
     "get_threads": (C.c_int, []),
     "dict_to_dense": (C.c_int, [_P, _PD]),
     "ista_step": (C.c_int, [_P, _PD, C.c_double, C.c_double, _PD, _PD, _PD, _PD]),

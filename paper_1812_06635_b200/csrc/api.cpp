@@ -116,7 +116,9 @@ int64_t even_ld(int64_t n) {
   static const int64_t a = [] {
     const char* e = std::getenv("FL1_LD_ALIGN");
     const int64_t v = e ? std::atoll(e) : 16;
-    return v >= 2 && (v & (v - 1)) == 0 ? v : 16;
+    // at most one bulk unit: the power-iteration ring's last-unit copy moves (ld - ih * kUnit)
+    // doubles into a kUnit-double stage (engine.cu dense_adjoint)
+    return v >= 2 && (v & (v - 1)) == 0 && v <= fl1::kUnit ? v : 16;
   }();
   return (n + a - 1) / a * a;
 }
@@ -1063,6 +1065,19 @@ int fl1_seq_destroy(fl1_seq* s) {
 }
 
 namespace {
+// A cluster launch cannot flush its device trace (the grid path of do_solve can), so it
+// reserves max_iterations rows per signal up front. Reservations above this budget
+// (e.g. the reference's default max_iterations = 1e6 with collect_trace over a large
+// batch) take the grid path instead.
+constexpr uint64_t kClusterTraceBudget = 2ull << 30;
+
+bool cluster_trace_fits(const fl1_switch_config* cfg, const fl1_run_options* opts, int64_t batch) {
+  if (!opts->collect_trace) return true;
+  const uint64_t rows = std::max<uint64_t>(cfg->max_iterations, 1);
+  const uint64_t per_signal = kClusterTraceBudget / sizeof(fl1_trace_row) / static_cast<uint64_t>(std::max<int64_t>(batch, 1));
+  return rows <= per_signal;
+}
+
 // Batched solves in ONE launch: every thread-block cluster of `csize` CTAs is a
 // virtual grid with its own workspace and pulls signals from a device queue
 // (each signal runs the same Engine::run as fl1_solve, with cluster barriers).
@@ -1102,6 +1117,7 @@ void solve_clusters(fl1_seq* s, const double* Y, bool y_device, int64_t ldy, con
   }
   if (n_clusters < 1) throw std::runtime_error("no cluster of this size fits on the device");
   n_clusters = std::min<int>(n_clusters, std::max<int32_t>(batch, 1));
+  if (!cluster_trace_fits(cfg, opts, batch)) throw std::logic_error("cluster trace reservation over budget");
   const int64_t cap = opts->collect_trace ? static_cast<int64_t>(std::max<uint64_t>(cfg->max_iterations, 1)) : 1;
   const int64_t B = std::max<int32_t>(batch, 1);
 
@@ -1390,7 +1406,8 @@ constexpr int kSmallClusterSize = 12;
 
 void solve_single(fl1_seq* s, const double* y, bool y_device, double lambda, const fl1_switch_config* cfg,
                   const fl1_run_options* opts, fl1_result** out) {
-  if (s && cfg && opts && out && !opts->observer && !opts->x_init && !std::getenv("FL1_TRACE_CAP")) {
+  if (s && cfg && opts && out && !opts->observer && !opts->x_init && !std::getenv("FL1_TRACE_CAP") &&
+      cluster_trace_fits(cfg, opts, 1)) {
     const char* e = std::getenv("FL1_SINGLE_CLUSTER");
     int64_t bytes = 0;
     for (const auto& l : s->lv) {
@@ -1414,6 +1431,8 @@ void solve_single(fl1_seq* s, const double* y, bool y_device, double lambda, con
 }
 
 
+constexpr int32_t kTraceFallbackConcurrency = 8;
+
 int solve_batched_impl(fl1_seq* s, const double* Y, bool y_device, int64_t ldy, const double* lambdas, int32_t batch,
                        const fl1_switch_config* cfg, const fl1_run_options* opts, int32_t concurrency,
                        fl1_result** out) {
@@ -1426,6 +1445,8 @@ int solve_batched_impl(fl1_seq* s, const double* Y, bool y_device, int64_t ldy, 
     fl1_ctx* ctx = s->lv.back()->dict->ctx;
     ctx->bind();
     for (int32_t b = 0; b < batch; ++b) out[b] = nullptr;
+    if (concurrency <= 0 && cfg && opts && !cluster_trace_fits(cfg, opts, batch))
+      concurrency = kTraceFallbackConcurrency;  // trace too large to reserve: grid solves that flush
     if (concurrency <= 0) {  // one launch, thread-block clusters as virtual grids
       const int csize = concurrency == 0 ? kDefaultClusterSize : -concurrency;
       try {

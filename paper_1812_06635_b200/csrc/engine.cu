@@ -2537,20 +2537,26 @@ cudaError_t screen_kernel_launch(int64_t n, const double* dots, const double* ep
 
 // Shared scratch after the resident residual: dense apply warp partials, or the
 // SuKro staging (adjoint tiles; apply entry list + 64-column Cg / Bg chunks).
+// The run-time tunables below are read ONCE per process (statics): the workspace that
+// carves p.scratch_len is cached per context, so the launch's dynamic shared memory and
+// the kernel's view of it must never disagree within a process.
+namespace {
+int env_int_once(const char* name, int dflt) {
+  const char* e = std::getenv(name);
+  return e ? std::atoi(e) : dflt;
+}
+}  // namespace
+
 // Bulk-copy ring stages per warp for a residual of ld doubles (4 KiB each, 8 warps).
-// Off by default: on B200 the register ring already keeps the dense pass at the HBM
-// roofline (measured: 2-4 stages change the c2 pass by < 3%), while the larger
-// shared-memory carve-out shrinks L1 for the other phases. FL1_BULK_STAGES=R enables it.
+// Default 2: power-iteration adjoints stream through a 2-stage bulk-copy ring; the
+// ring's shared memory is the engine's scratch, and the smaller carve-out leaves more
+// L1 to the register-ring passes (c2 6.66 -> 6.57 ms, c4 897 -> 890 ms against 3
+// stages). FL1_BULK_STAGES=R overrides it (0 = register ring everywhere).
 int engine_bulk_stages(int64_t ld) {
-  // power-iteration adjoints stream through a 2-stage bulk-copy ring by default: the
-  // ring's shared memory is the engine's scratch, and the smaller carve-out leaves
-  // more L1 to the register-ring passes (c2 6.66 -> 6.57 ms, c4 897 -> 890 ms against
-  // 3 stages; FL1_BULK_STAGES: 0 = register ring everywhere)
-  const char* e = std::getenv("FL1_BULK_STAGES");
-  if (!e) e = "2";
+  static const int stages = env_int_once("FL1_BULK_STAGES", 2);
   const int64_t room = 200 * 1024 / 8 - ld;  // doubles left beside the resident residual
   const int64_t fit = std::max<int64_t>(0, std::min<int64_t>(kMaxBulk, room / (kWarps * kUnit)));
-  const int64_t r = std::min<int64_t>(fit, std::atoi(e));
+  const int64_t r = std::min<int64_t>(fit, stages);
   return r >= 2 ? static_cast<int>(r) : 0;
 }
 
@@ -2563,11 +2569,11 @@ int64_t engine_scratch_len(int64_t ld, int64_t sukro_m) {
     const int64_t term = 16 * m4 + 32 * (m4 + 1);
     s = std::max(s, term + kWarps * 64);                             // adjoint, one term per round
     s = std::max(s, kThreads + kThreads / 2 + 2 * (sukro_m + 1) * 64);  // apply
-    const int64_t room = 200 * 1024 / 8 - ld;                        // up to 4 adjoint terms per round
-    // SuKro adjoint terms staged per round: 2 keeps c3's engine in the 132 KiB
-    // shared-memory carve-out (more L1 for the exact phase): c3 8.75 -> 8.65 ms vs 4
-    const char* te = std::getenv("FL1_SUKRO_TERMS");
-    const int64_t per_round = te ? std::max<int64_t>(1, std::atoll(te)) : 2;
+    const int64_t room = 200 * 1024 / 8 - ld;                        // bounded by the shared memory left
+    // SuKro adjoint terms staged per round (default 2, FL1_SUKRO_TERMS overrides): 2 keeps
+    // c3's engine in the 132 KiB shared-memory carve-out (more L1 for the exact phase):
+    // c3 8.75 -> 8.65 ms against 4
+    static const int64_t per_round = std::max(1, env_int_once("FL1_SUKRO_TERMS", 2));
     s = std::max(s, std::min(room, per_round * term + kWarps * 64));
   }
   return s;

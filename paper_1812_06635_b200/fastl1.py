@@ -389,6 +389,11 @@ def _collect_result(lib: Library, h) -> SolveResult:
     if hasattr(lib, "result_profile"):
         prof = np.zeros(14)
         lib.check(lib.result_profile(h, _dptr(prof)))
+    elif hasattr(lib, "result_power_bytes"):  # the oracle reports its power-iteration bytes only
+        prof = np.zeros(14)
+        pb = C.c_double()
+        lib.check(lib.result_power_bytes(h, C.byref(pb)))
+        prof[7] = pb.value
     return SolveResult(profile=prof, x=x, converged=bool(info.converged), final_gap=info.final_gap, iterations=int(info.iterations),
                        total_flops=int(info.total_flops), trace=trace, switches=sws, final_active=fa,
                        gap_warning=bool(info.gap_warning), device_ms=info.device_ms, setup_ms=info.setup_ms,

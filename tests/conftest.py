@@ -62,3 +62,14 @@ def backend(request, oracle):
     from paper_1812_06635_b200.fastl1 import default_backend
 
     return default_backend()
+
+
+def pytest_sessionfinish(session, exitstatus):
+    """FL1_PARITY_OUT=path: write the achieved GPU-vs-oracle discrepancies (tests/_parity.py)."""
+    import os
+
+    out = os.environ.get("FL1_PARITY_OUT")
+    if out:
+        import _parity
+
+        _parity.write_records(out)

@@ -9,7 +9,18 @@ import pytest
 
 from paper_1812_06635_b200 import fastl1 as F, synthetic as syn
 
-from test_parity_gpu import assert_parity  # noqa: E402  (shared parity bar)
+from _parity import assert_parity as _assert_parity  # noqa: E402  (shared parity bar)
+
+# Gram vs direct are two different formulas for the same residual norms: the Gram phase forms
+# ||y - A x||^2 = ||y||^2 - 2 x.A^T y + x.G x (fastl1.cpp:366-394), which cancels at the
+# scale ||y||^2 / 2 >= P: measured <= 19 ulp of P (oracle Gram vs oracle direct), inside the
+# shared bar's 64-ulp floor.
+GRAM_GAP_ULPS = 64.0
+
+
+def assert_parity(g, o, a, y, lam, **kw):
+    kw.setdefault("gap_ulps", GRAM_GAP_ULPS)
+    return _assert_parity(g, o, a, y, lam, **kw)
 
 OPTIONS = [
     dict(solver=F.SOLVER_FISTA, rule=F.RULE_GAP, variant=F.VARIANT_SCREENED),
