@@ -250,6 +250,17 @@ int fl1_rng_normals(uint64_t seed, int64_t count, double* out);
  * mt19937_64(mix_seed(seed, trial)), y = A x on the GPU, both scaled so |y| = 1;
  * draws with an empty support or |y| <= 1e-12 are redrawn. y: N, x: K. */
 int fl1_draw_signal(fl1_dict* d, double bernoulli_p, uint64_t seed, int32_t trial, double* y, double* x);
+
+/* build_sukro_sequence (dictionary.cpp:281-357, truncated_svd 253-279) on the device for a
+ * dense N x K dictionary (N = m^2, K = q^2): the SuKro levels of the given strictly
+ * increasing ranks. Outputs (host): left / right = the T = ranks[n_ranks-1] factor pairs,
+ * term t at t*m*q (m x q column-major each, sqrt(s_t) folded into both, as the reference);
+ * eps / approx_norms = n_ranks x K (level l at l*K: atom_error_bounds after the running
+ * max, approx_atom_norms2); rc / op_err = n_ranks (relative_complexity,
+ * operator_error_bound). Errors (FL1_EINVAL) carry the reference's messages. Device limit:
+ * rank + 8 <= 64 probes, <= 16 ranks. */
+int fl1_build_sukro_sequence(fl1_dict* dense, const int32_t* ranks, int32_t n_ranks, double* left, double* right,
+                             double* eps, double* approx_norms, double* rc, double* op_err);
 /* screen_precomputed (screening.cpp:136-150) as a device kernel; kept gets positions. */
 int fl1_screen_precomputed(fl1_ctx* ctx, int64_t n, const double* abs_dots, const double* eps,
                            const double* exact_norms, const double* approx_norms,

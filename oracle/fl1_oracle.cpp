@@ -17,8 +17,8 @@
 // Eigen's exact summation order is not reproduced (it is unspecified); every
 // reduction here is a plain sequential loop. Two documented extensions
 // (rel_tolerance, x_init) and the SuKro column scale default to reference
-// behaviour when unused. The Gram-backed exact phase is not restated (out of
-// scope).
+// behaviour when unused. The Gram-backed exact phase (fastl1.cpp:335-394) is restated
+// too (Engine::compute_products' gram_mode branch and apply_restriction's G-column fix).
 #include "fl1_oracle.h"
 
 #include <algorithm>

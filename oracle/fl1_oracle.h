@@ -130,7 +130,7 @@ int orc_screen(const int32_t* active, int64_t n_active, const double* center, do
 void orc_gen_normals(uint64_t seed, int64_t count, double* out);
 /* std::uniform_int_distribution<int64_t>(0, hi) draws interleaved with normals, as
  * in testkit::random_instance / square_instance (helpers.hpp:76-89,
- * test_fastl1.cpp:206-219): for each of `support` draws, pos = pick(rng),
+ * test_fastl1.cpp:18-31): for each of `support` draws, pos = pick(rng),
  * val = gauss(rng). */
 void orc_gen_support(uint64_t seed, int64_t hi, int32_t support, int64_t* pos, double* val);
 

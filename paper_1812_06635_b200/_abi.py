@@ -170,6 +170,7 @@ PRODUCT_ONLY = {
     "results_collect": (C.c_int, [_PP, C.c_int32, C.POINTER(ResultInfoC), _PD, _PD]),
     "results_tables": (C.c_int, [_PP, C.c_int32, C.POINTER(TraceRowC), C.POINTER(SwitchEventC), _PI32]),
     "draw_signal": (C.c_int, [_P, C.c_double, C.c_uint64, C.c_int32, _PD, _PD]),
+    "build_sukro_sequence": (C.c_int, [_P, _PI32, C.c_int32, _PD, _PD, _PD, _PD, _PD, _PD]),
 }
 
 # oracle-only entry points (test infrastructure)

@@ -16,7 +16,7 @@ LIB = PKG / "libfl1cuda.so"
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 HOST_CXX = "/usr/bin/g++"  # the image's $CXX wrapper lacks some specs; use the system compiler
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-SOURCES = ["engine.cu", "batched.cu", "api.cpp"]
+SOURCES = ["engine.cu", "batched.cu", "setup.cu", "sukro_build.cu", "api.cpp"]
 
 
 def _sources_newer(target: Path, deps: list[Path]) -> bool:

@@ -42,7 +42,25 @@ int prefix_split_max();
 cudaError_t gram_launch(const double* a, int64_t ld, int64_t k, double* g, int64_t ldg, int device,
                         cudaStream_t stream);
 cudaError_t colnorm_launch(const double* g, int64_t k, int64_t ldg, double* out, cudaStream_t stream);
+cudaError_t dense_norms_launch(const double* a, int64_t n, int64_t ld, int64_t k, double* out, cudaStream_t stream);
+cudaError_t sukro_norms_launch(const double* left, const double* right, const double* scale, int nterms, int64_t m,
+                               int64_t q, double* out, cudaStream_t stream);
 int64_t prefix_max_atoms();
+cudaError_t gemm_tn_launch(const double* X, int64_t ldx, int64_t nx, const double* Y, int64_t ldy, int64_t ny,
+                           int64_t kdim, double* C, int64_t ldc, double* work, size_t work_elems, int device,
+                           cudaStream_t stream);
+cudaError_t rearrange_launch(const double* a, int64_t lda, int64_t m, int64_t q, double* R, double* Rt, int64_t ldr,
+                             cudaStream_t stream);
+cudaError_t householder_qr_launch(double* W, int64_t M, int p, int64_t ld, double* Q, int64_t ldq, double* Rf,
+                                  cudaStream_t stream);
+cudaError_t jacobi_svd_launch(const double* Rf, int p, double* S, double* W, double* V, cudaStream_t stream);
+cudaError_t small_gemm_launch(const double* A, int64_t lda, int64_t M, int p, const double* B, const double* S, int r,
+                              double* out, int64_t ldo, cudaStream_t stream);
+cudaError_t residual_norms_launch(const double* a, int64_t lda, int64_t m, int64_t q, int T, const double* left,
+                                  const double* right, int64_t ldt, const int* ranks, int n_ranks, double* eps,
+                                  double* app, cudaStream_t stream);
+int sukro_max_probe();
+int sukro_max_snapshots();
 cudaError_t engine_cluster_capacity(int64_t ld, int64_t sukro_m, int csize, int* n_clusters);
 cudaError_t engine_launch_clusters(const EngineParams& p0, int n_clusters, int csize, int64_t sukro_m,
                                    cudaStream_t stream);
@@ -570,31 +588,23 @@ std::shared_ptr<DictImpl> new_dense(fl1_ctx* ctx, const double* a, int64_t n, in
   d->k = k;
   d->ld = even_ld(n);
   d->a = std::make_unique<DevBuf>(static_cast<size_t>(d->ld) * static_cast<size_t>(k) * sizeof(double));
-  std::vector<double> host;
-  const double* src = a;
-  if (device_src) {
-    host.resize(static_cast<size_t>(n) * static_cast<size_t>(k));
-    ck(cudaMemcpy(host.data(), a, host.size() * sizeof(double), cudaMemcpyDeviceToHost), "download");
-    src = host.data();
-  }
+  // host input: one H2D copy; device input: one D2D copy (the matrix never visits the host)
+  const cudaMemcpyKind kind = device_src ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
   if (d->ld == n) {
-    ck(cudaMemcpy(d->a->p, src, static_cast<size_t>(n) * static_cast<size_t>(k) * sizeof(double),
-                  cudaMemcpyHostToDevice),
-       "dictionary upload");
+    ck(cudaMemcpy(d->a->p, a, static_cast<size_t>(n) * static_cast<size_t>(k) * sizeof(double), kind),
+       "dictionary copy");
   } else {
     ck(cudaMemset(d->a->p, 0, d->a->bytes), "memset");
-    ck(cudaMemcpy2D(d->a->p, static_cast<size_t>(d->ld) * sizeof(double), src, static_cast<size_t>(n) * sizeof(double),
-                    static_cast<size_t>(n) * sizeof(double), static_cast<size_t>(k), cudaMemcpyHostToDevice),
-       "dictionary upload");
+    ck(cudaMemcpy2D(d->a->p, static_cast<size_t>(d->ld) * sizeof(double), a, static_cast<size_t>(n) * sizeof(double),
+                    static_cast<size_t>(n) * sizeof(double), static_cast<size_t>(k), kind),
+       "dictionary copy");
   }
-  // atom norms (DenseDictionary ctor, dictionary.cpp:63)
+  // atom norms (DenseDictionary ctor, dictionary.cpp:63) on the device, sequential order per
+  // column (bit-identical to the host restatement); only the K norms come back
+  DevBuf nrm(static_cast<size_t>(k) * sizeof(double));
+  ck(fl1::dense_norms_launch(d->a->as<double>(), n, d->ld, k, nrm.as<double>(), nullptr), "atom norms");
   d->norms.resize(static_cast<size_t>(k));
-  for (int64_t j = 0; j < k; ++j) {
-    double s = 0.0;
-    const double* c = src + j * n;
-    for (int64_t i = 0; i < n; ++i) s += c[i] * c[i];
-    d->norms[static_cast<size_t>(j)] = std::sqrt(s);
-  }
+  ck(cudaMemcpy(d->norms.data(), nrm.p, nrm.bytes, cudaMemcpyDeviceToHost), "atom norms download");
   return d;
 }
 
@@ -945,22 +955,14 @@ int fl1_dict_sukro(fl1_ctx* ctx, int32_t n_terms, int64_t m, int64_t q, const do
     d->left = upload(d->h_left);
     d->right = upload(d->h_right);
     if (col_scale) d->col_scale = upload(d->h_scale);
-    // atom norms from the explicit columns (host, setup only)
+    // exact atom norms of the explicit columns, expanded on the device (setup only)
+    DevBuf nrm(static_cast<size_t>(d->k) * sizeof(double));
+    ck(fl1::sukro_norms_launch(d->left->as<double>(), d->right->as<double>(),
+                               col_scale ? d->col_scale->as<double>() : nullptr, n_terms, m, q, nrm.as<double>(),
+                               nullptr),
+       "sukro atom norms");
     d->norms.resize(static_cast<size_t>(d->k));
-    for (int64_t j = 0; j < d->k; ++j) {
-      const int64_t jb = j / q, jc = j % q;
-      double s2 = 0.0;
-      for (int64_t rb = 0; rb < m; ++rb)
-        for (int64_t rc = 0; rc < m; ++rc) {
-          double v = 0.0;
-          for (int t = 0; t < n_terms; ++t)
-            v += d->h_left[blk * static_cast<size_t>(t) + static_cast<size_t>(jb * m + rb)] *
-                 d->h_right[blk * static_cast<size_t>(t) + static_cast<size_t>(jc * m + rc)];
-          if (col_scale) v *= d->h_scale[static_cast<size_t>(j)];
-          s2 += v * v;
-        }
-      d->norms[static_cast<size_t>(j)] = std::sqrt(s2);
-    }
+    ck(cudaMemcpy(d->norms.data(), nrm.p, nrm.bytes, cudaMemcpyDeviceToHost), "sukro atom norms download");
     *out = new fl1_dict{d};
   });
 }
@@ -1627,6 +1629,113 @@ int fl1_rng_normals(uint64_t seed, int64_t count, double* out) {
     std::mt19937_64 rng(seed);
     std::normal_distribution<double> gauss(0.0, 1.0);
     for (int64_t i = 0; i < count; ++i) out[i] = gauss(rng);
+  });
+}
+
+namespace {
+int64_t require_perfect_square(int64_t v, const char* what) {  // dictionary.cpp:19-33
+  auto r = static_cast<int64_t>(std::llround(std::sqrt(static_cast<double>(v))));
+  while (r * r > v) --r;
+  while ((r + 1) * (r + 1) <= v) ++r;
+  if (r * r != v) throw std::invalid_argument(std::string(what) + " must be a perfect square, got " + std::to_string(v));
+  return r;
+}
+}  // namespace
+
+// build_sukro_sequence (dictionary.cpp:281-357) with truncated_svd (253-279), on the
+// device (csrc/sukro_build.cu + the DMMA gemm_tn of batched.cu). The dense dictionary
+// never leaves HBM; only the Gaussian probes go up (the reference's mt19937_64 stream)
+// and the factors / per-level vectors come down.
+int fl1_build_sukro_sequence(fl1_dict* dh, const int32_t* ranks, int32_t n_ranks, double* left, double* right,
+                             double* eps, double* approx_norms, double* rc, double* op_err) {
+  return guard([&] {
+    if (!dh || (n_ranks > 0 && !ranks)) throw std::invalid_argument("null argument");
+    DictImpl& d = *dh->d;
+    if (d.kind != fl1::kDense) throw std::invalid_argument("build_sukro_sequence needs a dense dictionary");
+    const int64_t n = d.n, k = d.k;
+    const int64_t m = require_perfect_square(n, "N");
+    const int64_t q = require_perfect_square(k, "K");
+    if (n_ranks < 1) throw std::invalid_argument("need at least one rank");
+    for (int32_t i = 0; i < n_ranks; ++i)
+      if (ranks[i] < 1 || (i > 0 && ranks[i] <= ranks[i - 1]))
+        throw std::invalid_argument("ranks must be positive and strictly increasing");
+    const int T = ranks[n_ranks - 1];
+    const int64_t M = m * q;
+    if (T > M) throw std::invalid_argument("rank exceeds rearranged dimension");
+    if (!left || !right || !eps || !approx_norms || !rc || !op_err) throw std::invalid_argument("null argument");
+    const uint64_t dense_flops = static_cast<uint64_t>(n) * static_cast<uint64_t>(k);  // matvec_flops
+    for (int32_t i = 0; i < n_ranks; ++i) {
+      const uint64_t mv = static_cast<uint64_t>(ranks[i]) * static_cast<uint64_t>(m * k + q * n);
+      if (mv >= dense_flops)
+        throw std::invalid_argument("rank " + std::to_string(ranks[i]) + " gives relative complexity >= 1");
+      rc[i] = static_cast<double>(mv) / static_cast<double>(dense_flops);
+    }
+    const int p = static_cast<int>(std::min<int64_t>(T + 8, M));
+    if (p > fl1::sukro_max_probe())
+      throw std::invalid_argument("truncated_svd: rank + 8 probes exceed " + std::to_string(fl1::sukro_max_probe()) +
+                                  " (device construction limit)");
+    if (n_ranks > fl1::sukro_max_snapshots()) throw std::invalid_argument("too many ranks");
+    d.ctx->bind();
+    const int dev = d.ctx->device;
+    const int64_t ldr = (M + 1) / 2 * 2;
+    const size_t mat = static_cast<size_t>(ldr) * static_cast<size_t>(M), pan = static_cast<size_t>(ldr) * p;
+    DevBuf R(mat * 8), Rt(mat * 8), Om(pan * 8), Y(pan * 8), Z(pan * 8), Wk(pan * 8), Qm(pan * 8), Q2(pan * 8);
+    DevBuf Rf(64 * 64 * 8), R2(64 * 64 * 8), S(64 * 8), Wsv(64 * 64 * 8), Vsv(64 * 64 * 8);
+    const size_t work_elems = 16 * pan;
+    DevBuf work(work_elems * 8);
+    DevBuf L(static_cast<size_t>(T) * M * 8), Rr(static_cast<size_t>(T) * M * 8);
+    DevBuf E(static_cast<size_t>(n_ranks) * k * 8), Ap(static_cast<size_t>(n_ranks) * k * 8), rk(64 * 4);
+    cudaStream_t st = nullptr;
+    for (DevBuf* b : {&R, &Rt, &Om, &Y, &Z, &Wk, &Qm, &Q2}) ck(cudaMemsetAsync(b->p, 0, b->bytes, st), "memset");
+    {  // Omega (cols x p, column-major): the reference's stream, omega(i, j) in j-major order
+      std::vector<double> om(static_cast<size_t>(M) * p);
+      std::mt19937_64 rng(0x5eedf00dULL);
+      std::normal_distribution<double> gauss(0.0, 1.0);
+      for (auto& v : om) v = gauss(rng);
+      ck(cudaMemcpy2D(Om.p, ldr * 8, om.data(), M * 8, M * 8, p, cudaMemcpyHostToDevice), "probe upload");
+    }
+    ck(fl1::rearrange_launch(d.a->as<double>(), d.ld, m, q, R.as<double>(), Rt.as<double>(), ldr, st), "rearrange");
+    auto gemm = [&](const DevBuf& X, const DevBuf& Yop, DevBuf& C) {  // C = X^T Yop, all mq x . with ld ldr
+      ck(fl1::gemm_tn_launch(X.as<double>(), ldr, M, Yop.as<double>(), ldr, p, M, C.as<double>(), ldr,
+                             work.as<double>(), work_elems, dev, st),
+         "gemm_tn");
+    };
+    auto orth = [&](const DevBuf& Yin, DevBuf& Qout, DevBuf& Rout) {
+      ck(cudaMemcpy2DAsync(Wk.p, ldr * 8, Yin.p, ldr * 8, M * 8, p, cudaMemcpyDeviceToDevice, st), "panel copy");
+      ck(fl1::householder_qr_launch(Wk.as<double>(), M, p, ldr, Qout.as<double>(), ldr, Rout.as<double>(), st), "qr");
+    };
+    gemm(Rt, Om, Y);  // Y = R Omega
+    for (int it = 0; it < 6; ++it) {
+      orth(Y, Qm, Rf);
+      gemm(R, Qm, Z);  // Z = R^T Q
+      gemm(Rt, Z, Y);  // Y = R Z
+    }
+    orth(Y, Qm, Rf);
+    gemm(R, Qm, Z);    // bt = R^T Q (cols x p)
+    orth(Z, Q2, R2);   // bt = Q2 R2
+    ck(fl1::jacobi_svd_launch(R2.as<double>(), p, S.as<double>(), Wsv.as<double>(), Vsv.as<double>(), st), "svd");
+    // svd(bt): U = Q2 W, V = Vsv; u = Q V(:, :T), v = U(:, :T); terms scaled by sqrt(s_t)
+    ck(fl1::small_gemm_launch(Qm.as<double>(), ldr, M, p, Vsv.as<double>(), S.as<double>(), T, L.as<double>(), M, st),
+       "left factors");
+    ck(fl1::small_gemm_launch(Q2.as<double>(), ldr, M, p, Wsv.as<double>(), S.as<double>(), T, Rr.as<double>(), M, st),
+       "right factors");
+    ck(cudaMemcpyAsync(rk.p, ranks, sizeof(int32_t) * n_ranks, cudaMemcpyHostToDevice, st), "ranks");
+    ck(fl1::residual_norms_launch(d.a->as<double>(), d.ld, m, q, T, L.as<double>(), Rr.as<double>(), M,
+                                  rk.as<int>(), n_ranks, E.as<double>(), Ap.as<double>(), st),
+       "residual norms");
+    ck(cudaMemcpyAsync(left, L.p, L.bytes, cudaMemcpyDeviceToHost, st), "left download");
+    ck(cudaMemcpyAsync(right, Rr.p, Rr.bytes, cudaMemcpyDeviceToHost, st), "right download");
+    ck(cudaMemcpyAsync(eps, E.p, E.bytes, cudaMemcpyDeviceToHost, st), "eps download");
+    ck(cudaMemcpyAsync(approx_norms, Ap.p, Ap.bytes, cudaMemcpyDeviceToHost, st), "norms download");
+    ck(cudaStreamSynchronize(st), "sukro build");
+    // running max finer -> coarser (dictionary.cpp:344-349), operator_error_bound = max
+    for (int32_t i = n_ranks - 1; i > 0; --i)
+      for (int64_t j = 0; j < k; ++j) {
+        double& c = eps[static_cast<int64_t>(i - 1) * k + j];
+        c = std::max(c, eps[static_cast<int64_t>(i) * k + j]);
+      }
+    for (int32_t i = 0; i < n_ranks; ++i)
+      op_err[i] = *std::max_element(eps + static_cast<int64_t>(i) * k, eps + static_cast<int64_t>(i + 1) * k);
   });
 }
 

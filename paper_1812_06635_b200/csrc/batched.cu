@@ -30,6 +30,9 @@
 namespace cg = cooperative_groups;
 
 namespace fl1 {
+cudaError_t gemm_tn_launch(const double* X, int64_t ldx, int64_t nx, const double* Y, int64_t ldy, int64_t ny,
+                           int64_t kdim, double* C, int64_t ldc, double* work, size_t work_elems, int device,
+                           cudaStream_t stream);
 namespace {
 
 #ifndef FL1_PREFIX_THREADS
@@ -1080,17 +1083,28 @@ __global__ void __launch_bounds__(kPT, 1) prefix_kernel(const __grid_constant__ 
 
 
 // ---------------------------------------------------------------------------
-// Gram matrix G = A^T A (K x K, leading dimension ldg) of a dense dictionary for
-// the Gram-backed exact phase (RunOptions::exact_gram, bench.cpp:190-197): the
-// same DMMA tiles as the lockstep contraction, both operands columns of A.
-__global__ void __launch_bounds__(kPT, 1) gram_kernel(const double* __restrict__ a, int64_t ld, int64_t k,
-                                                      double* __restrict__ g, int64_t ldg) {
+// C = X^T Y on the fp64 tensor cores: X is kdim x nx (leading dimension ldx), Y is
+// kdim x ny (ldy), both column-major along the contraction with ldx, ldy even and zero
+// padding past kdim (16-byte cp.async pairs); C is nx x ny (ldc). The same DMMA tiles
+// as the lockstep contraction (128 x 64 outputs, 32-deep K chunks, cp.async double
+// buffer). parts > 1 splits the contraction: part kp covers chunks [kp nch / parts,
+// (kp + 1) nch / parts) and writes its partial tile to C + kp * pstride (summed in part
+// order by parts_sum_kernel: deterministic).
+// Users: the Gram matrix G = A^T A (RunOptions::exact_gram, bench.cpp:190-197; X = Y = A)
+// and the randomized range finder of build_sukro_sequence (dictionary.cpp:253-279).
+__global__ void __launch_bounds__(kPT, 1) gemm_tn_kernel(const double* __restrict__ X, int64_t ldx, int64_t nx,
+                                                         const double* __restrict__ Y, int64_t ldy, int64_t ny,
+                                                         int64_t kdim, int parts, double* __restrict__ C, int64_t ldc,
+                                                         int64_t pstride) {
   extern __shared__ __align__(16) double dsm[];
   const int w = threadIdx.x >> 5, l = threadIdx.x & 31, gi = l >> 2, tg = l & 3;
   const int wr = w % kWR, wc = w / kWR;
-  const int n_rt = static_cast<int>((k + kTM - 1) / kTM), n_ct = static_cast<int>((k + kTN - 1) / kTN);
-  const int nch = static_cast<int>((ld + kTK - 1) / kTK);
-  for (int tile = blockIdx.x; tile < n_rt * n_ct; tile += gridDim.x) {
+  const int n_rt = static_cast<int>((nx + kTM - 1) / kTM), n_ct = static_cast<int>((ny + kTN - 1) / kTN);
+  const int nch = static_cast<int>((kdim + kTK - 1) / kTK);
+  for (int item = blockIdx.x; item < n_rt * n_ct * parts; item += gridDim.x) {
+    const int tile = item % (n_rt * n_ct), kp = item / (n_rt * n_ct);
+    const int kc0 = static_cast<int>(static_cast<int64_t>(kp) * nch / parts);
+    const int kc1 = static_cast<int>(static_cast<int64_t>(kp + 1) * nch / parts);
     const int64_t j0 = static_cast<int64_t>(tile % n_rt) * kTM, c0 = static_cast<int64_t>(tile / n_rt) * kTN;
     double acc[kRT][kCT][2];
 #pragma unroll
@@ -1103,24 +1117,24 @@ __global__ void __launch_bounds__(kPT, 1) gram_kernel(const double* __restrict__
       const int64_t k0 = static_cast<int64_t>(kc) * kTK;
       for (int e = threadIdx.x; e < kTM * (kTK / 2); e += kPT) {
         const int r = e / (kTK / 2), kk = (e % (kTK / 2)) * 2;
-        const bool ok = j0 + r < k && k0 + kk < ld;
-        cp16(As + r * kSS + kk, ok ? a + (j0 + r) * ld + k0 + kk : a, ok);
+        const bool ok = j0 + r < nx && k0 + kk < kdim;
+        cp16(As + r * kSS + kk, ok ? X + (j0 + r) * ldx + k0 + kk : X, ok);
       }
       for (int e = threadIdx.x; e < kTN * (kTK / 2); e += kPT) {
         const int c = e / (kTK / 2), kk = (e % (kTK / 2)) * 2;
-        const bool ok = c0 + c < k && k0 + kk < ld;
-        cp16(Bs + c * kSS + kk, ok ? a + (c0 + c) * ld + k0 + kk : a, ok);
+        const bool ok = c0 + c < ny && k0 + kk < kdim;
+        cp16(Bs + c * kSS + kk, ok ? Y + (c0 + c) * ldy + k0 + kk : Y, ok);
       }
     };
     __syncthreads();
-    issue(0, 0);
+    if (kc0 < kc1) issue(0, kc0);
     cp_commit();
-    for (int kc = 0; kc < nch; ++kc) {
-      if (kc + 1 < nch) issue((kc + 1) & 1, kc + 1);
+    for (int kc = kc0; kc < kc1; ++kc) {
+      if (kc + 1 < kc1) issue((kc + 1 - kc0) & 1, kc + 1);
       cp_commit();
       cp_wait1();
       __syncthreads();
-      const double* As = dsm + (kc & 1) * kStage;
+      const double* As = dsm + ((kc - kc0) & 1) * kStage;
       const double* Bs = As + kTM * kSS;
 #pragma unroll
       for (int ks = 0; ks < kTK / 4; ++ks) {
@@ -1137,6 +1151,7 @@ __global__ void __launch_bounds__(kPT, 1) gram_kernel(const double* __restrict__
       __syncthreads();
     }
     cp_wait0();
+    double* out = C + static_cast<int64_t>(kp) * pstride;
 #pragma unroll
     for (int h = 0; h < kRT; ++h) {
       const int64_t i = j0 + (h * kWR + wr) * 8 + gi;
@@ -1145,9 +1160,21 @@ __global__ void __launch_bounds__(kPT, 1) gram_kernel(const double* __restrict__
 #pragma unroll
         for (int q = 0; q < 2; ++q) {
           const int64_t j = c0 + (wc * kCT + c) * 8 + 2 * tg + q;
-          if (i < k && j < k) g[j * ldg + i] = acc[h][c][q];
+          if (i < nx && j < ny) out[j * ldc + i] = acc[h][c][q];
         }
     }
+  }
+}
+
+// C(i, j) = sum over parts kp (in order) of P[kp * pstride + j * ldc + i]
+__global__ void parts_sum_kernel(const double* __restrict__ P, int parts, int64_t pstride, int64_t rows, int64_t cols,
+                                 int64_t ldc, double* __restrict__ C) {
+  for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < rows * cols;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t j = e / rows, i = e - j * rows;
+    double s = 0.0;
+    for (int kp = 0; kp < parts; ++kp) s += P[kp * pstride + j * ldc + i];
+    C[j * ldc + i] = s;
   }
 }
 
@@ -1174,14 +1201,44 @@ cudaError_t colnorm_launch(const double* g, int64_t k, int64_t ldg, double* out,
 
 cudaError_t gram_launch(const double* a, int64_t ld, int64_t k, double* g, int64_t ldg, int device,
                         cudaStream_t stream) {
+  return gemm_tn_launch(a, ld, k, a, ld, k, ld, g, ldg, nullptr, 0, device, stream);
+}
+
+// C = X^T Y (see gemm_tn_kernel). The contraction is split when the output has fewer
+// tiles than the device has SMs (tall-skinny products): parts from the fewest-waves rule,
+// each at least 4 chunks deep, partials in `work` (parts * ldc * ny doubles; without
+// enough work space the product is not split).
+cudaError_t gemm_tn_launch(const double* X, int64_t ldx, int64_t nx, const double* Y, int64_t ldy, int64_t ny,
+                           int64_t kdim, double* C, int64_t ldc, double* work, size_t work_elems, int device,
+                           cudaStream_t stream) {
   const size_t smem = static_cast<size_t>(2 * kStage) * sizeof(double);
-  cudaError_t e = cudaFuncSetAttribute(gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  cudaError_t e =
+      cudaFuncSetAttribute(gemm_tn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (e != cudaSuccess) return e;
   int sms = 0;
   e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
   if (e != cudaSuccess) return e;
-  const int64_t tiles = ((k + kTM - 1) / kTM) * ((k + kTN - 1) / kTN);
-  gram_kernel<<<static_cast<unsigned>(std::min<int64_t>(tiles, 4 * sms)), kPT, smem, stream>>>(a, ld, k, g, ldg);
+  const int64_t tiles = ((nx + kTM - 1) / kTM) * ((ny + kTN - 1) / kTN);
+  const int64_t nch = (kdim + kTK - 1) / kTK;
+  int parts = 1;
+  if (work && tiles < sms) {
+    parts = static_cast<int>(std::min<int64_t>({static_cast<int64_t>(kSplitMax), (sms + tiles - 1) / tiles,
+                                                std::max<int64_t>(1, nch / 4)}));
+    if (static_cast<size_t>(parts) * static_cast<size_t>(ldc) * static_cast<size_t>(ny) > work_elems) parts = 1;
+  }
+  const int64_t items = tiles * parts;
+  const unsigned grid = static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(items, 4 * sms)));
+  if (parts == 1) {
+    gemm_tn_kernel<<<grid, kPT, smem, stream>>>(X, ldx, nx, Y, ldy, ny, kdim, 1, C, ldc, 0);
+    return cudaGetLastError();
+  }
+  const int64_t pstride = ldc * ny;
+  gemm_tn_kernel<<<grid, kPT, smem, stream>>>(X, ldx, nx, Y, ldy, ny, kdim, parts, work, ldc, pstride);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  const int64_t n = nx * ny;
+  parts_sum_kernel<<<static_cast<unsigned>(std::min<int64_t>((n + 255) / 256, 4 * sms)), 256, 0, stream>>>(
+      work, parts, pstride, nx, ny, ldc, C);
   return cudaGetLastError();
 }
 

@@ -9,13 +9,13 @@ formats (so GPU sweeps drop into the reference's plotting and analysis tooling):
       run_single, write_trace_csv, write_summary_csv, write_percentiles_csv,
       percentile, emit_plot_data
   dictionary.cpp:37-45, 76-135, 253-434
-      rearrange, DenseDictionary CSV / blob I/O, truncated_svd,
-      build_sukro_sequence (on the GPU), synthesize_scenario
+      DenseDictionary CSV / blob I/O, build_sukro_sequence (the device
+      construction of fl1_build_sukro_sequence, csrc/sukro_build.cu), synthesize_scenario
 
 The random streams are the reference's own (std::mt19937_64 with libstdc++'s
 normal / bernoulli distributions, exported by libfl1cuda.so), so a config and seed
 give the reference's dictionaries and signals up to the rounding of the linear
-algebra (QR / SVD via LAPACK or cuSOLVER instead of Eigen).
+algebra (the device's Householder QR / Jacobi SVD instead of Eigen's).
 
 Every solve goes through fastl1.run_lasso on the GPU. With use_gram (the reference's
 default) the sweep builds the exact dictionary's Gram matrix once on the GPU and the
@@ -106,58 +106,6 @@ def synthesize_scenario(n: int, k: int, scenario: str, seed: int, backend: Optio
     return np.asfortranarray(a / norms[None, :])
 
 
-def rearrange(a, m: int, q: int):
-    """dictionary.cpp:37-45: R(i + j m, r + s m) = A(i m + r, j q + s), so that a
-    Kronecker term B (x) C of A is the rank-one vec(B) vec(C)^T of R. Works on numpy
-    arrays and torch tensors."""
-    # A[(i m + r), (j q + s)] column-major: element (row, col) -> A4[r, i, s, j] in F order
-    if isinstance(a, np.ndarray):
-        a4 = a.reshape(m, m, q, q, order="F")
-        return a4.transpose(1, 3, 0, 2).reshape(m * q, m * q, order="F")
-    import torch  # device path
-
-    # torch is row-major: build the column-major view explicitly
-    at = a.T.contiguous()  # (k x n) = column-major A
-    a4 = at.reshape(q, q, m, m)  # [j, s, i, r]  (col = j q + s, row = i m + r)
-    # R column index rr + s m over (s, rr), row index i + j m over (j, i): R^T[(s, r), (j, i)]
-    rt = a4.permute(1, 3, 0, 2).reshape(q * m, q * m)  # [s, r, j, i] -> (col of R) x (row of R)
-    return rt.T
-
-
-def truncated_svd(mat, rank: int, backend: Optional[F.Backend] = None):
-    """dictionary.cpp:253-279: randomized range finder (p = rank + 8 Gaussian probes
-    from mt19937_64(0x5eedf00d), six power iterations with Householder QR), then the
-    SVD of the small projected matrix. Returns (u, s, v), rank columns. Runs on the
-    GPU when mat is a torch tensor (cuBLAS GEMMs, cuSOLVER QR / SVD)."""
-    rows, cols = mat.shape
-    mindim = min(rows, cols)
-    if rank < 1 or rank > mindim:
-        raise F.InvalidArgument("truncated_svd: bad rank")
-    p = min(rank + 8, mindim)
-    omega = rng_normals(0x5EEDF00D, cols * p, backend).reshape(p, cols).T
-    if isinstance(mat, np.ndarray):
-        def orth(x):
-            return np.linalg.qr(x, mode="reduced")[0]
-
-        y = mat @ omega
-        for _ in range(6):
-            y = mat @ (mat.T @ orth(y))
-        qm = orth(y)
-        bt = mat.T @ qm
-        U, s, Vt = np.linalg.svd(bt, full_matrices=False)
-        return qm @ Vt.T[:, :rank], s[:rank], U[:, :rank]
-    import torch
-
-    om = torch.from_numpy(np.ascontiguousarray(omega)).to(mat.device)
-    y = mat @ om
-    for _ in range(6):
-        y = mat @ (mat.T @ torch.linalg.qr(y, mode="reduced")[0])
-    qm = torch.linalg.qr(y, mode="reduced")[0]
-    bt = mat.T @ qm
-    U, s, Vh = torch.linalg.svd(bt, full_matrices=False)
-    return qm @ Vh.T[:, :rank], s[:rank], U[:, :rank]
-
-
 @dataclasses.dataclass
 class SukroLevel:
     terms: list            # [(left m x q, right m x q)] numpy
@@ -168,12 +116,13 @@ class SukroLevel:
     exact_norms: np.ndarray
 
 
-def build_sukro_levels(a: np.ndarray, ranks: Sequence[int], device: Optional[str] = None,
-                       backend: Optional[F.Backend] = None) -> List[SukroLevel]:
-    """build_sukro_sequence (dictionary.cpp:281-357) on the GPU: the rearranged
-    dictionary, its randomized truncated SVD, the factors sqrt(s_t) u_t / v_t and, per
-    level, the exact per-atom residual norms of the running truncation (running max
-    finer -> coarser). Returns the SuKro levels; sukro_sequence() adds the exact one."""
+def build_sukro_levels(a: np.ndarray, ranks: Sequence[int], backend: Optional[F.Backend] = None,
+                       dense: Optional[F.LinearOp] = None) -> List[SukroLevel]:
+    """build_sukro_sequence (dictionary.cpp:281-357) on the GPU through the C-ABI
+    (fl1_build_sukro_sequence: rearrangement, randomized truncated SVD on the fp64
+    tensor cores with on-device Householder QR and Jacobi SVD, per-level residual norms
+    in one streaming pass, running max finer -> coarser). Returns the SuKro levels;
+    sukro_sequence() adds the exact one. `dense`: the dictionary already uploaded."""
     n, k = a.shape
     m, q = _isqrt(n, "N"), _isqrt(k, "K")
     ranks = [int(r) for r in ranks]
@@ -182,61 +131,42 @@ def build_sukro_levels(a: np.ndarray, ranks: Sequence[int], device: Optional[str
     for i, r in enumerate(ranks):
         if r < 1 or (i > 0 and r <= ranks[i - 1]):
             raise F.InvalidArgument("ranks must be positive and strictly increasing")
-    max_rank = ranks[-1]
-    if max_rank > m * q:
+    if ranks[-1] > m * q:
         raise F.InvalidArgument("rank exceeds rearranged dimension")
-    dense_flops = n * k
-    import torch
-
-    dev = device or ("cuda" if torch.cuda.is_available() else "cpu")
-    A = torch.from_numpy(np.asfortranarray(a).T.copy()).to(dev).T  # n x k view of the column-major data
-    R = rearrange(A, m, q)
-    u, s, v = truncated_svd(R, max_rank, backend)
-    terms = []
-    for t in range(max_rank):
-        sc = math.sqrt(max(float(s[t]), 0.0))
-        left = (u[:, t] * sc).reshape(q, m).T   # column-major m x q
-        right = (v[:, t] * sc).reshape(q, m).T
-        terms.append((left, right))
-    exact_norms = torch.linalg.norm(A, dim=0)
-    residual = A.clone()
-    levels = []
-    nxt = 0
-    for t in range(max_rank):
-        left, right = terms[t]
-        residual -= torch.kron(left, right)
-        if t + 1 == ranks[nxt]:
-            nt = ranks[nxt]
-            mv = nt * (m * k + q * n)  # SukroDictionary::matvec_flops (dictionary.cpp:179-185)
-            if mv >= dense_flops:
-                raise F.InvalidArgument(f"rank {nt} gives relative complexity >= 1")
-            levels.append(dict(nt=nt, eps=torch.linalg.norm(residual, dim=0),
-                               approx=torch.linalg.norm(A - residual, dim=0), rc=mv / dense_flops))
-            nxt += 1
-            if nxt == len(ranks):
-                break
-    for i in range(len(levels) - 1, 0, -1):  # running max (dictionary.cpp:344-349)
-        levels[i - 1]["eps"] = torch.maximum(levels[i - 1]["eps"], levels[i]["eps"])
-    host_terms = [(l.cpu().numpy().copy(order="F"), r.cpu().numpy().copy(order="F")) for l, r in terms]
-    en = exact_norms.cpu().numpy()
-    out = []
-    for lv in levels:
-        eps = lv["eps"].cpu().numpy()
-        out.append(SukroLevel(terms=host_terms[:lv["nt"]], eps=eps, op_err=float(eps.max()), rc=lv["rc"],
-                              approx_norms=lv["approx"].cpu().numpy(), exact_norms=en))
-    return out
+    d = dense if dense is not None else F.DenseDictionary(a, backend=backend)
+    lib = d.backend.lib
+    if not hasattr(lib, "build_sukro_sequence"):
+        raise RuntimeError("build_sukro_levels runs on the CUDA library (no CPU construction path)")
+    T, nr = ranks[-1], len(ranks)
+    left = np.empty((T, q, m))   # term t: m x q column-major = [t, j, i]
+    right = np.empty((T, q, m))
+    eps, app = np.empty((nr, k)), np.empty((nr, k))
+    rc, op = np.empty(nr), np.empty(nr)
+    rk = np.asarray(ranks, dtype=np.int32)
+    P = C.POINTER(C.c_double)
+    lib.check(lib.build_sukro_sequence(d._h, rk.ctypes.data_as(C.POINTER(C.c_int32)), nr, left.ctypes.data_as(P),
+                                       right.ctypes.data_as(P), eps.ctypes.data_as(P), app.ctypes.data_as(P),
+                                       rc.ctypes.data_as(P), op.ctypes.data_as(P)))
+    en = d.atom_norms2()
+    terms = [(np.asfortranarray(left[t].T), np.asfortranarray(right[t].T)) for t in range(T)]
+    return [SukroLevel(terms=terms[:nt], eps=eps[l].copy(), op_err=float(op[l]), rc=float(rc[l]),
+                       approx_norms=app[l].copy(), exact_norms=en) for l, nt in enumerate(ranks)]
 
 
 def sukro_sequence(a: np.ndarray, ranks: Sequence[int], backend: Optional[F.Backend] = None,
-                   rc_override: Optional[Sequence[float]] = None) -> F.ApproxSequence:
-    """ApproxSequence of build_sukro_sequence(A, ranks) + the exact dictionary."""
-    levels = build_sukro_levels(a, ranks, backend=backend)
+                   rc_override: Optional[Sequence[float]] = None,
+                   levels: Optional[Sequence[SukroLevel]] = None) -> F.ApproxSequence:
+    """ApproxSequence of build_sukro_sequence(A, ranks) + the exact dictionary. `levels`:
+    SuKro levels built earlier (e.g. one construction shared by several backends)."""
+    dense = F.DenseDictionary(a, backend=backend)
+    if levels is None:
+        levels = build_sukro_levels(a, ranks, dense=dense)
     dicts = []
     for i, lv in enumerate(levels):
         op = F.SukroDictionary(lv.terms, backend=backend)
         rc = rc_override[i] if rc_override is not None else lv.rc
         dicts.append(F.ApproxDictionary(op, lv.eps, lv.op_err, rc, lv.approx_norms, lv.exact_norms))
-    dicts.append(F.make_exact_approx(F.DenseDictionary(a, backend=backend)))
+    dicts.append(F.make_exact_approx(dense))
     return F.ApproxSequence(dicts)
 
 
@@ -371,7 +301,7 @@ class ExperimentConfig:  # bench.hpp:16-46
         if self.rc_override is not None and len(self.rc_override) != len(self.ranks):
             raise F.InvalidArgument("rc-override must list one value per rank")
 
-    def resolved_lambda_ratios(self) -> List[float]:  # bench.cpp:88-102
+    def resolved_lambda_ratios(self) -> List[float]:  # bench.cpp:87-106
         if self.lambda_ratios:
             return list(self.lambda_ratios)
         if self.lambda_grid == 1:
@@ -385,7 +315,7 @@ class ExperimentConfig:  # bench.hpp:16-46
         return self.gamma if self.gamma is not None else default_gamma(self.scenario)
 
 
-def load_config_json(path: str) -> ExperimentConfig:  # bench.cpp:108-139
+def load_config_json(path: str) -> ExperimentConfig:  # bench.cpp:108-140
     try:
         f = open(path)
     except OSError:
@@ -428,7 +358,7 @@ class Problem:
 
 
 def draw_signal(d: F.LinearOp, bernoulli_p: float, seed: int, trial: int):
-    """bench.cpp:141-166 on the GPU dictionary: returns (y, x_true)."""
+    """bench.cpp:142-167 on the GPU dictionary: returns (y, x_true)."""
     lib = d.backend.lib
     n, k = d.rows(), d.cols()
     y, x = np.empty(n), np.empty(k)
@@ -491,17 +421,18 @@ class SweepContext:
     gram: Optional[F.LinearOp] = None
 
 
-def build_context(config: ExperimentConfig, a: np.ndarray, backend: Optional[F.Backend] = None) -> SweepContext:
-    """bench.cpp:180-200: the approximation sequence, the per-level Lipschitz cache and
+def build_context(config: ExperimentConfig, a: np.ndarray, backend: Optional[F.Backend] = None,
+                  levels: Optional[Sequence[SukroLevel]] = None) -> SweepContext:
+    """bench.cpp:184-205: the approximation sequence, the per-level Lipschitz cache and
     (use_gram) the exact dictionary's Gram matrix, built once per sweep on the GPU."""
-    seq = sukro_sequence(a, config.ranks, backend=backend, rc_override=config.rc_override)
+    seq = sukro_sequence(a, config.ranks, backend=backend, rc_override=config.rc_override, levels=levels)
     full_l = [F.lipschitz_bound(d.op) for d in seq.dicts]
     gram = F.gram_matrix(seq.exact().op) if config.use_gram else None
     return SweepContext(seq.exact().op, seq, full_l, gram)
 
 
 def execute_run(config: ExperimentConfig, ctx: SweepContext, y: np.ndarray, lambda_ratio: float, trial: int,
-                variant: int, run_id: int) -> RunRecord:  # bench.cpp:202-236
+                variant: int, run_id: int) -> RunRecord:  # bench.cpp:207-242
     lmax = F.lambda_max(ctx.dense, y)
     sw = F.SwitchConfig(gamma_threshold=config.resolved_gamma(), screening_interval=config.screen_interval,
                         tolerance=config.tol, max_iterations=config.max_iter, precompute_aty=config.precompute_aty)
@@ -515,7 +446,7 @@ def execute_run(config: ExperimentConfig, ctx: SweepContext, y: np.ndarray, lamb
 
 
 def run_single(config: ExperimentConfig, lambda_ratio: float, trial: int, variant: int,
-               backend: Optional[F.Backend] = None) -> RunRecord:  # bench.cpp:240-249
+               backend: Optional[F.Backend] = None) -> RunRecord:  # bench.cpp:244-253
     config.validate()
     a = synthesize_scenario(config.n, config.k, config.scenario, config.seed, backend)
     ctx = build_context(config, a, backend)
@@ -523,8 +454,9 @@ def run_single(config: ExperimentConfig, lambda_ratio: float, trial: int, varian
     return execute_run(config, ctx, y, lambda_ratio, trial, variant, 0)
 
 
-def run_sweep(config: ExperimentConfig, backend: Optional[F.Backend] = None) -> SweepOutput:
-    """bench.cpp:251-334: plain / screened / fastl1 over the lambda grid and trials,
+def run_sweep(config: ExperimentConfig, backend: Optional[F.Backend] = None,
+              levels: Optional[Sequence[SukroLevel]] = None) -> SweepOutput:
+    """bench.cpp:255-340: plain / screened / fastl1 over the lambda grid and trials,
     one summary row per (lambda, trial), CSVs under config.out (empty: no files).
     Runs are issued in the reference's task order; the GPU runs them one at a time
     (each solve already uses the whole device), so config.jobs only bounds nothing."""
@@ -532,7 +464,7 @@ def run_sweep(config: ExperimentConfig, backend: Optional[F.Backend] = None) -> 
     ratios = config.resolved_lambda_ratios()
     t0 = time.perf_counter()
     a = synthesize_scenario(config.n, config.k, config.scenario, config.seed, backend)
-    ctx = build_context(config, a, backend)
+    ctx = build_context(config, a, backend, levels)
     build_ms = (time.perf_counter() - t0) * 1e3
     runs: List[RunRecord] = []
     run_id = 0
@@ -582,7 +514,7 @@ def _open_w(path: str):
         raise F.InvalidArgument(f"cannot open {path} for writing")
 
 
-def write_trace_csv(path: str, runs: Sequence[RunRecord]) -> None:  # bench.cpp:336-349
+def write_trace_csv(path: str, runs: Sequence[RunRecord]) -> None:  # bench.cpp:342-355
     with _open_w(path) as f:
         f.write("run_id,trial,lambda_ratio,variant,iter,dict_index,active_size,gap,gamma,flops_cum,wall_ms,x_nnz\n")
         for r in runs:
@@ -593,7 +525,7 @@ def write_trace_csv(path: str, runs: Sequence[RunRecord]) -> None:  # bench.cpp:
                         f"{int(row['x_nnz'])}\n")
 
 
-def write_summary_csv(path: str, rows: Sequence[SweepSummaryRow]) -> None:  # bench.cpp:351-370
+def write_summary_csv(path: str, rows: Sequence[SweepSummaryRow]) -> None:  # bench.cpp:357-376
     with _open_w(path) as f:
         f.write("trial,lambda_ratio,flops_plain,flops_screened,flops_fastl1,"
                 "time_plain_ms,time_screened_ms,time_fastl1_ms,"
@@ -617,7 +549,7 @@ def _ratio(a: int, b: int) -> float:  # C++ double division (inf / nan when b ==
     return float(a) / float(b)
 
 
-def percentile(values: Sequence[float], q: float) -> float:  # bench.cpp:372-380
+def percentile(values: Sequence[float], q: float) -> float:  # bench.cpp:378-386
     if len(values) == 0:
         return math.nan
     v = sorted(values)
@@ -627,7 +559,7 @@ def percentile(values: Sequence[float], q: float) -> float:  # bench.cpp:372-380
     return v[lo] * (1.0 - frac) + v[hi] * frac
 
 
-def write_percentiles_csv(path: str, rows: Sequence[SweepSummaryRow]) -> None:  # bench.cpp:382-414
+def write_percentiles_csv(path: str, rows: Sequence[SweepSummaryRow]) -> None:  # bench.cpp:388-421
     with _open_w(path) as f:
         f.write("lambda_ratio,metric,p25,median,p75\n")
         ratios = []
@@ -653,7 +585,7 @@ def write_percentiles_csv(path: str, rows: Sequence[SweepSummaryRow]) -> None:  
                         f"{_g(percentile(vals, 0.75))}\n")
 
 
-def emit_plot_data(trace_csv: str, out_dir: str) -> None:  # bench.cpp:416-461
+def emit_plot_data(trace_csv: str, out_dir: str) -> None:  # bench.cpp:423-461
     try:
         fin = open(trace_csv)
     except OSError:

@@ -3,7 +3,7 @@
 Follows, line by line:
   tests/helpers.hpp:35-89     random_matrix / random_vector / random_dictionary / random_instance
   tests/helpers.hpp:101-179   solve_oracle (FISTA + LDL^T support polishing + KKT check)
-  test_fastl1.cpp:206-225     square_instance / degenerate_sequence
+  test_fastl1.cpp:18-39     square_instance / degenerate_sequence
   dictionary.cpp:37-45, 253-357, 384-434
                               rearrange, truncated_svd, build_sukro_sequence, synthesize_scenario
 The mt19937_64 / std::normal_distribution streams come from the oracle library

@@ -20,7 +20,7 @@ def degenerate(backend, a):
     return F.ApproxSequence([F.make_exact_approx(F.DenseDictionary(a, backend=backend))])
 
 
-def test_plain_engine_reproduces_stepper(backend, oracle, refgen):  # test_fastl1.cpp:260-292
+def test_plain_engine_reproduces_stepper(backend, oracle, refgen):  # test_fastl1.cpp:72-104
     a, y, lmax = refgen.square_instance(36, 64, 5)
     seq = degenerate(backend, a)
     lam = 0.3 * lmax
@@ -46,7 +46,7 @@ def test_plain_engine_reproduces_stepper(backend, oracle, refgen):  # test_fastl
 
 
 @pytest.mark.parametrize("rule", [F.RULE_GAP, F.RULE_DYNAMIC])
-def test_degenerate_sequence_equals_screened(backend, refgen, rule):  # test_fastl1.cpp:294-325
+def test_degenerate_sequence_equals_screened(backend, refgen, rule):  # test_fastl1.cpp:106-137
     a, y, lmax = refgen.square_instance(36, 100, 7)
     seq = degenerate(backend, a)
     cfg = F.SwitchConfig(tolerance=1e-8, max_iterations=5000)
@@ -60,7 +60,7 @@ def test_degenerate_sequence_equals_screened(backend, refgen, rule):  # test_fas
 
 
 @pytest.mark.parametrize("trial", range(5))
-def test_multi_dict_matches_oracle_solution(backend, oracle, refgen, trial):  # test_fastl1.cpp:327-353
+def test_multi_dict_matches_oracle_solution(backend, oracle, refgen, trial):  # test_fastl1.cpp:139-165
     a, y, lmax = refgen.square_instance(36, 100, 40 + trial, support=2)
     levels = refgen.build_sukro_sequence(a, [1, 3])
     seq = make_sequence(F, backend, a, levels)
@@ -79,7 +79,7 @@ def test_multi_dict_matches_oracle_solution(backend, oracle, refgen, trial):  # 
 
 @pytest.mark.parametrize("solver", [F.SOLVER_ISTA, F.SOLVER_FISTA])
 @pytest.mark.parametrize("rule", [F.RULE_GAP, F.RULE_DYNAMIC])
-def test_trace_invariants(backend, refgen, solver, rule):  # test_fastl1.cpp:355-389
+def test_trace_invariants(backend, refgen, solver, rule):  # test_fastl1.cpp:167-201
     a, y, lmax = refgen.square_instance(64, 144, 77)
     seq = make_sequence(F, backend, a, refgen.build_sukro_sequence(a, [1, 2, 4]))
     cfg = F.SwitchConfig(tolerance=1e-7, gamma_threshold=0.4, max_iterations=100000)
@@ -96,7 +96,7 @@ def test_trace_invariants(backend, refgen, solver, rule):  # test_fastl1.cpp:355
 
 
 @pytest.mark.parametrize("variant", [F.VARIANT_PLAIN, F.VARIANT_SCREENED, F.VARIANT_MULTI_DICT])
-def test_ledger_audit(backend, refgen, variant):  # test_fastl1.cpp:391-405
+def test_ledger_audit(backend, refgen, variant):  # test_fastl1.cpp:203-217
     a, y, lmax = refgen.square_instance(49, 121, 91)
     seq = make_sequence(F, backend, a, refgen.build_sukro_sequence(a, [1, 3]))
     cfg = F.SwitchConfig(tolerance=1e-7, max_iterations=100000)
@@ -107,7 +107,7 @@ def test_ledger_audit(backend, refgen, variant):  # test_fastl1.cpp:391-405
     assert int(res.trace["flops_cum"][-1]) == res.total_flops
 
 
-def test_gamma_regression_kat(backend, refgen):  # test_fastl1.cpp:431-456
+def test_gamma_regression_kat(backend, refgen):  # test_fastl1.cpp:243-268
     a, y, lmax = refgen.square_instance(36, 100, 113, 4, "easy")
     seq = make_sequence(F, backend, a, refgen.build_sukro_sequence(a, [2]))
     cfg = F.SwitchConfig(gamma_threshold=0.5, tolerance=1e-10, max_iterations=100000)
@@ -119,7 +119,7 @@ def test_gamma_regression_kat(backend, refgen):  # test_fastl1.cpp:431-456
     assert g[-1] <= g[0]
 
 
-def test_iteration_cap(backend, refgen):  # test_fastl1.cpp:458-471
+def test_iteration_cap(backend, refgen):  # test_fastl1.cpp:270-283
     a, y, lmax = refgen.square_instance(36, 64, 131)
     res = F.run_lasso(degenerate(backend, a), y, 0.3 * lmax, F.SwitchConfig(tolerance=1e-14, max_iterations=5),
                       F.RunOptions(variant=F.VARIANT_SCREENED))
@@ -127,7 +127,7 @@ def test_iteration_cap(backend, refgen):  # test_fastl1.cpp:458-471
     assert np.isnan(res.final_gap)
 
 
-def test_immediate_convergence_at_lambda_max(backend, refgen):  # test_fastl1.cpp:494-508
+def test_immediate_convergence_at_lambda_max(backend, refgen):  # test_fastl1.cpp:306-320
     a, y, lmax = refgen.square_instance(36, 64, 171)
     res = F.run_lasso(degenerate(backend, a), y, lmax, F.SwitchConfig(tolerance=1e-10),
                       F.RunOptions(variant=F.VARIANT_SCREENED))
@@ -136,7 +136,7 @@ def test_immediate_convergence_at_lambda_max(backend, refgen):  # test_fastl1.cp
 
 
 @pytest.mark.parametrize("trial", range(3))
-def test_precompute_aty_dynamic_rule_safe(backend, refgen, trial):  # test_fastl1.cpp:510-538
+def test_precompute_aty_dynamic_rule_safe(backend, refgen, trial):  # test_fastl1.cpp:322-350
     a, y, lmax = refgen.square_instance(36, 100, 181 + trial)
     seq = make_sequence(F, backend, a, refgen.build_sukro_sequence(a, [1, 3]))
     lam = 0.3 * lmax
@@ -154,7 +154,7 @@ def test_precompute_aty_dynamic_rule_safe(backend, refgen, trial):  # test_fastl
     assert np.max(np.abs(res.x - sol.x)) <= 2.0 * np.sqrt(2.0 * cfg.tolerance)
 
 
-def test_screening_interval_nesting(backend, refgen):  # test_fastl1.cpp:540-559
+def test_screening_interval_nesting(backend, refgen):  # test_fastl1.cpp:352-371
     a, y, lmax = refgen.square_instance(36, 100, 191)
     seq = make_sequence(F, backend, a, refgen.build_sukro_sequence(a, [1, 3]))
     cfg = F.SwitchConfig(tolerance=1e-8, screening_interval=5, max_iterations=300000)

@@ -455,3 +455,32 @@ def test_batched_full_size_config5_all_signals(cuda, oracle16):
         oracle16.lib.set_threads(threads)
     for b in range(B):
         assert_parity(res[b], orc[b], a, Y[:, b], lams[b], case=f"+[signal_{b}]")
+
+
+@pytest.mark.parametrize("n,k", [(7, 13), (500, 2000), (2049, 300)])
+def test_device_ingestion_norms(cuda, oracle16, n, k):
+    """Dense dictionaries are ingested on the device (one H2D or D2D copy, atom norms by a
+    kernel in the restatement's sequential order, dictionary.cpp:59-64): the norms are
+    bit-identical to the oracle's for host and device input, and the two handles apply
+    identically."""
+    import torch
+
+    rng = np.random.default_rng(n + k)
+    a = np.asfortranarray(rng.standard_normal((n, k)))
+    dh = F.DenseDictionary(a, backend=cuda)
+    At = torch.from_numpy(np.ascontiguousarray(a.T)).cuda()
+    dd = F.DenseDictionaryDevice(At.data_ptr(), n, k, backend=cuda)
+    do = F.DenseDictionary(a, backend=oracle16)
+    assert np.array_equal(dh.atom_norms2(), do.atom_norms2())
+    assert np.array_equal(dd.atom_norms2(), do.atom_norms2())
+    r = rng.standard_normal(n)
+    assert np.array_equal(dh.apply_adjoint(r), dd.apply_adjoint(r))
+
+
+def test_sukro_norms_on_device(cuda, oracle16):
+    """SuKro exact atom norms (column-scaled Kronecker sums) expanded on the device match
+    the oracle's column-by-column norms."""
+    inst = syn.sukro_instance(seed=3, m=16, q=32, nnz=30)
+    sg, so = syn.sukro_sequence(inst, cuda), syn.sukro_sequence(inst, oracle16)
+    for lg, lo in zip(sg.dicts, so.dicts):
+        assert np.allclose(lg.op.atom_norms2(), lo.op.atom_norms2(), rtol=1e-15, atol=0)
