@@ -506,7 +506,10 @@ def run_path(args) -> None:
                 "d2h_bytes_per_step": int(sum(r.d2h_bytes for r in e2e_last))},
         "gpu_launches": int(launches),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": None, "peak_source": peak_src, "algorithmic_bytes_per_launch": alg / len(last),
+                     "traffic": ncu_traffic("c4"),
+                     "traffic_note": "ncu dram__bytes_read + write per launch, averaged over the 10 solve launches of "
+                                     "one path (profiles/r02_ncu_c4_path_launches.json: 0.98 of the algorithmic bytes)",
+                     "peak_source": peak_src, "algorithmic_bytes_per_launch": alg / len(last),
                      "kernel": "fl1::engine_kernel (one launch per lambda)",
                      "hot_pass": {"name": "fused A_S^T r + dual-scaling maxima", "achieved_GBps": hot_b / hot_ns,
                                   "frac": hot_b / hot_ns / peak, "bytes": hot_b, "ms": hot_ns / 1e6}},

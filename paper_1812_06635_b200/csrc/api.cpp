@@ -153,6 +153,7 @@ struct Workspace {
   int64_t units = 1;
   int64_t trace_cap = 0;
   std::unique_ptr<DevBuf> mem;
+  std::unique_ptr<DevBuf> cbuf;  // FL1_COMPACT copies (allocated on first use)
   cudaStream_t stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   EngineParams base{};  // pointers filled
@@ -407,6 +408,7 @@ size_t carve(EngineParams& p, char* base, int64_t n, int64_t k, int64_t ld, int 
     bk.atye = c.take<double>(kk);
     bk.lead = c.take<double>(kk);
     bk.keep = c.take<int8_t>(kk);
+    bk.cix = c.take<int32_t>(kk);
   }
   p.trace = c.take<fl1_trace_row>(std::max<int64_t>(trace_cap, 1));
   p.sw = c.take<fl1_switch_event>(fl1::kMaxLevels);
@@ -727,6 +729,21 @@ void do_solve(fl1_seq* s, const double* y, bool y_device, double lambda, const f
   EngineParams p = w.base;
   fill_params(p, pl, s, lambda, cfg, opts);
   p.trace_cap = cap;  // <= w.trace_cap (a cached workspace may be larger)
+  // FL1_COMPACT=1: physically compacted preserved columns (the A/B alternative to the
+  // index gather); two ping-pong copies of up to ceil(K/2) columns
+  static const bool compact = [] {
+    const char* e = std::getenv("FL1_COMPACT");
+    return e && e[0] == '1';
+  }();
+  bool any_dense = false;
+  for (const auto& l : s->lv) any_dense = any_dense || l->dict->kind == fl1::kDense;
+  if (compact && any_dense) {
+    const size_t half = static_cast<size_t>((k + 1) / 2) * static_cast<size_t>(w.ld);
+    if (!w.cbuf || w.cbuf->bytes < 2 * half * sizeof(double)) w.cbuf = std::make_unique<DevBuf>(2 * half * sizeof(double));
+    p.compact = 1;
+    p.cbuf[0] = w.cbuf->as<double>();
+    p.cbuf[1] = w.cbuf->as<double>() + half;
+  }
   std::unique_ptr<DevBuf> timeline;
   const char* tl_path = std::getenv("FL1_TIMELINE_OUT");  // instrumented builds only
   if (tl_path) {

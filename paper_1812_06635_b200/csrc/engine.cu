@@ -1254,6 +1254,44 @@ __device__ __noinline__ double power_iteration(const EngineParams& p, Sh& sh, co
   return estimate;
 }
 
+// Physical compaction (FL1_COMPACT=1, the A/B alternative to the index gather): the
+// column view the streaming passes (A_S^T r, power-iteration apply / adjoint) read --
+// the level's matrix through the global index, or the compact copy through cix.
+__device__ __forceinline__ DevLevel col_view(const EngineParams& p, const EngineState& s, const DevLevel& lv,
+                                             Bank& bk) {
+  DevLevel v = lv;
+  if (s.csel != 0) {
+    v.a = p.cbuf[s.csel - 1];
+    bk.idx = bk.cix;
+  }
+  return v;
+}
+
+// Copy the CTA's columns at new positions [o0, o1) into dst (column o at dst + o ld):
+// the source slot of position o is slot[o] in src; slot[o] becomes o. One warp per
+// column, four 16-byte loads in flight per lane.
+__device__ void copy_columns(const double* __restrict__ src, int32_t* slot, double* __restrict__ dst, int64_t o0,
+                             int64_t o1, int64_t ld) {
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  const int64_t n2 = ld >> 1;
+  for (int64_t o = o0 + w; o < o1; o += kWarps) {
+    const double2* s2 = reinterpret_cast<const double2*>(src + static_cast<int64_t>(slot[o]) * ld);
+    double2* d2 = reinterpret_cast<double2*>(dst + o * ld);
+    int64_t e = l;
+    for (; e + 96 < n2; e += 128) {
+      const double2 a = ldg_stream2(s2 + e), b = ldg_stream2(s2 + e + 32), c = ldg_stream2(s2 + e + 64),
+                    d = ldg_stream2(s2 + e + 96);
+      d2[e] = a;
+      d2[e + 32] = b;
+      d2[e + 64] = c;
+      d2[e + 96] = d;
+    }
+    for (; e < n2; e += 32) d2[e] = ldg_stream2(s2 + e);
+    __syncwarp();
+    if (l == 0) slot[o] = static_cast<int32_t>(o);
+  }
+}
+
 // ActiveOp::gather_metadata (189-201) for the CTA slice; per-CTA max eps to a slot.
 __device__ void gather_metadata(const EngineParams& p, Sh& sh, const DevLevel& lv, const Bank& bk, int64_t S) {
   int64_t lo, hi;
@@ -1698,6 +1736,19 @@ __device__ __noinline__ void setup_dictionary(const EngineParams& p, Sh& sh, boo
   Bank bk = p.bank[s.cur];
   if (!first) {  // ActiveOp::rebase (105-112)
     gather_metadata(p, sh, lv, bk, s.S);
+    // rebase drops the compact copy and re-runs maybe_compact on the new level (107-110)
+    const bool cp = p.compact && lv.kind == kDense && lv.rows == 0 && 2 * s.S <= p.k;
+    if (cp) {
+      int64_t lo, hi;
+      slice(s.S, lo, hi);
+      for (int64_t q = lo + threadIdx.x; q < hi; q += kThreads) bk.cix[q] = bk.idx[q];
+      __syncthreads();
+      copy_columns(lv.a, bk.cix, p.cbuf[0], lo, hi, p.ld);
+    }
+    if (threadIdx.x == 0) {
+      s.csel = cp ? 1 : 0;
+      s.cwidth = cp ? s.S : p.k;
+    }
     vsync();
     grid_reduce(p, sh, 0u, 1u << kSlMaxEps);
     if (threadIdx.x == 0) s.max_eps = s.S > 0 ? sh.res[kSlMaxEps] : 0.0;
@@ -1718,7 +1769,9 @@ __device__ __noinline__ void setup_dictionary(const EngineParams& p, Sh& sh, boo
   if (p.has_full_l && s.S == p.k) {
     if (threadIdx.x == 0) s.lipschitz = p.full_l[s.dict_index];
   } else {
-    const double sq = power_iteration(p, sh, lv, bk, s.S, s.lead_valid != 0, sc);
+    Bank cb = bk;
+    const DevLevel cv = col_view(p, s, lv, cb);
+    const double sq = power_iteration(p, sh, cv, cb, s.S, s.lead_valid != 0, sc);
     if (threadIdx.x == 0) {
       s.lead_valid = 1;
       s.lipschitz = fmax(sq, 1e-300) * 1.05;
@@ -1835,6 +1888,8 @@ __device__ __noinline__ void engine_body(const EngineParams& p, Sh& sh, double* 
     if (threadIdx.x == 0) {
       s.S = S0;
       s.cur = 0;
+      s.csel = 0;
+      s.cwidth = p.k;
     }
     __syncthreads();
     gather_metadata(p, sh, p.lv[s.dict_index], bk, S0);
@@ -1979,7 +2034,9 @@ __device__ __noinline__ void engine_body(const EngineParams& p, Sh& sh, double* 
     } else if (!exact_fit) {
       // corr = A_S^T rho_g fused with the dual-scaling maxima (414-418)
       PassOut po{p.corr, 1, sh.rho_norm, false, kSlMaxPlain, kSlMaxStable, nullptr};
-      op_adjoint(p, sh, lv, bk.idx, bk.eps, S, sc.vec, sc.rt, po);
+      Bank cb = bk;
+      const DevLevel cv = col_view(p, s, lv, cb);
+      op_adjoint(p, sh, cv, cb.idx, bk.eps, S, sc.vec, sc.rt, po);
     } else {
       // exact fit (428-449): corr = A^T 0 = 0, dual point along y
       for (int64_t q = lo + threadIdx.x; q < hi; q += kThreads) p.corr[q] = 0.0;
@@ -2307,6 +2364,10 @@ __device__ __noinline__ void engine_body(const EngineParams& p, Sh& sh, double* 
       const bool lead_ok = s.lead_valid != 0;
       const bool dyn = p.rule == FL1_RULE_DYNAMIC;
       const bool atye = s.atye_valid != 0;
+      // restrict_to_local copies the kept columns once compacted; maybe_compact copies
+      // them from the level's matrix at every halving of the compaction width (115-129, 176-187)
+      const bool cpy = p.compact && lv.kind == kDense && lv.rows == 0 && !gram &&
+                       (s.csel != 0 || 2 * S_new <= s.cwidth);
       int64_t out_base = sh.scan_base;
       double me = -DBL_MAX;
       const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
@@ -2333,9 +2394,20 @@ __device__ __noinline__ void engine_body(const EngineParams& p, Sh& sh, double* 
           if (dyn) nb.aty[off] = bk.aty[q];
           if (atye) nb.atye[off] = bk.atye[q];
           if (lead_ok) nb.lead[off] = bk.lead[q];
+          if (cpy) nb.cix[off] = s.csel != 0 ? bk.cix[q] : bk.idx[q];
           me = fmax(me, bk.eps[q]);
         }
         out_base += tot;
+        __syncthreads();
+      }
+      if (cpy) {
+        copy_columns(s.csel != 0 ? p.cbuf[s.csel - 1] : lv.a, nb.cix, p.cbuf[s.csel == 1 ? 1 : 0], sh.scan_base,
+                     out_base, p.ld);
+        __syncthreads();
+        if (threadIdx.x == 0) {
+          if (2 * S_new <= s.cwidth) s.cwidth = S_new;
+          s.csel = s.csel == 1 ? 2 : 1;
+        }
         __syncthreads();
       }
       double v[1] = {me};
@@ -2380,7 +2452,9 @@ __device__ __noinline__ void engine_body(const EngineParams& p, Sh& sh, double* 
     }
     // Lipschitz refresh after a halving (603-608)
     if (s.S * 2 <= s.active_at_last_l && s.S > 0 && sh.next_dict == s.dict_index) {
-      const double sq = power_iteration(p, sh, lv, p.bank[s.cur], s.S, s.lead_valid != 0, sc);
+      Bank cb = p.bank[s.cur];
+      const DevLevel cv = col_view(p, s, lv, cb);
+      const double sq = power_iteration(p, sh, cv, cb, s.S, s.lead_valid != 0, sc);
       if (threadIdx.x == 0) {
         s.lead_valid = 1;
         s.lipschitz = fmax(sq, 1e-300) * 1.05;

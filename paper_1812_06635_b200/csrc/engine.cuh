@@ -59,6 +59,7 @@ struct Bank {
   double* atye;   // A^T y (precompute_aty variant)
   double* lead;   // power-iteration leading vector
   int8_t* keep;   // screening decision of the last pass
+  int32_t* cix;   // column slot in the physically compacted copy (EngineState::csel != 0)
 };
 
 enum Mode : int32_t { kModeSolve = 0, kModeResume = 1, kModePower = 2, kModeApply = 3, kModeAdjoint = 4 };
@@ -121,6 +122,12 @@ struct EngineState {
   double prof_full_ns;     // A-phase time of full-dictionary passes (|S| = K)
   double prof_full_bytes;
   double prof_pw[4];  // power-iteration sub-phases: apply, combine, adjoint+norms, reduce
+  // physical compaction (FL1_COMPACT, ActiveOp::maybe_compact / restrict_to_local,
+  // fastl1.cpp:115-129, 176-187): 0 = the streaming passes gather columns of the level's
+  // matrix by index; 1 / 2 = they read the compact copy in EngineParams::cbuf[csel - 1]
+  int64_t cwidth;  // compaction_width_
+  int32_t csel;
+  int32_t cpad_;
 };
 
 struct EngineParams;
@@ -280,6 +287,8 @@ struct alignas(16) EngineParams {
   int32_t list_apply;  // 1: dense u = A x from the lists in phase E (FL1_LIST_APPLY)
   int32_t power_onchip;  // 1: cluster-mode power iterations on chip when they fit (FL1_POWER_ONCHIP)
   int32_t early_prox;    // 1: non-screening dense iterations run the prox before the first barrier (FL1_EARLY_PROX)
+  int32_t compact;       // 1: preserved columns physically compacted into cbuf (FL1_COMPACT, A/B switch)
+  double* cbuf[2];       // ping-pong compact copies, ld x ceil(K/2) each
   double* pv;       // K
   double* pw;       // K
   double* PU;       // ld: power-iteration A v (combined)

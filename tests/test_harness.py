@@ -277,7 +277,7 @@ def test_sukro_construction_on_gpu_matches_restatement(cuda, oracle, n, k, scena
 
 
 @pytest.mark.gpu
-def test_sweep_csvs_match_oracle(cuda, oracle, tmp_path):
+def test_sweep_csvs_match_oracle(cuda, oracle, tmp_path, monkeypatch):
     """one ExperimentConfig swept on the CUDA library and on the oracle (the
     same SuKro levels, built once on the device, feed both): trace / summary / percentile
     CSVs are identical in every integer and string column (iterations, dictionary index,
@@ -289,6 +289,15 @@ def test_sweep_csvs_match_oracle(cuda, oracle, tmp_path):
     cfg.lambda_ratios = [0.3, 0.6]
     a = H.synthesize_scenario(cfg.n, cfg.k, cfg.scenario, cfg.seed)
     levels = H.build_sukro_levels(a, cfg.ranks, backend=cuda)
+    drawn = {}
+    draw = H.draw_signal
+
+    def draw_once(d, p, seed, trial):  # the signals of the CUDA sweep feed the oracle sweep too
+        if trial not in drawn:
+            drawn[trial] = draw(d, p, seed, trial)
+        return drawn[trial]
+
+    monkeypatch.setattr(H, "draw_signal", draw_once)
     H.run_sweep(cfg, backend=cuda, levels=levels)
     cfg_o = small_config(tmp_path / "orc")
     cfg_o.lambda_ratios = [0.3, 0.6]

@@ -28,15 +28,22 @@ import sys, numpy as np
 sys.path.insert(0, sys.argv[1])
 from paper_1812_06635_b200 import fastl1 as F, synthetic as syn
 name, out = sys.argv[2], sys.argv[3]
-inst = syn.dense_instance(name, seed=int(sys.argv[4]), n=int(sys.argv[5]), k=int(sys.argv[6]), nnz=int(sys.argv[7]))
-d = F.DenseDictionary(inst.a)
-L = F.lipschitz_bound(d)
-seq = F.ApproxSequence([F.make_exact_approx(d)])
-cfg = F.SwitchConfig(screening_interval=10, max_iterations=5000, rel_tolerance=1e-6)
-r = F.run_lasso(seq, inst.y, inst.lam, cfg, F.RunOptions(variant=F.VARIANT_SCREENED, full_lipschitz=[L],
-                                                          collect_trace=True))
+if name == "sukro":
+    inst = syn.sukro_instance(seed=int(sys.argv[4]), m=16, q=32, nnz=int(sys.argv[7]))
+    seq = syn.sukro_sequence(inst)
+    L = 0.0
+    cfg = F.SwitchConfig(screening_interval=10, max_iterations=5000, rel_tolerance=1e-6, gamma_threshold=0.5)
+    r = F.run_lasso(seq, inst.y, inst.lam, cfg, F.RunOptions(collect_trace=True))
+else:
+    inst = syn.dense_instance(name, seed=int(sys.argv[4]), n=int(sys.argv[5]), k=int(sys.argv[6]), nnz=int(sys.argv[7]))
+    d = F.DenseDictionary(inst.a)
+    L = F.lipschitz_bound(d)
+    seq = F.ApproxSequence([F.make_exact_approx(d)])
+    cfg = F.SwitchConfig(screening_interval=10, max_iterations=5000, rel_tolerance=1e-6)
+    r = F.run_lasso(seq, inst.y, inst.lam, cfg, F.RunOptions(variant=F.VARIANT_SCREENED, full_lipschitz=[L],
+                                                              collect_trace=True))
 np.savez(out, x=r.x, it=r.iterations, conv=r.converged, gap=r.final_gap, flops=r.total_flops,
-         active=r.final_active, L=L, **{"t_" + k: r.trace[k] for k in r.trace.dtype.names})
+         active=r.final_active, L=L, sw=r.switches, **{"t_" + k: r.trace[k] for k in r.trace.dtype.names})
 """
 
 # (switch, value): each one selects a different code path than the default
@@ -48,11 +55,13 @@ SWITCHES = [
     ("FL1_SINGLE_CLUSTER", "0"),   # small dictionaries on the full grid
     ("FL1_POWER_ONCHIP", "0"),     # cluster-mode power iterations streamed, not resident
     ("FL1_SINGLE_CLUSTER_SIZE", "16"),  # the single-cluster route on 16 CTAs (default 12 up to 8 MiB)
+    ("FL1_COMPACT", "1"),          # preserved columns physically compacted (ActiveOp::maybe_compact)
 ]
 
 CASES = {  # name, seed, n, k, nnz: c1 (single-cluster route) and a full-grid dense solve
     "small": ("c1", 1, 500, 2000, 50),
     "grid": ("c2", 2, 1500, 6000, 150),
+    "sukro": ("sukro", 3, 256, 1024, 30),
 }
 
 
@@ -73,15 +82,26 @@ class _Res:  # the fields assert_parity reads
         self.final_gap = float(z["gap"])
         self.total_flops = int(z["flops"])
         self.final_active = z["active"]
-        self.switches = np.zeros(0, dtype=F.SWITCH_DTYPE)  # single-level sequences never switch
+        self.switches = z["sw"]
         names = [k[2:] for k in z.files if k.startswith("t_")]
         self.trace = {k: z["t_" + k] for k in names}
 
 
-@pytest.mark.parametrize("case", sorted(CASES))
-@pytest.mark.parametrize("switch,value", SWITCHES)
+# the SuKro case covers the compaction's rebase path (the other switches are dense-only)
+PARAMS = [(c, sw, v) for c in sorted(CASES) for sw, v in SWITCHES if c != "sukro" or sw == "FL1_COMPACT"]
+
+
+@pytest.mark.parametrize("case,switch,value", PARAMS)
 def test_switch_matches_oracle(tmp_path, oracle, case, switch, value):
     name, seed, n, k, nnz = CASES[case]
+    if name == "sukro":  # multi-level: the switch to the exact level rebases (and compacts) the column view
+        inst = syn.sukro_instance(seed=seed, m=16, q=32, nnz=nnz)
+        g = _Res(child_solve(tmp_path, case, {switch: value}))
+        cfg = F.SwitchConfig(screening_interval=10, max_iterations=5000, rel_tolerance=1e-6, gamma_threshold=0.5)
+        o = F.run_lasso(syn.sukro_sequence(inst, oracle), inst.y, inst.lam, cfg, F.RunOptions(collect_trace=True))
+        assert g.switches.size >= 1
+        assert_parity(g, o, inst.a, inst.y, inst.lam)
+        return
     inst = syn.dense_instance(name, seed=seed, n=n, k=k, nnz=nnz)
     z = child_solve(tmp_path, case, {switch: value})
     g = _Res(z)
