@@ -618,10 +618,17 @@ def run_batched(args) -> None:
         if dist:
             dist.destroy_process_group()
         return
-    # C5 FLOPs_t = 2 N K B_active per iteration (the dense masked A^T R)
+    # C5 FLOPs_t = 2 N K B_active per step of the dense masked contraction.
+    # Dominant kernel = the lockstep launch (prefix_kernel): per step it runs A^T R over all
+    # B_active unfinished signals and W = A V over the signals in a power step, both dense
+    # masked (2 N K flops per column); widths summed by the kernel itself, launch time by a
+    # CUDA event at its end (profile of signal 0, include/fl1cuda.h).
+    pr = last[0].profile
+    lk_ms, w_act, w_pow, lk_steps = float(pr[0]), float(pr[1]), float(pr[2]), int(pr[3])
+    lk_flops = 2.0 * n * k * (w_act + w_pow)
     flops = 2.0 * n * k * float(sum(r.iterations for r in last))
     peak_t, peak_src_t = _fp64_peak()
-    achieved = flops / per_batch / 1e12
+    achieved = lk_flops / (lk_ms / 1e3) / 1e12 if lk_ms > 0 else 0.0
     cpu = None if args.no_cpu_baseline else cpu_baseline_batched(a, Y, lams, L)
     line = {
         "metric": METRIC, "value": per_batch, "unit": "s", "n_gpus": world, "steps": args.steps,
@@ -642,10 +649,16 @@ def run_batched(args) -> None:
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak_t, "unit": "TFLOP/s",
                      "frac": achieved / peak_t, "traffic": ncu_traffic("c5"),
                      "traffic_note": "DRAM bytes of the lockstep launch (prefix_kernel)", "peak_source": peak_src_t,
-                     "algorithmic_flops_per_launch": flops,
-                     "kernel": "fl1::prefix_kernel (lockstep batched engine, DMMA m8n8k4) + fl1::engine_kernel",
-                     "note": "algorithmic FLOPs = 2 N K per signal-iteration (SURVEY 8d); the lockstep also runs "
-                             "the restricted power iterations as contractions, not counted"},
+                     "algorithmic_flops_per_launch": lk_flops,
+                     "kernel": "fl1::prefix_kernel (lockstep batched engine: DMMA m8n8k4 contractions)",
+                     "launch_ms": lk_ms, "lockstep_steps": lk_steps,
+                     "note": "algorithmic FLOPs of the lockstep launch = 2 N K x (sum over steps of the A^T R width "
+                             "B_active + the A V width of the power-step signals), SURVEY 8(d)'s dense masked "
+                             "contraction unit; launch time = CUDA event at the end of the lockstep launch",
+                     "whole_batch": {"flops": flops, "TFLOPs": flops / per_batch / 1e12,
+                                     "frac": flops / per_batch / 1e12 / peak_t,
+                                     "note": "2 N K per signal-iteration over the whole batched call (lockstep + "
+                                             "per-signal cluster engines); power steps not counted"}},
         "clocks": clk.summary(),
         "cpu_baseline": cpu,
     }

@@ -221,7 +221,10 @@ int fl1_result_final_active(const fl1_result* r, int32_t* out);
  * [5] bytes streamed by the A^T r passes, [6] bytes streamed by the sparse applies
  * (8 N nnz), [7] bytes streamed by power iterations (16 N |S| per step), [8..11] power-iteration
  * sub-phases (apply, combine, adjoint + norms, reduce; ns), [12] ns and [13] bytes of the
- * A^T r passes over the full dictionary (|S| = K). out has 14 entries. */
+ * A^T r passes over the full dictionary (|S| = K). out has 14 entries. Signal 0 of a
+ * batched call that ran the lockstep engine: [0] device ms from the batch start to the end
+ * of the lockstep launch, [1] sum over lockstep steps of the unfinished signals (A^T R
+ * widths), [2] the same for the power-step signals (A V widths), [3] lockstep steps. */
 int fl1_result_profile(const fl1_result* r, double* out);
 /* Bulk accessors for batched results (one call instead of one per result): infos
  * (count), x (count x K), profiles (count x 14), and the traces / switch events /

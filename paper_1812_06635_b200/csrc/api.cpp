@@ -207,7 +207,7 @@ struct fl1_ctx {
   std::mutex batch_mu;
   std::unique_ptr<DevBuf> batch_buf[3];
   cudaStream_t batch_stream = nullptr;
-  cudaEvent_t batch_ev[2] = {nullptr, nullptr};
+  cudaEvent_t batch_ev[3] = {nullptr, nullptr, nullptr};
   void* batch_pinned = nullptr;
   size_t batch_pinned_bytes = 0;
   void* trace_pinned = nullptr;  // packed trace rows of a batched call
@@ -1167,7 +1167,7 @@ void solve_clusters(fl1_seq* s, const double* Y, bool y_device, int64_t ldy, con
   char* base = ctx->batch_scratch(0, top + 256).as<char>();
   ctx->batch_objects();
   cudaStream_t stream = ctx->batch_stream;
-  cudaEvent_t ev0 = ctx->batch_ev[0], ev1 = ctx->batch_ev[1];
+  cudaEvent_t ev0 = ctx->batch_ev[0], ev1 = ctx->batch_ev[1], evp = ctx->batch_ev[2];
   // pinned host image of [params .. offsets] (+ y), then the final sets
   const size_t img = down_end - o_params;
   const size_t ybytes = y_device ? 0 : sizeof(double) * static_cast<size_t>(ld) * ub;
@@ -1257,7 +1257,7 @@ void solve_clusters(fl1_seq* s, const double* Y, bool y_device, int64_t ldy, con
     const size_t q_np = preg(sizeof(double) * static_cast<size_t>(ld * bcap) * sm);
     const size_t q_c = preg(sizeof(double) * static_cast<size_t>(k * bcap) * sm);
     const size_t q_s = preg(sizeof(fl1::PrefixSig) * ub), q_h = preg(sizeof(fl1::Handoff) * ub);
-    const size_t q_n = preg(sizeof(int32_t) * 4);  // steps, two signal-queue counters
+    const size_t q_n = preg(sizeof(int64_t) * 4);  // steps, two signal-queue counters | work: sum n_act, sum n_pow
     (void)kt;
     char* pb = ctx->batch_scratch(1, ptop + 256).as<char>();
     pp.n = n;
@@ -1286,6 +1286,8 @@ void solve_clusters(fl1_seq* s, const double* Y, bool y_device, int64_t ldy, con
     if (const char* pol = std::getenv("FL1_LOCKSTEP_POLICY")) pp.policy = std::atoi(pol);
     const char* smode = std::getenv("FL1_SPLIT_MODE");
     pp.split_mode = smode ? std::atoi(smode) : 1;
+    const char* nm = std::getenv("FL1_LOCKSTEP_NARROW");
+    pp.narrow = nm ? std::atoi(nm) : 1;
     pp.X3[0] = reinterpret_cast<double*>(pb + q_x0);
     pp.X3[1] = reinterpret_cast<double*>(pb + q_x1);
     pp.X3[2] = reinterpret_cast<double*>(pb + q_x2);
@@ -1310,6 +1312,7 @@ void solve_clusters(fl1_seq* s, const double* Y, bool y_device, int64_t ldy, con
     pp.trace_cap = cap;
     pp.steps_out = reinterpret_cast<int32_t*>(pb + q_n);
     pp.queue = pp.steps_out + 1;
+    pp.work_out = reinterpret_cast<int64_t*>(pb + q_n) + 2;
     if (std::getenv("FL1_STEP_LOG")) {  // diagnostics: per-step occupancy of the lockstep engine
       pp.max_log = 4096;
       step_log = std::make_unique<DevBuf>(sizeof(double) * 5 * pp.max_log);
@@ -1321,6 +1324,7 @@ void solve_clusters(fl1_seq* s, const double* Y, bool y_device, int64_t ldy, con
   *reinterpret_cast<fl1::BatchDesc*>(at(o_desc)) = bd;
   ck(cudaMemcpyAsync(base + o_params, pin, up_end - o_params, cudaMemcpyHostToDevice, stream), "upload");
   if (use_prefix) ck(fl1::prefix_launch(pp, ctx->device, stream), "prefix launch");
+  ck(cudaEventRecord(evp, stream), "event");
   if (batch > 0) ck(fl1::engine_launch_clusters(p0, n_clusters, csize, pl.sk_m, stream), "cluster launch");
   ck(cudaEventRecord(ev1, stream), "event");
   ck(cudaMemcpyAsync(at(o_st), base + o_st, down_end - o_st, cudaMemcpyDeviceToHost, stream), "state download");
@@ -1375,8 +1379,15 @@ void solve_clusters(fl1_seq* s, const double* Y, bool y_device, int64_t ldy, con
   }
   ck(cudaStreamSynchronize(stream), "download sync");
   hlog("downloaded");
-  float batch_ms = 0.f;
+  float batch_ms = 0.f, lockstep_ms = 0.f;
   ck(cudaEventElapsedTime(&batch_ms, ev0, ev1), "elapsed");
+  ck(cudaEventElapsedTime(&lockstep_ms, ev0, evp), "elapsed");
+  int32_t lk_steps = 0;
+  int64_t lk_work[2] = {0, 0};
+  if (use_prefix) {  // lockstep accounting (signal 0's profile): steps and contraction widths
+    ck(cudaMemcpy(&lk_steps, d_steps, sizeof(lk_steps), cudaMemcpyDeviceToHost), "steps");
+    ck(cudaMemcpy(lk_work, pp.work_out, sizeof(lk_work), cudaMemcpyDeviceToHost), "work");
+  }
   if (step_log && d_steps) {
     int32_t steps = 0;
     ck(cudaMemcpy(&steps, d_steps, sizeof(steps), cudaMemcpyDeviceToHost), "steps");
@@ -1404,6 +1415,12 @@ void solve_clusters(fl1_seq* s, const double* Y, bool y_device, int64_t ldy, con
     res->batch_ms = batch_ms;
     res->launches = 0;  // one launch for the whole batch (fl1_result_info.kernel_launches of signal 0 = 1)
     if (b == 0) res->launches = (use_prefix ? 2 : 1) + (packed_launch ? 1 : 0);  // + the trace packing kernel
+    if (b == 0 && use_prefix) {  // fl1_result_profile of signal 0 of a batched call (include/fl1cuda.h)
+      res->prof[0] = lockstep_ms;
+      res->prof[1] = static_cast<double>(lk_work[0]);
+      res->prof[2] = static_cast<double>(lk_work[1]);
+      res->prof[3] = static_cast<double>(lk_steps);
+    }
     res->h2d = h2d_sig;
     res->d2h = static_cast<int64_t>(sizeof(EngineState)) + 12 * st.S +
                st.n_switches * static_cast<int64_t>(sizeof(fl1_switch_event)) +

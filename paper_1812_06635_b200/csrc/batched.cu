@@ -954,6 +954,115 @@ __device__ __noinline__ void fista_step(const PrefixParams& p, PSh& sh, int64_t 
   }
 }
 
+// ---------------------------------------------------------------------------
+// Narrow steps (few unfinished signals: the lockstep's tail, where most signals have
+// left and the rest are in their cold power iterations). A 128 x 64 DMMA tile would be
+// 1-12 signals wide and the contraction latency-bound (~30 us each at any width), so
+// the two products run on the CUDA cores instead, each reading A once from L2:
+//   Corr = A^T R: one warp per atom, the n residual columns staged in shared memory,
+//                 n warp-shuffle dot products per atom (written as split part 0);
+//   W = A V:      CTA (g, r) sums the atoms of column group g (kNarrowParts groups) for
+//                 the rows of slice r (128 rows), four column subsets per row combined in
+//                 shared memory in fixed order; the group partials are summed in group
+//                 order by the combine (deterministic).
+constexpr int kNarrow = 12;        // widest narrow step (R columns staged in shared memory)
+constexpr int kNarrowParts = 16;   // column groups of W = A V
+constexpr int kNarrowRows = 128;   // rows per CTA of W = A V (kPT / 4 threads per subset)
+
+__device__ __forceinline__ bool narrow_fits(int n, int64_t ld) {
+  return n <= kNarrow && static_cast<int64_t>(n) * ld <= static_cast<int64_t>(kStages) * kStage;
+}
+
+__device__ __noinline__ void narrow_corr(const PrefixParams& p, int n_act, const int32_t* act, double* stage) {
+  const int64_t K = p.k, ld = p.ld;
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  for (int64_t e = threadIdx.x; e < static_cast<int64_t>(n_act) * ld; e += kPT) {
+    const int64_t a = e / ld, i = e - a * ld;
+    stage[e] = __ldcg(p.R + static_cast<int64_t>(act[a]) * ld + i);
+  }
+  __syncthreads();
+  const int64_t gw = static_cast<int64_t>(blockIdx.x) * kPW + w, nw = static_cast<int64_t>(gridDim.x) * kPW;
+  for (int64_t j = gw; j < K; j += nw) {
+    double acc[kNarrow];
+#pragma unroll
+    for (int a = 0; a < kNarrow; ++a) acc[a] = 0.0;
+    const double2* col = reinterpret_cast<const double2*>(p.a + j * ld);
+    const int64_t n2 = ld >> 1;
+    for (int64_t e0 = l; e0 < n2; e0 += 128) {
+      double2 v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v[u] = e0 + 32 * u < n2 ? __ldg(col + e0 + 32 * u) : make_double2(0.0, 0.0);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int64_t i = 2 * (e0 + 32 * u);
+        if (i < ld) {
+#pragma unroll
+          for (int a = 0; a < kNarrow; ++a)
+            if (a < n_act) {
+              const double2 r = *reinterpret_cast<const double2*>(stage + a * ld + i);
+              acc[a] = fma(v[u].x, r.x, fma(v[u].y, r.y, acc[a]));
+            }
+        }
+      }
+    }
+#pragma unroll
+    for (int a = 0; a < kNarrow; ++a) {
+      if (a < n_act) {
+        double t = acc[a];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(kAll, t, o);
+        if (l == 0) __stcg(p.corr + static_cast<int64_t>(a) * K + j, t);
+      }
+    }
+  }
+  __syncthreads();  // the staging area is reused by the per-signal steps
+}
+
+// W partial of column group g = item % kNarrowParts, row slice r = item / kNarrowParts,
+// into np[(g * n_pow + c) * ld + i]
+__device__ __noinline__ void narrow_w(const PrefixParams& p, int n_pow, const int32_t* pact, const int32_t* act,
+                                      double* stage) {
+  const int64_t K = p.k, ld = p.ld;
+  const int n_slices = static_cast<int>((ld + kNarrowRows - 1) / kNarrowRows);
+  const int64_t gk = (K + kNarrowParts - 1) / kNarrowParts;
+  double* Vs = stage;                                              // [gk][n_pow]
+  double* Red = stage + gk * kNarrow;                              // [4][kNarrowRows][n_pow]
+  const int row = threadIdx.x % kNarrowRows, sub = threadIdx.x / kNarrowRows;
+  for (int item = blockIdx.x; item < kNarrowParts * n_slices; item += gridDim.x) {
+    const int g = item % kNarrowParts, r = item / kNarrowParts;
+    const int64_t j0 = g * gk, j1 = min(K, j0 + gk), i = static_cast<int64_t>(r) * kNarrowRows + row;
+    __syncthreads();
+    for (int64_t e = threadIdx.x; e < (j1 - j0) * n_pow; e += kPT) {
+      const int64_t jj = e / n_pow, c = e - jj * n_pow;
+      Vs[e] = __ldcg(p.vp + static_cast<int64_t>(act[pact[c]]) * K + j0 + jj);
+    }
+    __syncthreads();
+    double acc[kNarrow];
+#pragma unroll
+    for (int c = 0; c < kNarrow; ++c) acc[c] = 0.0;
+    if (i < ld) {
+      for (int64_t j = j0 + sub; j < j1; j += 4) {
+        const double av = __ldg(p.a + j * ld + i);
+        const double* vr = Vs + (j - j0) * n_pow;
+#pragma unroll
+        for (int c = 0; c < kNarrow; ++c)
+          if (c < n_pow) acc[c] = fma(av, vr[c], acc[c]);
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < kNarrow; ++c)
+      if (c < n_pow) Red[(sub * kNarrowRows + row) * n_pow + c] = acc[c];
+    __syncthreads();
+    if (sub == 0 && i < ld) {
+      for (int c = 0; c < n_pow; ++c) {
+        double t = Red[row * n_pow + c];
+        for (int s2 = 1; s2 < 4; ++s2) t += Red[(s2 * kNarrowRows + row) * n_pow + c];
+        __stcg(p.np + (static_cast<int64_t>(g) * n_pow + c) * ld + i, t);
+      }
+    }
+  }
+}
+
 }  // namespace
 
 __global__ void __launch_bounds__(kPT, 1) prefix_kernel(const __grid_constant__ PrefixParams p) {
@@ -1005,6 +1114,7 @@ __global__ void __launch_bounds__(kPT, 1) prefix_kernel(const __grid_constant__ 
   }
   grid.sync();
   int32_t steps = 0;
+  int64_t work_act = 0, work_pow = 0;  // contraction widths summed over the steps (roofline accounting)
   for (;; ++steps) {
     // unfinished signals in signal order, and the ones in a power step (identical in every CTA)
     int n_act = 0, n_pow = 0;
@@ -1022,14 +1132,28 @@ __global__ void __launch_bounds__(kPT, 1) prefix_kernel(const __grid_constant__ 
       n_pow = np;
     }
     if (n_act == 0) break;
+    work_act += n_act;
+    work_pow += n_pow;
     const bool logit = p.step_log && blockIdx.x == 0 && threadIdx.x == 0 && steps < p.max_log;
     if (logit) {
       p.step_log[5 * steps] = n_act;
       p.step_log[5 * steps + 1] = n_pow;
       p.step_log[5 * steps + 2] = gtimer() - t0;
     }
+    const bool narrow = p.narrow && narrow_fits(n_act, ld);
     // ---- power-step signals: w = A_S v (one contraction), then summed into R
-    if (n_pow > 0) {
+    if (n_pow > 0 && narrow) {
+      narrow_w(p, n_pow, pact, act, stage);
+      grid.sync();
+      for (int64_t e = static_cast<int64_t>(blockIdx.x) * kPT + threadIdx.x; e < static_cast<int64_t>(n_pow) * ld;
+           e += static_cast<int64_t>(gridDim.x) * kPT) {
+        const int64_t pc = e / ld, i = e - pc * ld;
+        double w = 0.0;
+        for (int g = 0; g < kNarrowParts; ++g) w += __ldcg(p.np + (static_cast<int64_t>(g) * n_pow + pc) * ld + i);
+        __stcg(p.R + static_cast<int64_t>(act[pact[pc]]) * ld + i, i < N ? w : 0.0);
+      }
+      grid.sync();
+    } else if (n_pow > 0) {
       const int n_rt = static_cast<int>((ld + kTM - 1) / kTM);
       const int n_ct = (n_pow + kTN - 1) / kTN;
       const int sk = p.split_mode ? split_for(n_rt * n_ct, gridDim.x, static_cast<int>((K + kTK - 1) / kTK))
@@ -1049,14 +1173,20 @@ __global__ void __launch_bounds__(kPT, 1) prefix_kernel(const __grid_constant__ 
       grid.sync();
     }
     if (logit) p.step_log[5 * steps + 3] = gtimer() - t0;
-    // ---- Corr = A^T [rho | w] for every unfinished signal (fp64 tensor cores)
-    const int n_rt = static_cast<int>((K + kTM - 1) / kTM);
-    const int n_ct = (n_act + kTN - 1) / kTN;
-    const int sk = p.split_mode ? split_for(n_rt * n_ct, gridDim.x, static_cast<int>((ld + kTK - 1) / kTK))
-                                : split_old(n_rt * n_ct, gridDim.x);
-    for (int item = blockIdx.x; item < n_rt * n_ct * sk; item += gridDim.x) {
-      const int tile = item % (n_rt * n_ct), kp = item / (n_rt * n_ct);
-      gemm_tile(p, tile % n_rt, tile / n_rt, kp, sk, n_act, act, stage);
+    // ---- Corr = A^T [rho | w] for every unfinished signal (fp64 tensor cores; CUDA
+    // cores when narrow)
+    int sk = 1;
+    if (narrow) {
+      narrow_corr(p, n_act, act, stage);
+    } else {
+      const int n_rt = static_cast<int>((K + kTM - 1) / kTM);
+      const int n_ct = (n_act + kTN - 1) / kTN;
+      sk = p.split_mode ? split_for(n_rt * n_ct, gridDim.x, static_cast<int>((ld + kTK - 1) / kTK))
+                        : split_old(n_rt * n_ct, gridDim.x);
+      for (int item = blockIdx.x; item < n_rt * n_ct * sk; item += gridDim.x) {
+        const int tile = item % (n_rt * n_ct), kp = item / (n_rt * n_ct);
+        gemm_tile(p, tile % n_rt, tile / n_rt, kp, sk, n_act, act, stage);
+      }
     }
     grid.sync();
     if (logit) p.step_log[5 * steps + 4] = gtimer() - t0;
@@ -1079,6 +1209,10 @@ __global__ void __launch_bounds__(kPT, 1) prefix_kernel(const __grid_constant__ 
     grid.sync();
   }
   if (blockIdx.x == 0 && threadIdx.x == 0 && p.steps_out) *p.steps_out = steps;
+  if (blockIdx.x == 0 && threadIdx.x == 0 && p.work_out) {
+    p.work_out[0] = work_act;
+    p.work_out[1] = work_pow;
+  }
 }
 
 

@@ -306,6 +306,31 @@ def test_batched_lockstep_prefix(cuda, oracle16, variant, solver):
         assert len(res[b].trace) == len(o.trace)
 
 
+@pytest.mark.parametrize("narrow", ["0", "1"])
+def test_batched_lockstep_narrow_steps(cuda, oracle16, monkeypatch, narrow):
+    """Lockstep steps with at most 12 unfinished signals run their products on the CUDA
+    cores (FL1_LOCKSTEP_NARROW=1, default) instead of the DMMA tiles: with hand-off policy
+    0 every signal stays in the lockstep to the end, so the narrow steps carry whole
+    power iterations and FISTA tails; each signal equals its own oracle solve."""
+    monkeypatch.setenv("FL1_LOCKSTEP_POLICY", "0")
+    monkeypatch.setenv("FL1_LOCKSTEP_NARROW", narrow)
+    rng = np.random.default_rng(31)
+    n, k, B = 300, 1200, 14
+    a = syn.gaussian_dictionary(rng, n, k)
+    Y = np.empty((n, B), order="F")
+    for b in range(B):
+        Y[:, b] = syn.observe(rng, a @ syn.sparse_signal(rng, k, 4 + 2 * b), None, 30.0)
+    lams = (0.15 + 0.05 * (np.arange(B) % 4)) * np.max(np.abs(a.T @ Y), axis=0)
+    L = F.lipschitz_bound(F.DenseDictionary(a, backend=cuda))
+    cfg = F.SwitchConfig(screening_interval=10, max_iterations=5000, rel_tolerance=1e-6)
+    opts = F.RunOptions(variant=F.VARIANT_SCREENED, full_lipschitz=[L], collect_trace=True)
+    seq_g = F.ApproxSequence([F.make_exact_approx(F.DenseDictionary(a, backend=cuda))])
+    seq_o = F.ApproxSequence([F.make_exact_approx(F.DenseDictionary(a, backend=oracle16))])
+    res = F.run_lasso_batched(seq_g, Y, lams, cfg, opts, concurrency=0)
+    for b in range(B):
+        assert_parity(res[b], F.run_lasso(seq_o, Y[:, b], lams[b], cfg, opts), a, Y[:, b], lams[b])
+
+
 @pytest.mark.parametrize("policy", ["0", "1", "2"])
 def test_batched_prefix_matches_engine_only(cuda, monkeypatch, policy):
     """The lockstep engine changes only the route, not the answer, under every
