@@ -408,7 +408,7 @@ size_t carve(EngineParams& p, char* base, int64_t n, int64_t k, int64_t ld, int 
     bk.atye = c.take<double>(kk);
     bk.lead = c.take<double>(kk);
     bk.keep = c.take<int8_t>(kk);
-    bk.cix = c.take<int32_t>(kk);
+    p.bcix[b] = c.take<int32_t>(kk);
   }
   p.trace = c.take<fl1_trace_row>(std::max<int64_t>(trace_cap, 1));
   p.sw = c.take<fl1_switch_event>(fl1::kMaxLevels);

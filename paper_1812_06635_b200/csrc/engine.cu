@@ -1262,7 +1262,7 @@ __device__ __forceinline__ DevLevel col_view(const EngineParams& p, const Engine
   DevLevel v = lv;
   if (s.csel != 0) {
     v.a = p.cbuf[s.csel - 1];
-    bk.idx = bk.cix;
+    bk.idx = p.bcix[s.cur];
   }
   return v;
 }
@@ -1730,6 +1730,60 @@ __device__ void combine_g(const EngineParams& p, int C, bool shift, bool fix) {
 }
 
 // setup_dictionary (fastl1.cpp:283-324). first: constructor call.
+// FL1_COMPACT paths, out of line so the default engine body keeps its register allocation.
+__device__ __noinline__ void compact_adjoint(const EngineParams& p, Sh& sh, const DevLevel& lv, int64_t S,
+                                             const Scratch& sc, const PassOut& po) {
+  Bank cb = p.bank[sh.s.cur];
+  const double* eps = cb.eps;
+  const DevLevel cv = col_view(p, sh.s, lv, cb);
+  op_adjoint(p, sh, cv, cb.idx, eps, S, sc.vec, sc.rt, po);
+}
+
+__device__ __noinline__ double compact_power_iteration(const EngineParams& p, Sh& sh, const DevLevel& lv,
+                                                       const Scratch& sc) {
+  Bank cb = p.bank[sh.s.cur];
+  const DevLevel cv = col_view(p, sh.s, lv, cb);
+  return power_iteration(p, sh, cv, cb, sh.s.S, sh.s.lead_valid != 0, sc);
+}
+
+// After the shrinking pass compacted bank cur into cur^1 (this CTA's kept atoms at new
+// positions [sh.scan_base, ...) in position order): the compact-copy slots of the kept
+// atoms, then the copy into the other buffer; the state flips to it.
+__device__ __noinline__ void compact_shrink(const EngineParams& p, Sh& sh, const DevLevel& lv, int64_t lo, int64_t hi,
+                                            int64_t S_new) {
+  EngineState& s = sh.s;
+  const Bank bk = p.bank[s.cur];
+  const int32_t* src_slot = s.csel != 0 ? p.bcix[s.cur] : bk.idx;
+  int32_t* dst_slot = p.bcix[s.cur ^ 1];
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  int64_t out = sh.scan_base;
+  for (int64_t q0 = lo; q0 < hi; q0 += kThreads) {  // the same ordered scan as the bank compaction
+    const int64_t q = q0 + threadIdx.x;
+    const int kp = q < hi ? bk.keep[q] : 0;
+    const unsigned bal = __ballot_sync(kFull, kp);
+    if (l == 0) sh.wscan[w] = __popc(bal);
+    __syncthreads();
+    int64_t off = out;
+    int tot = 0;
+    for (int ww = 0; ww < kWarps; ++ww) {
+      if (ww < w) off += sh.wscan[ww];
+      tot += sh.wscan[ww];
+    }
+    off += __popc(bal & ((1u << l) - 1u));
+    if (kp) dst_slot[off] = src_slot[q];
+    out += tot;
+    __syncthreads();
+  }
+  copy_columns(s.csel != 0 ? p.cbuf[s.csel - 1] : lv.a, dst_slot, p.cbuf[s.csel == 1 ? 1 : 0], sh.scan_base, out,
+               p.ld);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (2 * S_new <= s.cwidth) s.cwidth = S_new;
+    s.csel = s.csel == 1 ? 2 : 1;
+  }
+  __syncthreads();
+}
+
 __device__ __noinline__ void setup_dictionary(const EngineParams& p, Sh& sh, bool first, const Scratch& sc) {
   EngineState& s = sh.s;
   const DevLevel& lv = p.lv[s.dict_index];
@@ -1741,9 +1795,10 @@ __device__ __noinline__ void setup_dictionary(const EngineParams& p, Sh& sh, boo
     if (cp) {
       int64_t lo, hi;
       slice(s.S, lo, hi);
-      for (int64_t q = lo + threadIdx.x; q < hi; q += kThreads) bk.cix[q] = bk.idx[q];
+      int32_t* cix = p.bcix[s.cur];
+      for (int64_t q = lo + threadIdx.x; q < hi; q += kThreads) cix[q] = bk.idx[q];
       __syncthreads();
-      copy_columns(lv.a, bk.cix, p.cbuf[0], lo, hi, p.ld);
+      copy_columns(lv.a, cix, p.cbuf[0], lo, hi, p.ld);
     }
     if (threadIdx.x == 0) {
       s.csel = cp ? 1 : 0;
@@ -1769,9 +1824,8 @@ __device__ __noinline__ void setup_dictionary(const EngineParams& p, Sh& sh, boo
   if (p.has_full_l && s.S == p.k) {
     if (threadIdx.x == 0) s.lipschitz = p.full_l[s.dict_index];
   } else {
-    Bank cb = bk;
-    const DevLevel cv = col_view(p, s, lv, cb);
-    const double sq = power_iteration(p, sh, cv, cb, s.S, s.lead_valid != 0, sc);
+    const double sq = s.csel == 0 ? power_iteration(p, sh, lv, bk, s.S, s.lead_valid != 0, sc)
+                                  : compact_power_iteration(p, sh, lv, sc);
     if (threadIdx.x == 0) {
       s.lead_valid = 1;
       s.lipschitz = fmax(sq, 1e-300) * 1.05;
@@ -2034,9 +2088,8 @@ __device__ __noinline__ void engine_body(const EngineParams& p, Sh& sh, double* 
     } else if (!exact_fit) {
       // corr = A_S^T rho_g fused with the dual-scaling maxima (414-418)
       PassOut po{p.corr, 1, sh.rho_norm, false, kSlMaxPlain, kSlMaxStable, nullptr};
-      Bank cb = bk;
-      const DevLevel cv = col_view(p, s, lv, cb);
-      op_adjoint(p, sh, cv, cb.idx, bk.eps, S, sc.vec, sc.rt, po);
+      if (s.csel == 0) op_adjoint(p, sh, lv, bk.idx, bk.eps, S, sc.vec, sc.rt, po);
+      else compact_adjoint(p, sh, lv, S, sc, po);  // FL1_COMPACT: the compact copy
     } else {
       // exact fit (428-449): corr = A^T 0 = 0, dual point along y
       for (int64_t q = lo + threadIdx.x; q < hi; q += kThreads) p.corr[q] = 0.0;
@@ -2364,10 +2417,6 @@ __device__ __noinline__ void engine_body(const EngineParams& p, Sh& sh, double* 
       const bool lead_ok = s.lead_valid != 0;
       const bool dyn = p.rule == FL1_RULE_DYNAMIC;
       const bool atye = s.atye_valid != 0;
-      // restrict_to_local copies the kept columns once compacted; maybe_compact copies
-      // them from the level's matrix at every halving of the compaction width (115-129, 176-187)
-      const bool cpy = p.compact && lv.kind == kDense && lv.rows == 0 && !gram &&
-                       (s.csel != 0 || 2 * S_new <= s.cwidth);
       int64_t out_base = sh.scan_base;
       double me = -DBL_MAX;
       const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
@@ -2394,22 +2443,15 @@ __device__ __noinline__ void engine_body(const EngineParams& p, Sh& sh, double* 
           if (dyn) nb.aty[off] = bk.aty[q];
           if (atye) nb.atye[off] = bk.atye[q];
           if (lead_ok) nb.lead[off] = bk.lead[q];
-          if (cpy) nb.cix[off] = s.csel != 0 ? bk.cix[q] : bk.idx[q];
           me = fmax(me, bk.eps[q]);
         }
         out_base += tot;
         __syncthreads();
       }
-      if (cpy) {
-        copy_columns(s.csel != 0 ? p.cbuf[s.csel - 1] : lv.a, nb.cix, p.cbuf[s.csel == 1 ? 1 : 0], sh.scan_base,
-                     out_base, p.ld);
-        __syncthreads();
-        if (threadIdx.x == 0) {
-          if (2 * S_new <= s.cwidth) s.cwidth = S_new;
-          s.csel = s.csel == 1 ? 2 : 1;
-        }
-        __syncthreads();
-      }
+      // restrict_to_local copies the kept columns once compacted; maybe_compact copies
+      // them from the level's matrix at every halving of the compaction width (115-129, 176-187)
+      if (p.compact && lv.kind == kDense && lv.rows == 0 && !gram && (s.csel != 0 || 2 * S_new <= s.cwidth))
+        compact_shrink(p, sh, lv, lo, hi, S_new);
       double v[1] = {me};
       const bool mx[1] = {true};
       block_reduce<1>(v, mx, sh);
@@ -2452,9 +2494,8 @@ __device__ __noinline__ void engine_body(const EngineParams& p, Sh& sh, double* 
     }
     // Lipschitz refresh after a halving (603-608)
     if (s.S * 2 <= s.active_at_last_l && s.S > 0 && sh.next_dict == s.dict_index) {
-      Bank cb = p.bank[s.cur];
-      const DevLevel cv = col_view(p, s, lv, cb);
-      const double sq = power_iteration(p, sh, cv, cb, s.S, s.lead_valid != 0, sc);
+      const double sq = s.csel == 0 ? power_iteration(p, sh, lv, p.bank[s.cur], s.S, s.lead_valid != 0, sc)
+                                    : compact_power_iteration(p, sh, lv, sc);
       if (threadIdx.x == 0) {
         s.lead_valid = 1;
         s.lipschitz = fmax(sq, 1e-300) * 1.05;

@@ -59,7 +59,6 @@ struct Bank {
   double* atye;   // A^T y (precompute_aty variant)
   double* lead;   // power-iteration leading vector
   int8_t* keep;   // screening decision of the last pass
-  int32_t* cix;   // column slot in the physically compacted copy (EngineState::csel != 0)
 };
 
 enum Mode : int32_t { kModeSolve = 0, kModeResume = 1, kModePower = 2, kModeApply = 3, kModeAdjoint = 4 };
@@ -291,6 +290,7 @@ struct alignas(16) EngineParams {
   int32_t early_prox;    // 1: non-screening dense iterations run the prox before the first barrier (FL1_EARLY_PROX)
   int32_t compact;       // 1: preserved columns physically compacted into cbuf (FL1_COMPACT, A/B switch)
   double* cbuf[2];       // ping-pong compact copies, ld x ceil(K/2) each
+  int32_t* bcix[2];      // per bank: column slot of each position in the compact copy (csel != 0)
   double* pv;       // K
   double* pw;       // K
   double* PU;       // ld: power-iteration A v (combined)
