@@ -637,7 +637,7 @@ def run_batched(args) -> None:
         "config": {"workload": f"c5: {B} independent Lasso signals on one dense {n}x{k} dictionary, per-signal "
                                "FISTA + GAP every 10 to gap<=1e-6*P(x), lambda_b = 0.25 lambda_max_b",
                    "parallelism": f"replicas x{world}; per GPU: lockstep batched engine (DMMA contractions over "
-                                  f"all signals) then thread-block clusters of {-args.concurrency or 2} CTAs",
+                                  f"all signals) then thread-block clusters of {-args.concurrency or 1} CTA(s)",
                    "l2_policy": "A = 33.5 MB, L2-resident"},
         "timing": "CUDA events around the whole batched call on its stream (lockstep + cluster launches), "
                   "Y resident in HBM",
@@ -882,7 +882,7 @@ def main():
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
     ap.add_argument("--config", default="c4", choices=["c1", "c2", "c3", "c4", "c5"],
                     help="BASELINE config (default c4: the largest single-GPU config, the 10-lambda path)")
-    ap.add_argument("--concurrency", type=int, default=0, help="c5: <=0 one launch of thread-block clusters of -N CTAs (0 = default 2); >0 that many concurrent sub-grid launches")
+    ap.add_argument("--concurrency", type=int, default=0, help="c5: <=0 one launch of thread-block clusters of -N CTAs (0 = default 1); >0 that many concurrent sub-grid launches")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":

@@ -126,7 +126,10 @@ struct DevBuf {
   }
 };
 
-constexpr int kDefaultClusterSize = 2;  // batched solves: CTAs per signal
+// batched solves: CTAs per signal engine. 1 measured best on c5 (the per-signal tails
+// after the lockstep hand-off run on small preserved sets: 148 one-CTA engines beat 74
+// two-CTA clusters, 56.6 vs 57.0 ms; 4 CTAs: 62.2 ms)
+constexpr int kDefaultClusterSize = 1;
 
 // leading dimension of dense columns / vectors: 128-byte aligned (FL1_LD_ALIGN doubles,
 // default 16: every column starts on an L2 line; c1 -1.5%, no change where N % 16 == 0)
@@ -1288,6 +1291,8 @@ void solve_clusters(fl1_seq* s, const double* Y, bool y_device, int64_t ldy, con
     pp.split_mode = smode ? std::atoi(smode) : 1;
     const char* nm = std::getenv("FL1_LOCKSTEP_NARROW");
     pp.narrow = nm ? std::atoi(nm) : 1;
+    const char* wt = std::getenv("FL1_LOCKSTEP_WIDTH");
+    pp.width_tiles = wt ? std::atoi(wt) : 1;
     pp.X3[0] = reinterpret_cast<double*>(pb + q_x0);
     pp.X3[1] = reinterpret_cast<double*>(pb + q_x1);
     pp.X3[2] = reinterpret_cast<double*>(pb + q_x2);

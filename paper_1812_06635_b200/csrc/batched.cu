@@ -141,21 +141,25 @@ __device__ void block_sum3(double (&v)[3], PSh& sh) {
   __syncthreads();
 }
 
-// Corr tile (atoms j0..j0+63) x (slots a0..a0+63) over K-part kp of sk (rows of A /
-// rho), DMMA, into the split-K partial buffer kp.
-__device__ __noinline__ void gemm_tile(const PrefixParams& p, int rt, int ct, int kp, int sk, int64_t n_act,
+// Corr tile (atoms j0..j0+127) x (slots a0..a0+TN-1), TN = 8 kWC CT, over K-part kp of
+// sk (rows of A / rho), DMMA, into the split-K partial buffer kp. CT (column 8x8 tiles
+// per warp) is 4 for full 64-signal tiles and 2 / 1 for narrow steps (<= 32 / 16
+// signals), so every warp's DMMA work shrinks with the width instead of computing
+// empty columns (the slowest warp sets the tile's time).
+template <int CT>
+__device__ __noinline__ void gemm_tile(const PrefixParams& p, int rt, int64_t a0, int kp, int sk, int64_t n_act,
                                        const int32_t* act, double* stage) {
   const int w = threadIdx.x >> 5, l = threadIdx.x & 31, g = l >> 2, tg = l & 3;
-  const int64_t j0 = static_cast<int64_t>(rt) * kTM, a0 = static_cast<int64_t>(ct) * kTN;
+  const int64_t j0 = static_cast<int64_t>(rt) * kTM;
   const int64_t K = p.k, ld = p.ld;
   const int nch = static_cast<int>((ld + kTK - 1) / kTK);
   const int c_lo = nch * kp / sk, c_hi = nch * (kp + 1) / sk;
   const int wr = w % kWR, wc = w / kWR;
-  double acc[kRT][kCT][2];
+  double acc[kRT][CT][2];
 #pragma unroll
   for (int h = 0; h < kRT; ++h)
 #pragma unroll
-    for (int c = 0; c < kCT; ++c) acc[h][c][0] = acc[h][c][1] = 0.0;
+    for (int c = 0; c < CT; ++c) acc[h][c][0] = acc[h][c][1] = 0.0;
   auto issue = [&](int s, int kc) {
     double* As = stage + s * kStage;
     double* Rs = As + kTM * kSS;
@@ -169,7 +173,7 @@ __device__ __noinline__ void gemm_tile(const PrefixParams& p, int rt, int ct, in
       cp16(As + r * kSS + kk, ok ? p.a + j * ld + kg : p.a, ok);
     }
 #pragma unroll
-    for (int e0 = 0; e0 < kTN * (kTK / 2); e0 += kPT) {  // R columns (slots)
+    for (int e0 = 0; e0 < 8 * kWC * CT * (kTK / 2); e0 += kPT) {  // R columns (slots)
       const int e = e0 + threadIdx.x;
       const int c = e / (kTK / 2), kk = (e % (kTK / 2)) * 2;
       const int64_t a = a0 + c, kg = k0 + kk;
@@ -191,15 +195,15 @@ __device__ __noinline__ void gemm_tile(const PrefixParams& p, int rt, int ct, in
     const double* Rs = As + kTM * kSS;
 #pragma unroll
     for (int ks = 0; ks < kTK / 4; ++ks) {
-      double av[kRT], bv[kCT];
+      double av[kRT], bv[CT];
 #pragma unroll
       for (int h = 0; h < kRT; ++h) av[h] = As[((h * kWR + wr) * 8 + g) * kSS + ks * 4 + tg];
 #pragma unroll
-      for (int c = 0; c < kCT; ++c) bv[c] = Rs[((wc * kCT + c) * 8 + g) * kSS + ks * 4 + tg];
+      for (int c = 0; c < CT; ++c) bv[c] = Rs[((wc * CT + c) * 8 + g) * kSS + ks * 4 + tg];
 #pragma unroll
       for (int h = 0; h < kRT; ++h)
 #pragma unroll
-        for (int c = 0; c < kCT; ++c) dmma(acc[h][c], av[h], bv[c]);
+        for (int c = 0; c < CT; ++c) dmma(acc[h][c], av[h], bv[c]);
     }
   }
   cp_wait0();
@@ -209,14 +213,22 @@ __device__ __noinline__ void gemm_tile(const PrefixParams& p, int rt, int ct, in
   for (int h = 0; h < kRT; ++h) {
     const int64_t j = j0 + (h * kWR + wr) * 8 + g;
 #pragma unroll
-    for (int c = 0; c < kCT; ++c) {
+    for (int c = 0; c < CT; ++c) {
 #pragma unroll
       for (int i = 0; i < 2; ++i) {
-        const int64_t a = a0 + (wc * kCT + c) * 8 + 2 * tg + i;
+        const int64_t a = a0 + (wc * CT + c) * 8 + 2 * tg + i;
         if (j < K && a < n_act) __stcg(out + a * K + j, acc[h][c][i]);
       }
     }
   }
+}
+
+// column 8x8 tiles per warp for a column tile holding n (of up to 64) columns: the
+// narrowest of 16 / 32 / 48 / 64 that holds them when width tiles are on
+// (FL1_LOCKSTEP_WIDTH), else the full 64-column tile
+__device__ __forceinline__ int tile_ct(int n, int width_tiles) {
+  if (!width_tiles) return kCT;
+  return n <= 8 * kWC ? 1 : (n <= 16 * kWC ? 2 : (n <= 24 * kWC ? 3 : kCT));
 }
 
 // split-K factor for T output tiles of nch K-chunks on G CTAs: the fewest-waves choice,
@@ -244,20 +256,21 @@ __device__ __forceinline__ int split_old(int T, int G) {
 // ---------------------------------------------------------------------------
 // W = A V tile: rows i0..i0+63 of ld, power slots c0..c0+63 (index into pact),
 // atoms of K-part kp of sk; partial into np[kp][pslot][ld].
-__device__ __noinline__ void gemm_n_tile(const PrefixParams& p, int rt, int ct, int kp, int sk, int n_pow,
+template <int CT>
+__device__ __noinline__ void gemm_n_tile(const PrefixParams& p, int rt, int64_t c0, int kp, int sk, int n_pow,
                                          const int32_t* pact, const int32_t* act, double* stage) {
   const int w = threadIdx.x >> 5, l = threadIdx.x & 31, g = l >> 2, tg = l & 3;
-  const int64_t i0 = static_cast<int64_t>(rt) * kTM, c0 = static_cast<int64_t>(ct) * kTN;
+  const int64_t i0 = static_cast<int64_t>(rt) * kTM;
   const int64_t K = p.k, ld = p.ld;
   constexpr int kAS = kTM + 4;  // As[kk][i] row stride
   const int nch = static_cast<int>((K + kTK - 1) / kTK);
   const int c_lo = nch * kp / sk, c_hi = nch * (kp + 1) / sk;
   const int wr = w % kWR, wc = w / kWR;
-  double acc[kRT][kCT][2];
+  double acc[kRT][CT][2];
 #pragma unroll
   for (int h = 0; h < kRT; ++h)
 #pragma unroll
-    for (int c = 0; c < kCT; ++c) acc[h][c][0] = acc[h][c][1] = 0.0;
+    for (int c = 0; c < CT; ++c) acc[h][c][0] = acc[h][c][1] = 0.0;
   auto issue = [&](int s, int kc) {
     double* As = stage + s * kStage;
     double* Bs = As + kTK * kAS;
@@ -271,7 +284,7 @@ __device__ __noinline__ void gemm_n_tile(const PrefixParams& p, int rt, int ct, 
       cp16(As + kk * kAS + ii, ok ? p.a + kg * ld + ig : p.a, ok);
     }
 #pragma unroll
-    for (int e0 = 0; e0 < kTN * (kTK / 2); e0 += kPT) {  // V(k, slot): slot-major, k contiguous
+    for (int e0 = 0; e0 < 8 * kWC * CT * (kTK / 2); e0 += kPT) {  // V(k, slot): slot-major, k contiguous
       const int e = e0 + threadIdx.x;
       const int c = e / (kTK / 2), kk = (e % (kTK / 2)) * 2;
       const int64_t pc = c0 + c, kg = k0 + kk;
@@ -293,15 +306,15 @@ __device__ __noinline__ void gemm_n_tile(const PrefixParams& p, int rt, int ct, 
     const double* Bs = As + kTK * kAS;
 #pragma unroll
     for (int ks = 0; ks < kTK / 4; ++ks) {
-      double av[kRT], bv[kCT];
+      double av[kRT], bv[CT];
 #pragma unroll
       for (int h = 0; h < kRT; ++h) av[h] = As[(ks * 4 + tg) * kAS + (h * kWR + wr) * 8 + g];
 #pragma unroll
-      for (int c = 0; c < kCT; ++c) bv[c] = Bs[((wc * kCT + c) * 8 + g) * kSS + ks * 4 + tg];
+      for (int c = 0; c < CT; ++c) bv[c] = Bs[((wc * CT + c) * 8 + g) * kSS + ks * 4 + tg];
 #pragma unroll
       for (int h = 0; h < kRT; ++h)
 #pragma unroll
-        for (int c = 0; c < kCT; ++c) dmma(acc[h][c], av[h], bv[c]);
+        for (int c = 0; c < CT; ++c) dmma(acc[h][c], av[h], bv[c]);
     }
   }
   cp_wait0();
@@ -310,10 +323,10 @@ __device__ __noinline__ void gemm_n_tile(const PrefixParams& p, int rt, int ct, 
   for (int h = 0; h < kRT; ++h) {
     const int64_t i = i0 + (h * kWR + wr) * 8 + g;
 #pragma unroll
-    for (int c = 0; c < kCT; ++c) {
+    for (int c = 0; c < CT; ++c) {
 #pragma unroll
       for (int q = 0; q < 2; ++q) {
-        const int64_t pc = c0 + (wc * kCT + c) * 8 + 2 * tg + q;
+        const int64_t pc = c0 + (wc * CT + c) * 8 + 2 * tg + q;
         if (i < ld && pc < n_pow) __stcg(p.np + (static_cast<int64_t>(kp) * p.bcap + pc) * ld + i, acc[h][c][q]);
       }
     }
@@ -1160,7 +1173,13 @@ __global__ void __launch_bounds__(kPT, 1) prefix_kernel(const __grid_constant__ 
                                   : split_old(n_rt * n_ct, gridDim.x);
       for (int item = blockIdx.x; item < n_rt * n_ct * sk; item += gridDim.x) {
         const int tile = item % (n_rt * n_ct), kp = item / (n_rt * n_ct);
-        gemm_n_tile(p, tile % n_rt, tile / n_rt, kp, sk, n_pow, pact, act, stage);
+        const int64_t c0 = static_cast<int64_t>(tile / n_rt) * kTN;
+        switch (tile_ct(static_cast<int>(n_pow - c0), p.width_tiles)) {  // the last column tile may be narrow
+          case 1: gemm_n_tile<1>(p, tile % n_rt, c0, kp, sk, n_pow, pact, act, stage); break;
+          case 2: gemm_n_tile<2>(p, tile % n_rt, c0, kp, sk, n_pow, pact, act, stage); break;
+          case 3: gemm_n_tile<3>(p, tile % n_rt, c0, kp, sk, n_pow, pact, act, stage); break;
+          default: gemm_n_tile<kCT>(p, tile % n_rt, c0, kp, sk, n_pow, pact, act, stage);
+        }
       }
       grid.sync();
       for (int64_t e = static_cast<int64_t>(blockIdx.x) * kPT + threadIdx.x; e < static_cast<int64_t>(n_pow) * ld;
@@ -1185,7 +1204,13 @@ __global__ void __launch_bounds__(kPT, 1) prefix_kernel(const __grid_constant__ 
                         : split_old(n_rt * n_ct, gridDim.x);
       for (int item = blockIdx.x; item < n_rt * n_ct * sk; item += gridDim.x) {
         const int tile = item % (n_rt * n_ct), kp = item / (n_rt * n_ct);
-        gemm_tile(p, tile % n_rt, tile / n_rt, kp, sk, n_act, act, stage);
+        const int64_t a0 = static_cast<int64_t>(tile / n_rt) * kTN;
+        switch (tile_ct(static_cast<int>(n_act - a0), p.width_tiles)) {  // the last column tile may be narrow
+          case 1: gemm_tile<1>(p, tile % n_rt, a0, kp, sk, n_act, act, stage); break;
+          case 2: gemm_tile<2>(p, tile % n_rt, a0, kp, sk, n_act, act, stage); break;
+          case 3: gemm_tile<3>(p, tile % n_rt, a0, kp, sk, n_act, act, stage); break;
+          default: gemm_tile<kCT>(p, tile % n_rt, a0, kp, sk, n_act, act, stage);
+        }
       }
     }
     grid.sync();
