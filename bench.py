@@ -513,6 +513,10 @@ def run_path(args) -> None:
                      "kernel": "fl1::engine_kernel (one launch per lambda)",
                      "hot_pass": {"name": "fused A_S^T r + dual-scaling maxima", "achieved_GBps": hot_b / hot_ns,
                                   "frac": hot_b / hot_ns / peak, "bytes": hot_b, "ms": hot_ns / 1e6}},
+        "phase_ms": {k: sum(float(r.profile[i]) for r in last) / 1e6 for i, k in
+                     enumerate(("A_products_pass", "B_dual_screen_prox", "D_compact_apply", "power_iterations",
+                                "switch_setup"))},
+        "power_bytes": sum(float(r.profile[7]) for r in last),
         "clocks": clk.summary(),
         "cpu_baseline": cpu,
     }
