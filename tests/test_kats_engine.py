@@ -247,3 +247,45 @@ def test_warm_start_and_relative_tolerance_extensions(backend, refgen):
     r4 = F.run_lasso(seq, y, 0.3 * lmax, cfg, F.RunOptions(variant=F.VARIANT_SCREENED))
     assert r3.converged and r4.converged
     assert np.max(np.abs(r3.x - r4.x)) <= 2.0 * np.sqrt(2.0 * 1e-6 * 0.5 * (y @ y))
+
+
+@pytest.mark.gpu
+def test_gamma_regression_kat_device_sequence(cuda, refgen):  # test_fastl1.cpp:243-268
+    """The reference's first-gamma regression on a SuKro sequence built by the device
+    construction (fl1_build_sukro_sequence) instead of the LAPACK restatement."""
+    from paper_1812_06635_b200 import harness as H
+
+    a, y, lmax = refgen.square_instance(36, 100, 113, 4, "easy")
+    seq = H.sukro_sequence(a, [2], backend=cuda)
+    cfg = F.SwitchConfig(gamma_threshold=0.5, tolerance=1e-10, max_iterations=100000)
+    res = F.run_lasso(seq, y, 0.2 * lmax, cfg, F.RunOptions(rule=F.RULE_GAP))
+    g = res.trace["gamma"][res.trace["gamma"] != -1.0]
+    assert g.size > 0 and g[0] >= 0.9 and g[-1] <= g[0]
+    assert g[0] == pytest.approx(0.95470658293002786, rel=1e-9)
+
+
+@pytest.mark.gpu
+def test_build_sukro_sequence_abi_errors(cuda):
+    """fl1_build_sukro_sequence's own argument checks return FL1_EINVAL with the
+    reference's messages (dictionary.cpp:19-33, 284-296)."""
+    import ctypes as C
+
+    lib = cuda.lib
+    P = C.POINTER(C.c_double)
+    out = [np.zeros(4096) for _ in range(6)]
+
+    def call(a, ranks):
+        d = F.DenseDictionary(a, backend=cuda)
+        rk = np.asarray(ranks, dtype=np.int32)
+        lib.check(lib.build_sukro_sequence(d._h, rk.ctypes.data_as(C.POINTER(C.c_int32)), len(ranks),
+                                           *[o.ctypes.data_as(P) for o in out]))
+
+    rng = np.random.default_rng(1)
+    with pytest.raises(F.InvalidArgument, match="N must be a perfect square, got 35"):
+        call(rng.standard_normal((35, 64)), [1])
+    with pytest.raises(F.InvalidArgument, match="ranks must be positive and strictly increasing"):
+        call(rng.standard_normal((36, 64)), [2, 2])
+    with pytest.raises(F.InvalidArgument, match="rank exceeds rearranged dimension"):
+        call(rng.standard_normal((36, 64)), [49])
+    with pytest.raises(F.InvalidArgument, match="relative complexity >= 1"):
+        call(rng.standard_normal((36, 64)), [4])
