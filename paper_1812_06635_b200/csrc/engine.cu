@@ -1553,6 +1553,205 @@ __device__ __noinline__ void combine_u_lists(const EngineParams& p, Sh& sh, cons
   }
 }
 
+// Column-split apply (large N x nnz): the same result as combine_u_lists (u = A x_next
+// in list order, the v fix, the next rho and its statistics), organised for DRAM
+// locality. The row-slice gather reads ld / G rows (~440 B at N = 8192) of every listed
+// column per CTA, a latency-bound pattern (c4 lambda_9: 61 MB in 65 us per iteration);
+// here CTA c takes the contiguous global list range [E c / G, E (c+1) / G) and streams
+// whole columns (64 KiB contiguous at N = 8192) into a partial u of all ld rows (one
+// partial per CTA, list order inside it), then after one virtual-grid barrier every CTA
+// sums the non-empty partials in CTA order for its row slice (fixed order: reproducible).
+constexpr int kCsRows = 8;     // rows per thread per row tile (row tile = 8 * kThreads rows)
+constexpr int kCsStage = 512;  // list entries staged in shared memory per round
+constexpr int64_t kCsMinLd = 4096;  // shorter columns: the row-slice gather is as fast (c2: 6.45 vs 6.50 ms)
+
+__device__ __forceinline__ int64_t cs_lo(int64_t E, int c, int G) { return E * c / G; }
+
+// this CTA's partial of one list (entries [e0, e1) of the global list with prefix pp):
+// the entries are staged in shared memory (once when they fit), then every row tile
+// issues eight columns' loads (kCsRows rows each) before their FMAs
+__device__ __forceinline__ void colsplit_stage(const int32_t* pp, int G, int64_t S, const double* lv_v,
+                                               const int32_t* lv_j, int64_t eb, int ne, int32_t* ej, double* ev) {
+  __syncthreads();
+  for (int q = threadIdx.x; q < ne; q += kThreads) {  // list order
+    const int64_t e = eb + q;
+    int a = 0, b = G;  // largest CTA segment with pp[a] <= e
+    while (b - a > 1) {
+      const int mid = (a + b) >> 1;
+      if (pp[mid] <= e) a = mid;
+      else b = mid;
+    }
+    const int64_t at = S * a / G + (e - pp[a]);
+    ej[q] = __ldcg(lv_j + at);
+    ev[q] = __ldcg(lv_v + at);
+  }
+  __syncthreads();
+}
+
+__device__ void colsplit_partial(const EngineParams& p, const double* __restrict__ A, int64_t ld, int64_t S, int G,
+                                 const int32_t* pp, const double* lv_v, const int32_t* lv_j, int64_t e0, int64_t e1,
+                                 double* __restrict__ out, int32_t* ej, double* ev) {
+  constexpr int kB = 4;  // columns per batch of loads
+  const bool once = e1 - e0 <= kCsStage;
+  if (once) colsplit_stage(pp, G, S, lv_v, lv_j, e0, static_cast<int>(e1 - e0), ej, ev);
+  for (int64_t r0 = 0; r0 < ld; r0 += kCsRows * kThreads) {
+    double acc[kCsRows];
+#pragma unroll
+    for (int r = 0; r < kCsRows; ++r) acc[r] = 0.0;
+    for (int64_t eb = e0; eb < e1; eb += kCsStage) {
+      const int ne = static_cast<int>(e1 - eb < kCsStage ? e1 - eb : kCsStage);
+      if (!once) colsplit_stage(pp, G, S, lv_v, lv_j, eb, ne, ej, ev);
+      for (int q = 0; q < ne; q += kB) {
+        double av[kB][kCsRows];
+#pragma unroll
+        for (int u = 0; u < kB; ++u) {
+          const bool on = q + u < ne;
+          const double* col = A + static_cast<int64_t>(on ? ej[q + u] : 0) * ld + r0 + threadIdx.x;
+#pragma unroll
+          for (int r = 0; r < kCsRows; ++r)
+            av[u][r] = (on && r0 + threadIdx.x + r * kThreads < ld) ? __ldcs(col + r * kThreads) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < kB; ++u) {
+          const double x = q + u < ne ? ev[q + u] : 0.0;
+#pragma unroll
+          for (int r = 0; r < kCsRows; ++r) acc[r] = fma(x, av[u][r], acc[r]);
+        }
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < kCsRows; ++r) {
+      const int64_t i = r0 + threadIdx.x + r * kThreads;
+      if (i < ld) __stcg(out + i, acc[r]);
+    }
+  }
+}
+
+// Column split when the listed columns are long and many (identical decision in every
+// CTA: the list lengths are read by all): ld >= kCsMinLd and E entries x ld rows >=
+// p.colsplit_elems (FL1_COLSPLIT, default 4 Mi: c4 phase E 54 -> 46 ms over the path).
+__device__ __forceinline__ bool colsplit_apply(const EngineParams& p, Sh& sh, const ListPre& lp, const DevLevel& lv) {
+  if (p.colsplit_elems <= 0 || lv.kind != kDense || lv.rows != 0 || p.ld < kCsMinLd) return false;
+  const int G = vsize();
+  double v[1] = {0.0};
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    const int t = threadIdx.x + q * kThreads;
+    if (t < G) v[0] += static_cast<double>(lp.c[q]);  // apply-list lengths of the CTAs this thread read
+  }
+  const bool mx[1] = {false};
+  block_reduce<1>(v, mx, sh);  // exact: integers
+  return static_cast<int64_t>(v[0]) * p.ld >= p.colsplit_elems;
+}
+
+__device__ __noinline__ void combine_u_colsplit(const EngineParams& p, Sh& sh, const DevLevel& lv, int64_t S,
+                                                bool shift, bool fix, double m, double* scratch, const ListPre& lp) {
+  const int G = vsize(), c = vrank();
+  const bool mom = m != 0.0;
+  int32_t* pre = reinterpret_cast<int32_t*>(scratch);  // [2][G + 1] exclusive prefix of the list lengths
+  int32_t* ej = pre + 2 * (G + 1);                      // [kCsStage]
+  double* ev = scratch + (2 * (G + 1) + kCsStage + 1) / 2 + 1;  // [kCsStage]
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    const int t = threadIdx.x + q * kThreads;
+    if (t < 2 * G) pre[(t / G) * (G + 1) + 1 + t % G] = lp.c[q];
+  }
+  if (threadIdx.x < 2) pre[threadIdx.x * (G + 1)] = 0;
+  __syncthreads();
+  if (w < 2) {  // warp 0: apply lists, warp 1: fix lists
+    int32_t* pp = pre + w * (G + 1);
+    int carry = 0;
+    for (int c0 = 0; c0 < G; c0 += 32) {
+      int v = c0 + l < G ? pp[1 + c0 + l] : 0;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(kFull, v, o);
+        if (l >= o) v += t;
+      }
+      if (c0 + l < G) pp[1 + c0 + l] = v + carry;
+      carry += __shfl_sync(kFull, v, 31);
+    }
+  }
+  __syncthreads();
+  const int64_t ld = p.ld;
+  const int64_t Ea = pre[G], Ef = fix ? pre[(G + 1) + G] : 0;
+  // a CTA with an empty range writes nothing; the combine skips it (ranges are known to all)
+  if (cs_lo(Ea, c, G) < cs_lo(Ea, c + 1, G))
+    colsplit_partial(p, lv.a, ld, S, G, pre, p.nzv, p.nzj, cs_lo(Ea, c, G), cs_lo(Ea, c + 1, G),
+                     p.up + static_cast<int64_t>(c) * ld, ej, ev);
+  if (cs_lo(Ef, c, G) < cs_lo(Ef, c + 1, G))
+    colsplit_partial(p, lv.a, ld, S, G, pre + (G + 1), p.fxv, p.fxj, cs_lo(Ef, c, G), cs_lo(Ef, c + 1, G),
+                     p.dvp + static_cast<int64_t>(c) * ld, ej, ev);
+  vsync();
+  int64_t ilo, ihi;
+  slice(ld, ilo, ihi);
+  // partials summed by row slice: 4 groups of CTAs per row (contiguous CTA ranges, eight
+  // loads in flight), the group sums added in group order (a fixed order: reproducible)
+  constexpr int kGrp = 4, kRB = kThreads / kGrp;
+  double* gsum = ev;  // [2][kGrp][kRB] (the entry staging is free after the barrier)
+  double arr = 0.0, ary = 0.0, aee = 0.0;
+  const int rr = threadIdx.x % kRB, gq = threadIdx.x / kRB;
+  const int g0 = G * gq / kGrp, g1 = G * (gq + 1) / kGrp;
+  auto group_sum = [&](const double* P, int64_t E, int64_t i) {
+    double t = 0.0;
+    int cc = g0;
+    for (; cc + 8 <= g1; cc += 8) {
+      double v8[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        v8[u] = cs_lo(E, cc + u, G) < cs_lo(E, cc + u + 1, G) ? __ldcg(P + static_cast<int64_t>(cc + u) * ld + i) : 0.0;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) t += v8[u];
+    }
+    for (; cc < g1; ++cc)
+      if (cs_lo(E, cc, G) < cs_lo(E, cc + 1, G)) t += __ldcg(P + static_cast<int64_t>(cc) * ld + i);
+    return t;
+  };
+  for (int64_t rb = ilo; rb < ihi; rb += kRB) {
+    const int64_t ir = rb + rr;
+    __syncthreads();
+    gsum[gq * kRB + rr] = ir < ihi ? group_sum(p.up, Ea, ir) : 0.0;
+    if (fix) gsum[(kGrp + gq) * kRB + rr] = ir < ihi ? group_sum(p.dvp, Ef, ir) : 0.0;
+    __syncthreads();
+    if (threadIdx.x >= kRB || rb + threadIdx.x >= ihi) continue;
+    const int64_t i = rb + threadIdx.x;
+    double u = 0.0, f = 0.0;
+#pragma unroll
+    for (int q = 0; q < kGrp; ++q) u += gsum[q * kRB + threadIdx.x];
+    if (fix)
+#pragma unroll
+      for (int q = 0; q < kGrp; ++q) f += gsum[(kGrp + q) * kRB + threadIdx.x];
+    const bool first = rb == ilo && threadIdx.x < kLRB;  // prefetched by lists_issue
+    const double yi = first ? lp.y : p.y[i];
+    double v = 0.0;
+    if (shift) {
+      v = (first ? lp.u : __ldcg(p.U + i)) - f;  // v = u_old with the history fix (581-590, 673-684)
+      __stcg(p.V + i, v);
+    } else if (mom) {
+      v = first ? lp.v : __ldcg(p.V + i);
+    }
+    __stcg(p.U + i, u);
+    const double uw = mom ? (1.0 + m) * u - m * v : u;
+    const double r = i < p.n ? yi - uw : 0.0;
+    __stcg(p.rho + i, r);
+    arr = fma(r, r, arr);
+    ary = fma(yi, r, ary);
+    if (mom && i < p.n) {
+      const double e = yi - u;
+      aee = fma(e, e, aee);
+    }
+  }
+  double v[3] = {arr, ary, aee};
+  const bool mx[3] = {false, false, false};
+  block_reduce<3>(v, mx, sh);
+  if (threadIdx.x == 0) {
+    put_slot(p, kSlRhoSq, v[0]);
+    put_slot(p, kSlRhoY, v[1]);
+    put_slot(p, kSlRhoE, v[2]);
+  }
+}
+
 // ||x||_1 partial of this CTA's slice into the slot of iteration t
 __device__ __forceinline__ int l1_slot(uint64_t t) { return (t & 1) ? kSlL1b : kSlL1; }
 
@@ -2466,6 +2665,7 @@ __device__ __noinline__ void engine_body(const EngineParams& p, Sh& sh, double* 
     }
     {  // combine u (and v <- u_old - fix), then the next iteration's rho_g
       if (gram) combine_g(p, C_apply, fista, fix_pass);
+      else if (lists && colsplit_apply(p, sh, lp, lv)) combine_u_colsplit(p, sh, lv, S, shift_u, fix_pass, m_next, sc.red, lp);
       else if (lists) combine_u_lists(p, sh, lv, S, shift_u, fix_pass, m_next, sc.red, lp);
       else combine_u(p, sh, C_apply, shift_u, fix_pass, m_next);
     }

@@ -289,6 +289,7 @@ struct alignas(16) EngineParams {
   int32_t list_apply;  // 1: dense u = A x from the lists in phase E (FL1_LIST_APPLY)
   int32_t power_onchip;  // 1: cluster-mode power iterations on chip when they fit (FL1_POWER_ONCHIP)
   int32_t early_prox;    // 1: non-screening dense iterations run the prox before the first barrier (FL1_EARLY_PROX)
+  int64_t colsplit_elems;  // phase-E apply by column split when nnz x ld >= this (FL1_COLSPLIT; 0 = never)
   int32_t compact;       // 1: preserved columns physically compacted into cbuf (FL1_COMPACT, A/B switch)
   double* cbuf[2];       // ping-pong compact copies, ld x ceil(K/2) each
   int32_t* bcix[2];      // per bank: column slot of each position in the compact copy (csel != 0)

@@ -56,6 +56,7 @@ SWITCHES = [
     ("FL1_POWER_ONCHIP", "0"),     # cluster-mode power iterations streamed, not resident
     ("FL1_SINGLE_CLUSTER_SIZE", "16"),  # the single-cluster route on 16 CTAs (default 12 up to 8 MiB)
     ("FL1_COMPACT", "1"),          # preserved columns physically compacted (ActiveOp::maybe_compact)
+    ("FL1_COLSPLIT", "1"),         # phase-E apply by column split on every iteration
 ]
 
 CASES = {  # name, seed, n, k, nnz: c1 (single-cluster route) and a full-grid dense solve
