@@ -27,6 +27,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 
 namespace fl1 {
 
@@ -270,20 +271,30 @@ __global__ void __launch_bounds__(256) residual_norms_kernel(const double* __res
                                                               int64_t q, int T, const double* __restrict__ left,
                                                               const double* __restrict__ right, int64_t ldt,
                                                               const int* __restrict__ ranks, int n_ranks,
-                                                              double* __restrict__ eps, double* __restrict__ app) {
+                                                              double* __restrict__ eps, double* __restrict__ app,
+                                                              int smem_ok) {
   extern __shared__ double smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   const int64_t N = m * m, K = q * q;
+  const bool staged = smem_ok != 0;  // else the factors are read from global memory (L1 / L2)
   double* lsh = smem + static_cast<int64_t>(warp) * 2 * T * m;  // [t][i] left column jj, then [t][rr] right col s
   double* rsh = lsh + static_cast<int64_t>(T) * m;
   for (int64_t j = static_cast<int64_t>(blockIdx.x) * nw + warp; j < K; j += static_cast<int64_t>(gridDim.x) * nw) {
     const int64_t jj = j / q, s = j - jj * q;
-    for (int64_t e = lane; e < static_cast<int64_t>(T) * m; e += 32) {
-      const int64_t t = e / m, i = e - t * m;
-      lsh[e] = left[t * ldt + jj * m + i];   // left_t is m x q column-major: (i, jj)
-      rsh[e] = right[t * ldt + s * m + i];   // right_t (rr = i, s)
+    // left_t is m x q column-major: (i, jj); right_t (rr, s); stride between terms
+    const double* lg = left + jj * m;
+    const double* rg = right + s * m;
+    const int64_t ls = staged ? m : ldt;
+    if (staged) {
+      for (int64_t e = lane; e < static_cast<int64_t>(T) * m; e += 32) {
+        const int64_t t = e / m, i = e - t * m;
+        lsh[e] = lg[t * ldt + i];
+        rsh[e] = rg[t * ldt + i];
+      }
+      __syncwarp();
     }
-    __syncwarp();
+    const double* lp = staged ? lsh : lg;
+    const double* rp = staged ? rsh : rg;
     double e2[kMaxSnapshots], a2[kMaxSnapshots];
 #pragma unroll
     for (int l = 0; l < kMaxSnapshots; ++l) e2[l] = a2[l] = 0.0;
@@ -294,7 +305,7 @@ __global__ void __launch_bounds__(256) residual_norms_kernel(const double* __res
       double r = av;
       int l = 0;
       for (int t = 0; t < T && l < n_ranks; ++t) {
-        r = __dsub_rn(r, __dmul_rn(lsh[t * m + i], rsh[t * m + rr]));
+        r = __dsub_rn(r, __dmul_rn(lp[t * ls + i], rp[t * ls + rr]));
         if (t + 1 == ranks[l]) {
 #pragma unroll
           for (int z = 0; z < kMaxSnapshots; ++z)
@@ -359,15 +370,20 @@ cudaError_t residual_norms_launch(const double* a, int64_t lda, int64_t m, int64
                                   double* app, cudaStream_t stream) {
   if (n_ranks > kMaxSnapshots) return cudaErrorInvalidValue;
   const size_t per_warp = static_cast<size_t>(2) * T * m * sizeof(double);  // the warp's staged factor columns
-  const int warps = static_cast<int>(std::min<size_t>(8, (200 * 1024) / per_warp));
-  if (warps < 1) return cudaErrorInvalidValue;
-  const size_t smem = per_warp * warps;
+  const int fit = static_cast<int>(std::min<size_t>(8, (200 * 1024) / per_warp));
+  static const bool no_stage = [] {  // FL1_SUKRO_STAGE=0 forces the global-memory path (tests)
+    const char* e = std::getenv("FL1_SUKRO_STAGE");
+    return e && e[0] == '0';
+  }();
+  const bool staged = fit >= 1 && !no_stage;  // factor columns too long to stage: read them from global memory
+  const int warps = staged ? fit : 8;
+  const size_t smem = staged ? per_warp * warps : 0;
   cudaError_t e = cudaFuncSetAttribute(residual_norms_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
   if (e != cudaSuccess) return e;
   const int64_t K = q * q;
   residual_norms_kernel<<<static_cast<unsigned>(std::min<int64_t>((K + warps - 1) / warps, 8192)), 32 * warps, smem,
-                          stream>>>(a, lda, m, q, T, left, right, ldt, ranks, n_ranks, eps, app);
+                          stream>>>(a, lda, m, q, T, left, right, ldt, ranks, n_ranks, eps, app, staged ? 1 : 0);
   return cudaGetLastError();
 }
 

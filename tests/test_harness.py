@@ -6,6 +6,7 @@ from __future__ import annotations
 import json
 import math
 import os
+from pathlib import Path
 
 import numpy as np
 import pytest
@@ -274,6 +275,30 @@ def test_sukro_construction_on_gpu_matches_restatement(cuda, oracle, n, k, scena
             assert np.allclose(ko, kr, atol=1e-10)
     if n == 2500:
         assert [o.rc for o in ours] == [0.15, 0.30, 0.45, 0.60]
+
+
+@pytest.mark.gpu
+def test_sukro_residual_norms_unstaged_path(oracle, tmp_path):
+    """The residual-norm pass reads the factor columns from global memory when they are too
+    long to stage in shared memory (forced here with FL1_SUKRO_STAGE=0, in a child process):
+    same levels as the LAPACK restatement."""
+    import subprocess
+    import sys
+
+    code = (
+        "import sys, numpy as np; sys.path.insert(0, sys.argv[1]); sys.path.insert(0, sys.argv[1] + '/tests');"
+        "from paper_1812_06635_b200 import harness as H, _abi, fastl1 as F;"
+        "from _refgen import RefGen;"
+        "orc = F.Backend(_abi.Library(sys.argv[1] + '/oracle/_build/libfl1oracle.so', 'orc_', extra=_abi.ORACLE_ONLY));"
+        "rg = RefGen(orc); a = rg.synthesize_scenario(64, 256, 'moderate', 5);"
+        "ours = H.build_sukro_levels(a, [1, 2, 4]); ref = rg.build_sukro_sequence(a, [1, 2, 4]);"
+        "assert all(np.allclose(o.eps, r['eps'], rtol=1e-9, atol=1e-12) and "
+        "np.allclose(o.approx_norms, r['approx_norms'], rtol=1e-9, atol=1e-12) for o, r in zip(ours, ref));"
+        "print('ok')")
+    root = str(Path(__file__).resolve().parents[1])
+    env = dict(os.environ, FL1_SUKRO_STAGE="0")
+    out = subprocess.run([sys.executable, "-c", code, root], env=env, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]
 
 
 @pytest.mark.gpu
