@@ -1,5 +1,5 @@
 import os, sys, time
-sys.path.insert(0, os.path.join(os.path.dirname(__file__), '..'))
+sys.path.insert(0, os.path.join(os.path.dirname(__file__), '..', '..'))
 import numpy as np
 import bench
 from paper_1812_06635_b200 import fastl1 as F

@@ -1,6 +1,6 @@
 """c5 batched path: wall vs batch device time vs Python collection, per mode."""
 import os, sys, time
-sys.path.insert(0, os.path.join(os.path.dirname(__file__), '..'))
+sys.path.insert(0, os.path.join(os.path.dirname(__file__), '..', '..'))
 import numpy as np, torch
 import bench
 from paper_1812_06635_b200 import fastl1 as F

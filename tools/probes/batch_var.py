@@ -1,6 +1,6 @@
 """Per-call wall time of the batched cluster path, device vs host Y, alternating."""
 import os, sys, time
-sys.path.insert(0, os.path.join(os.path.dirname(__file__), '..'))
+sys.path.insert(0, os.path.join(os.path.dirname(__file__), '..', '..'))
 import numpy as np, torch
 import bench
 from paper_1812_06635_b200 import fastl1 as F

@@ -1,6 +1,6 @@
 """c1 single solve: full cooperative grid vs one thread-block cluster (batched entry, B = 1)."""
 import os, sys
-sys.path.insert(0, os.path.join(os.path.dirname(__file__), '..'))
+sys.path.insert(0, os.path.join(os.path.dirname(__file__), '..', '..'))
 import numpy as np
 from paper_1812_06635_b200 import fastl1 as F, synthetic as syn
 os.environ["FL1_BATCH_PREFIX"] = "0"

@@ -2,7 +2,7 @@
 mean preserved-set size and mean nnz of x (where the apply u = A x_next spends)."""
 import sys
 from pathlib import Path
-sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+sys.path.insert(0, str(Path(__file__).resolve().parents[2]))
 import numpy as np, torch
 import bench
 from paper_1812_06635_b200 import fastl1 as F, synthetic as syn

@@ -1,7 +1,7 @@
 """c5 signals on the per-signal engines only (FL1_BATCH_PREFIX=0; cluster size from argv):
 per-signal device time against iterations and power steps -> cost per iteration."""
 import os, sys
-sys.path.insert(0, os.path.join(os.path.dirname(__file__), '..'))
+sys.path.insert(0, os.path.join(os.path.dirname(__file__), '..', '..'))
 os.environ['FL1_BATCH_PREFIX'] = '0'
 import numpy as np, torch
 import bench

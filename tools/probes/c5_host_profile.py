@@ -1,7 +1,7 @@
 """Host-side cost of the batched entry point (c5): library call vs result collection vs free."""
 import os, sys, time
 import ctypes as C
-sys.path.insert(0, os.path.join(os.path.dirname(__file__), '..'))
+sys.path.insert(0, os.path.join(os.path.dirname(__file__), '..', '..'))
 import numpy as np
 import bench
 from paper_1812_06635_b200 import fastl1 as F, _abi

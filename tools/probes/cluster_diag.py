@@ -1,6 +1,6 @@
 """Where does a cluster-mode solve first differ from the oracle / the grid-mode solve?"""
 import os, sys
-sys.path.insert(0, os.path.join(os.path.dirname(__file__), '..'))
+sys.path.insert(0, os.path.join(os.path.dirname(__file__), '..', '..'))
 sys.path.insert(0, os.path.join(os.path.dirname(__file__), '..', 'tests'))
 import numpy as np
 from paper_1812_06635_b200 import fastl1 as F, synthetic as syn, _abi

@@ -1,6 +1,6 @@
 """Direct vs Gram-backed exact phase on BASELINE c1 / c2 (device time per solve)."""
 import os, sys, time
-sys.path.insert(0, os.path.join(os.path.dirname(__file__), '..'))
+sys.path.insert(0, os.path.join(os.path.dirname(__file__), '..', '..'))
 import numpy as np
 from paper_1812_06635_b200 import fastl1 as F, synthetic as syn
 for name in ("c1", "c2"):

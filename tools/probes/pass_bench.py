@@ -1,7 +1,7 @@
 """Streaming-pass bandwidth probe: a few unscreened iterations at a given shape,
 read back the device phase profile (A^T r bytes / phase-A time)."""
 import os, sys, time
-sys.path.insert(0, os.path.join(os.path.dirname(__file__), '..'))
+sys.path.insert(0, os.path.join(os.path.dirname(__file__), '..', '..'))
 import numpy as np
 import torch
 from paper_1812_06635_b200 import fastl1 as F

@@ -1,6 +1,6 @@
 """Per-step cost of the cold restricted power iteration vs working-set size."""
 import os, sys
-sys.path.insert(0, os.path.join(os.path.dirname(__file__), '..'))
+sys.path.insert(0, os.path.join(os.path.dirname(__file__), '..', '..'))
 import numpy as np
 import torch
 from paper_1812_06635_b200 import fastl1 as F

@@ -1,6 +1,6 @@
 """Cold restricted power iteration on dense 2500 x K dictionaries: per-step phase times (FL1_UTIL_LOG)."""
 import os, sys, time
-sys.path.insert(0, os.path.join(os.path.dirname(__file__), '..'))
+sys.path.insert(0, os.path.join(os.path.dirname(__file__), '..', '..'))
 os.environ['FL1_UTIL_LOG'] = '1'
 import numpy as np
 from paper_1812_06635_b200 import fastl1 as F

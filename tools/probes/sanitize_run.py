@@ -2,7 +2,7 @@
 synccheck): grid mode (bulk-ring power iterations), single cluster, SuKro switching,
 Gram mode, lockstep batched + cluster hand-off. Each result is checked for convergence."""
 import os, sys
-sys.path.insert(0, os.path.join(os.path.dirname(__file__), '..'))
+sys.path.insert(0, os.path.join(os.path.dirname(__file__), '..', '..'))
 import numpy as np
 from paper_1812_06635_b200 import fastl1 as F, synthetic as syn
 

@@ -1,6 +1,6 @@
 """Single-solve device time, grid vs one 16-CTA cluster, across dictionary sizes."""
 import os, sys
-sys.path.insert(0, os.path.join(os.path.dirname(__file__), '..'))
+sys.path.insert(0, os.path.join(os.path.dirname(__file__), '..', '..'))
 import numpy as np
 from paper_1812_06635_b200 import fastl1 as F, synthetic as syn
 import bench

@@ -1,6 +1,6 @@
 """One solve of a BASELINE config on the CUDA library; prints a one-line summary."""
 import os, sys
-sys.path.insert(0, os.path.join(os.path.dirname(__file__), '..'))
+sys.path.insert(0, os.path.join(os.path.dirname(__file__), '..', '..'))
 import numpy as np
 from paper_1812_06635_b200 import fastl1 as F, synthetic as syn
 name = sys.argv[1] if len(sys.argv) > 1 else 'c2'

@@ -1,6 +1,6 @@
 """One c3 (SuKro switching) solve on the CUDA library, after the per-level L cache."""
 import os, sys
-sys.path.insert(0, os.path.join(os.path.dirname(__file__), '..'))
+sys.path.insert(0, os.path.join(os.path.dirname(__file__), '..', '..'))
 from paper_1812_06635_b200 import fastl1 as F, synthetic as syn
 inst = syn.sukro_instance(seed=3)
 seq = syn.sukro_sequence(inst)
