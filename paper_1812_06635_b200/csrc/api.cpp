@@ -1291,6 +1291,11 @@ void solve_clusters(fl1_seq* s, const double* Y, bool y_device, int64_t ldy, con
     if (const char* pol = std::getenv("FL1_LOCKSTEP_POLICY")) pp.policy = std::atoi(pol);
     const char* smode = std::getenv("FL1_SPLIT_MODE");
     pp.split_mode = smode ? std::atoi(smode) : 1;
+    const char* sb = std::getenv("FL1_SPLIT_BUDGET_MB");
+    // split-K partials capped at 24 MiB per contraction: they stay L2-resident beside the
+    // 33.5 MB dictionary instead of round-tripping DRAM (c5: lockstep DRAM 19.8 -> ~9 GB,
+    // 55.7 -> 55.3 ms; 16 MiB costs waves, 32-48 MiB the same)
+    pp.split_budget = sb ? (std::atoll(sb) << 20) : (24ll << 20);
     const char* nm = std::getenv("FL1_LOCKSTEP_NARROW");
     pp.narrow = nm ? std::atoi(nm) : 1;
     const char* wt = std::getenv("FL1_LOCKSTEP_WIDTH");

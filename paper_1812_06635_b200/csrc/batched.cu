@@ -234,10 +234,10 @@ __device__ __forceinline__ int tile_ct(int n, int width_tiles) {
 // split-K factor for T output tiles of nch K-chunks on G CTAs: the fewest-waves choice,
 // cost ceil(T s / G) / s (tile waves in units of a whole tile) plus ~2% per extra part
 // (partial write + read, per-item prologue), each part at least 4 chunks deep
-__device__ __forceinline__ int split_for(int T, int G, int nch) {
+__device__ __forceinline__ int split_for(int T, int G, int nch, int smax = kSplitMax) {
   int best = 1;
   float best_cost = static_cast<float>((T + G - 1) / G) * 1.02f;
-  for (int s = 2; s <= kSplitMax && nch / s >= 4; ++s) {
+  for (int s = 2; s <= smax && s <= kSplitMax && nch / s >= 4; ++s) {
     const float cost = static_cast<float>((T * s + G - 1) / G) / static_cast<float>(s) * (1.0f + 0.02f * s);
     if (cost < best_cost) {
       best = s;
@@ -245,6 +245,14 @@ __device__ __forceinline__ int split_for(int T, int G, int nch) {
     }
   }
   return best;
+}
+
+// split parts allowed by the partial-buffer budget (FL1_SPLIT_BUDGET_MB: partials that
+// stay L2-resident instead of round-tripping DRAM); out = output elements of the product
+__device__ __forceinline__ int split_cap(const PrefixParams& p, int64_t out) {
+  if (p.split_budget <= 0 || out <= 0) return kSplitMax;
+  const int64_t c = p.split_budget / (out * 8);
+  return static_cast<int>(c < 1 ? 1 : (c > kSplitMax ? kSplitMax : c));
 }
 
 __device__ __forceinline__ int split_old(int T, int G) {
@@ -1169,7 +1177,8 @@ __global__ void __launch_bounds__(kPT, 1) prefix_kernel(const __grid_constant__ 
     } else if (n_pow > 0) {
       const int n_rt = static_cast<int>((ld + kTM - 1) / kTM);
       const int n_ct = (n_pow + kTN - 1) / kTN;
-      const int sk = p.split_mode ? split_for(n_rt * n_ct, gridDim.x, static_cast<int>((K + kTK - 1) / kTK))
+      const int sk = p.split_mode ? split_for(n_rt * n_ct, gridDim.x, static_cast<int>((K + kTK - 1) / kTK),
+                                              split_cap(p, ld * n_pow))
                                   : split_old(n_rt * n_ct, gridDim.x);
       for (int item = blockIdx.x; item < n_rt * n_ct * sk; item += gridDim.x) {
         const int tile = item % (n_rt * n_ct), kp = item / (n_rt * n_ct);
@@ -1200,7 +1209,8 @@ __global__ void __launch_bounds__(kPT, 1) prefix_kernel(const __grid_constant__ 
     } else {
       const int n_rt = static_cast<int>((K + kTM - 1) / kTM);
       const int n_ct = (n_act + kTN - 1) / kTN;
-      sk = p.split_mode ? split_for(n_rt * n_ct, gridDim.x, static_cast<int>((ld + kTK - 1) / kTK))
+      sk = p.split_mode ? split_for(n_rt * n_ct, gridDim.x, static_cast<int>((ld + kTK - 1) / kTK),
+                                    split_cap(p, K * n_act))
                         : split_old(n_rt * n_ct, gridDim.x);
       for (int item = blockIdx.x; item < n_rt * n_ct * sk; item += gridDim.x) {
         const int tile = item % (n_rt * n_ct), kp = item / (n_rt * n_ct);
