@@ -49,7 +49,10 @@ constexpr int kRT = kTM / 8 / kWR, kCT = kTN / 8 / kWC;
 constexpr int kTK = 32;             // K chunk (rows of A / rho)
 constexpr int kSS = kTK + 4;        // padded smem row stride (doubles)
 constexpr int kStage = (kTM + kTN) * kSS;  // doubles per pipeline stage
-constexpr int kStages = 2;                 // cp.async pipeline depth (3 measured no faster)
+#ifndef FL1_PREFIX_STAGES
+#define FL1_PREFIX_STAGES 2
+#endif
+constexpr int kStages = FL1_PREFIX_STAGES;  // cp.async pipeline depth (3 measured no faster)
 constexpr unsigned kAll = 0xffffffffu;
 constexpr int kSplitMax = 16;      // split-K parts of the contractions (load balance)
 
