@@ -1325,6 +1325,13 @@ void solve_clusters(fl1_seq* s, const double* Y, bool y_device, int64_t ldy, con
     pp.steps_out = reinterpret_cast<int32_t*>(pb + q_n);
     pp.queue = pp.steps_out + 1;
     pp.work_out = reinterpret_cast<int64_t*>(pb + q_n) + 2;
+    static std::unique_ptr<DevBuf> sigprof;
+    if (const char* sp = std::getenv("FL1_SIGPROF_OUT")) {  // diagnostics builds only (FL1_SIGPROF)
+      if (!sigprof) sigprof = std::make_unique<DevBuf>(16 * sizeof(double));
+      ck(cudaMemset(sigprof->p, 0, 16 * sizeof(double)), "sigprof");
+      pp.sigprof = sigprof->as<double>();
+      (void)sp;
+    }
     if (std::getenv("FL1_STEP_LOG")) {  // diagnostics: per-step occupancy of the lockstep engine
       pp.max_log = 4096;
       step_log = std::make_unique<DevBuf>(sizeof(double) * 5 * pp.max_log);
@@ -1399,6 +1406,14 @@ void solve_clusters(fl1_seq* s, const double* Y, bool y_device, int64_t ldy, con
   if (use_prefix) {  // lockstep accounting (signal 0's profile): steps and contraction widths
     ck(cudaMemcpy(&lk_steps, d_steps, sizeof(lk_steps), cudaMemcpyDeviceToHost), "steps");
     ck(cudaMemcpy(lk_work, pp.work_out, sizeof(lk_work), cudaMemcpyDeviceToHost), "work");
+  }
+  if (const char* sp = std::getenv("FL1_SIGPROF_OUT"); sp && pp.sigprof) {
+    double h[16];
+    ck(cudaMemcpy(h, pp.sigprof, sizeof(h), cudaMemcpyDeviceToHost), "sigprof");
+    if (FILE* f = std::fopen(sp, "w")) {
+      for (double v : h) std::fprintf(f, "%g\n", v);
+      std::fclose(f);
+    }
   }
   if (step_log && d_steps) {
     int32_t steps = 0;

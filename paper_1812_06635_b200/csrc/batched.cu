@@ -72,6 +72,20 @@ __device__ __forceinline__ void cp_wait1() { asm volatile("cp.async.wait_group 1
 __device__ __forceinline__ void cp_wait_pipe() { asm volatile("cp.async.wait_group %0;\n" ::"n"(kStages - 2)); }
 __device__ __forceinline__ void cp_wait0() { asm volatile("cp.async.wait_group 0;\n" ::); }
 
+#ifdef FL1_SIGPROF  // diagnostics build: per-phase time of CTA 0's per-signal FISTA steps
+#define SIGPROF(k)                                                            \
+  do {                                                                        \
+    if (p.sigprof && blockIdx.x == 0 && threadIdx.x == 0) {                   \
+      const double t_ = gtimer();                                             \
+      p.sigprof[k] += t_ - p.sigprof[15];                                     \
+      p.sigprof[15] = t_;                                                     \
+    }                                                                         \
+  } while (0)
+#else
+#define SIGPROF(k) \
+  do {             \
+  } while (0)
+#endif
 __device__ __forceinline__ double gtimer() {
   uint64_t t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -765,6 +779,7 @@ __device__ __noinline__ void fista_step(const PrefixParams& p, PSh& sh, int64_t 
   const WarpRange wr(K);
   double* cr = p.corr + a * K;
   int8_t* mk = p.mask + b * K;
+  SIGPROF(14);
   // corr = sum of the split-K parts, written back to part 0; max |corr| over the set
   // (all kIt atoms of a lane loaded together: one L2 round trip per split part)
   double dp = 0.0;
@@ -781,6 +796,7 @@ __device__ __noinline__ void fista_step(const PrefixParams& p, PSh& sh, int64_t 
     }
   }
   dp = block_max(dp, sh);
+  SIGPROF(0);
   if (threadIdx.x == 0) {
     double m = 0.0, t_next = sg.t_k;  // 465-470
     if (p.solver == FL1_FISTA && sg.ready) {
@@ -818,6 +834,7 @@ __device__ __noinline__ void fista_step(const PrefixParams& p, PSh& sh, int64_t 
     sh.screen = screen;
   }
   __syncthreads();
+  SIGPROF(1);
   if (sh.release == 3) {
     handoff_signal(p, sh, b, t0);
     return;
@@ -924,6 +941,7 @@ __device__ __noinline__ void fista_step(const PrefixParams& p, PSh& sh, int64_t 
     sh.fxc[w] = fx_c;
   }
   block_sum3(red3, sh);  // (syncs: the warp counts are visible after it)
+  SIGPROF(2);
   const int64_t S_new = static_cast<int64_t>(red3[0]);
   const double nnz = red3[1], l1n = red3[2];
   // FISTA bookkeeping (581-590): x_prev = x, v = u (the old u buffer, minus the fix), x = x_next
@@ -937,10 +955,12 @@ __device__ __noinline__ void fista_step(const PrefixParams& p, PSh& sh, int64_t 
     apply_segments(p, us, fx_v, fx_j, seg, sh.fxc, 1.0);
     for (int64_t i = threadIdx.x; i < ld; i += kPT) const_cast<double*>(uo)[i] = us[i];
   }
+  SIGPROF(3);
   for (int64_t i = threadIdx.x; i < ld; i += kPT) us[i] = 0.0;
   __syncthreads();
   apply_segments(p, us, nz_v, nz_j, seg, sh.nzc, 1.0);  // u = A x (ActiveOp::apply 131-146)
   for (int64_t i = threadIdx.x; i < ld; i += kPT) un[i] = us[i];
+  SIGPROF(4);
   if (threadIdx.x == 0) {
     if (fista) {
       if (sg.ready) sg.t_k = sh.t_next;
@@ -976,6 +996,8 @@ __device__ __noinline__ void fista_step(const PrefixParams& p, PSh& sh, int64_t 
   } else {
     compute_rho(p, sh, b);
   }
+  SIGPROF(5);
+  if (p.sigprof && blockIdx.x == 0 && threadIdx.x == 0) p.sigprof[13] += 1.0;
 }
 
 // ---------------------------------------------------------------------------

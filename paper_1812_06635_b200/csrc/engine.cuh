@@ -192,6 +192,7 @@ struct PrefixParams {
   int32_t policy;             // hand-off: 0 never, 1 at the first shrink, 2 after the first power iteration
   int32_t split_mode;         // split-K choice of the contractions: 1 fewest waves, 0 fill-only (FL1_SPLIT_MODE)
   int32_t narrow;             // 1: steps with <= 12 unfinished signals use the CUDA-core products (FL1_LOCKSTEP_NARROW)
+  double* sigprof;            // diagnostics builds (FL1_SIGPROF): 16 accumulators, CTA 0's per-signal phases
   int64_t split_budget;       // bytes of split-K partials per contraction (FL1_SPLIT_BUDGET_MB; 0 = unlimited)
   int32_t width_tiles;        // 1: contraction tiles 16 / 32 / 64 signals wide by step width (FL1_LOCKSTEP_WIDTH)
   int64_t* work_out;          // [2]: sum over steps of the unfinished / power-step signal counts
