@@ -301,8 +301,16 @@ def test_sukro_residual_norms_unstaged_path(oracle, tmp_path):
     assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]
 
 
+def _paper_config(tmp):
+    """The paper's SuKro experiment shape: N = 2500, K = 10000, SuKro
+    ranks 5 / 10 / 15 / 20 (RC 0.15 / 0.30 / 0.45 / 0.60), one trial, one lambda."""
+    return H.ExperimentConfig(n=2500, k=10000, scenario="moderate", lambda_ratios=[0.3], tol=1e-5, ranks=[5, 10, 15, 20],
+                              trials=1, seed=3, out=str(tmp), use_gram=False, screen_interval=10)
+
+
 @pytest.mark.gpu
-def test_sweep_csvs_match_oracle(cuda, oracle, tmp_path, monkeypatch):
+@pytest.mark.parametrize("shape", ["small", "paper"])
+def test_sweep_csvs_match_oracle(cuda, oracle, tmp_path, monkeypatch, shape):
     """one ExperimentConfig swept on the CUDA library and on the oracle (the
     same SuKro levels, built once on the device, feed both): trace / summary / percentile
     CSVs are identical in every integer and string column (iterations, dictionary index,
@@ -310,8 +318,14 @@ def test_sweep_csvs_match_oracle(cuda, oracle, tmp_path, monkeypatch):
     the floating ones (gap, gamma); only the wall-clock columns differ (bench.cpp:255-421)."""
     import _parity as P
 
-    cfg = small_config(tmp_path / "gpu")
-    cfg.lambda_ratios = [0.3, 0.6]
+    if shape == "small":
+        cfg = small_config(tmp_path / "gpu")
+        cfg.lambda_ratios = [0.3, 0.6]
+        cfg_o = small_config(tmp_path / "orc")
+        cfg_o.lambda_ratios = [0.3, 0.6]
+    else:
+        cfg, cfg_o = _paper_config(tmp_path / "gpu"), _paper_config(tmp_path / "orc")
+        oracle.lib.set_threads(os.cpu_count() or 1)
     a = H.synthesize_scenario(cfg.n, cfg.k, cfg.scenario, cfg.seed)
     levels = H.build_sukro_levels(a, cfg.ranks, backend=cuda)
     drawn = {}
@@ -324,8 +338,6 @@ def test_sweep_csvs_match_oracle(cuda, oracle, tmp_path, monkeypatch):
 
     monkeypatch.setattr(H, "draw_signal", draw_once)
     H.run_sweep(cfg, backend=cuda, levels=levels)
-    cfg_o = small_config(tmp_path / "orc")
-    cfg_o.lambda_ratios = [0.3, 0.6]
     H.run_sweep(cfg_o, backend=oracle, levels=levels)
     walls = {"trace.csv": {10}, "summary.csv": {5, 6, 7, 13, 14}, "percentiles.csv": set()}
     floats = {"trace.csv": {7, 8}, "summary.csv": set(), "percentiles.csv": set()}

@@ -52,6 +52,32 @@ def test_dense_configs_full_size(cuda, oracle16, name):
     assert g.final_gap <= 1e-6 * primal(inst.a, inst.y, inst.lam, g.x) * (1 + 1e-9)
 
 
+@pytest.mark.parametrize("solver,rule,pre", [(F.SOLVER_ISTA, F.RULE_GAP, False), (F.SOLVER_FISTA, F.RULE_DYNAMIC, False),
+                                             (F.SOLVER_FISTA, F.RULE_DYNAMIC, True)])
+def test_c2_full_size_solver_rule_variants(cuda, oracle16, solver, rule, pre):
+    """BASELINE configs[1] at full size under the other solver / rule / precompute_aty
+    settings of the reference (fastl1.hpp:25-31, 85-96): ISTA with GAP, FISTA with the
+    Dynamic Safe rule, and Dynamic with precompute_aty (fastl1.cpp:291-304, 521-548)."""
+    inst = syn.dense_instance("c2")
+    L = F.lipschitz_bound(F.DenseDictionary(inst.a, backend=cuda))
+    cfg = F.SwitchConfig(screening_interval=10, max_iterations=5000, rel_tolerance=1e-6, precompute_aty=pre)
+    opts = F.RunOptions(solver=solver, rule=rule, variant=F.VARIANT_SCREENED, full_lipschitz=[L])
+    g, o = run_both(cuda, oracle16, lambda b: F.ApproxSequence([F.make_exact_approx(F.DenseDictionary(inst.a, backend=b))]),
+                    inst.y, inst.lam, cfg, opts)
+    assert_parity(g, o, inst.a, inst.y, inst.lam)
+
+
+@pytest.mark.parametrize("rule,pre", [(F.RULE_DYNAMIC, False), (F.RULE_DYNAMIC, True)])
+def test_kronecker_sum_config_dynamic_rule(cuda, oracle16, rule, pre):
+    """BASELINE configs[2] at full size (4096 x 16384, A1 -> A2 -> A4 -> A) with the stable
+    Dynamic Safe rule (and precompute_aty: the exact level's A^T y for the dots)."""
+    inst = syn.sukro_instance(seed=3)
+    cfg = F.SwitchConfig(screening_interval=10, max_iterations=5000, rel_tolerance=1e-6, gamma_threshold=0.5,
+                         precompute_aty=pre)
+    g, o = run_both(cuda, oracle16, lambda b: _sukro_seq(inst, b), inst.y, inst.lam, cfg, F.RunOptions(rule=rule))
+    assert_parity(g, o, inst.a, inst.y, inst.lam)
+
+
 def test_cold_lipschitz_matches_oracle(cuda, oracle16):
     inst = syn.dense_instance("c1")
     lg = F.lipschitz_bound(F.DenseDictionary(inst.a, backend=cuda))
