@@ -1180,6 +1180,13 @@ void solve_clusters(fl1_seq* s, const double* Y, bool y_device, int64_t ldy, con
   auto at = [&](size_t off) { return pin + (off - o_params); };
 
   EngineParams* params = reinterpret_cast<EngineParams*>(at(o_params));
+  // instrumented builds (FL1_TIMELINE): per-iteration phase marks of a one-signal call
+  std::unique_ptr<DevBuf> timeline;
+  const char* tl_path = batch == 1 ? std::getenv("FL1_TIMELINE_OUT") : nullptr;
+  if (tl_path) {
+    timeline = std::make_unique<DevBuf>(static_cast<size_t>(4096) * csize * 8 * sizeof(uint64_t));
+    ck(cudaMemset(timeline->p, 0, timeline->bytes), "timeline memset");
+  }
   for (int q = 0; q < n_clusters; ++q) {
     EngineParams& p = params[q];
     p = EngineParams{};
@@ -1190,6 +1197,7 @@ void solve_clusters(fl1_seq* s, const double* Y, bool y_device, int64_t ldy, con
     p.k = k;
     p.ld = ld;
     p.trace_cap = cap;
+    if (timeline) p.timeline = timeline->as<uint64_t>();
   }
   fl1::BatchDesc bd{};
   bd.batch = batch;
@@ -1398,6 +1406,14 @@ void solve_clusters(fl1_seq* s, const double* Y, bool y_device, int64_t ldy, con
   }
   ck(cudaStreamSynchronize(stream), "download sync");
   hlog("downloaded");
+  if (timeline) {
+    std::vector<uint64_t> h(timeline->bytes / sizeof(uint64_t));
+    ck(cudaMemcpy(h.data(), timeline->p, timeline->bytes, cudaMemcpyDeviceToHost), "timeline");
+    if (FILE* f = std::fopen(tl_path, "wb")) {
+      std::fwrite(h.data(), sizeof(uint64_t), h.size(), f);
+      std::fclose(f);
+    }
+  }
   float batch_ms = 0.f, lockstep_ms = 0.f;
   ck(cudaEventElapsedTime(&batch_ms, ev0, ev1), "elapsed");
   ck(cudaEventElapsedTime(&lockstep_ms, ev0, evp), "elapsed");

@@ -1,11 +1,11 @@
-"""Per-phase timeline of a dense solve (c1/c2), instrumented build (FL1_TIMELINE=1)."""
+"""Per-phase timeline of a dense solve (c1 on the single-cluster route, or c2 with FL1_SINGLE_CLUSTER=0), instrumented build."""
 import os, sys
 sys.path.insert(0, os.path.join(os.path.dirname(__file__), '..'))
 import numpy as np
 os.environ['FL1_LIB'] = os.path.join(os.path.dirname(__file__), '..', 'paper_1812_06635_b200/_build/libfl1cuda_timeline.so')
 os.environ['FL1_TIMELINE_OUT'] = '/tmp/fl1_timeline.bin'
 from paper_1812_06635_b200 import fastl1 as F, synthetic as syn
-name = sys.argv[1] if len(sys.argv) > 1 else 'c2'
+name = sys.argv[1] if len(sys.argv) > 1 else 'c1'
 inst = syn.dense_instance(name)
 d = F.DenseDictionary(inst.a); L = F.lipschitz_bound(d)
 seq = F.ApproxSequence([F.make_exact_approx(d)])
@@ -18,7 +18,7 @@ G = raw.size // (4096 * 8)
 tl = raw.reshape(4096, G, 8).astype(np.float64)
 its = out.iterations
 names = ['A', 'sync1', 'Bscal', 'Bapply', 'sync2', 'E', 'sync3', 'tail']
-print(f"{name}: {its} iterations, grid {G}, device {out.device_ms:.3f} ms, power steps {out.power_iterations}, "
+print(f"{name}: {its} iterations, CTAs {G}, device {out.device_ms:.3f} ms, power steps {out.power_iterations}, "
       f"profile {np.round(out.profile[:5]/1e6,3)}")
 tot = np.zeros(8)
 for t in range(its - 1):
