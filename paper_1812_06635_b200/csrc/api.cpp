@@ -392,7 +392,7 @@ size_t carve(EngineParams& p, char* base, int64_t n, int64_t k, int64_t ld, int 
     const char* ep = std::getenv("FL1_EARLY_PROX");
     p.early_prox = ep ? std::atoi(ep) : 1;
     const char* cs = std::getenv("FL1_COLSPLIT");
-    p.colsplit_elems = cs ? std::atoll(cs) : (4ll << 20);
+    p.colsplit_elems = cs ? std::atoll(cs) : (2ll << 20);
   }
   p.pv = c.take<double>(kk);
   p.pw = c.take<double>(kk);

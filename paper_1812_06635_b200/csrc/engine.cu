@@ -1563,7 +1563,9 @@ __device__ __noinline__ void combine_u_lists(const EngineParams& p, Sh& sh, cons
 // sums the non-empty partials in CTA order for its row slice (fixed order: reproducible).
 constexpr int kCsRows = 8;     // rows per thread per row tile (row tile = 8 * kThreads rows)
 constexpr int kCsStage = 512;  // list entries staged in shared memory per round
-constexpr int64_t kCsMinLd = 4096;  // shorter columns: the row-slice gather is as fast (c2: 6.45 vs 6.50 ms)
+constexpr int64_t kCsMinLd = 8192;  // shorter columns: the row-slice gather is faster (c2 6.43 vs 6.48-7.67 ms, c3 8.64 vs 9.24)
+constexpr int64_t kCsRowGroup = 2048;  // rows per row group of the 2D partition (16 KiB column pieces)
+constexpr int kCsMaxRG = 8;
 
 __device__ __forceinline__ int64_t cs_lo(int64_t E, int c, int G) { return E * c / G; }
 
@@ -1590,11 +1592,11 @@ __device__ __forceinline__ void colsplit_stage(const int32_t* pp, int G, int64_t
 
 __device__ void colsplit_partial(const EngineParams& p, const double* __restrict__ A, int64_t ld, int64_t S, int G,
                                  const int32_t* pp, const double* lv_v, const int32_t* lv_j, int64_t e0, int64_t e1,
-                                 double* __restrict__ out, int32_t* ej, double* ev) {
+                                 int64_t row_lo, int64_t row_hi, double* __restrict__ out, int32_t* ej, double* ev) {
   constexpr int kB = 4;  // columns per batch of loads
   const bool once = e1 - e0 <= kCsStage;
   if (once) colsplit_stage(pp, G, S, lv_v, lv_j, e0, static_cast<int>(e1 - e0), ej, ev);
-  for (int64_t r0 = 0; r0 < ld; r0 += kCsRows * kThreads) {
+  for (int64_t r0 = row_lo; r0 < row_hi; r0 += kCsRows * kThreads) {
     double acc[kCsRows];
 #pragma unroll
     for (int r = 0; r < kCsRows; ++r) acc[r] = 0.0;
@@ -1609,7 +1611,7 @@ __device__ void colsplit_partial(const EngineParams& p, const double* __restrict
           const double* col = A + static_cast<int64_t>(on ? ej[q + u] : 0) * ld + r0 + threadIdx.x;
 #pragma unroll
           for (int r = 0; r < kCsRows; ++r)
-            av[u][r] = (on && r0 + threadIdx.x + r * kThreads < ld) ? __ldcs(col + r * kThreads) : 0.0;
+            av[u][r] = (on && r0 + threadIdx.x + r * kThreads < row_hi) ? __ldcs(col + r * kThreads) : 0.0;
         }
 #pragma unroll
         for (int u = 0; u < kB; ++u) {
@@ -1622,14 +1624,14 @@ __device__ void colsplit_partial(const EngineParams& p, const double* __restrict
 #pragma unroll
     for (int r = 0; r < kCsRows; ++r) {
       const int64_t i = r0 + threadIdx.x + r * kThreads;
-      if (i < ld) __stcg(out + i, acc[r]);
+      if (i < row_hi) __stcg(out + i, acc[r]);
     }
   }
 }
 
 // Column split when the listed columns are long and many (identical decision in every
 // CTA: the list lengths are read by all): ld >= kCsMinLd and E entries x ld rows >=
-// p.colsplit_elems (FL1_COLSPLIT, default 4 Mi: c4 phase E 54 -> 46 ms over the path).
+// p.colsplit_elems (FL1_COLSPLIT, default 2 Mi: c4 phase E 54 -> 37 ms over the path).
 __device__ __forceinline__ bool colsplit_apply(const EngineParams& p, Sh& sh, const ListPre& lp, const DevLevel& lv) {
   if (p.colsplit_elems <= 0 || lv.kind != kDense || lv.rows != 0 || p.ld < kCsMinLd) return false;
   const int G = vsize();
@@ -1676,13 +1678,22 @@ __device__ __noinline__ void combine_u_colsplit(const EngineParams& p, Sh& sh, c
   __syncthreads();
   const int64_t ld = p.ld;
   const int64_t Ea = pre[G], Ef = fix ? pre[(G + 1) + G] : 0;
-  // a CTA with an empty range writes nothing; the combine skips it (ranges are known to all)
-  if (cs_lo(Ea, c, G) < cs_lo(Ea, c + 1, G))
-    colsplit_partial(p, lv.a, ld, S, G, pre, p.nzv, p.nzj, cs_lo(Ea, c, G), cs_lo(Ea, c + 1, G),
-                     p.up + static_cast<int64_t>(c) * ld, ej, ev);
-  if (cs_lo(Ef, c, G) < cs_lo(Ef, c + 1, G))
-    colsplit_partial(p, lv.a, ld, S, G, pre + (G + 1), p.fxv, p.fxj, cs_lo(Ef, c, G), cs_lo(Ef, c + 1, G),
-                     p.dvp + static_cast<int64_t>(c) * ld, ej, ev);
+  // 2D partition: RG row groups x CG column groups; CTA c = rg + RG cg takes the rows of
+  // group rg for the entries [E cg / CG, E (cg+1) / CG) (contiguous 16 KiB+ column pieces),
+  // so a row sums CG partials instead of G. A CTA with an empty range writes nothing; the
+  // combine skips it (the ranges are known to all).
+  const int RG = static_cast<int>(ld / kCsRowGroup < 1 ? 1 : (ld / kCsRowGroup > kCsMaxRG ? kCsMaxRG : ld / kCsRowGroup));
+  const int CG = G / RG;
+  const int rg = c % RG, cg = c / RG;
+  const int64_t row_lo = ld * rg / RG / 2 * 2, row_hi = rg + 1 == RG ? ld : ld * (rg + 1) / RG / 2 * 2;
+  if (cg < CG) {
+    if (cs_lo(Ea, cg, CG) < cs_lo(Ea, cg + 1, CG))
+      colsplit_partial(p, lv.a, ld, S, G, pre, p.nzv, p.nzj, cs_lo(Ea, cg, CG), cs_lo(Ea, cg + 1, CG), row_lo, row_hi,
+                       p.up + static_cast<int64_t>(c) * ld, ej, ev);
+    if (cs_lo(Ef, cg, CG) < cs_lo(Ef, cg + 1, CG))
+      colsplit_partial(p, lv.a, ld, S, G, pre + (G + 1), p.fxv, p.fxj, cs_lo(Ef, cg, CG), cs_lo(Ef, cg + 1, CG),
+                       row_lo, row_hi, p.dvp + static_cast<int64_t>(c) * ld, ej, ev);
+  }
   vsync();
   int64_t ilo, ihi;
   slice(ld, ilo, ihi);
@@ -1692,20 +1703,24 @@ __device__ __noinline__ void combine_u_colsplit(const EngineParams& p, Sh& sh, c
   double* gsum = ev;  // [2][kGrp][kRB] (the entry staging is free after the barrier)
   double arr = 0.0, ary = 0.0, aee = 0.0;
   const int rr = threadIdx.x % kRB, gq = threadIdx.x / kRB;
-  const int g0 = G * gq / kGrp, g1 = G * (gq + 1) / kGrp;
+  const int g0 = CG * gq / kGrp, g1 = CG * (gq + 1) / kGrp;
   auto group_sum = [&](const double* P, int64_t E, int64_t i) {
+    int rgi = 0;  // the row group holding row i
+    while (rgi + 1 < RG && i >= (rgi + 1 == RG ? ld : ld * (rgi + 1) / RG / 2 * 2)) ++rgi;
     double t = 0.0;
     int cc = g0;
     for (; cc + 8 <= g1; cc += 8) {
       double v8[8];
 #pragma unroll
       for (int u = 0; u < 8; ++u)
-        v8[u] = cs_lo(E, cc + u, G) < cs_lo(E, cc + u + 1, G) ? __ldcg(P + static_cast<int64_t>(cc + u) * ld + i) : 0.0;
+        v8[u] = cs_lo(E, cc + u, CG) < cs_lo(E, cc + u + 1, CG)
+                    ? __ldcg(P + static_cast<int64_t>(rgi + RG * (cc + u)) * ld + i)
+                    : 0.0;
 #pragma unroll
       for (int u = 0; u < 8; ++u) t += v8[u];
     }
     for (; cc < g1; ++cc)
-      if (cs_lo(E, cc, G) < cs_lo(E, cc + 1, G)) t += __ldcg(P + static_cast<int64_t>(cc) * ld + i);
+      if (cs_lo(E, cc, CG) < cs_lo(E, cc + 1, CG)) t += __ldcg(P + static_cast<int64_t>(rgi + RG * cc) * ld + i);
     return t;
   };
   for (int64_t rb = ilo; rb < ihi; rb += kRB) {

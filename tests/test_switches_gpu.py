@@ -63,6 +63,7 @@ CASES = {  # name, seed, n, k, nnz: c1 (single-cluster route) and a full-grid de
     "small": ("c1", 1, 500, 2000, 50),
     "grid": ("c2", 2, 1500, 6000, 150),
     "sukro": ("sukro", 3, 256, 1024, 30),
+    "long": ("c2", 4, 8192, 2000, 300),  # long columns: the phase-E column split applies (ld >= 8192)
 }
 
 
@@ -88,8 +89,9 @@ class _Res:  # the fields assert_parity reads
         self.trace = {k: z["t_" + k] for k in names}
 
 
-# the SuKro case covers the compaction's rebase path (the other switches are dense-only)
-PARAMS = [(c, sw, v) for c in sorted(CASES) for sw, v in SWITCHES if c != "sukro" or sw == "FL1_COMPACT"]
+# the SuKro case covers the compaction's rebase path, the long case the column split
+PARAMS = [(c, sw, v) for c in sorted(CASES) for sw, v in SWITCHES
+          if (c != "sukro" or sw == "FL1_COMPACT") and (c != "long" or sw == "FL1_COLSPLIT")]
 
 
 @pytest.mark.parametrize("case,switch,value", PARAMS)

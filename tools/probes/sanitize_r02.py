@@ -9,7 +9,7 @@ sys.path.insert(0, os.path.join(os.path.dirname(__file__), '..', '..'))
 import numpy as np, torch
 from paper_1812_06635_b200 import fastl1 as F, synthetic as syn, harness as H
 
-inst = syn.dense_instance("c1", seed=31, n=4096, k=600, nnz=12)
+inst = syn.dense_instance("c1", seed=31, n=8192, k=600, nnz=12)
 d = F.DenseDictionary(inst.a)
 At = torch.from_numpy(np.ascontiguousarray(inst.a.T)).cuda()
 dd = F.DenseDictionaryDevice(At.data_ptr(), inst.a.shape[0], inst.a.shape[1])
