@@ -28,6 +28,33 @@
 
 #include "engine.cuh"
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda): a 2D
+// fp64 tensor of dims (d0, d1), row pitch d0 doubles, box (b0, b1), no swizzle,
+// out-of-bounds elements zero-filled.
+static cudaError_t encode_tensor_map_2d(CUtensorMap* tm, const double* base, int64_t d0, int64_t d1, uint32_t b0,
+                                        uint32_t b1) {
+  using Encode = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+  static Encode fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      f = nullptr;
+    return reinterpret_cast<Encode>(f);
+  }();
+  if (!fn) return cudaErrorNotSupported;
+  const cuuint64_t dims[2] = {static_cast<cuuint64_t>(d0), static_cast<cuuint64_t>(d1)};
+  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(d0) * sizeof(double)};
+  const cuuint32_t box[2] = {b0, b1};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r = fn(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
 namespace fl1 {
 size_t engine_smem_bytes(int64_t ld, int64_t sukro_m);
 int64_t engine_scratch_len(int64_t ld, int64_t sukro_m);
@@ -46,6 +73,8 @@ cudaError_t dense_norms_launch(const double* a, int64_t n, int64_t ld, int64_t k
 cudaError_t sukro_norms_launch(const double* left, const double* right, const double* scale, int nterms, int64_t m,
                                int64_t q, double* out, cudaStream_t stream);
 int64_t prefix_max_atoms();
+int64_t prefix_part_elems(int grid);
+int prefix_stream_k_max_grid();
 cudaError_t gemm_tn_launch(const double* X, int64_t ldx, int64_t nx, const double* Y, int64_t ldy, int64_t ny,
                            int64_t kdim, double* C, int64_t ldc, double* work, size_t work_elems, int device,
                            cudaStream_t stream);
@@ -1271,6 +1300,8 @@ void solve_clusters(fl1_seq* s, const double* Y, bool y_device, int64_t ldy, con
     const size_t q_c = preg(sizeof(double) * static_cast<size_t>(k * bcap) * sm);
     const size_t q_s = preg(sizeof(fl1::PrefixSig) * ub), q_h = preg(sizeof(fl1::Handoff) * ub);
     const size_t q_n = preg(sizeof(int64_t) * 4);  // steps, two signal-queue counters | work: sum n_act, sum n_pow
+    const size_t q_pt = preg(sizeof(double) * static_cast<size_t>(fl1::prefix_part_elems(ctx->sms)));  // stream-K
+    const size_t q_fl = preg(sizeof(int32_t) * 2 * static_cast<size_t>(ctx->sms));
     (void)kt;
     char* pb = ctx->batch_scratch(1, ptop + 256).as<char>();
     pp.n = n;
@@ -1333,6 +1364,24 @@ void solve_clusters(fl1_seq* s, const double* Y, bool y_device, int64_t ldy, con
     pp.steps_out = reinterpret_cast<int32_t*>(pb + q_n);
     pp.queue = pp.steps_out + 1;
     pp.work_out = reinterpret_cast<int64_t*>(pb + q_n) + 2;
+    // stream-K contractions on the TMA ring (default); FL1_LOCKSTEP_TMA=0: split-K cp.async tiles
+    const char* tma = std::getenv("FL1_LOCKSTEP_TMA");
+    pp.tma = (tma ? std::atoi(tma) : 1) && k % 2 == 0 &&  // tensor rows of V need a 16-byte pitch
+             ctx->sms <= fl1::prefix_stream_k_max_grid();
+    const char* fi = std::getenv("FL1_SK_FANIN");
+    pp.sk_fanin = fi ? std::atoi(fi) : 4;
+    if (pp.tma) {
+      pp.part = reinterpret_cast<double*>(pb + q_pt);
+      pp.flags = reinterpret_cast<int32_t*>(pb + q_fl);
+      // slot-ordered inputs reuse the split-K partial regions (unused on this route)
+      pp.rc = pp.np;                                        // ld x bcap
+      pp.vc = pp.corr + static_cast<size_t>(k) * bcap;      // k x bcap (corr part 1)
+      // A is ld x k column-major; boxes over-fetch into the padded tile layouts (batched.cu)
+      ck(encode_tensor_map_2d(&pp.tm_corr, pp.a, ld, k, 36, 128), "tensor map (Corr A)");
+      ck(encode_tensor_map_2d(&pp.tm_w, pp.a, ld, k, 132, 32), "tensor map (W A)");
+      ck(encode_tensor_map_2d(&pp.tm_rc, pp.rc, ld, bcap, 36, 64), "tensor map (Rc)");
+      ck(encode_tensor_map_2d(&pp.tm_vc, pp.vc, k, bcap, 36, 64), "tensor map (Vc)");
+    }
     static std::unique_ptr<DevBuf> sigprof;
     if (const char* sp = std::getenv("FL1_SIGPROF_OUT")) {  // diagnostics builds only (FL1_SIGPROF)
       if (!sigprof) sigprof = std::make_unique<DevBuf>(16 * sizeof(double));

@@ -358,6 +358,331 @@ __device__ __noinline__ void gemm_n_tile(const PrefixParams& p, int rt, int64_t 
   }
 }
 
+// ---------------------------------------------------------------------------
+// Stream-K contractions on a TMA / mbarrier ring (FL1_LOCKSTEP_TMA, default).
+//
+// One product (Corr = A^T R or W = A V) is a list of (tile, 32-deep chunk) units,
+// tiles in (column tile, row tile) order; a unit costs its tile's DMMA width CT, and
+// CTA g takes the contiguous unit range covering costs [W g / G, W (g+1) / G). A tile
+// the range covers whole is written from registers; a range shares at most two tiles
+// with other CTAs (its first and its last), whose segment partials go to the CTA's two
+// slots of p.part, flagged with the product's epoch. Each shared tile is then reduced
+// by its own contributors, every one a slice of the elements, adding the partials in
+// chunk (= CTA) order -- a narrow W tile spans ~20 CTAs, so a single reducer would
+// chain ~20 L2 round trips. Corr goes to p.corr (one part: no split-K sum in the
+// per-signal steps), W straight into the power slots' Rc columns (no combine pass and
+// grid barrier). The reduction order is fixed by (tile count, grid), so results are
+// reproducible run to run.
+//
+// Loads: thread 0 keeps kRing - 1 units ahead of the CTA's consumption. Per unit it arms
+// the stage's full barrier with the unit's bytes and issues two 2D tensor copies: the A
+// tile and the 64 slot-ordered R / V columns (p.rc / p.vc, staged in slot order at the
+// start of the step: gathering the columns by signal instead -- per-thread cp.async,
+// bulk copies or tile::gather4 -- measured 1.2-1.9x slower per unit, tools/sk_bench.cu).
+// The boxes over-fetch rows / atoms so that each dense box lands in the padded,
+// bank-conflict-free layout the DMMA fragments read (Corr [atom][36], W [atom][132],
+// R / V [slot][36]). Every warp releases a stage through its empty barrier: no CTA-wide
+// barrier per chunk, and the ring runs on across tile boundaries.
+constexpr int kRing = 3;
+constexpr int kPartTile = kTM * kTN;  // doubles per partial slot (two per CTA)
+constexpr int kStageBufs = kStages > kRing ? kStages : kRing;  // staging area, in kStage units
+__shared__ __align__(8) uint64_t s_full[kRing];
+__shared__ __align__(8) uint64_t s_empty[kRing];
+constexpr int kMaxGrid = 256;             // stream-K route: CTAs (one per SM) at most
+__shared__ int32_t s_contrib[kMaxGrid];   // a shared tile's contributor slots, chunk order
+__shared__ int32_t sh_scal[2];
+__shared__ int64_t s_begin[kMaxGrid + 1];  // the product's unit-range starts of every CTA
+
+__device__ __forceinline__ uint32_t su32(const void* ptr) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(ptr));
+}
+__device__ __forceinline__ void mb_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t ok = 0;
+  while (!ok) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(su32(bar)), "r"(parity)
+        : "memory");
+  }
+}
+__device__ void sk_init_barriers() {
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kRing; ++s) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&s_full[s])));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(&s_empty[s])), "r"(kPW));
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+}
+
+struct SkShape {
+  int which;       // 0: W = A V (rows of ld, depth K), 1: Corr = A^T R (atoms, depth ld)
+  int64_t M, D;    // output rows, contraction depth
+  int nch, n_rt, n_ct, ct_last;
+  int64_t n_cols;  // output columns (signals)
+  int64_t F, W;    // cost of the full-width column tiles; total cost
+  __device__ SkShape(const PrefixParams& p, int wh, int64_t ncols) {
+    which = wh;
+    M = wh ? p.k : p.ld;
+    D = wh ? p.ld : p.k;
+    nch = static_cast<int>((D + kTK - 1) / kTK);
+    n_rt = static_cast<int>((M + kTM - 1) / kTM);
+    n_cols = ncols;
+    n_ct = static_cast<int>((ncols + kTN - 1) / kTN);
+    ct_last = tile_ct(static_cast<int>(ncols - static_cast<int64_t>(n_ct - 1) * kTN), p.width_tiles);
+    F = static_cast<int64_t>(n_ct - 1) * n_rt * nch * kCT;
+    W = F + static_cast<int64_t>(n_rt) * nch * ct_last;
+  }
+  // first unit whose starting cost is >= c
+  __device__ int64_t pos(int64_t c) const {
+    if (c <= F) return (c + kCT - 1) / kCT;
+    return F / kCT + (c - F + ct_last - 1) / ct_last;
+  }
+  __device__ int64_t begin(int g, int G) const { return pos(W * g / G); }
+  __device__ int ct_of(int64_t tile) const { return tile / n_rt == n_ct - 1 ? ct_last : kCT; }
+};
+
+// issue unit u's loads into stage st (one thread): a 2D tensor copy of the A tile and one
+// of the 64 slot-ordered R / V columns, both on the stage's full barrier
+__device__ __forceinline__ void sk_issue(const PrefixParams& p, const SkShape& sh, int64_t u, int st, double* stage) {
+  const int64_t tile = u / sh.nch;
+  const int kc = static_cast<int>(u - tile * sh.nch);
+  const int rt = static_cast<int>(tile % sh.n_rt);
+  const int c0 = static_cast<int>((tile / sh.n_rt) * kTN);
+  const int d0 = kc * kTK;
+  double* Xs = stage + st * kStage;
+  const uint32_t xbytes = sh.which ? kTM * kSS * 8 : kTK * (kTM + 4) * 8;
+  double* Ys = Xs + (sh.which ? kTM * kSS : kTK * (kTM + 4));
+  uint64_t* full = &s_full[st];
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(full)),
+               "r"(xbytes + static_cast<uint32_t>(kTN * kSS * 8))
+               : "memory");
+  const int x_in = sh.which ? d0 : rt * kTM;    // coordinate along ld
+  const int x_out = sh.which ? rt * kTM : d0;  // coordinate along the atoms
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
+      "[%4];" ::"r"(su32(Xs)),
+      "l"(reinterpret_cast<uint64_t>(sh.which ? &p.tm_corr : &p.tm_w)), "r"(x_in), "r"(x_out), "r"(su32(full))
+      : "memory");
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
+      "[%4];" ::"r"(su32(Ys)),
+      "l"(reinterpret_cast<uint64_t>(sh.which ? &p.tm_rc : &p.tm_vc)), "r"(d0), "r"(c0), "r"(su32(full))
+      : "memory");
+}
+
+// DMMA over one landed unit (layouts as sk_issue)
+template <int WHICH, int CT>
+__device__ __forceinline__ void sk_mma(const double* Xs, double (&acc)[kRT][kCT][2]) {
+  constexpr int which = WHICH;
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31, g = l >> 2, tg = l & 3;
+  const int wr = w % kWR, wc = w / kWR;
+  const double* Ys = Xs + (which ? kTM * kSS : kTK * (kTM + 4));
+#pragma unroll
+  for (int ks = 0; ks < kTK / 4; ++ks) {
+    double av[kRT], bv[CT];
+#pragma unroll
+    for (int h = 0; h < kRT; ++h)
+      av[h] = which ? Xs[((h * kWR + wr) * 8 + g) * kSS + ks * 4 + tg]
+                    : Xs[(ks * 4 + tg) * (kTM + 4) + (h * kWR + wr) * 8 + g];
+#pragma unroll
+    for (int c = 0; c < CT; ++c) bv[c] = Ys[((wc * CT + c) * 8 + g) * kSS + ks * 4 + tg];
+#pragma unroll
+    for (int h = 0; h < kRT; ++h)
+#pragma unroll
+      for (int c = 0; c < CT; ++c) dmma(acc[h][c], av[h], bv[c]);
+  }
+}
+
+// the CTAs whose ranges hold units of the tile [ta, tb): gA .. gB (consecutive), n_ne of
+// them non-empty, j of those before this CTA (s_begin of the current product)
+struct SkContrib {
+  int gA, gB, n_ne, j;
+};
+__device__ __forceinline__ SkContrib sk_contrib(int64_t ta, int64_t tb, int gi, int G) {
+  SkContrib t{gi, gi, 0, 0};
+  while (s_begin[t.gA] > ta) --t.gA;  // the range holding the tile's first unit
+  while (t.gA + 1 < G && s_begin[t.gA + 1] <= ta) ++t.gA;
+  while (t.gB + 1 < G && s_begin[t.gB + 1] < tb) ++t.gB;  // ... and its last unit
+  for (int g2 = t.gA; g2 <= t.gB; ++g2)
+    if (s_begin[g2 + 1] > s_begin[g2]) {
+      if (g2 < gi) ++t.j;
+      ++t.n_ne;
+    }
+  return t;
+}
+
+// output element (h, c, e) of thread tid's fragments of `tile`: Corr into p.corr (slot
+// columns), W into the power slots' Rc columns (zero past row n)
+__device__ __forceinline__ void sk_store(const PrefixParams& p, const SkShape& sh, const int32_t* pact, int64_t tile,
+                                         int CT, int h, int c, int e, int tid, double v) {
+  const int w = tid >> 5, l = tid & 31;
+  const int64_t r = (tile % sh.n_rt) * kTM + (h * kWR + w % kWR) * 8 + (l >> 2);
+  const int64_t col = (tile / sh.n_rt) * kTN + ((w / kWR) * CT + c) * 8 + 2 * (l & 3) + e;
+  if (r >= sh.M || col >= sh.n_cols) return;
+  if (sh.which) __stcg(p.corr + col * p.k + r, v);
+  else __stcg(p.rc + static_cast<int64_t>(pact[col]) * p.ld + r, r < p.n ? v : 0.0);
+}
+
+// One stream-K product over this CTA's unit range. ring: the CTA's running unit count
+// (stage and phase of the ring; identical in every thread). epoch: unique per product
+// within the launch (the flags are zeroed at the launch's start).
+__device__ __noinline__ void sk_contract(const PrefixParams& p, int which, int64_t ncols, const int32_t* pact,
+                                         double* stage, uint32_t& ring, int32_t epoch) {
+  const SkShape sh(p, which, ncols);
+  const int G = gridDim.x, gi = blockIdx.x;
+  const int l = threadIdx.x & 31;
+  for (int g2 = threadIdx.x; g2 <= G; g2 += kPT) s_begin[g2] = sh.begin(g2, G);
+  // the per-signal phases' generic-proxy writes into the staging area precede the
+  // async-proxy copies below
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  __syncthreads();
+  const int64_t u0 = s_begin[gi], u1 = s_begin[gi + 1];
+  if (u0 >= u1) return;
+  const int64_t nu = u1 - u0;
+  if (threadIdx.x == 0)
+    for (int64_t i = 0; i < kRing - 1 && i < nu; ++i) sk_issue(p, sh, u0 + i, static_cast<int>((ring + i) % kRing), stage);
+  double acc[kRT][kCT][2];
+  int64_t u = u0;
+  while (u < u1) {
+    const int64_t tile = u / sh.nch;
+    const int kc0 = static_cast<int>(u - tile * sh.nch);
+    const int64_t useg = min(u1, (tile + 1) * sh.nch);
+    const int CT = sh.ct_of(tile);
+#pragma unroll
+    for (int h = 0; h < kRT; ++h)
+#pragma unroll
+      for (int c = 0; c < kCT; ++c) acc[h][c][0] = acc[h][c][1] = 0.0;
+    for (; u < useg; ++u) {
+      const int64_t i = u - u0;
+      if (threadIdx.x == 0 && i + kRing - 1 < nu) {  // refill the stage released at unit i - 1
+        const uint32_t qn = ring + static_cast<uint32_t>(i + kRing - 1);
+        mb_wait(&s_empty[qn % kRing], ((qn / kRing) & 1u) ^ 1u);
+        sk_issue(p, sh, u + kRing - 1, static_cast<int>(qn % kRing), stage);
+      }
+      const uint32_t q = ring + static_cast<uint32_t>(i);
+      mb_wait(&s_full[q % kRing], (q / kRing) & 1u);
+      const double* Xs = stage + (q % kRing) * kStage;
+      switch (CT + 8 * which) {
+        case 1: sk_mma<0, 1>(Xs, acc); break;
+        case 2: sk_mma<0, 2>(Xs, acc); break;
+        case 3: sk_mma<0, 3>(Xs, acc); break;
+        case 4: sk_mma<0, 4>(Xs, acc); break;
+        case 9: sk_mma<1, 1>(Xs, acc); break;
+        case 10: sk_mma<1, 2>(Xs, acc); break;
+        case 11: sk_mma<1, 3>(Xs, acc); break;
+        default: sk_mma<1, 4>(Xs, acc);
+      }
+      __syncwarp();
+      if (l == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(&s_empty[q % kRing])) : "memory");
+    }
+    // ---- segment epilogue
+    if (kc0 == 0 && useg == (tile + 1) * sh.nch) {  // the whole tile: write it
+#pragma unroll
+      for (int h = 0; h < kRT; ++h)
+#pragma unroll
+        for (int c = 0; c < kCT; ++c)
+          if (c < CT)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) sk_store(p, sh, pact, tile, CT, h, c, e, threadIdx.x, acc[h][c][e]);
+      continue;
+    }
+    // a segment of a shared tile. The range's last segment holding the tile's chunk 0 of
+    // a tile with few contributors: this CTA reduces the tile alone after the loop, from
+    // these registers. Otherwise: partial into this CTA's slot (0: its first segment, 1:
+    // its last), flagged with the product's epoch.
+    if (useg == u1 && kc0 == 0 && sk_contrib(tile * sh.nch, (tile + 1) * sh.nch, gi, G).n_ne <= p.sk_fanin) break;
+    const int slot = u0 >= tile * sh.nch ? 0 : 1;
+    double* dst = p.part + (2 * static_cast<int64_t>(gi) + slot) * kPartTile;
+#pragma unroll
+    for (int h = 0; h < kRT; ++h)
+#pragma unroll
+      for (int c = 0; c < kCT; ++c)
+        if (c < CT)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) __stcg(dst + ((h * kCT + c) * 2 + e) * kPT + threadIdx.x, acc[h][c][e]);
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0)
+      asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p.flags + 2 * gi + slot), "r"(epoch) : "memory");
+  }
+  ring += static_cast<uint32_t>(nu);
+  // ---- shared tiles (at most the first and the last of this CTA's range). A tile with at
+  // most p.sk_fanin contributors is reduced by its chunk-0 holder alone (it reaches the
+  // tile last, at the end of its range, so the others' partials are there: no wait),
+  // starting from its registers; one with more contributors (narrow products: ~20) by
+  // all of them, each a slice of the elements. Partials are added in chunk (= CTA) order.
+  const int64_t tiles[2] = {u0 / sh.nch, (u1 - 1) / sh.nch};
+  for (int s2 = 0; s2 < 2; ++s2) {
+    const int64_t tile = tiles[s2];
+    if (s2 == 1 && tile == tiles[0]) break;
+    const int64_t ta = tile * sh.nch, tb = ta + sh.nch;
+    if (u0 <= ta && u1 >= tb) continue;  // whole tile here (written above)
+    const SkContrib tc = sk_contrib(ta, tb, gi, G);
+    const bool solo = tc.n_ne <= p.sk_fanin;
+    if (solo && gi != tc.gA) continue;
+    __syncthreads();  // s_contrib of the previous tile is no longer read
+    if (threadIdx.x == 0) {
+      int n = 0;
+      for (int g2 = tc.gA; g2 <= tc.gB; ++g2)
+        if (s_begin[g2 + 1] > s_begin[g2]) s_contrib[n++] = 2 * g2 + (s_begin[g2] >= ta ? 0 : 1);
+    }
+    __syncthreads();
+    const int first = solo ? 1 : 0;  // solo: the holder's own segment is in registers
+    if (threadIdx.x >= first && threadIdx.x < tc.n_ne) {
+      int32_t f = 0;
+      do {
+        asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(f) : "l"(p.flags + s_contrib[threadIdx.x]) : "memory");
+      } while (f != epoch);
+    }
+    __syncthreads();
+    if (solo) {
+      const int CT = sh.ct_of(tile);
+      for (int k2 = 1; k2 < tc.n_ne; ++k2) {
+        const double* s2p = p.part + static_cast<int64_t>(s_contrib[k2]) * kPartTile;
+#pragma unroll
+        for (int h = 0; h < kRT; ++h)
+#pragma unroll
+          for (int c = 0; c < kCT; ++c)
+            if (c < CT)
+#pragma unroll
+              for (int e = 0; e < 2; ++e) acc[h][c][e] += __ldcg(s2p + ((h * kCT + c) * 2 + e) * kPT + threadIdx.x);
+      }
+#pragma unroll
+      for (int h = 0; h < kRT; ++h)
+#pragma unroll
+        for (int c = 0; c < kCT; ++c)
+          if (c < CT)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) sk_store(p, sh, pact, tile, CT, h, c, e, threadIdx.x, acc[h][c][e]);
+      continue;
+    }
+    const int n_ne = tc.n_ne, nr = n_ne, j = tc.j;
+    const int CT = sh.ct_of(tile);
+    const int E = kRT * CT * 2 * kPT;  // valid elements of the tile
+    const int q0 = E * j / nr, q1 = E * (j + 1) / nr;
+    for (int q = q0 + threadIdx.x; q < q1; q += kPT) {
+      const int h = q / (CT * 2 * kPT);
+      const int rem = q - h * CT * 2 * kPT;
+      const int c = rem / (2 * kPT), e = (rem / kPT) & 1, tid = rem % kPT;
+      const int off = ((h * kCT + c) * 2 + e) * kPT + tid;
+      double v = 0.0;
+      int k2 = 0;
+      for (; k2 + 4 <= n_ne; k2 += 4) {  // four loads in flight, added in order
+        double t[4];
+#pragma unroll
+        for (int z = 0; z < 4; ++z) t[z] = __ldcg(p.part + static_cast<int64_t>(s_contrib[k2 + z]) * kPartTile + off);
+#pragma unroll
+        for (int z = 0; z < 4; ++z) v += t[z];
+      }
+      for (; k2 < n_ne; ++k2) v += __ldcg(p.part + static_cast<int64_t>(s_contrib[k2]) * kPartTile + off);
+      sk_store(p, sh, pact, tile, CT, h, c, e, tid, v);
+    }
+  }
+}
+
+
 // ordered compaction of one 256-wide batch: returns the running total; writes the
 // flagged items at base offset `tot` (position order)
 __device__ __forceinline__ int block_compact(PSh& sh, bool flag, int tot, int* at) {
@@ -1113,13 +1438,19 @@ __device__ __noinline__ void narrow_w(const PrefixParams& p, int n_pow, const in
 
 __global__ void __launch_bounds__(kPT, 1) prefix_kernel(const __grid_constant__ PrefixParams p) {
   cg::grid_group grid = cg::this_grid();
-  extern __shared__ __align__(16) double dsm[];
+  extern __shared__ __align__(128) double dsm[];
   __shared__ PSh sh;
   const int64_t B = p.batch, K = p.k, N = p.n, ld = p.ld;
   const double t0 = gtimer();
-  // dynamic smem: [staging (contraction tiles; lists in the per-signal steps) | u | act | pact]
-  double* stage = dsm;
-  double* us = stage + kStages * kStage;
+  // dynamic smem: [staging (contraction tiles; lists in the per-signal steps) | u | act | pact],
+  // the staging area 128-byte aligned (tensor-copy destinations)
+  double* stage = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(dsm) + 127) & ~static_cast<uintptr_t>(127));
+  double* us = stage + kStageBufs * kStage;
+  uint32_t ring = 0;  // stream-K ring: units consumed by this CTA (identical in every thread)
+  if (p.tma) {
+    sk_init_barriers();
+    for (int g = blockIdx.x * kPT + threadIdx.x; g < 2 * static_cast<int>(gridDim.x); g += gridDim.x * kPT) p.flags[g] = 0;
+  }
   int32_t* act = reinterpret_cast<int32_t*>(us + ld);
   int32_t* pact = act + B;
   // ---- Engine ctor (254-276) with x = 0, S = K, cached full L: u = 0, momentum off
@@ -1187,6 +1518,25 @@ __global__ void __launch_bounds__(kPT, 1) prefix_kernel(const __grid_constant__ 
       p.step_log[5 * steps + 2] = gtimer() - t0;
     }
     const bool narrow = p.narrow && narrow_fits(n_act, ld);
+    if (p.tma && !narrow) {
+      // stage the contraction inputs in slot order (2D tensor boxes, no per-column gather):
+      // Rc[a] = R[act[a]] (the power slots' columns are overwritten by W below) and
+      // Vc[c] = v of power slot c
+      const int64_t hl = ld / 2, hk = K / 2, nr = static_cast<int64_t>(n_act) * hl, nv = static_cast<int64_t>(n_pow) * hk;
+      for (int64_t e = static_cast<int64_t>(blockIdx.x) * kPT + threadIdx.x; e < nr + nv;
+           e += static_cast<int64_t>(gridDim.x) * kPT) {
+        if (e < nr) {
+          const int64_t a = e / hl, i = e - a * hl;
+          __stcg(reinterpret_cast<double2*>(p.rc + a * ld) + i,
+                 __ldcg(reinterpret_cast<const double2*>(p.R + static_cast<int64_t>(act[a]) * ld) + i));
+        } else {
+          const int64_t f = e - nr, c = f / hk, j = f - c * hk;
+          __stcg(reinterpret_cast<double2*>(p.vc + c * K) + j,
+                 __ldcg(reinterpret_cast<const double2*>(p.vp + static_cast<int64_t>(act[pact[c]]) * K) + j));
+        }
+      }
+      grid.sync();
+    }
     // ---- power-step signals: w = A_S v (one contraction), then summed into R
     if (n_pow > 0 && narrow) {
       narrow_w(p, n_pow, pact, act, stage);
@@ -1198,6 +1548,9 @@ __global__ void __launch_bounds__(kPT, 1) prefix_kernel(const __grid_constant__ 
         for (int g = 0; g < kNarrowParts; ++g) w += __ldcg(p.np + (static_cast<int64_t>(g) * n_pow + pc) * ld + i);
         __stcg(p.R + static_cast<int64_t>(act[pact[pc]]) * ld + i, i < N ? w : 0.0);
       }
+      grid.sync();
+    } else if (n_pow > 0 && p.tma) {
+      sk_contract(p, 0, n_pow, pact, stage, ring, 2 * steps + 1);  // writes the power slots' Rc columns
       grid.sync();
     } else if (n_pow > 0) {
       const int n_rt = static_cast<int>((ld + kTM - 1) / kTM);
@@ -1231,6 +1584,8 @@ __global__ void __launch_bounds__(kPT, 1) prefix_kernel(const __grid_constant__ 
     int sk = 1;
     if (narrow) {
       narrow_corr(p, n_act, act, stage);
+    } else if (p.tma) {
+      sk_contract(p, 1, n_act, pact, stage, ring, 2 * steps + 2);  // one part in p.corr
     } else {
       const int n_rt = static_cast<int>((K + kTM - 1) / kTM);
       const int n_ct = (n_act + kTN - 1) / kTN;
@@ -1290,7 +1645,7 @@ __global__ void __launch_bounds__(kPT, 1) gemm_tn_kernel(const double* __restric
                                                          const double* __restrict__ Y, int64_t ldy, int64_t ny,
                                                          int64_t kdim, int parts, double* __restrict__ C, int64_t ldc,
                                                          int64_t pstride) {
-  extern __shared__ __align__(16) double dsm[];
+  extern __shared__ __align__(128) double dsm[];
   const int w = threadIdx.x >> 5, l = threadIdx.x & 31, gi = l >> 2, tg = l & 3;
   const int wr = w % kWR, wc = w / kWR;
   const int n_rt = static_cast<int>((nx + kTM - 1) / kTM), n_ct = static_cast<int>((ny + kTN - 1) / kTN);
@@ -1437,8 +1792,11 @@ cudaError_t gemm_tn_launch(const double* X, int64_t ldx, int64_t nx, const doubl
 }
 
 size_t prefix_smem_bytes(int64_t ld, int64_t batch) {
-  return static_cast<size_t>(kStages * kStage + ld) * sizeof(double) + static_cast<size_t>(2 * batch) * sizeof(int32_t);
+  return 128 + static_cast<size_t>(kStageBufs * kStage + ld) * sizeof(double) +
+         static_cast<size_t>(2 * batch) * sizeof(int32_t);
 }
+int64_t prefix_part_elems(int grid) { return 2 * static_cast<int64_t>(grid) * kPartTile; }
+int prefix_stream_k_max_grid() { return kMaxGrid; }
 int prefix_split_max() { return kSplitMax; }
 // two per-signal atom lists (12 bytes per entry each) live in the staging area
 int64_t prefix_max_atoms() { return (2 * kStage * 8) / 24 / kPW * kPW; }

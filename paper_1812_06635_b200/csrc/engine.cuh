@@ -5,6 +5,8 @@
 // scalar ever needs a host round trip.
 #pragma once
 
+#include <cuda.h>  // CUtensorMap (the lockstep contraction's TMA descriptors)
+
 #include <cstdint>
 
 #include "../../include/fl1cuda.h"
@@ -177,6 +179,18 @@ struct PrefixSig {
 // power step, Corr = A^T [rho | w] for all. Preserved sets are per-signal masks
 // (atom order = the reference's compacted order).
 struct PrefixParams {
+  // TMA descriptors of A for the stream-K contractions (FL1_LOCKSTEP_TMA): dims (ld, k),
+  // boxes over-fetched into the padded shared-memory layouts of the DMMA tiles
+  CUtensorMap tm_corr;        // box {36 rows, 128 atoms}: Corr tile [atom][36]
+  CUtensorMap tm_w;           // box {132 rows, 32 atoms}: W tile [atom][132]
+  CUtensorMap tm_rc;          // Rc (ld x bcap), box {36 rows, 64 slots}: Corr R tile [slot][36]
+  CUtensorMap tm_vc;          // Vc (k x bcap), box {36 atoms, 64 power slots}: W V tile [slot][36]
+  double* rc;                 // ld x bcap: the step's contraction input columns in slot order
+  double* vc;                 // k x bcap: the step's power-iteration vectors in power-slot order
+  int32_t tma;                // 1: stream-K TMA contractions; 0: split-K cp.async tiles
+  int32_t sk_fanin;           // shared tiles with <= this many contributors: one reducer (FL1_SK_FANIN)
+  double* part;               // grid x 8192: stream-K partial tiles (one per CTA)
+  int32_t* flags;             // grid: stream-K partial-ready epochs (zeroed by the kernel)
   int64_t n, k, ld;
   int32_t batch, bcap;        // signals; column capacity of R / corr (multiple of 64)
   const double* a;            // ld x k, zero-padded rows
