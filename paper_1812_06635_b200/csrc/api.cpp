@@ -1324,10 +1324,14 @@ void solve_clusters(fl1_seq* s, const double* Y, bool y_device, int64_t ldy, con
     pp.variant = opts->variant;
     pp.collect_trace = opts->collect_trace ? 1 : 0;
     // default: signals stay in the lockstep through their first (cold) restricted power
-    // iteration — the dense part of the solve — and the per-signal engine finishes the
-    // short, small-set tail (measured best on B200; 0 and 1 are the other policies)
-    pp.policy = 2;
+    // iteration -- the dense part of the solve -- and until their preserved set is at
+    // most 512 atoms; the per-signal engine finishes the short, small-set tail (policy 3,
+    // measured best on B200 with the stream-K contractions: c5 53.7 -> 53.0 ms against
+    // policy 2, leaving right after the power iteration; 0 and 1 are the other policies)
+    pp.policy = 3;
     if (const char* pol = std::getenv("FL1_LOCKSTEP_POLICY")) pp.policy = std::atoi(pol);
+    const char* hs = std::getenv("FL1_HANDOFF_S");
+    pp.handoff_s = hs ? std::atoll(hs) : 512;
     const char* smode = std::getenv("FL1_SPLIT_MODE");
     pp.split_mode = smode ? std::atoi(smode) : 1;
     const char* sb = std::getenv("FL1_SPLIT_BUDGET_MB");

@@ -946,7 +946,6 @@ __device__ void enter_power(const PrefixParams& p, PSh& sh, int64_t b) {
   const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
   const int8_t* mk = p.mask + b * K;
   const double* ldv = p.lead + b * K;
-  double* src = p.psrc + b * K;
   double* vp = p.vp + b * K;
   const WarpRange wr(K);
   // pass 1: |lead|^2 over the set and the warp's active count (rank offsets)
@@ -963,22 +962,26 @@ __device__ void enter_power(const PrefixParams& p, PSh& sh, int64_t b) {
   const bool warm = sg.lead_valid && a_lead > 0.0;
   int off = 0;
   for (int ww = 0; ww < w; ++ww) off += sh.wcnt[ww];
-  // pass 2: the start vector
-  double acc = 0.0;
-  for (int64_t base = wr.lo; base < wr.hi; base += 32) {
-    const int64_t j = base + l;
+  // pass 2: the start vector (this lane's atoms wr.lo + l + 32 i, in registers)
+  double acc = 0.0, sv[kIt];
+#pragma unroll
+  for (int i = 0; i < kIt; ++i) {
+    const int64_t j = wr.lo + l + 32 * i;
+    sv[i] = 0.0;
+    if (wr.lo + 32 * i >= wr.hi) continue;  // warp-uniform
     const bool on = j < wr.hi && mk[j] != 0;
     const unsigned bal = __ballot_sync(kAll, on);
-    if (j < wr.hi) {
-      const double gv = on ? (warm ? ldv[j] : p.gauss0[off + __popc(bal & ((1u << l) - 1u))]) : 0.0;
-      src[j] = gv;
-      acc = fma(gv, gv, acc);
-    }
+    if (on) sv[i] = warm ? ldv[j] : p.gauss0[off + __popc(bal & ((1u << l) - 1u))];
+    acc = fma(sv[i], sv[i], acc);
     off += __popc(bal);
   }
   const double nrm2 = warm ? a_lead : block_sum(acc, sh);
   const double div = sqrt(nrm2);
-  for (int64_t j = wr.lo + l; j < wr.hi; j += 32) vp[j] = src[j] / div;  // same thread wrote src[j]
+#pragma unroll
+  for (int i = 0; i < kIt; ++i) {
+    const int64_t j = wr.lo + l + 32 * i;
+    if (j < wr.hi) vp[j] = sv[i] / div;
+  }
   if (threadIdx.x == 0) {
     sg.mode = 1;
     sg.p_div = div;
@@ -1025,23 +1028,27 @@ __device__ __noinline__ void power_step(const PrefixParams& p, PSh& sh, int64_t 
   const int64_t K = p.k, part = K * p.bcap;
   const double* cr = p.corr + a * K;
   const int8_t* mk = p.mask + b * K;
-  double* src = p.psrc + b * K;
   double* vp = p.vp + b * K;
   const WarpRange wr(K);
   const int l = threadIdx.x & 31;
   double v[3] = {0.0, 0.0, 0.0};  // |v_new|^2, v.v_new
-  double cv[kIt];
+  // v_new (unnormalised, the reference's cur_src) stays in registers: every load of the
+  // pass (corr, mask, v) is issued before the first is used
+  double cv[kIt], vv[kIt];
+  bool on[kIt];
   sum_parts(cr, part, sk, wr, cv);
 #pragma unroll
   for (int i = 0; i < kIt; ++i) {
     const int64_t j = wr.lo + l + 32 * i;
-    if (j < wr.hi && mk[j]) {
-      const double c = cv[i];
-      src[j] = c;  // v_new (unnormalised) = the next cur_src
-      v[0] = fma(c, c, v[0]);
-      v[1] = fma(vp[j], c, v[1]);
-    }
+    on[i] = j < wr.hi && mk[j] != 0;
+    vv[i] = j < wr.hi ? vp[j] : 0.0;
   }
+#pragma unroll
+  for (int i = 0; i < kIt; ++i)
+    if (on[i]) {
+      v[0] = fma(cv[i], cv[i], v[0]);
+      v[1] = fma(vv[i], cv[i], v[1]);
+    }
   block_sum3(v, sh);
   if (threadIdx.x == 0) {
     sg.power_steps += 1;
@@ -1067,11 +1074,15 @@ __device__ __noinline__ void power_step(const PrefixParams& p, PSh& sh, int64_t 
   __syncthreads();
   const int stop = sh.release;
   const double div = sh.m;
-  for (int64_t j = wr.lo + l; j < wr.hi; j += 32) {  // same thread mapping as above
+  const bool have_w = stop == 2 && sg.p_have_w;
+#pragma unroll
+  for (int i = 0; i < kIt; ++i) {  // same thread mapping as above
+    const int64_t j = wr.lo + l + 32 * i;
+    if (j >= wr.hi) break;
     if (stop == 2) {
-      p.lead[b * K + j] = sg.p_have_w ? 0.0 : vp[j];
+      p.lead[b * K + j] = have_w ? 0.0 : vv[i];
     } else {
-      const double v1 = mk[j] ? src[j] / div : 0.0;
+      const double v1 = on[i] ? cv[i] / div : 0.0;
       if (stop) p.lead[b * K + j] = v1;
       else vp[j] = v1;
     }
@@ -1097,6 +1108,10 @@ __device__ __noinline__ void power_step(const PrefixParams& p, PSh& sh, int64_t 
 __device__ __noinline__ void fista_step(const PrefixParams& p, PSh& sh, int64_t a, int64_t b, double t0, int sk,
                                         double* us, double* stage) {
   PrefixSig& sg = p.sig[b];
+  if (p.policy == 3 && sg.lead_valid && sg.S <= p.handoff_s) {  // leave at the start of this iteration
+    handoff_signal(p, sh, b, t0);
+    return;
+  }
   const int64_t K = p.k, ld = p.ld, part = K * p.bcap;
   const double lambda = p.lambdas[b];
   const uint64_t t = sg.t;
@@ -1108,6 +1123,20 @@ __device__ __noinline__ void fista_step(const PrefixParams& p, PSh& sh, int64_t 
   // corr = sum of the split-K parts, written back to part 0; max |corr| over the set
   // (all kIt atoms of a lane loaded together: one L2 round trip per split part)
   double dp = 0.0;
+  // thread 0's scalars, loaded before the reduction so that their L2 round trip overlaps it
+  double q_tk = 0.0, q_rsq = 0.0, q_rdy = 0.0, q_ree = 0.0, q_xl1 = 0.0, q_ysq = 0.0;
+  int q_ready = 0;
+  int64_t q_S = 0;
+  if (threadIdx.x == 0) {
+    q_tk = sg.t_k;
+    q_rsq = sg.rsq;
+    q_rdy = sg.rdy;
+    q_ree = sg.ree;
+    q_xl1 = sg.x_l1;
+    q_ysq = sg.y_sq;
+    q_ready = sg.ready;
+    q_S = sg.S;
+  }
   {
     double cv[kIt];
     sum_parts(cr, part, sk, wr, cv);
@@ -1123,24 +1152,24 @@ __device__ __noinline__ void fista_step(const PrefixParams& p, PSh& sh, int64_t 
   dp = block_max(dp, sh);
   SIGPROF(0);
   if (threadIdx.x == 0) {
-    double m = 0.0, t_next = sg.t_k;  // 465-470
-    if (p.solver == FL1_FISTA && sg.ready) {
-      t_next = 0.5 * (1.0 + sqrt(1.0 + 4.0 * sg.t_k * sg.t_k));
-      m = (sg.t_k - 1.0) / t_next;
+    double m = 0.0, t_next = q_tk;  // 465-470
+    if (p.solver == FL1_FISTA && q_ready) {
+      t_next = 0.5 * (1.0 + sqrt(1.0 + 4.0 * q_tk * q_tk));
+      m = (q_tk - 1.0) / t_next;
     }
-    const double rsq = sg.rsq, rdy = sg.rdy;
-    const double rho_x_sq = m != 0.0 ? sg.ree : rsq;
-    const double primal = 0.5 * rho_x_sq + lambda * sg.x_l1;
+    const double rsq = q_rsq, rdy = q_rdy;
+    const double rho_x_sq = m != 0.0 ? q_ree : rsq;
+    const double primal = 0.5 * rho_x_sq + lambda * q_xl1;
     int rel = 0, screen = 0;
     double sp = 0.0, radius = 0.0, gt = 0.0;
     if (!(rsq > 0.0)) {
       rel = 3;  // exact fit: the per-signal engine takes the y-ray branch (428-449)
     } else {
       const double projection = rdy / (lambda * rsq);  // dual_scalars (406-450), eps = 0
-      const double ap = (sg.S > 0 && dp > 0) ? 1.0 / dp : CUDART_INF;
+      const double ap = (q_S > 0 && dp > 0) ? 1.0 / dp : CUDART_INF;
       sp = fmin(fmax(projection, -ap), ap);
-      const double dist_sq = sp * sp * rsq - 2.0 * sp * rdy / lambda + sg.y_sq / (lambda * lambda);
-      const double dual = 0.5 * sg.y_sq - 0.5 * lambda * lambda * dist_sq;  // 453-457
+      const double dist_sq = sp * sp * rsq - 2.0 * sp * rdy / lambda + q_ysq / (lambda * lambda);
+      const double dual = 0.5 * q_ysq - 0.5 * lambda * lambda * dist_sq;  // 453-457
       double gp = primal - dual;  // scale' == scale~ on the exact dictionary
       if (gp < -1e-10) sg.warning = 1;
       gp = fmax(gp, 0.0);

@@ -203,7 +203,9 @@ struct PrefixParams {
   double tol, rel_tol;
   uint64_t max_it;
   int32_t interval, solver, variant, collect_trace;
-  int32_t policy;             // hand-off: 0 never, 1 at the first shrink, 2 after the first power iteration
+  int32_t policy;             // hand-off: 0 never, 1 at the first shrink, 2 after the first power iteration,
+                              // 3 at the first iteration after it with |S| <= handoff_s
+  int64_t handoff_s;
   int32_t split_mode;         // split-K choice of the contractions: 1 fewest waves, 0 fill-only (FL1_SPLIT_MODE)
   int32_t narrow;             // 1: steps with <= 12 unfinished signals use the CUDA-core products (FL1_LOCKSTEP_NARROW)
   double* sigprof;            // diagnostics builds (FL1_SIGPROF): 16 accumulators, CTA 0's per-signal phases

@@ -357,11 +357,43 @@ def test_batched_lockstep_narrow_steps(cuda, oracle16, monkeypatch, narrow):
         assert_parity(res[b], F.run_lasso(seq_o, Y[:, b], lams[b], cfg, opts), a, Y[:, b], lams[b])
 
 
-@pytest.mark.parametrize("policy", ["0", "1", "2"])
+@pytest.mark.parametrize("env", [("FL1_LOCKSTEP_TMA", "0"), ("FL1_SK_FANIN", "1"), ("FL1_SK_FANIN", "64"),
+                                 ("FL1_LOCKSTEP_WIDTH", "0")])
+def test_batched_lockstep_contraction_routes(cuda, oracle16, monkeypatch, env):
+    """The lockstep's contraction variants against per-signal oracle solves: the split-K
+    cp.async tiles (FL1_LOCKSTEP_TMA=0) and the stream-K TMA ring with every shared tile
+    reduced by all its contributors (FL1_SK_FANIN=1) or by its chunk-0 holder alone (64),
+    and full-width tiles only. Policy 0 keeps every signal in the lockstep to the end and
+    no narrow CUDA-core steps, so wide, medium and one-signal-wide products all occur;
+    with 70 signals (two column tiles) and 1200 atoms the tiles span several CTAs."""
+    monkeypatch.setenv("FL1_LOCKSTEP_POLICY", "0")
+    monkeypatch.setenv("FL1_LOCKSTEP_NARROW", "0")
+    monkeypatch.setenv(*env)
+    rng = np.random.default_rng(37)
+    n, k, B = 300, 1200, 70
+    a = syn.gaussian_dictionary(rng, n, k)
+    Y = np.empty((n, B), order="F")
+    for b in range(B):
+        Y[:, b] = syn.observe(rng, a @ syn.sparse_signal(rng, k, 4 + b % 9), None, 30.0)
+    lams = (0.15 + 0.05 * (np.arange(B) % 4)) * np.max(np.abs(a.T @ Y), axis=0)
+    L = F.lipschitz_bound(F.DenseDictionary(a, backend=cuda))
+    cfg = F.SwitchConfig(screening_interval=10, max_iterations=5000, rel_tolerance=1e-6)
+    opts = F.RunOptions(variant=F.VARIANT_SCREENED, full_lipschitz=[L], collect_trace=True)
+    seq_g = F.ApproxSequence([F.make_exact_approx(F.DenseDictionary(a, backend=cuda))])
+    seq_o = F.ApproxSequence([F.make_exact_approx(F.DenseDictionary(a, backend=oracle16))])
+    res = F.run_lasso_batched(seq_g, Y, lams, cfg, opts, concurrency=0)
+    for b in range(B):
+        assert_parity(res[b], F.run_lasso(seq_o, Y[:, b], lams[b], cfg, opts), a, Y[:, b], lams[b])
+
+
+@pytest.mark.parametrize("policy", ["0", "1", "2", "3"])
 def test_batched_prefix_matches_engine_only(cuda, monkeypatch, policy):
     """The lockstep engine changes only the route, not the answer, under every
     hand-off policy (0: never, 1: at the first shrink, 2: after the first power
-    iteration): same supports, iteration counts and ledgers as the engine-only path."""
+    iteration, 3: at the first iteration after it with |S| <= FL1_HANDOFF_S): same
+    supports, iteration counts and ledgers as the engine-only path."""
+    if policy == "3":
+        monkeypatch.setenv("FL1_HANDOFF_S", "64")
     monkeypatch.setenv("FL1_LOCKSTEP_POLICY", policy)
     rng = np.random.default_rng(23)
     n, k, B = 128, 512, 20
@@ -383,7 +415,7 @@ def test_batched_prefix_matches_engine_only(cuda, monkeypatch, policy):
         assert np.max(np.abs(x.x - y.x)) <= 1e-9 * max(1.0, np.max(np.abs(y.x)))
 
 
-@pytest.mark.parametrize("policy", ["0", "2"])
+@pytest.mark.parametrize("policy", ["0", "2", "3"])
 def test_batched_lockstep_edge_cases(cuda, oracle16, monkeypatch, policy):
     """Lockstep corner cases against per-signal oracle solves: a zero signal (exact
     fit: hand-off to the per-signal engine at iteration 0), lambda >= lambda_max
