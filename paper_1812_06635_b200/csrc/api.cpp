@@ -75,6 +75,7 @@ cudaError_t sukro_norms_launch(const double* left, const double* right, const do
 int64_t prefix_max_atoms();
 int64_t prefix_part_elems(int grid);
 int prefix_stream_k_max_grid();
+constexpr int kStepLogW = 10;  // batched.cu kLogW
 cudaError_t gemm_tn_launch(const double* X, int64_t ldx, int64_t nx, const double* Y, int64_t ldy, int64_t ny,
                            int64_t kdim, double* C, int64_t ldc, double* work, size_t work_elems, int device,
                            cudaStream_t stream);
@@ -1393,9 +1394,17 @@ void solve_clusters(fl1_seq* s, const double* Y, bool y_device, int64_t ldy, con
       pp.sigprof = sigprof->as<double>();
       (void)sp;
     }
+    static std::unique_ptr<DevBuf> sk_trace;
+    if (const char* st = std::getenv("FL1_SK_TRACE")) {  // diagnostics: per-CTA times of one step's products
+      if (!sk_trace) sk_trace = std::make_unique<DevBuf>(sizeof(double) * 2 * 4 * 256);
+      ck(cudaMemset(sk_trace->p, 0, sizeof(double) * 2 * 4 * 256), "sk trace");
+      pp.sk_trace = sk_trace->as<double>();
+      pp.sk_trace_step = std::atoi(st);
+    }
     if (std::getenv("FL1_STEP_LOG")) {  // diagnostics: per-step occupancy of the lockstep engine
       pp.max_log = 4096;
-      step_log = std::make_unique<DevBuf>(sizeof(double) * 5 * pp.max_log);
+      step_log = std::make_unique<DevBuf>(sizeof(double) * fl1::kStepLogW * pp.max_log);
+      ck(cudaMemset(step_log->p, 0, sizeof(double) * fl1::kStepLogW * pp.max_log), "step log");
       pp.step_log = step_log->as<double>();
     }
     bd.handoff = pp.hand;
@@ -1484,14 +1493,27 @@ void solve_clusters(fl1_seq* s, const double* Y, bool y_device, int64_t ldy, con
       std::fclose(f);
     }
   }
+  if (pp.sk_trace) {
+    std::vector<double> h(2 * 4 * 256);
+    ck(cudaMemcpy(h.data(), pp.sk_trace, h.size() * sizeof(double), cudaMemcpyDeviceToHost), "sk trace");
+    if (FILE* f = std::fopen("fl1_sk_trace.txt", "w")) {
+      for (size_t i = 0; i < h.size(); i += 4) std::fprintf(f, "%.17g %.17g %.17g %.17g\n", h[i], h[i + 1], h[i + 2], h[i + 3]);
+      std::fclose(f);
+    }
+  }
   if (step_log && d_steps) {
     int32_t steps = 0;
     ck(cudaMemcpy(&steps, d_steps, sizeof(steps), cudaMemcpyDeviceToHost), "steps");
-    std::vector<double> lg(5 * static_cast<size_t>(std::min(steps, 4096)));
+    std::vector<double> lg(fl1::kStepLogW * static_cast<size_t>(std::min(steps, 4096)));
     if (!lg.empty()) ck(cudaMemcpy(lg.data(), step_log->p, lg.size() * sizeof(double), cudaMemcpyDeviceToHost), "log");
+    // per step: n_act n_pow | %globaltimer at the step start, after the W barrier, after the
+    // Corr barrier | (stream-K route) after the staging barrier, CTA 0 done with W, with
+    // Corr, with its per-signal work (0 when not reached)
     if (FILE* f = std::fopen(std::getenv("FL1_STEP_LOG"), "w")) {
-      for (size_t i = 0; i + 4 < lg.size(); i += 5)
-        std::fprintf(f, "%g %g %g %g %g\n", lg[i], lg[i + 1], lg[i + 2], lg[i + 3], lg[i + 4]);
+      for (size_t i = 0; i + fl1::kStepLogW <= lg.size(); i += fl1::kStepLogW) {
+        for (int c = 0; c < 9; ++c) std::fprintf(f, c ? " %g" : "%g", lg[i + c]);
+        std::fprintf(f, "\n");
+      }
       std::fclose(f);
     }
   }

@@ -384,6 +384,7 @@ __device__ __noinline__ void gemm_n_tile(const PrefixParams& p, int rt, int64_t 
 // R / V [slot][36]). Every warp releases a stage through its empty barrier: no CTA-wide
 // barrier per chunk, and the ring runs on across tile boundaries.
 constexpr int kRing = 3;
+constexpr int kLogW = 10;  // step-log fields per step (FL1_STEP_LOG diagnostics)
 constexpr int kPartTile = kTM * kTN;  // doubles per partial slot (two per CTA)
 constexpr int kStageBufs = kStages > kRing ? kStages : kRing;  // staging area, in kStage units
 __shared__ __align__(8) uint64_t s_full[kRing];
@@ -539,6 +540,12 @@ __device__ __noinline__ void sk_contract(const PrefixParams& p, int which, int64
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   __syncthreads();
   const int64_t u0 = s_begin[gi], u1 = s_begin[gi + 1];
+  double* trc = (p.sk_trace && (epoch - 1 - which) / 2 == p.sk_trace_step && threadIdx.x == 0)
+                    ? p.sk_trace + (which * kMaxGrid + gi) * 4 : nullptr;
+  if (trc) {
+    trc[0] = gtimer();
+    trc[3] = static_cast<double>(u1 - u0);
+  }
   if (u0 >= u1) return;
   const int64_t nu = u1 - u0;
   if (threadIdx.x == 0)
@@ -608,6 +615,7 @@ __device__ __noinline__ void sk_contract(const PrefixParams& p, int which, int64
       asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p.flags + 2 * gi + slot), "r"(epoch) : "memory");
   }
   ring += static_cast<uint32_t>(nu);
+  if (trc) trc[1] = gtimer();
   // ---- shared tiles (at most the first and the last of this CTA's range). A tile with at
   // most p.sk_fanin contributors is reduced by its chunk-0 holder alone (it reaches the
   // tile last, at the end of its range, so the others' partials are there: no wait),
@@ -680,6 +688,7 @@ __device__ __noinline__ void sk_contract(const PrefixParams& p, int which, int64
       sk_store(p, sh, pact, tile, CT, h, c, e, tid, v);
     }
   }
+  if (trc) trc[2] = gtimer();
 }
 
 
@@ -1542,9 +1551,9 @@ __global__ void __launch_bounds__(kPT, 1) prefix_kernel(const __grid_constant__ 
     work_pow += n_pow;
     const bool logit = p.step_log && blockIdx.x == 0 && threadIdx.x == 0 && steps < p.max_log;
     if (logit) {
-      p.step_log[5 * steps] = n_act;
-      p.step_log[5 * steps + 1] = n_pow;
-      p.step_log[5 * steps + 2] = gtimer() - t0;
+      p.step_log[kLogW * steps] = n_act;
+      p.step_log[kLogW * steps + 1] = n_pow;
+      p.step_log[kLogW * steps + 2] = gtimer() - t0;
     }
     const bool narrow = p.narrow && narrow_fits(n_act, ld);
     if (p.tma && !narrow) {
@@ -1565,6 +1574,7 @@ __global__ void __launch_bounds__(kPT, 1) prefix_kernel(const __grid_constant__ 
         }
       }
       grid.sync();
+      if (logit) p.step_log[kLogW * steps + 5] = gtimer() - t0;
     }
     // ---- power-step signals: w = A_S v (one contraction), then summed into R
     if (n_pow > 0 && narrow) {
@@ -1580,6 +1590,7 @@ __global__ void __launch_bounds__(kPT, 1) prefix_kernel(const __grid_constant__ 
       grid.sync();
     } else if (n_pow > 0 && p.tma) {
       sk_contract(p, 0, n_pow, pact, stage, ring, 2 * steps + 1);  // writes the power slots' Rc columns
+      if (logit) p.step_log[kLogW * steps + 6] = gtimer() - t0;
       grid.sync();
     } else if (n_pow > 0) {
       const int n_rt = static_cast<int>((ld + kTM - 1) / kTM);
@@ -1607,7 +1618,7 @@ __global__ void __launch_bounds__(kPT, 1) prefix_kernel(const __grid_constant__ 
       }
       grid.sync();
     }
-    if (logit) p.step_log[5 * steps + 3] = gtimer() - t0;
+    if (logit) p.step_log[kLogW * steps + 3] = gtimer() - t0;
     // ---- Corr = A^T [rho | w] for every unfinished signal (fp64 tensor cores; CUDA
     // cores when narrow)
     int sk = 1;
@@ -1615,6 +1626,7 @@ __global__ void __launch_bounds__(kPT, 1) prefix_kernel(const __grid_constant__ 
       narrow_corr(p, n_act, act, stage);
     } else if (p.tma) {
       sk_contract(p, 1, n_act, pact, stage, ring, 2 * steps + 2);  // one part in p.corr
+      if (logit) p.step_log[kLogW * steps + 7] = gtimer() - t0;
     } else {
       const int n_rt = static_cast<int>((K + kTM - 1) / kTM);
       const int n_ct = (n_act + kTN - 1) / kTN;
@@ -1633,7 +1645,7 @@ __global__ void __launch_bounds__(kPT, 1) prefix_kernel(const __grid_constant__ 
       }
     }
     grid.sync();
-    if (logit) p.step_log[5 * steps + 4] = gtimer() - t0;
+    if (logit) p.step_log[kLogW * steps + 4] = gtimer() - t0;
     // ---- the rest of each signal's unit of work, one signal per CTA; CTAs take the
     // next signal from a counter (FISTA and power steps differ in cost), which the
     // result does not depend on. The other step's counter is reset for the next step
@@ -1650,6 +1662,7 @@ __global__ void __launch_bounds__(kPT, 1) prefix_kernel(const __grid_constant__ 
       if (mode == 0) fista_step(p, sh, a, b, t0, sk, us, stage);
       else if (mode == 1) power_step(p, sh, a, b, sk, t0);
     }
+    if (logit) p.step_log[kLogW * steps + 8] = gtimer() - t0;
     grid.sync();
   }
   if (blockIdx.x == 0 && threadIdx.x == 0 && p.steps_out) *p.steps_out = steps;
@@ -1827,8 +1840,9 @@ size_t prefix_smem_bytes(int64_t ld, int64_t batch) {
 int64_t prefix_part_elems(int grid) { return 2 * static_cast<int64_t>(grid) * kPartTile; }
 int prefix_stream_k_max_grid() { return kMaxGrid; }
 int prefix_split_max() { return kSplitMax; }
-// two per-signal atom lists (12 bytes per entry each) live in the staging area
-int64_t prefix_max_atoms() { return (2 * kStage * 8) / 24 / kPW * kPW; }
+// the per-signal lists live in the staging area: two atom lists (12 bytes per entry each)
+// and the flattened copy the apply walks (12 more): 36 bytes per atom
+int64_t prefix_max_atoms() { return (static_cast<int64_t>(kStageBufs) * kStage * 8) / 36 / kPW * kPW; }
 
 cudaError_t prefix_launch(const PrefixParams& p, int device, cudaStream_t stream) {
   const size_t smem = prefix_smem_bytes(p.ld, p.batch);

@@ -189,6 +189,8 @@ struct PrefixParams {
   double* vc;                 // k x bcap: the step's power-iteration vectors in power-slot order
   int32_t tma;                // 1: stream-K TMA contractions; 0: split-K cp.async tiles
   int32_t sk_fanin;           // shared tiles with <= this many contributors: one reducer (FL1_SK_FANIN)
+  double* sk_trace;           // diagnostics (FL1_SK_TRACE=step): per product, per CTA: start, units done, end
+  int32_t sk_trace_step;
   double* part;               // grid x 8192: stream-K partial tiles (one per CTA)
   int32_t* flags;             // grid: stream-K partial-ready epochs (zeroed by the kernel)
   int64_t n, k, ld;

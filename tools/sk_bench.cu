@@ -12,6 +12,9 @@
 //   7  TMA A + R columns by tile::gather4 (four columns per copy), lane 0
 //   8  TMA A + one 1D bulk copy per R column, spread over warp 0's lanes
 //   9  TMA A + one 2D TMA box of 64 consecutive R columns (slot-ordered R: no gather)
+//  10  latency: one A box (36 x 128) at a time, issue -> full barrier, no compute
+//  11  latency: one W-layout A box (132 x 32) at a time
+//  12  latency: the A tile by all threads' cp.async (wait_group 0 + CTA barrier), one at a time
 // R columns are gathered through a permutation (signal = 37 c mod 512), as the lockstep
 // gathers its unfinished signals.
 // Prints us per unit and the DMMA rate. Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 sk_bench.cu -o sk_bench
@@ -52,21 +55,22 @@ __device__ __forceinline__ void mb_wait(uint64_t* bar, uint32_t parity) {
                  : "memory");
 }
 
+template <int CT = kCT>
 __device__ __forceinline__ void mma_unit(const double* Xs, double (&acc)[kRT][kCT][2]) {
   const int w = threadIdx.x >> 5, l = threadIdx.x & 31, g = l >> 2, tg = l & 3;
   const int wr = w % kWR, wc = w / kWR;
   const double* Ys = Xs + kTM * kSS;
 #pragma unroll
   for (int ks = 0; ks < kTK / 4; ++ks) {
-    double av[kRT], bv[kCT];
+    double av[kRT], bv[CT];
 #pragma unroll
     for (int h = 0; h < kRT; ++h) av[h] = Xs[((h * kWR + wr) * 8 + g) * kSS + ks * 4 + tg];
 #pragma unroll
-    for (int c = 0; c < kCT; ++c) bv[c] = Ys[((wc * kCT + c) * 8 + g) * kSS + ks * 4 + tg];
+    for (int c = 0; c < CT; ++c) bv[c] = Ys[((wc * CT + c) * 8 + g) * kSS + ks * 4 + tg];
 #pragma unroll
     for (int h = 0; h < kRT; ++h)
 #pragma unroll
-      for (int c = 0; c < kCT; ++c) dmma(acc[h][c], av[h], bv[c]);
+      for (int c = 0; c < CT; ++c) dmma(acc[h][c], av[h], bv[c]);
   }
 }
 
@@ -74,8 +78,10 @@ struct Args {
   CUtensorMap tm;
   CUtensorMap tmr;  // R, box {36, 1}
   CUtensorMap tmr64;  // R, box {36, 64}
+  CUtensorMap tmw;    // A, box {132, 32}
   int validate;
-  int stagger;  // 1: each CTA starts its chunk walk at a different depth (no CTAs on the same R lines at once)
+  int stagger;
+  int ct;  // DMMA width of the ring modes' units (4: 64 signals, 2: 32)  // 1: each CTA starts its chunk walk at a different depth (no CTAs on the same R lines at once)
   const double* a;
   const double* r;
   int64_t ld, k, b;
@@ -112,7 +118,7 @@ __global__ void __launch_bounds__(kPT, 1) bench_kernel(const __grid_constant__ A
   const bool producer = p.mode == 5 ? (w % 4 == 0) : (w == 0);
   if (threadIdx.x == 0) {
     for (int s = 0; s < kRing; ++s) {
-      const int cnt = 1 + 32 * nprod;
+      const int cnt = (p.mode >= 10) ? 1 : 1 + 32 * nprod;  // latency modes: the expect_tx arrival alone
       asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(&s_full[s])), "r"(cnt));
       asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(&s_empty[s])), "r"(kPW));
     }
@@ -122,6 +128,39 @@ __global__ void __launch_bounds__(kPT, 1) bench_kernel(const __grid_constant__ A
   __syncthreads();
   if (p.mode == 0) {
     for (int u = 0; u < p.units; ++u) mma_unit(stage + (u % kRing) * kStage, acc);
+  } else if (p.mode == 10 || p.mode == 11) {
+    for (int u = 0; u < p.units; ++u) {
+      int j0, a0, k0;
+      unit_coords(p, u, j0, a0, k0);
+      if (threadIdx.x == 0) {
+        const bool w = p.mode == 11;
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(&s_full[0])),
+                     "r"(w ? 32 * 132 * 8 : kTM * kSS * 8)
+                     : "memory");
+        asm volatile(
+            "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
+            "[%4];" ::"r"(su32(stage)),
+            "l"(reinterpret_cast<uint64_t>(w ? &p.tmw : &p.tm)), "r"(w ? j0 % 1024 : k0), "r"(w ? (u * 32) % 4096 : j0),
+            "r"(su32(&s_full[0]))
+            : "memory");
+        mb_wait(&s_full[0], u & 1u);
+      }
+      __syncthreads();
+    }
+    acc[0][0][0] = stage[threadIdx.x];
+  } else if (p.mode == 12) {
+    for (int u = 0; u < p.units; ++u) {
+      int j0, a0, k0;
+      unit_coords(p, u, j0, a0, k0);
+      for (int e = threadIdx.x; e < kTM * 16; e += kPT) {
+        const int r = e / 16, kk = (e % 16) * 2;
+        cp16(stage + r * kSS + kk, p.a + (j0 + r) * p.ld + k0 + kk);
+      }
+      asm volatile("cp.async.commit_group;\n" ::);
+      asm volatile("cp.async.wait_group 0;\n" ::);
+      __syncthreads();
+    }
+    acc[0][0][0] = stage[threadIdx.x];
   } else if (p.mode == 4) {
     auto issue = [&](int s, int u) {
       int j0, a0, k0;
@@ -214,7 +253,8 @@ __global__ void __launch_bounds__(kPT, 1) bench_kernel(const __grid_constant__ A
         issue(qn, qn % kRing);
       }
       mb_wait(&s_full[u % kRing], (u / kRing) & 1u);
-      mma_unit(stage + (u % kRing) * kStage, acc);
+      if (p.ct == 2) mma_unit<2>(stage + (u % kRing) * kStage, acc);
+      else mma_unit(stage + (u % kRing) * kStage, acc);
       __syncwarp();
       if (l == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(&s_empty[u % kRing])) : "memory");
     }
@@ -267,6 +307,10 @@ int main() {
                                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (cr != CUDA_SUCCESS) printf("encode R failed %d\n", cr);
+    const cuuint32_t wbox[2] = {132, 32};
+    cr = reinterpret_cast<Encode>(f)(&p.tmw, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, a, dims, strides, wbox, es,
+                                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     const cuuint32_t rbox64[2] = {36, 64};
     cr = reinterpret_cast<Encode>(f)(&p.tmr64, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, r, rd, strides, rbox64, es,
                                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
@@ -288,11 +332,14 @@ int main() {
   const char* names[] = {"compute only", "TMA A + warp-0 cp.async R (3-stage ring)", "TMA A only",
                          "warp-0 cp.async R only", "all-thread cp.async, 2 stages + CTA barrier",
                          "TMA A + 4 producer warps for R", "TMA A + per-column 2D TMA R", "TMA A + gather4 R",
-                         "TMA A + per-column 1D bulk R", "TMA A + 2D TMA box of 64 R columns"};
+                         "TMA A + per-column 1D bulk R", "TMA A + 2D TMA box of 64 R columns",
+                         "latency: Corr A box alone", "latency: W A box alone", "latency: A tile by cp.async"};
   // mode 6 is listed for the record: a tile-mode tensor copy needs a 128-byte aligned
   // destination, which a 288-byte padded column stride cannot give (misaligned address)
   for (int stg = 0; stg < 1; ++stg)
-  for (int mode : {0, 1, 2, 3, 4, 5, 8, 7, 9}) {
+  for (int mode : {0, 1, 2, 3, 4, 5, 8, 7, 9, 10, 11, 12, 109}) {
+    p.ct = mode == 109 ? 2 : 4;
+    if (mode == 109) mode = 9;
     p.stagger = stg;
     p.mode = mode;
     p.units = 448;
@@ -304,10 +351,10 @@ int main() {
     float ms = 0;
     cudaEventElapsedTime(&ms, e0, e1);
     const cudaError_t err = cudaGetLastError();
-    const double flops = double(sms) * p.units * 2.0 * kTM * kTN * kTK;
+    const double flops = double(sms) * p.units * 2.0 * kTM * (kTN * p.ct / 4) * kTK;
     // validation: CTA 0's last unit's R tile against the host gather
     double bad = -1;
-    if (mode >= 1 && mode != 2) {
+    if (mode >= 1 && mode != 2 && mode < 10) {
       p.validate = 1;
       bench_kernel<<<sms, kPT, smem>>>(p);
       std::vector<double> got(kTN * kTK);
@@ -321,7 +368,7 @@ int main() {
         }
       p.validate = 0;
     }
-    printf("stagger %d mode %d %-45s %7.3f us/unit  %6.2f TFLOP/s  %s  max|R tile err| %g\n", stg, mode, names[mode],
+    printf("ct %d mode %d %-45s %7.3f us/unit  %6.2f TFLOP/s  %s  max|R tile err| %g\n", p.ct, mode, names[mode],
            ms * 1e3 / p.units, flops / (ms * 1e-3) / 1e12, cudaGetErrorString(cudaGetLastError()), bad);
   }
   return 0;

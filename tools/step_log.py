@@ -20,6 +20,16 @@ dt = np.diff(t)
 gn = (lg[:, 3] - lg[:, 2]) / 1e3   # us: power contraction W = A V + combine
 gt = (lg[:, 4] - lg[:, 3]) / 1e3   # us: A^T R contraction
 print('batch ms', rs[0].batch_device_ms, 'steps', len(lg), 'lockstep ms', t[-1])
+if lg.shape[1] >= 9:  # stream-K route: CTA 0's own completion times inside the step (us from the step start)
+    st = lg[:, 2]
+    rel = lambda c: np.where(lg[:, c] > 0, (lg[:, c] - st) / 1e3, np.nan)
+    stg, wd, wb, cd, cb, pd = rel(5), rel(6), rel(3), rel(7), rel(4), rel(8)
+    nxt = np.append((lg[1:, 2] - st[:-1]) / 1e3, np.nan)
+    for lo, hi in [(0, 40), (40, 80), (80, 120), (120, 160), (160, 200), (200, 240)]:
+        sel = slice(lo, min(hi, len(lg) - 1))
+        m = lambda x: np.nanmean(x[sel])
+        print(f"  steps {lo:3d}-{hi:3d}: staged {m(stg):6.1f} | CTA0 W done {m(wd):6.1f} W barrier {m(wb):6.1f} | "
+              f"CTA0 Corr done {m(cd):6.1f} Corr barrier {m(cb):6.1f} | CTA0 per-signal done {m(pd):6.1f} next step {m(nxt):6.1f}")
 for lo, hi in [(0, 40), (40, 80), (80, 120), (120, 160), (160, 200), (200, 240), (240, 300)]:
     sel = slice(lo, min(hi, len(dt)))
     if lo >= len(dt): break
