@@ -688,6 +688,9 @@ __device__ __noinline__ void sk_contract(const PrefixParams& p, int which, int64
       sk_store(p, sh, pact, tile, CT, h, c, e, tid, v);
     }
   }
+  // W's Rc columns are read by the next product's tensor copies (async proxy) after the
+  // caller's grid barrier
+  asm volatile("fence.proxy.async.global;" ::: "memory");
   if (trc) trc[2] = gtimer();
 }
 
@@ -1573,6 +1576,8 @@ __global__ void __launch_bounds__(kPT, 1) prefix_kernel(const __grid_constant__ 
                  __ldcg(reinterpret_cast<const double2*>(p.vp + static_cast<int64_t>(act[pact[c]]) * K) + j));
         }
       }
+      // the staged columns are read by tensor copies (async proxy) after the barrier
+      asm volatile("fence.proxy.async.global;" ::: "memory");
       grid.sync();
       if (logit) p.step_log[kLogW * steps + 5] = gtimer() - t0;
     }
