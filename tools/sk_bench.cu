@@ -15,6 +15,7 @@
 //  10  latency: one A box (36 x 128) at a time, issue -> full barrier, no compute
 //  11  latency: one W-layout A box (132 x 32) at a time
 //  12  latency: the A tile by all threads' cp.async (wait_group 0 + CTA barrier), one at a time
+//  13  as 9 with a dedicated producer warp (17 warps: the 16 DMMA warps never issue copies)
 // R columns are gathered through a permutation (signal = 37 c mod 512), as the lockstep
 // gathers its unfinished signals.
 // Prints us per unit and the DMMA rate. Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 sk_bench.cu -o sk_bench
@@ -271,6 +272,59 @@ __global__ void __launch_bounds__(kPT, 1) bench_kernel(const __grid_constant__ A
   if (s == 123.456) p.out[threadIdx.x] = s;
 }
 
+// mode 13: warp 16 only issues (TMA A + TMA box of 64 R columns), warps 0-15 only compute
+__global__ void __launch_bounds__(kPT + 32, 1) bench_kernel_ws(const __grid_constant__ Args p) {
+  extern __shared__ __align__(128) double dsm[];
+  double* stage = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(dsm) + 127) & ~uintptr_t(127));
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kRing; ++s) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&s_full[s])));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(&s_empty[s])), "r"(kPW));
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (w == kPW) {  // producer
+    if (l == 0) {
+      for (int u = 0; u < p.units; ++u) {
+        const int st = u % kRing;
+        mb_wait(&s_empty[st], ((u / kRing) & 1u) ^ 1u);
+        int j0, a0, k0;
+        unit_coords(p, u, j0, a0, k0);
+        double* Xs = stage + st * kStage;
+        uint64_t* full = &s_full[st];
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(full)),
+                     "r"(kTM * kSS * 8 + kTN * kSS * 8)
+                     : "memory");
+        asm volatile(
+            "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
+            "[%4];" ::"r"(su32(Xs)),
+            "l"(reinterpret_cast<uint64_t>(&p.tm)), "r"(k0), "r"(j0), "r"(su32(full))
+            : "memory");
+        asm volatile(
+            "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
+            "[%4];" ::"r"(su32(Xs + kTM * kSS)),
+            "l"(reinterpret_cast<uint64_t>(&p.tmr64)), "r"(k0), "r"(a0), "r"(su32(full))
+            : "memory");
+      }
+    }
+    return;
+  }
+  double acc[kRT][kCT][2] = {};
+  for (int u = 0; u < p.units; ++u) {
+    mb_wait(&s_full[u % kRing], (u / kRing) & 1u);
+    if (p.ct == 2) mma_unit<2>(stage + (u % kRing) * kStage, acc);
+    else mma_unit(stage + (u % kRing) * kStage, acc);
+    __syncwarp();
+    if (l == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(&s_empty[u % kRing])) : "memory");
+  }
+  double s = 0;
+  for (int h = 0; h < kRT; ++h)
+    for (int c = 0; c < kCT; ++c) s += acc[h][c][0] + acc[h][c][1];
+  if (s == 123.456) p.out[threadIdx.x] = s;
+}
+
 int main() {
   const int64_t ld = 1024, k = 4096, b = 512;
   double *a, *r, *out;
@@ -326,6 +380,7 @@ int main() {
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   const size_t smem = kRing * kStage * 8 + 128;
   cudaFuncSetAttribute(bench_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  cudaFuncSetAttribute(bench_kernel_ws, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
@@ -333,19 +388,22 @@ int main() {
                          "warp-0 cp.async R only", "all-thread cp.async, 2 stages + CTA barrier",
                          "TMA A + 4 producer warps for R", "TMA A + per-column 2D TMA R", "TMA A + gather4 R",
                          "TMA A + per-column 1D bulk R", "TMA A + 2D TMA box of 64 R columns",
-                         "latency: Corr A box alone", "latency: W A box alone", "latency: A tile by cp.async"};
+                         "latency: Corr A box alone", "latency: W A box alone", "latency: A tile by cp.async",
+                         "as 9, dedicated producer warp"};
   // mode 6 is listed for the record: a tile-mode tensor copy needs a 128-byte aligned
   // destination, which a 288-byte padded column stride cannot give (misaligned address)
   for (int stg = 0; stg < 1; ++stg)
-  for (int mode : {0, 1, 2, 3, 4, 5, 8, 7, 9, 10, 11, 12, 109}) {
-    p.ct = mode == 109 ? 2 : 4;
-    if (mode == 109) mode = 9;
+  for (int mode : {0, 9, 13, 109, 113, 1, 2, 3, 4, 5, 8, 7, 10, 11, 12}) {
+    p.ct = mode >= 100 ? 2 : 4;
+    if (mode >= 100) mode -= 100;
     p.stagger = stg;
     p.mode = mode;
     p.units = 448;
-    bench_kernel<<<sms, kPT, smem>>>(p);
+    if (mode == 13) bench_kernel_ws<<<sms, kPT + 32, smem>>>(p);
+    else bench_kernel<<<sms, kPT, smem>>>(p);
     cudaEventRecord(e0);
-    bench_kernel<<<sms, kPT, smem>>>(p);
+    if (mode == 13) bench_kernel_ws<<<sms, kPT + 32, smem>>>(p);
+    else bench_kernel<<<sms, kPT, smem>>>(p);
     cudaEventRecord(e1);
     cudaEventSynchronize(e1);
     float ms = 0;
@@ -354,7 +412,7 @@ int main() {
     const double flops = double(sms) * p.units * 2.0 * kTM * (kTN * p.ct / 4) * kTK;
     // validation: CTA 0's last unit's R tile against the host gather
     double bad = -1;
-    if (mode >= 1 && mode != 2 && mode < 10) {
+    if (mode >= 1 && mode != 2 && mode < 10) {  // (mode 13 loads what mode 9 loads)
       p.validate = 1;
       bench_kernel<<<sms, kPT, smem>>>(p);
       std::vector<double> got(kTN * kTK);
