@@ -1396,8 +1396,9 @@ void solve_clusters(fl1_seq* s, const double* Y, bool y_device, int64_t ldy, con
     }
     static std::unique_ptr<DevBuf> sk_trace;
     if (const char* st = std::getenv("FL1_SK_TRACE")) {  // diagnostics: per-CTA times of one step's products
-      if (!sk_trace) sk_trace = std::make_unique<DevBuf>(sizeof(double) * 2 * 4 * 256);
-      ck(cudaMemset(sk_trace->p, 0, sizeof(double) * 2 * 4 * 256), "sk trace");
+      // per product and CTA: 4 times | CTAs 0-3: per unit, the times before / after its full-barrier wait
+      if (!sk_trace) sk_trace = std::make_unique<DevBuf>(sizeof(double) * (2 * 4 * 256 + 2 * 4 * 128 * 2));
+      ck(cudaMemset(sk_trace->p, 0, sizeof(double) * (2 * 4 * 256 + 2 * 4 * 128 * 2)), "sk trace");
       pp.sk_trace = sk_trace->as<double>();
       pp.sk_trace_step = std::atoi(st);
     }
@@ -1494,7 +1495,7 @@ void solve_clusters(fl1_seq* s, const double* Y, bool y_device, int64_t ldy, con
     }
   }
   if (pp.sk_trace) {
-    std::vector<double> h(2 * 4 * 256);
+    std::vector<double> h(2 * 4 * 256 + 2 * 4 * 128 * 2);
     ck(cudaMemcpy(h.data(), pp.sk_trace, h.size() * sizeof(double), cudaMemcpyDeviceToHost), "sk trace");
     if (FILE* f = std::fopen("fl1_sk_trace.txt", "w")) {
       for (size_t i = 0; i < h.size(); i += 4) std::fprintf(f, "%.17g %.17g %.17g %.17g\n", h[i], h[i + 1], h[i + 2], h[i + 3]);

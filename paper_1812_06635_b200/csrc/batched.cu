@@ -446,12 +446,31 @@ struct SkShape {
 
 // issue unit u's loads into stage st (one thread): a 2D tensor copy of the A tile and one
 // of the 64 slot-ordered R / V columns, both on the stage's full barrier
-__device__ __forceinline__ void sk_issue(const PrefixParams& p, const SkShape& sh, int64_t u, int st, double* stage) {
-  const int64_t tile = u / sh.nch;
-  const int kc = static_cast<int>(u - tile * sh.nch);
-  const int rt = static_cast<int>(tile % sh.n_rt);
-  const int c0 = static_cast<int>((tile / sh.n_rt) * kTN);
-  const int d0 = kc * kTK;
+// The issue cursor: unit -> (row tile, column offset, chunk) advanced incrementally (the
+// issuing thread is a DMMA warp's lane: 64-bit divisions per unit cost ~10% of the unit)
+struct SkCursor {
+  int kc, rt, c0;
+  __device__ SkCursor(const SkShape& sh, int64_t u) {
+    const int64_t tile = u / sh.nch;
+    kc = static_cast<int>(u - tile * sh.nch);
+    rt = static_cast<int>(tile % sh.n_rt);
+    c0 = static_cast<int>((tile / sh.n_rt) * kTN);
+  }
+  __device__ __forceinline__ void advance(const SkShape& sh) {
+    if (++kc == sh.nch) {
+      kc = 0;
+      if (++rt == sh.n_rt) {
+        rt = 0;
+        c0 += kTN;
+      }
+    }
+  }
+};
+
+__device__ __forceinline__ void sk_issue(const PrefixParams& p, const SkShape& sh, const SkCursor& cu, int st,
+                                         double* stage) {
+  const int rt = cu.rt, c0 = cu.c0;
+  const int d0 = cu.kc * kTK;
   double* Xs = stage + st * kStage;
   const uint32_t xbytes = sh.which ? kTM * kSS * 8 : kTK * (kTM + 4) * 8;
   double* Ys = Xs + (sh.which ? kTM * kSS : kTK * (kTM + 4));
@@ -548,8 +567,12 @@ __device__ __noinline__ void sk_contract(const PrefixParams& p, int which, int64
   }
   if (u0 >= u1) return;
   const int64_t nu = u1 - u0;
+  SkCursor cur(sh, u0);  // next unit to issue (thread 0)
   if (threadIdx.x == 0)
-    for (int64_t i = 0; i < kRing - 1 && i < nu; ++i) sk_issue(p, sh, u0 + i, static_cast<int>((ring + i) % kRing), stage);
+    for (int64_t i = 0; i < kRing - 1 && i < nu; ++i) {
+      sk_issue(p, sh, cur, static_cast<int>((ring + i) % kRing), stage);
+      cur.advance(sh);
+    }
   double acc[kRT][kCT][2];
   int64_t u = u0;
   while (u < u1) {
@@ -566,10 +589,13 @@ __device__ __noinline__ void sk_contract(const PrefixParams& p, int which, int64
       if (threadIdx.x == 0 && i + kRing - 1 < nu) {  // refill the stage released at unit i - 1
         const uint32_t qn = ring + static_cast<uint32_t>(i + kRing - 1);
         mb_wait(&s_empty[qn % kRing], ((qn / kRing) & 1u) ^ 1u);
-        sk_issue(p, sh, u + kRing - 1, static_cast<int>(qn % kRing), stage);
+        sk_issue(p, sh, cur, static_cast<int>(qn % kRing), stage);
+        cur.advance(sh);
       }
       const uint32_t q = ring + static_cast<uint32_t>(i);
+      if (trc && gi < 4 && i < 128) p.sk_trace[2 * kMaxGrid * 4 + ((which * 4 + gi) * 128 + i) * 2] = gtimer();
       mb_wait(&s_full[q % kRing], (q / kRing) & 1u);
+      if (trc && gi < 4 && i < 128) p.sk_trace[2 * kMaxGrid * 4 + ((which * 4 + gi) * 128 + i) * 2 + 1] = gtimer();
       const double* Xs = stage + (q % kRing) * kStage;
       switch (CT + 8 * which) {
         case 1: sk_mma<0, 1>(Xs, acc); break;

@@ -16,6 +16,10 @@
 //  11  latency: one W-layout A box (132 x 32) at a time
 //  12  latency: the A tile by all threads' cp.async (wait_group 0 + CTA barrier), one at a time
 //  13  as 9 with a dedicated producer warp (17 warps: the 16 DMMA warps never issue copies)
+//  15  as 9 the way the lockstep issues: thread 0 alone (expect_tx + two boxes), full
+//      barrier count 1, no cp.async arrivals
+//  14  as 9 with a lookahead of kRing - 2 units: warp 0 refills the stage released two
+//      units ago (no wait on the slowest warp's previous unit)
 // R columns are gathered through a permutation (signal = 37 c mod 512), as the lockstep
 // gathers its unfinished signals.
 // Prints us per unit and the DMMA rate. Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 sk_bench.cu -o sk_bench
@@ -119,7 +123,7 @@ __global__ void __launch_bounds__(kPT, 1) bench_kernel(const __grid_constant__ A
   const bool producer = p.mode == 5 ? (w % 4 == 0) : (w == 0);
   if (threadIdx.x == 0) {
     for (int s = 0; s < kRing; ++s) {
-      const int cnt = (p.mode >= 10) ? 1 : 1 + 32 * nprod;  // latency modes: the expect_tx arrival alone
+      const int cnt = (p.mode >= 10 && p.mode != 14) ? 1 : 1 + 32 * nprod;  // 15: the issuing thread alone  // latency modes: the expect_tx arrival alone
       asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(&s_full[s])), "r"(cnt));
       asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(&s_empty[s])), "r"(kPW));
     }
@@ -192,7 +196,7 @@ __global__ void __launch_bounds__(kPT, 1) bench_kernel(const __grid_constant__ A
       uint64_t* full = &s_full[st];
       const int pw = p.mode == 5 ? w / 4 : 0;
       const bool tma_y = p.mode >= 6;
-      const bool box_y = p.mode == 9;
+      const bool box_y = p.mode == 9 || p.mode == 14 || p.mode == 15;
       if (pw == 0 && l == 0) {
         const uint32_t xb = (do_x ? kTM * kSS * 8 : 0) + (tma_y ? (p.mode == 8 ? kTN * kTK * 8 : kTN * kSS * 8) : 0);
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(full)), "r"(xb) : "memory");
@@ -242,13 +246,14 @@ __global__ void __launch_bounds__(kPT, 1) bench_kernel(const __grid_constant__ A
       } else if (do_y) {
         issue_y(p, u, Xs + kTM * kSS, pw * 32, 32 * nprod, l);
       }
-      asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(su32(full)) : "memory");
+      if (p.mode != 15) asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(su32(full)) : "memory");
     };
+    const int ahead = p.mode == 14 ? kRing - 2 : kRing - 1;
     if (producer)
-      for (int i = 0; i < kRing - 1 && i < p.units; ++i) issue(i, i % kRing);
+      for (int i = 0; i < ahead && i < p.units; ++i) issue(i, i % kRing);
     for (int u = 0; u < p.units; ++u) {
-      if (producer && u + kRing - 1 < p.units) {
-        const uint32_t qn = u + kRing - 1;
+      if (producer && u + ahead < p.units) {
+        const uint32_t qn = u + ahead;
         if (l == 0) mb_wait(&s_empty[qn % kRing], ((qn / kRing) & 1u) ^ 1u);
         __syncwarp();
         issue(qn, qn % kRing);
@@ -389,11 +394,11 @@ int main() {
                          "TMA A + 4 producer warps for R", "TMA A + per-column 2D TMA R", "TMA A + gather4 R",
                          "TMA A + per-column 1D bulk R", "TMA A + 2D TMA box of 64 R columns",
                          "latency: Corr A box alone", "latency: W A box alone", "latency: A tile by cp.async",
-                         "as 9, dedicated producer warp"};
+                         "as 9, dedicated producer warp", "as 9, lookahead kRing - 2", "as 9, thread 0 alone"};
   // mode 6 is listed for the record: a tile-mode tensor copy needs a 128-byte aligned
   // destination, which a 288-byte padded column stride cannot give (misaligned address)
   for (int stg = 0; stg < 1; ++stg)
-  for (int mode : {0, 9, 13, 109, 113, 1, 2, 3, 4, 5, 8, 7, 10, 11, 12}) {
+  for (int mode : {0, 9, 13, 14, 15, 109, 113, 114, 115, 1, 2, 3, 4, 5, 8, 7, 10, 11, 12}) {
     p.ct = mode >= 100 ? 2 : 4;
     if (mode >= 100) mode -= 100;
     p.stagger = stg;

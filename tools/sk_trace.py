@@ -17,7 +17,9 @@ opts = F.RunOptions(variant=F.VARIANT_SCREENED, full_lipschitz=[L])
 Yd = torch.from_numpy(np.ascontiguousarray(Y.T)).cuda()
 for _ in range(2):
     F.run_lasso_batched(seq, (n, B), lams, cfg, opts, -2, y_dev_ptr=Yd.data_ptr())
-t = np.loadtxt('fl1_sk_trace.txt').reshape(2, 256, 4)
+raw = np.loadtxt('fl1_sk_trace.txt').reshape(-1)
+t = raw[:2 * 256 * 4].reshape(2, 256, 4)
+units = raw[2 * 256 * 4:].reshape(2, 4, 128, 2)  # [product][CTA 0-3][unit][before wait, after wait]
 for w, name in ((0, 'W'), (1, 'Corr')):
     x = t[w, :148]
     if not x[:, 0].any():
@@ -26,5 +28,14 @@ for w, name in ((0, 'W'), (1, 'Corr')):
     st, ud, en = (x[:, 0] - t0) / 1e3, (x[:, 1] - t0) / 1e3, (x[:, 2] - t0) / 1e3
     print(f"{name} step {step}: start max {st.max():.1f} us | units done min {ud.min():.1f} p50 {np.median(ud):.1f} max {ud.max():.1f} "
           f"| end min {en.min():.1f} p50 {np.median(en):.1f} max {en.max():.1f} | units/CTA {x[:, 3].min():.0f}-{x[:, 3].max():.0f}")
+    for g in range(2):
+        u = units[w, g]
+        m = u[:, 0] > 0
+        if m.sum() > 1:
+            aft = u[m, 1]
+            per = np.diff(aft) / 1e3
+            waits = (u[m, 1] - u[m, 0]) / 1e3
+            print(f"   CTA {g}: {m.sum()} units, unit period p50 {np.median(per):.2f} us (min {per.min():.2f}, max {per.max():.2f}), "
+                  f"full-barrier wait p50 {np.median(waits):.2f} us, first wait {waits[0]:.2f} us after start {(u[0, 0] - x[g, 0]) / 1e3:.2f} us")
     worst = np.argsort(-en)[:5]
     print('   slowest CTAs', worst.tolist(), 'units done', np.round(ud[worst], 1).tolist(), 'end', np.round(en[worst], 1).tolist())
