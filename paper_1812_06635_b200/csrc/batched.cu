@@ -545,6 +545,32 @@ __device__ __forceinline__ void sk_store(const PrefixParams& p, const SkShape& s
   else __stcg(p.rc + static_cast<int64_t>(pact[col]) * p.ld + r, r < p.n ? v : 0.0);
 }
 
+// The units [ub, ue) of one segment (a single tile: DMMA width CT): thread 0 refills the
+// stage released at the previous unit, every warp waits for its unit's stage, computes and
+// releases it. utr (diagnostics): per unit, the times around the full-barrier wait.
+template <int WHICH, int CT>
+__device__ __forceinline__ void sk_units(const PrefixParams& p, const SkShape& sh, double* stage, SkCursor& cur,
+                                         uint32_t ring, int64_t u0, int64_t nu, int64_t ub, int64_t ue,
+                                         double (&acc)[kRT][kCT][2], double* utr) {
+  const int l = threadIdx.x & 31;
+  for (int64_t u = ub; u < ue; ++u) {
+    const int64_t i = u - u0;
+    if (threadIdx.x == 0 && i + kRing - 1 < nu) {  // refill the stage released at unit i - 1
+      const uint32_t qn = ring + static_cast<uint32_t>(i + kRing - 1);
+      mb_wait(&s_empty[qn % kRing], ((qn / kRing) & 1u) ^ 1u);
+      sk_issue(p, sh, cur, static_cast<int>(qn % kRing), stage);
+      cur.advance(sh);
+    }
+    const uint32_t q = ring + static_cast<uint32_t>(i);
+    if (utr && i < 128) utr[2 * i] = gtimer();
+    mb_wait(&s_full[q % kRing], (q / kRing) & 1u);
+    if (utr && i < 128) utr[2 * i + 1] = gtimer();
+    sk_mma<WHICH, CT>(stage + (q % kRing) * kStage, acc);
+    __syncwarp();
+    if (l == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(&s_empty[q % kRing])) : "memory");
+  }
+}
+
 // One stream-K product over this CTA's unit range. ring: the CTA's running unit count
 // (stage and phase of the ring; identical in every thread). epoch: unique per product
 // within the launch (the flags are zeroed at the launch's start).
@@ -584,32 +610,18 @@ __device__ __noinline__ void sk_contract(const PrefixParams& p, int which, int64
     for (int h = 0; h < kRT; ++h)
 #pragma unroll
       for (int c = 0; c < kCT; ++c) acc[h][c][0] = acc[h][c][1] = 0.0;
-    for (; u < useg; ++u) {
-      const int64_t i = u - u0;
-      if (threadIdx.x == 0 && i + kRing - 1 < nu) {  // refill the stage released at unit i - 1
-        const uint32_t qn = ring + static_cast<uint32_t>(i + kRing - 1);
-        mb_wait(&s_empty[qn % kRing], ((qn / kRing) & 1u) ^ 1u);
-        sk_issue(p, sh, cur, static_cast<int>(qn % kRing), stage);
-        cur.advance(sh);
-      }
-      const uint32_t q = ring + static_cast<uint32_t>(i);
-      if (trc && gi < 4 && i < 128) p.sk_trace[2 * kMaxGrid * 4 + ((which * 4 + gi) * 128 + i) * 2] = gtimer();
-      mb_wait(&s_full[q % kRing], (q / kRing) & 1u);
-      if (trc && gi < 4 && i < 128) p.sk_trace[2 * kMaxGrid * 4 + ((which * 4 + gi) * 128 + i) * 2 + 1] = gtimer();
-      const double* Xs = stage + (q % kRing) * kStage;
-      switch (CT + 8 * which) {
-        case 1: sk_mma<0, 1>(Xs, acc); break;
-        case 2: sk_mma<0, 2>(Xs, acc); break;
-        case 3: sk_mma<0, 3>(Xs, acc); break;
-        case 4: sk_mma<0, 4>(Xs, acc); break;
-        case 9: sk_mma<1, 1>(Xs, acc); break;
-        case 10: sk_mma<1, 2>(Xs, acc); break;
-        case 11: sk_mma<1, 3>(Xs, acc); break;
-        default: sk_mma<1, 4>(Xs, acc);
-      }
-      __syncwarp();
-      if (l == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(&s_empty[q % kRing])) : "memory");
+    double* utr = (trc && gi < 4) ? p.sk_trace + 2 * kMaxGrid * 4 + (which * 4 + gi) * 128 * 2 : nullptr;
+    switch (CT + 8 * which) {  // one instantiation of the unit loop per segment
+      case 1: sk_units<0, 1>(p, sh, stage, cur, ring, u0, nu, u, useg, acc, utr); break;
+      case 2: sk_units<0, 2>(p, sh, stage, cur, ring, u0, nu, u, useg, acc, utr); break;
+      case 3: sk_units<0, 3>(p, sh, stage, cur, ring, u0, nu, u, useg, acc, utr); break;
+      case 4: sk_units<0, 4>(p, sh, stage, cur, ring, u0, nu, u, useg, acc, utr); break;
+      case 9: sk_units<1, 1>(p, sh, stage, cur, ring, u0, nu, u, useg, acc, utr); break;
+      case 10: sk_units<1, 2>(p, sh, stage, cur, ring, u0, nu, u, useg, acc, utr); break;
+      case 11: sk_units<1, 3>(p, sh, stage, cur, ring, u0, nu, u, useg, acc, utr); break;
+      default: sk_units<1, 4>(p, sh, stage, cur, ring, u0, nu, u, useg, acc, utr);
     }
+    u = useg;
     // ---- segment epilogue
     if (kc0 == 0 && useg == (tile + 1) * sh.nch) {  // the whole tile: write it
 #pragma unroll
