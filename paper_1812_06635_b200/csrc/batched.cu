@@ -390,7 +390,7 @@ constexpr int kStageBufs = kStages > kRing ? kStages : kRing;  // staging area, 
 __shared__ __align__(8) uint64_t s_full[kRing];
 __shared__ __align__(8) uint64_t s_empty[kRing];
 constexpr int kMaxGrid = 256;             // stream-K route: CTAs (one per SM) at most
-__shared__ int32_t s_contrib[kMaxGrid];   // a shared tile's contributor slots, chunk order
+__shared__ int32_t s_contrib[2 * kMaxGrid];  // the shared tiles' contributor slots, chunk order
 __shared__ int32_t sh_scal[2];
 __shared__ int64_t s_begin[kMaxGrid + 1];  // the product's unit-range starts of every CTA
 
@@ -587,10 +587,7 @@ __device__ __noinline__ void sk_contract(const PrefixParams& p, int which, int64
   const int64_t u0 = s_begin[gi], u1 = s_begin[gi + 1];
   double* trc = (p.sk_trace && (epoch - 1 - which) / 2 == p.sk_trace_step && threadIdx.x == 0)
                     ? p.sk_trace + (which * kMaxGrid + gi) * 4 : nullptr;
-  if (trc) {
-    trc[0] = gtimer();
-    trc[3] = static_cast<double>(u1 - u0);
-  }
+  if (trc) trc[0] = gtimer();
   if (u0 >= u1) return;
   const int64_t nu = u1 - u0;
   SkCursor cur(sh, u0);  // next unit to issue (thread 0)
@@ -660,6 +657,9 @@ __device__ __noinline__ void sk_contract(const PrefixParams& p, int which, int64
   // starting from its registers; one with more contributors (narrow products: ~20) by
   // all of them, each a slice of the elements. Partials are added in chunk (= CTA) order.
   const int64_t tiles[2] = {u0 / sh.nch, (u1 - 1) / sh.nch};
+  int nt = 0, solo_k = -1;  // shared tiles this CTA reduces (solo: the holder's, from registers)
+  int64_t rtile[2];
+  SkContrib rtc[2];
   for (int s2 = 0; s2 < 2; ++s2) {
     const int64_t tile = tiles[s2];
     if (s2 == 1 && tile == tiles[0]) break;
@@ -668,25 +668,45 @@ __device__ __noinline__ void sk_contract(const PrefixParams& p, int which, int64
     const SkContrib tc = sk_contrib(ta, tb, gi, G);
     const bool solo = tc.n_ne <= p.sk_fanin;
     if (solo && gi != tc.gA) continue;
-    __syncthreads();  // s_contrib of the previous tile is no longer read
-    if (threadIdx.x == 0) {
-      int n = 0;
-      for (int g2 = tc.gA; g2 <= tc.gB; ++g2)
-        if (s_begin[g2 + 1] > s_begin[g2]) s_contrib[n++] = 2 * g2 + (s_begin[g2] >= ta ? 0 : 1);
+    if (solo) solo_k = nt;
+    rtile[nt] = tile;
+    rtc[nt++] = tc;
+  }
+  if (nt > 0) {
+    // contributor slots of both tiles (chunk order), then every flag waited at once
+    __syncthreads();  // s_contrib of the previous product is no longer read
+    if (threadIdx.x == 0)
+      for (int k = 0; k < nt; ++k) {
+        int n = 0;
+        const int64_t ta = rtile[k] * sh.nch;
+        for (int g2 = rtc[k].gA; g2 <= rtc[k].gB; ++g2)
+          if (s_begin[g2 + 1] > s_begin[g2]) s_contrib[k * kMaxGrid + n++] = 2 * g2 + (s_begin[g2] >= ta ? 0 : 1);
+      }
+    __syncthreads();
+    for (int k = 0; k < nt; ++k) {
+      const int first = k == solo_k ? 1 : 0;  // the holder's own segment is in registers
+      const int t = static_cast<int>(threadIdx.x) - (k == 0 ? 0 : rtc[0].n_ne);
+      if (t >= first && t < rtc[k].n_ne) {
+        int32_t f = 0;
+        do {
+          asm volatile("ld.acquire.gpu.global.b32 %0, [%1];"
+                       : "=r"(f)
+                       : "l"(p.flags + s_contrib[k * kMaxGrid + t])
+                       : "memory");
+        } while (f != epoch);
+      }
     }
     __syncthreads();
-    const int first = solo ? 1 : 0;  // solo: the holder's own segment is in registers
-    if (threadIdx.x >= first && threadIdx.x < tc.n_ne) {
-      int32_t f = 0;
-      do {
-        asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(f) : "l"(p.flags + s_contrib[threadIdx.x]) : "memory");
-      } while (f != epoch);
-    }
-    __syncthreads();
-    if (solo) {
-      const int CT = sh.ct_of(tile);
-      for (int k2 = 1; k2 < tc.n_ne; ++k2) {
-        const double* s2p = p.part + static_cast<int64_t>(s_contrib[k2]) * kPartTile;
+  }
+  if (trc) trc[3] = gtimer();
+  for (int k = 0; k < nt; ++k) {
+    const int64_t tile = rtile[k];
+    const int CT = sh.ct_of(tile);
+    const int32_t* con = s_contrib + k * kMaxGrid;
+    const int n_ne = rtc[k].n_ne;
+    if (k == solo_k) {
+      for (int k2 = 1; k2 < n_ne; ++k2) {
+        const double* s2p = p.part + static_cast<int64_t>(con[k2]) * kPartTile;
 #pragma unroll
         for (int h = 0; h < kRT; ++h)
 #pragma unroll
@@ -704,31 +724,30 @@ __device__ __noinline__ void sk_contract(const PrefixParams& p, int which, int64
             for (int e = 0; e < 2; ++e) sk_store(p, sh, pact, tile, CT, h, c, e, threadIdx.x, acc[h][c][e]);
       continue;
     }
-    const int n_ne = tc.n_ne, nr = n_ne, j = tc.j;
-    const int CT = sh.ct_of(tile);
+    const int j = rtc[k].j;
     const int E = kRT * CT * 2 * kPT;  // valid elements of the tile
-    const int q0 = E * j / nr, q1 = E * (j + 1) / nr;
+    const int q0 = E * j / n_ne, q1 = E * (j + 1) / n_ne;
     for (int q = q0 + threadIdx.x; q < q1; q += kPT) {
       const int h = q / (CT * 2 * kPT);
       const int rem = q - h * CT * 2 * kPT;
       const int c = rem / (2 * kPT), e = (rem / kPT) & 1, tid = rem % kPT;
       const int off = ((h * kCT + c) * 2 + e) * kPT + tid;
       double v = 0.0;
-      int k2 = 0;
-      for (; k2 + 4 <= n_ne; k2 += 4) {  // four loads in flight, added in order
-        double t[4];
+      for (int k0 = 0; k0 < n_ne; k0 += 16) {  // up to 16 partials' loads in flight, added in order
+        double t[16];
 #pragma unroll
-        for (int z = 0; z < 4; ++z) t[z] = __ldcg(p.part + static_cast<int64_t>(s_contrib[k2 + z]) * kPartTile + off);
+        for (int z = 0; z < 16; ++z)
+          t[z] = k0 + z < n_ne ? __ldcg(p.part + static_cast<int64_t>(con[k0 + z]) * kPartTile + off) : 0.0;
 #pragma unroll
-        for (int z = 0; z < 4; ++z) v += t[z];
+        for (int z = 0; z < 16; ++z)
+          if (k0 + z < n_ne) v += t[z];
       }
-      for (; k2 < n_ne; ++k2) v += __ldcg(p.part + static_cast<int64_t>(s_contrib[k2]) * kPartTile + off);
       sk_store(p, sh, pact, tile, CT, h, c, e, tid, v);
     }
   }
   // W's Rc columns are read by the next product's tensor copies (async proxy) after the
-  // caller's grid barrier
-  asm volatile("fence.proxy.async.global;" ::: "memory");
+  // caller's grid barrier (Corr is read by generic loads only)
+  if (!which) asm volatile("fence.proxy.async.global;" ::: "memory");
   if (trc) trc[2] = gtimer();
 }
 

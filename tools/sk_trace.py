@@ -26,8 +26,9 @@ for w, name in ((0, 'W'), (1, 'Corr')):
         print(name, 'not run at step', step); continue
     t0 = x[:, 0].min()
     st, ud, en = (x[:, 0] - t0) / 1e3, (x[:, 1] - t0) / 1e3, (x[:, 2] - t0) / 1e3
+    fl = np.where(x[:, 3] > 0, (x[:, 3] - t0) / 1e3, np.nan)  # flags waited (CTAs that reduce a shared tile)
     print(f"{name} step {step}: start max {st.max():.1f} us | units done min {ud.min():.1f} p50 {np.median(ud):.1f} max {ud.max():.1f} "
-          f"| end min {en.min():.1f} p50 {np.median(en):.1f} max {en.max():.1f} | units/CTA {x[:, 3].min():.0f}-{x[:, 3].max():.0f}")
+          f"| flags waited p50 {np.nanmedian(fl):.1f} max {np.nanmax(fl):.1f} | end min {en.min():.1f} p50 {np.median(en):.1f} max {en.max():.1f}")
     for g in range(2):
         u = units[w, g]
         m = u[:, 0] > 0
@@ -38,4 +39,5 @@ for w, name in ((0, 'W'), (1, 'Corr')):
             print(f"   CTA {g}: {m.sum()} units, unit period p50 {np.median(per):.2f} us (min {per.min():.2f}, max {per.max():.2f}), "
                   f"full-barrier wait p50 {np.median(waits):.2f} us, first wait {waits[0]:.2f} us after start {(u[0, 0] - x[g, 0]) / 1e3:.2f} us")
     worst = np.argsort(-en)[:5]
-    print('   slowest CTAs', worst.tolist(), 'units done', np.round(ud[worst], 1).tolist(), 'end', np.round(en[worst], 1).tolist())
+    print('   slowest CTAs', worst.tolist(), 'units done', np.round(ud[worst], 1).tolist(), 'flags',
+          np.round(fl[worst], 1).tolist(), 'end', np.round(en[worst], 1).tolist())
