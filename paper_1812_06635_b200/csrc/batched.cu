@@ -41,7 +41,10 @@ namespace {
 constexpr int kPT = FL1_PREFIX_THREADS;  // threads per CTA
 constexpr int kPW = kPT / 32;
 constexpr int kIt = 9;  // atoms per lane of a warp range: K <= prefix_max_atoms() = 4608 -> 288 per warp
-constexpr int kItB = 3; // atoms per lane loaded together in the prox pass
+#ifndef FL1_ITB
+#define FL1_ITB 3
+#endif
+constexpr int kItB = FL1_ITB;  // atoms per lane loaded together in the prox pass
 constexpr int kTM = 128, kTN = 64;  // output tile: 128 rows (atoms / samples) x 64 signals
 // warp grid over a 128 x 64 output tile: kWR x kWC warps, each kRT x kCT 8x8 DMMA tiles
 constexpr int kWR = 8, kWC = (kPT / 32) / kWR;
@@ -950,7 +953,10 @@ __device__ __forceinline__ int warp_append(bool flag, double v, int32_t j, doubl
 // The entries are walked as one list across the segments (a uniform cursor), eight
 // per round, two rows per thread: 16 loads in flight and ~nnz/8 L2 round trips
 // instead of one per entry at every segment's tail.
-constexpr int kApE = 8, kApR = 2;
+#ifndef FL1_APE
+#define FL1_APE 8
+#endif
+constexpr int kApE = FL1_APE, kApR = 2;
 __device__ __forceinline__ void apply_segments(const PrefixParams& p, double* us, const double* ev, const int32_t* ej,
                                                int64_t seg, const int32_t* cnt, double sign) {
   const int64_t ld = p.ld;
