@@ -74,6 +74,7 @@ cudaError_t sukro_norms_launch(const double* left, const double* right, const do
                                int64_t q, double* out, cudaStream_t stream);
 int64_t prefix_max_atoms();
 int64_t prefix_part_elems(int grid);
+bool prefix_fits(int64_t ld, int64_t batch, int device);
 int prefix_stream_k_max_grid();
 constexpr int kStepLogW = 10;  // batched.cu kLogW
 cudaError_t gemm_tn_launch(const double* X, int64_t ldx, int64_t nx, const double* Y, int64_t ldy, int64_t ny,
@@ -1280,6 +1281,7 @@ void solve_clusters(fl1_seq* s, const double* Y, bool y_device, int64_t ldy, con
                           opts->rule == FL1_RULE_GAP &&
                           (opts->variant == FL1_SCREENED || opts->variant == FL1_PLAIN) &&
                           opts->full_lipschitz != nullptr && k <= fl1::prefix_max_atoms() &&
+                          fl1::prefix_fits(ld, batch, ctx->device) &&
                           !(pe && pe[0] == '0');
   fl1::PrefixParams pp{};
   if (use_prefix) {

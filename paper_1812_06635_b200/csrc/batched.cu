@@ -1557,6 +1557,7 @@ __global__ void __launch_bounds__(kPT, 1) prefix_kernel(const __grid_constant__ 
   }
   int32_t* act = reinterpret_cast<int32_t*>(us + ld);
   int32_t* pact = act + B;
+  int32_t* qord = pact + B;  // per-signal queue order: the FISTA slots first, then the power steps
   // ---- Engine ctor (254-276) with x = 0, S = K, cached full L: u = 0, momentum off
   for (int64_t b = blockIdx.x; b < B; b += gridDim.x) {
     double acc = 0.0;
@@ -1598,7 +1599,7 @@ __global__ void __launch_bounds__(kPT, 1) prefix_kernel(const __grid_constant__ 
   int64_t work_act = 0, work_pow = 0;  // contraction widths summed over the steps (roofline accounting)
   for (;; ++steps) {
     // unfinished signals in signal order, and the ones in a power step (identical in every CTA)
-    int n_act = 0, n_pow = 0;
+    int n_act = 0, n_pow = 0, n_fista = 0;
     for (int64_t base = 0; base < B; base += kPT) {
       const int64_t b = base + threadIdx.x;
       const int mode = b < B ? __ldcg(&p.sig[b].mode) : 2;
@@ -1609,9 +1610,17 @@ __global__ void __launch_bounds__(kPT, 1) prefix_kernel(const __grid_constant__ 
       int atp;
       const int np = block_compact(sh, mode == 1, n_pow, &atp);
       if (mode == 1) pact[atp] = at;
+      int atf;
+      const int nf = block_compact(sh, mode == 0, n_fista, &atf);
+      if (mode == 0) qord[atf] = at;
       n_act = na;
       n_pow = np;
+      n_fista = nf;
     }
+    // the power steps (~12 us on one CTA) queue behind the FISTA steps (~25-30 us at the full
+    // set): longest first, so that the step's last CTA is not one that took a FISTA step late
+    for (int i = threadIdx.x; i < n_pow; i += kPT) qord[n_fista + i] = pact[i];
+    __syncthreads();
     if (n_act == 0) break;
     work_act += n_act;
     work_pow += n_pow;
@@ -1722,9 +1731,10 @@ __global__ void __launch_bounds__(kPT, 1) prefix_kernel(const __grid_constant__ 
     for (;;) {
       if (threadIdx.x == 0) sh.qnext = atomicAdd(p.queue + (steps & 1), 1);
       __syncthreads();
-      const int64_t a = sh.qnext;
+      const int64_t qi = sh.qnext;
       __syncthreads();
-      if (a >= n_act) break;
+      if (qi >= n_act) break;
+      const int64_t a = qord[qi];
       const int64_t b = act[a];
       const int mode = __ldcg(&p.sig[b].mode);
       if (mode == 0) fista_step(p, sh, a, b, t0, sk, us, stage);
@@ -1903,7 +1913,7 @@ cudaError_t gemm_tn_launch(const double* X, int64_t ldx, int64_t nx, const doubl
 
 size_t prefix_smem_bytes(int64_t ld, int64_t batch) {
   return 128 + static_cast<size_t>(kStageBufs * kStage + ld) * sizeof(double) +
-         static_cast<size_t>(2 * batch) * sizeof(int32_t);
+         static_cast<size_t>(3 * batch) * sizeof(int32_t);
 }
 int64_t prefix_part_elems(int grid) { return 2 * static_cast<int64_t>(grid) * kPartTile; }
 int prefix_stream_k_max_grid() { return kMaxGrid; }
@@ -1911,6 +1921,15 @@ int prefix_split_max() { return kSplitMax; }
 // the per-signal lists live in the staging area: two atom lists (12 bytes per entry each)
 // and the flattened copy the apply walks (12 more): 36 bytes per atom
 int64_t prefix_max_atoms() { return (static_cast<int64_t>(kStageBufs) * kStage * 8) / 36 / kPW * kPW; }
+
+// the lockstep's shared memory (staging, u, three per-signal index lists) fits one CTA
+bool prefix_fits(int64_t ld, int64_t batch, int device) {
+  int optin = 0;
+  if (cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device) != cudaSuccess) return false;
+  cudaFuncAttributes fa{};
+  if (cudaFuncGetAttributes(&fa, prefix_kernel) != cudaSuccess) return false;
+  return prefix_smem_bytes(ld, batch) + fa.sharedSizeBytes <= static_cast<size_t>(optin);
+}
 
 cudaError_t prefix_launch(const PrefixParams& p, int device, cudaStream_t stream) {
   const size_t smem = prefix_smem_bytes(p.ld, p.batch);
