@@ -4,8 +4,9 @@
 // step, each unfinished signal performs its own next unit of Engine::run
 // (fastl1.cpp:459-645): one FISTA iteration, or one step of its restricted power
 // iteration (solver.cpp:72-104). The dictionary products of all signals are then
-// two dense contractions on the fp64 tensor cores (DMMA m8n8k4, cp.async
-// double-buffered shared-memory tiles, split-K for load balance):
+// two dense contractions on the fp64 tensor cores (DMMA m8n8k4 over shared-memory
+// tiles; by default stream-K over a TMA / mbarrier ring, `sk_contract`; the earlier
+// split-K cp.async double buffer stays behind FL1_LOCKSTEP_TMA=0):
 //     W    = A  V            for the signals in a power step   (N x K times K x P)
 //     Corr = A^T [rho | w]   for every signal                  (K x N times N x B)
 // reading each A tile once per 64 signals instead of once per signal. Preserved
