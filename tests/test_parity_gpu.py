@@ -446,6 +446,38 @@ def test_batched_lockstep_edge_cases(cuda, oracle16, monkeypatch, policy):
             assert_parity(res[b], o, a, Y[:, b], lams[b])
 
 
+def test_batched_beyond_lockstep_shared_memory(cuda, oracle16):
+    """A batch whose per-signal index lists (3 x 4 B per signal) would overflow the
+    lockstep's shared memory takes the per-signal engines instead (prefix_fits): 6,000
+    small signals; every 500th, and every one that does not converge, against its own
+    oracle solve. (Signal 581 oscillates to the iteration cap on both sides: after
+    screening leaves 2 atoms, the warm-started restricted power iteration converges on
+    the lower eigenvalue, so L is underestimated -- the reference's own behaviour.)"""
+    rng = np.random.default_rng(43)
+    n, k, B = 48, 96, 6000
+    a = syn.gaussian_dictionary(rng, n, k)
+    X0 = np.zeros((k, B))
+    for b in range(B):
+        X0[rng.choice(k, 3, replace=False), b] = rng.standard_normal(3)
+    Y = np.asfortranarray(a @ X0 + 0.01 * rng.standard_normal((n, B)))
+    lams = 0.3 * np.max(np.abs(a.T @ Y), axis=0)
+    L = F.lipschitz_bound(F.DenseDictionary(a, backend=cuda))
+    cfg = F.SwitchConfig(screening_interval=10, max_iterations=5000, rel_tolerance=1e-6)
+    opts = F.RunOptions(variant=F.VARIANT_SCREENED, full_lipschitz=[L])
+    res = F.run_lasso_batched(F.ApproxSequence([F.make_exact_approx(F.DenseDictionary(a, backend=cuda))]), Y, lams,
+                              cfg, opts, concurrency=0)
+    assert res[0].kernel_launches == 2  # per-signal engines + trace packing: no lockstep launch
+    seq_o = F.ApproxSequence([F.make_exact_approx(F.DenseDictionary(a, backend=oracle16))])
+    stuck = [b for b in range(B) if not res[b].converged]
+    assert len(stuck) < 10
+    for b in stuck:
+        o = F.run_lasso(seq_o, Y[:, b], lams[b], cfg, opts)
+        assert not o.converged and o.iterations == res[b].iterations
+    for b in range(0, B, 500):
+        if b not in stuck:
+            assert_parity(res[b], F.run_lasso(seq_o, Y[:, b], lams[b], cfg, opts), a, Y[:, b], lams[b])
+
+
 def test_single_cluster_route_matches_grid(cuda, oracle16, monkeypatch):
     """Small dictionaries solve on one 16-CTA cluster (cheaper barriers); the grid
     route gives the same trajectory and both match the oracle."""
