@@ -497,21 +497,30 @@ __device__ __forceinline__ void sk_issue(const PrefixParams& p, const SkShape& s
 }
 
 // DMMA over one landed unit (layouts as sk_issue)
+__device__ __forceinline__ double lds64(uint32_t a) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
+  return v;
+}
+// (the operands are read through 32-bit shared-window addresses: from the staging pointer
+// the compiler would emit generic loads, measurably slower than LDS in the DMMA loop)
 template <int WHICH, int CT>
 __device__ __forceinline__ void sk_mma(const double* Xs, double (&acc)[kRT][kCT][2]) {
   constexpr int which = WHICH;
   const int w = threadIdx.x >> 5, l = threadIdx.x & 31, g = l >> 2, tg = l & 3;
   const int wr = w % kWR, wc = w / kWR;
-  const double* Ys = Xs + (which ? kTM * kSS : kTK * (kTM + 4));
+  const uint32_t xa = su32(Xs) +
+                      8u * static_cast<uint32_t>(which ? (wr * 8 + g) * kSS + tg : tg * (kTM + 4) + wr * 8 + g);
+  const uint32_t ya = su32(Xs) + 8u * static_cast<uint32_t>((which ? kTM * kSS : kTK * (kTM + 4)) +
+                                                            (wc * CT * 8 + g) * kSS + tg);
 #pragma unroll
   for (int ks = 0; ks < kTK / 4; ++ks) {
     double av[kRT], bv[CT];
 #pragma unroll
     for (int h = 0; h < kRT; ++h)
-      av[h] = which ? Xs[((h * kWR + wr) * 8 + g) * kSS + ks * 4 + tg]
-                    : Xs[(ks * 4 + tg) * (kTM + 4) + (h * kWR + wr) * 8 + g];
+      av[h] = lds64(xa + 8u * (which ? h * kWR * 8 * kSS + ks * 4 : ks * 4 * (kTM + 4) + h * kWR * 8));
 #pragma unroll
-    for (int c = 0; c < CT; ++c) bv[c] = Ys[((wc * CT + c) * 8 + g) * kSS + ks * 4 + tg];
+    for (int c = 0; c < CT; ++c) bv[c] = lds64(ya + 8u * (c * 8 * kSS + ks * 4));
 #pragma unroll
     for (int h = 0; h < kRT; ++h)
 #pragma unroll
