@@ -1282,6 +1282,7 @@ void solve_clusters(fl1_seq* s, const double* Y, bool y_device, int64_t ldy, con
                           (opts->variant == FL1_SCREENED || opts->variant == FL1_PLAIN) &&
                           opts->full_lipschitz != nullptr && k <= fl1::prefix_max_atoms() &&
                           fl1::prefix_fits(ld, batch, ctx->device) &&
+                          k % 2 == 0 &&  // per-signal K-strided rows take 16-byte copies (V tiles, staging)
                           !(pe && pe[0] == '0');
   fl1::PrefixParams pp{};
   if (use_prefix) {
@@ -1373,8 +1374,7 @@ void solve_clusters(fl1_seq* s, const double* Y, bool y_device, int64_t ldy, con
     pp.work_out = reinterpret_cast<int64_t*>(pb + q_n) + 2;
     // stream-K contractions on the TMA ring (default); FL1_LOCKSTEP_TMA=0: split-K cp.async tiles
     const char* tma = std::getenv("FL1_LOCKSTEP_TMA");
-    pp.tma = (tma ? std::atoi(tma) : 1) && k % 2 == 0 &&  // tensor rows of V need a 16-byte pitch
-             ctx->sms <= fl1::prefix_stream_k_max_grid();
+    pp.tma = (tma ? std::atoi(tma) : 1) && ctx->sms <= fl1::prefix_stream_k_max_grid();
     const char* fi = std::getenv("FL1_SK_FANIN");
     pp.sk_fanin = fi ? std::atoi(fi) : 4;
     if (pp.tma) {

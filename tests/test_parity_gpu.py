@@ -357,6 +357,31 @@ def test_batched_lockstep_narrow_steps(cuda, oracle16, monkeypatch, narrow):
         assert_parity(res[b], F.run_lasso(seq_o, Y[:, b], lams[b], cfg, opts), a, Y[:, b], lams[b])
 
 
+@pytest.mark.parametrize("k", [401, 1200])
+def test_batched_lockstep_odd_atom_count(cuda, oracle16, monkeypatch, k):
+    """An odd atom count leaves the per-signal K-strided rows (the power-iteration vectors
+    the lockstep copies in 16-byte pieces) without a 16-byte pitch: such a batch runs on
+    the per-signal engines instead (k = 401), an even one in the lockstep (k = 1200); both
+    match the per-signal oracle solves."""
+    monkeypatch.setenv("FL1_LOCKSTEP_POLICY", "0")
+    rng = np.random.default_rng(47)
+    n, B = 200, 24
+    a = syn.gaussian_dictionary(rng, n, k)
+    Y = np.empty((n, B), order="F")
+    for b in range(B):
+        Y[:, b] = syn.observe(rng, a @ syn.sparse_signal(rng, k, 3 + b % 5), None, 30.0)
+    lams = 0.25 * np.max(np.abs(a.T @ Y), axis=0)
+    L = F.lipschitz_bound(F.DenseDictionary(a, backend=cuda))
+    cfg = F.SwitchConfig(screening_interval=10, max_iterations=5000, rel_tolerance=1e-6)
+    opts = F.RunOptions(variant=F.VARIANT_SCREENED, full_lipschitz=[L], collect_trace=True)
+    seq_g = F.ApproxSequence([F.make_exact_approx(F.DenseDictionary(a, backend=cuda))])
+    seq_o = F.ApproxSequence([F.make_exact_approx(F.DenseDictionary(a, backend=oracle16))])
+    res = F.run_lasso_batched(seq_g, Y, lams, cfg, opts, concurrency=0)
+    assert res[0].kernel_launches == (3 if k % 2 == 0 else 2)  # lockstep + engines + trace packing
+    for b in range(B):
+        assert_parity(res[b], F.run_lasso(seq_o, Y[:, b], lams[b], cfg, opts), a, Y[:, b], lams[b])
+
+
 @pytest.mark.parametrize("env", [("FL1_LOCKSTEP_TMA", "0"), ("FL1_SK_FANIN", "1"), ("FL1_SK_FANIN", "64"),
                                  ("FL1_LOCKSTEP_WIDTH", "0")])
 def test_batched_lockstep_contraction_routes(cuda, oracle16, monkeypatch, env):
