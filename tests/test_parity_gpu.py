@@ -357,12 +357,13 @@ def test_batched_lockstep_narrow_steps(cuda, oracle16, monkeypatch, narrow):
         assert_parity(res[b], F.run_lasso(seq_o, Y[:, b], lams[b], cfg, opts), a, Y[:, b], lams[b])
 
 
-@pytest.mark.parametrize("k", [401, 1200])
-def test_batched_lockstep_odd_atom_count(cuda, oracle16, monkeypatch, k):
+@pytest.mark.parametrize("k", [401, 1200, 4608])
+def test_batched_lockstep_atom_counts(cuda, oracle16, monkeypatch, k):
     """An odd atom count leaves the per-signal K-strided rows (the power-iteration vectors
     the lockstep copies in 16-byte pieces) without a 16-byte pitch: such a batch runs on
     the per-signal engines instead (k = 401), an even one in the lockstep (k = 1200); both
-    match the per-signal oracle solves."""
+    match the per-signal oracle solves. k = 4608 is the largest atom count whose
+    per-signal lists fit the lockstep's staging area (prefix_max_atoms)."""
     monkeypatch.setenv("FL1_LOCKSTEP_POLICY", "0")
     rng = np.random.default_rng(47)
     n, B = 200, 24
