@@ -1645,16 +1645,17 @@ __global__ void __launch_bounds__(kPT, 1) prefix_kernel(const __grid_constant__ 
       // stage the contraction inputs in slot order (2D tensor boxes, no per-column gather):
       // Rc[a] = R[act[a]] (the power slots' columns are overwritten by W below) and
       // Vc[c] = v of power slot c
-      const int64_t hl = ld / 2, hk = K / 2, nr = static_cast<int64_t>(n_act) * hl, nv = static_cast<int64_t>(n_pow) * hk;
-      for (int64_t e = static_cast<int64_t>(blockIdx.x) * kPT + threadIdx.x; e < nr + nv;
-           e += static_cast<int64_t>(gridDim.x) * kPT) {
+      // (32-bit index arithmetic: the element count of one staging pass is far below 2^31)
+      const uint32_t hl = static_cast<uint32_t>(ld / 2), hk = static_cast<uint32_t>(K / 2);
+      const uint32_t nr = static_cast<uint32_t>(n_act) * hl, nv = static_cast<uint32_t>(n_pow) * hk;
+      for (uint32_t e = blockIdx.x * kPT + threadIdx.x; e < nr + nv; e += gridDim.x * kPT) {
         if (e < nr) {
-          const int64_t a = e / hl, i = e - a * hl;
-          __stcg(reinterpret_cast<double2*>(p.rc + a * ld) + i,
+          const uint32_t a = e / hl, i = e - a * hl;
+          __stcg(reinterpret_cast<double2*>(p.rc + static_cast<int64_t>(a) * ld) + i,
                  __ldcg(reinterpret_cast<const double2*>(p.R + static_cast<int64_t>(act[a]) * ld) + i));
         } else {
-          const int64_t f = e - nr, c = f / hk, j = f - c * hk;
-          __stcg(reinterpret_cast<double2*>(p.vc + c * K) + j,
+          const uint32_t f = e - nr, c = f / hk, j = f - c * hk;
+          __stcg(reinterpret_cast<double2*>(p.vc + static_cast<int64_t>(c) * K) + j,
                  __ldcg(reinterpret_cast<const double2*>(p.vp + static_cast<int64_t>(act[pact[c]]) * K) + j));
         }
       }
