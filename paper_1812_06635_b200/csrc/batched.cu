@@ -584,6 +584,40 @@ __device__ __forceinline__ void sk_units(const PrefixParams& p, const SkShape& s
   }
 }
 
+// Stage the step's contraction inputs in slot order: Rc[a] = R[act[a]] and Vc[c] = the
+// power vector of power slot c (32-bit index arithmetic: one pass is far below 2^31
+// elements; four elements per thread and round, their loads in flight together; out of
+// line, so that its registers do not weigh on the kernel body's allocation).
+__device__ __noinline__ void sk_stage(const PrefixParams& p, int n_act, int n_pow, const int32_t* act,
+                                      const int32_t* pact) {
+  const int64_t ld = p.ld, K = p.k;
+  const uint32_t hl = static_cast<uint32_t>(ld / 2), hk = static_cast<uint32_t>(K / 2);
+  const uint32_t nr = static_cast<uint32_t>(n_act) * hl, nv = static_cast<uint32_t>(n_pow) * hk;
+  const uint32_t stride = gridDim.x * kPT;
+  for (uint32_t e0 = blockIdx.x * kPT + threadIdx.x; e0 < nr + nv; e0 += 4 * stride) {
+    double2 v[4];
+    double2* d[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const uint32_t e = e0 + q * stride;
+      d[q] = nullptr;
+      if (e >= nr + nv) continue;
+      if (e < nr) {
+        const uint32_t a = e / hl, i = e - a * hl;
+        d[q] = reinterpret_cast<double2*>(p.rc + static_cast<int64_t>(a) * ld) + i;
+        v[q] = __ldcg(reinterpret_cast<const double2*>(p.R + static_cast<int64_t>(act[a]) * ld) + i);
+      } else {
+        const uint32_t f = e - nr, c = f / hk, j = f - c * hk;
+        d[q] = reinterpret_cast<double2*>(p.vc + static_cast<int64_t>(c) * K) + j;
+        v[q] = __ldcg(reinterpret_cast<const double2*>(p.vp + static_cast<int64_t>(act[pact[c]]) * K) + j);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      if (d[q]) __stcg(d[q], v[q]);
+  }
+}
+
 // One stream-K product over this CTA's unit range. ring: the CTA's running unit count
 // (stage and phase of the ring; identical in every thread). epoch: unique per product
 // within the launch (the flags are zeroed at the launch's start).
@@ -1645,20 +1679,7 @@ __global__ void __launch_bounds__(kPT, 1) prefix_kernel(const __grid_constant__ 
       // stage the contraction inputs in slot order (2D tensor boxes, no per-column gather):
       // Rc[a] = R[act[a]] (the power slots' columns are overwritten by W below) and
       // Vc[c] = v of power slot c
-      // (32-bit index arithmetic: the element count of one staging pass is far below 2^31)
-      const uint32_t hl = static_cast<uint32_t>(ld / 2), hk = static_cast<uint32_t>(K / 2);
-      const uint32_t nr = static_cast<uint32_t>(n_act) * hl, nv = static_cast<uint32_t>(n_pow) * hk;
-      for (uint32_t e = blockIdx.x * kPT + threadIdx.x; e < nr + nv; e += gridDim.x * kPT) {
-        if (e < nr) {
-          const uint32_t a = e / hl, i = e - a * hl;
-          __stcg(reinterpret_cast<double2*>(p.rc + static_cast<int64_t>(a) * ld) + i,
-                 __ldcg(reinterpret_cast<const double2*>(p.R + static_cast<int64_t>(act[a]) * ld) + i));
-        } else {
-          const uint32_t f = e - nr, c = f / hk, j = f - c * hk;
-          __stcg(reinterpret_cast<double2*>(p.vc + static_cast<int64_t>(c) * K) + j,
-                 __ldcg(reinterpret_cast<const double2*>(p.vp + static_cast<int64_t>(act[pact[c]]) * K) + j));
-        }
-      }
+      sk_stage(p, n_act, n_pow, act, pact);
       // the staged columns are read by tensor copies (async proxy) after the barrier
       asm volatile("fence.proxy.async.global;" ::: "memory");
       grid.sync();
