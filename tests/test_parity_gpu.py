@@ -151,6 +151,29 @@ def test_bit_reproducible(cuda):
     assert np.array_equal(r1.trace["gap"], r2.trace["gap"])
 
 
+def test_batched_bit_reproducible(cuda):
+    """The lockstep's stream-K products reduce shared tiles in a fixed chunk order and the
+    per-signal queue order does not enter the arithmetic: two runs of a batch give the
+    same bits for every signal (x, gap trace, iteration counts)."""
+    rng = np.random.default_rng(53)
+    n, k, B = 256, 1024, 96
+    a = syn.gaussian_dictionary(rng, n, k)
+    Y = np.empty((n, B), order="F")
+    for b in range(B):
+        Y[:, b] = syn.observe(rng, a @ syn.sparse_signal(rng, k, 4 + b % 7), None, 30.0)
+    lams = 0.25 * np.max(np.abs(a.T @ Y), axis=0)
+    d = F.DenseDictionary(a, backend=cuda)
+    seq = F.ApproxSequence([F.make_exact_approx(d)])
+    cfg = F.SwitchConfig(screening_interval=10, max_iterations=5000, rel_tolerance=1e-6)
+    opts = F.RunOptions(variant=F.VARIANT_SCREENED, full_lipschitz=[F.lipschitz_bound(d)], collect_trace=True)
+    r1 = F.run_lasso_batched(seq, Y, lams, cfg, opts, concurrency=0)
+    r2 = F.run_lasso_batched(seq, Y, lams, cfg, opts, concurrency=0)
+    assert r1[0].kernel_launches == 3
+    for x, y in zip(r1, r2):
+        assert x.iterations == y.iterations and np.array_equal(x.x, y.x)
+        assert np.array_equal(x.trace["gap"], y.trace["gap"])
+
+
 def test_trace_flush_and_resume(cuda, monkeypatch):
     """A device trace buffer smaller than the run forces kernel exits + resumes; the
     trajectory is unchanged bit for bit (both runs on the full grid: the flush path
