@@ -625,7 +625,6 @@ __device__ __noinline__ void sk_contract(const PrefixParams& p, int which, int64
                                          double* stage, uint32_t& ring, int32_t epoch) {
   const SkShape sh(p, which, ncols);
   const int G = gridDim.x, gi = blockIdx.x;
-  const int l = threadIdx.x & 31;
   for (int g2 = threadIdx.x; g2 <= G; g2 += kPT) s_begin[g2] = sh.begin(g2, G);
   // the per-signal phases' generic-proxy writes into the staging area precede the
   // async-proxy copies below
