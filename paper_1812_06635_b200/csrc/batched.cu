@@ -1583,6 +1583,63 @@ __device__ __noinline__ void narrow_w(const PrefixParams& p, int n_pow, const in
 
 }  // namespace
 
+// The split-K route's products (FL1_LOCKSTEP_TMA=0) and the narrow W combine, out of the
+// kernel body (its register allocation is shared by every step's control flow).
+constexpr int kNarrowTag = -1;  // legacy_w_combine: the narrow W partials' layout
+__device__ __noinline__ int legacy_w_tiles(const PrefixParams& p, int n_pow, const int32_t* pact, const int32_t* act,
+                                           double* stage) {
+  const int64_t ld = p.ld, K = p.k;
+  const int n_rt = static_cast<int>((ld + kTM - 1) / kTM);
+  const int n_ct = (n_pow + kTN - 1) / kTN;
+  const int sk = p.split_mode ? split_for(n_rt * n_ct, gridDim.x, static_cast<int>((K + kTK - 1) / kTK),
+                                          split_cap(p, ld * n_pow))
+                              : split_old(n_rt * n_ct, gridDim.x);
+  for (int item = blockIdx.x; item < n_rt * n_ct * sk; item += gridDim.x) {
+    const int tile = item % (n_rt * n_ct), kp = item / (n_rt * n_ct);
+    const int64_t c0 = static_cast<int64_t>(tile / n_rt) * kTN;
+    switch (tile_ct(static_cast<int>(n_pow - c0), p.width_tiles)) {  // the last column tile may be narrow
+      case 1: gemm_n_tile<1>(p, tile % n_rt, c0, kp, sk, n_pow, pact, act, stage); break;
+      case 2: gemm_n_tile<2>(p, tile % n_rt, c0, kp, sk, n_pow, pact, act, stage); break;
+      case 3: gemm_n_tile<3>(p, tile % n_rt, c0, kp, sk, n_pow, pact, act, stage); break;
+      default: gemm_n_tile<kCT>(p, tile % n_rt, c0, kp, sk, n_pow, pact, act, stage);
+    }
+  }
+  return sk;
+}
+// w of power slot pc = the partials in part order into R (split-K: parts of bcap columns;
+// narrow: kNarrowParts groups of n_pow columns)
+__device__ __noinline__ void legacy_w_combine(const PrefixParams& p, int n_pow, const int32_t* pact,
+                                              const int32_t* act, int layout, int parts) {
+  const int64_t ld = p.ld, N = p.n;
+  const int64_t pstride = layout == kNarrowTag ? static_cast<int64_t>(n_pow) : static_cast<int64_t>(p.bcap);
+  for (int64_t e = static_cast<int64_t>(blockIdx.x) * kPT + threadIdx.x; e < static_cast<int64_t>(n_pow) * ld;
+       e += static_cast<int64_t>(gridDim.x) * kPT) {
+    const int64_t pc = e / ld, i = e - pc * ld;
+    double w = 0.0;
+    for (int kp = 0; kp < parts; ++kp) w += __ldcg(p.np + (static_cast<int64_t>(kp) * pstride + pc) * ld + i);
+    __stcg(p.R + static_cast<int64_t>(act[pact[pc]]) * ld + i, i < N ? w : 0.0);
+  }
+}
+__device__ __noinline__ int legacy_corr_tiles(const PrefixParams& p, int n_act, const int32_t* act, double* stage) {
+  const int64_t ld = p.ld, K = p.k;
+  const int n_rt = static_cast<int>((K + kTM - 1) / kTM);
+  const int n_ct = (n_act + kTN - 1) / kTN;
+  const int sk = p.split_mode ? split_for(n_rt * n_ct, gridDim.x, static_cast<int>((ld + kTK - 1) / kTK),
+                                          split_cap(p, K * n_act))
+                              : split_old(n_rt * n_ct, gridDim.x);
+  for (int item = blockIdx.x; item < n_rt * n_ct * sk; item += gridDim.x) {
+    const int tile = item % (n_rt * n_ct), kp = item / (n_rt * n_ct);
+    const int64_t a0 = static_cast<int64_t>(tile / n_rt) * kTN;
+    switch (tile_ct(static_cast<int>(n_act - a0), p.width_tiles)) {  // the last column tile may be narrow
+      case 1: gemm_tile<1>(p, tile % n_rt, a0, kp, sk, n_act, act, stage); break;
+      case 2: gemm_tile<2>(p, tile % n_rt, a0, kp, sk, n_act, act, stage); break;
+      case 3: gemm_tile<3>(p, tile % n_rt, a0, kp, sk, n_act, act, stage); break;
+      default: gemm_tile<kCT>(p, tile % n_rt, a0, kp, sk, n_act, act, stage);
+    }
+  }
+  return sk;
+}
+
 __global__ void __launch_bounds__(kPT, 1) prefix_kernel(const __grid_constant__ PrefixParams p) {
   cg::grid_group grid = cg::this_grid();
   extern __shared__ __align__(128) double dsm[];
@@ -1688,42 +1745,16 @@ __global__ void __launch_bounds__(kPT, 1) prefix_kernel(const __grid_constant__ 
     if (n_pow > 0 && narrow) {
       narrow_w(p, n_pow, pact, act, stage);
       grid.sync();
-      for (int64_t e = static_cast<int64_t>(blockIdx.x) * kPT + threadIdx.x; e < static_cast<int64_t>(n_pow) * ld;
-           e += static_cast<int64_t>(gridDim.x) * kPT) {
-        const int64_t pc = e / ld, i = e - pc * ld;
-        double w = 0.0;
-        for (int g = 0; g < kNarrowParts; ++g) w += __ldcg(p.np + (static_cast<int64_t>(g) * n_pow + pc) * ld + i);
-        __stcg(p.R + static_cast<int64_t>(act[pact[pc]]) * ld + i, i < N ? w : 0.0);
-      }
+      legacy_w_combine(p, n_pow, pact, act, kNarrowTag, kNarrowParts);
       grid.sync();
     } else if (n_pow > 0 && p.tma) {
       sk_contract(p, 0, n_pow, pact, stage, ring, 2 * steps + 1);  // writes the power slots' Rc columns
       if (logit) p.step_log[kLogW * steps + 6] = gtimer() - t0;
       grid.sync();
     } else if (n_pow > 0) {
-      const int n_rt = static_cast<int>((ld + kTM - 1) / kTM);
-      const int n_ct = (n_pow + kTN - 1) / kTN;
-      const int sk = p.split_mode ? split_for(n_rt * n_ct, gridDim.x, static_cast<int>((K + kTK - 1) / kTK),
-                                              split_cap(p, ld * n_pow))
-                                  : split_old(n_rt * n_ct, gridDim.x);
-      for (int item = blockIdx.x; item < n_rt * n_ct * sk; item += gridDim.x) {
-        const int tile = item % (n_rt * n_ct), kp = item / (n_rt * n_ct);
-        const int64_t c0 = static_cast<int64_t>(tile / n_rt) * kTN;
-        switch (tile_ct(static_cast<int>(n_pow - c0), p.width_tiles)) {  // the last column tile may be narrow
-          case 1: gemm_n_tile<1>(p, tile % n_rt, c0, kp, sk, n_pow, pact, act, stage); break;
-          case 2: gemm_n_tile<2>(p, tile % n_rt, c0, kp, sk, n_pow, pact, act, stage); break;
-          case 3: gemm_n_tile<3>(p, tile % n_rt, c0, kp, sk, n_pow, pact, act, stage); break;
-          default: gemm_n_tile<kCT>(p, tile % n_rt, c0, kp, sk, n_pow, pact, act, stage);
-        }
-      }
+      const int sk = legacy_w_tiles(p, n_pow, pact, act, stage);
       grid.sync();
-      for (int64_t e = static_cast<int64_t>(blockIdx.x) * kPT + threadIdx.x; e < static_cast<int64_t>(n_pow) * ld;
-           e += static_cast<int64_t>(gridDim.x) * kPT) {
-        const int64_t pc = e / ld, i = e - pc * ld;
-        double w = 0.0;
-        for (int kp = 0; kp < sk; ++kp) w += __ldcg(p.np + (static_cast<int64_t>(kp) * p.bcap + pc) * ld + i);
-        __stcg(p.R + static_cast<int64_t>(act[pact[pc]]) * ld + i, i < N ? w : 0.0);
-      }
+      legacy_w_combine(p, n_pow, pact, act, sk, sk == kNarrowTag ? kNarrowParts : sk);
       grid.sync();
     }
     if (logit) p.step_log[kLogW * steps + 3] = gtimer() - t0;
@@ -1736,21 +1767,7 @@ __global__ void __launch_bounds__(kPT, 1) prefix_kernel(const __grid_constant__ 
       sk_contract(p, 1, n_act, pact, stage, ring, 2 * steps + 2);  // one part in p.corr
       if (logit) p.step_log[kLogW * steps + 7] = gtimer() - t0;
     } else {
-      const int n_rt = static_cast<int>((K + kTM - 1) / kTM);
-      const int n_ct = (n_act + kTN - 1) / kTN;
-      sk = p.split_mode ? split_for(n_rt * n_ct, gridDim.x, static_cast<int>((ld + kTK - 1) / kTK),
-                                    split_cap(p, K * n_act))
-                        : split_old(n_rt * n_ct, gridDim.x);
-      for (int item = blockIdx.x; item < n_rt * n_ct * sk; item += gridDim.x) {
-        const int tile = item % (n_rt * n_ct), kp = item / (n_rt * n_ct);
-        const int64_t a0 = static_cast<int64_t>(tile / n_rt) * kTN;
-        switch (tile_ct(static_cast<int>(n_act - a0), p.width_tiles)) {  // the last column tile may be narrow
-          case 1: gemm_tile<1>(p, tile % n_rt, a0, kp, sk, n_act, act, stage); break;
-          case 2: gemm_tile<2>(p, tile % n_rt, a0, kp, sk, n_act, act, stage); break;
-          case 3: gemm_tile<3>(p, tile % n_rt, a0, kp, sk, n_act, act, stage); break;
-          default: gemm_tile<kCT>(p, tile % n_rt, a0, kp, sk, n_act, act, stage);
-        }
-      }
+      sk = legacy_corr_tiles(p, n_act, act, stage);
     }
     grid.sync();
     if (logit) p.step_log[kLogW * steps + 4] = gtimer() - t0;
