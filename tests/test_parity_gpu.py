@@ -648,3 +648,15 @@ def test_sukro_norms_on_device(cuda, oracle16):
     sg, so = syn.sukro_sequence(inst, cuda), syn.sukro_sequence(inst, oracle16)
     for lg, lo in zip(sg.dicts, so.dicts):
         assert np.allclose(lg.op.atom_norms2(), lo.op.atom_norms2(), rtol=1e-15, atol=0)
+
+
+def test_random_sweep(cuda, oracle16):
+    """Seeded random instances (tests/_fuzz.py): ragged shapes, both single-solve routes, every
+    solver / rule / variant / precompute_aty setting, absolute and relative tolerances, iteration
+    caps, warm starts, multi-level sequences, and a batched call every fourth case -- each against
+    its own oracle solve (integer trajectory, objective and x at the shared bar; gap floor per
+    _fuzz.FUZZ_GAP_ULPS)."""
+    import _fuzz
+
+    fails = _fuzz.sweep(cuda, oracle16, 80, 20261021, verbose=False)
+    assert not fails, fails
