@@ -147,3 +147,73 @@ def sweep(gpu, orc, cases, seed, verbose=True):
     print(f"{cases} cases, {len(fails)} failures, {time.time() - t0:.1f} s")
     return fails
 
+
+def draw_sukro_case(rng):
+    """A sum-of-Kronecker instance with ragged factor shapes (m, q not multiples of the DMMA tile),
+    random term counts and level subsets, as synthetic.sukro_instance builds BASELINE configs[2]."""
+    from paper_1812_06635_b200 import synthetic as syn
+
+    m = int(rng.integers(3, 23))
+    q = int(rng.integers(m, 41))
+    terms = int(rng.integers(2, 7))
+    # relative complexity t (1/m + 1/q) of every level must stay in (0, 1) (dictionary.cpp:227-251)
+    cand = [t for t in (1, 2, 3, 4, 5) if t < terms and t * (1.0 / m + 1.0 / q) < 1.0]
+    nlev = int(rng.integers(1, min(3, len(cand)) + 1))
+    levels = tuple(sorted(rng.choice(cand, nlev, replace=False).tolist()))
+    nnz = int(max(1, min(q * q // 2, rng.integers(1, max(2, m * m // 3 + 2)))))
+    inst = syn.sukro_instance(seed=int(rng.integers(1, 1 << 30)), m=m, q=q, terms=terms, levels=levels, nnz=nnz,
+                              snr_db=float(rng.choice([10.0, 20.0, 30.0, 40.0])),
+                              lam_ratio=float(rng.choice([0.8, 0.5, 0.3, 0.2, 0.1])))
+    cfg = dict(screening_interval=int(rng.choice([1, 2, 5, 10])), max_iterations=int(rng.choice([5000, 5000, 41])),
+               precompute_aty=bool(rng.random() < 0.3), gamma_threshold=float(rng.choice([0.5, 0.2, 0.8])),
+               rel_tolerance=float(rng.choice([1e-6, 1e-4, 1e-8])))
+    opts = dict(solver=int(rng.choice([F.SOLVER_ISTA, F.SOLVER_FISTA, F.SOLVER_FISTA])),
+                rule=int(rng.choice([F.RULE_GAP, F.RULE_GAP, F.RULE_DYNAMIC])),
+                variant=int(rng.choice([F.VARIANT_MULTI_DICT, F.VARIANT_MULTI_DICT, F.VARIANT_SCREENED])))
+    return dict(inst=inst, cfg=cfg, opts=opts, gram=bool(rng.random() < 0.25), batched=bool(rng.random() < 0.25),
+                desc=f"sukro m {m} q {q} terms {terms} levels {levels} nnz {nnz} lam {inst.lam:.3e}")
+
+
+def run_sukro_case(gpu, orc, c):
+    from paper_1812_06635_b200 import synthetic as syn
+
+    inst = c["inst"]
+    cfg = F.SwitchConfig(**c["cfg"])
+    res, seqs = {}, {}
+    for tag, b in (("gpu", gpu), ("orc", orc)):
+        seq = syn.sukro_sequence(inst, backend=b)
+        seqs[tag] = seq
+        gram = F.gram_matrix(seq.exact().op) if c["gram"] else None
+        res[tag] = F.run_lasso(seq, inst.y, inst.lam, cfg, F.RunOptions(exact_gram=gram, **c["opts"]))
+    assert_parity(res["gpu"], res["orc"], inst.a, inst.y, inst.lam, case="fuzz-sukro", gap_ulps=FUZZ_GAP_ULPS)
+    if c["batched"]:
+        g = np.random.default_rng(inst.seed + 1)
+        B = int(g.integers(2, 6))
+        n = inst.y.size
+        Y = np.asfortranarray(inst.y[:, None] * g.uniform(0.5, 1.5, size=B)[None, :]
+                              + 0.05 * np.linalg.norm(inst.y) / np.sqrt(n) * g.standard_normal((n, B)))
+        lams = np.maximum(inst.lam * g.uniform(0.6, 1.4, size=B), 1e-12)
+        opts = F.RunOptions(**c["opts"])
+        outs = F.run_lasso_batched(seqs["gpu"], Y, lams, cfg, opts, 0)
+        for bi in range(B):
+            o = F.run_lasso(seqs["orc"], Y[:, bi].copy(), float(lams[bi]), cfg, opts)
+            assert_parity(outs[bi], o, inst.a, Y[:, bi], float(lams[bi]), case="fuzz-sukro-batched",
+                          gap_ulps=FUZZ_GAP_ULPS)
+
+
+def sweep_sukro(gpu, orc, cases, seed, verbose=True):
+    rng = np.random.default_rng(seed)
+    fails = []
+    t0 = time.time()
+    for i in range(cases):
+        c = draw_sukro_case(rng)
+        desc = f"case {i}: {c['desc']} cfg {c['cfg']} opts {c['opts']} gram {c['gram']} batched {c['batched']}"
+        try:
+            run_sukro_case(gpu, orc, c)
+            if verbose:
+                print("ok  ", desc, flush=True)
+        except Exception as e:  # noqa: BLE001
+            fails.append((i, desc, repr(e)[:600]))
+            print("FAIL", desc, "\n", traceback.format_exc()[-1500:], flush=True)
+    print(f"{cases} sukro cases, {len(fails)} failures, {time.time() - t0:.1f} s")
+    return fails

@@ -660,3 +660,16 @@ def test_random_sweep(cuda, oracle16):
 
     fails = _fuzz.sweep(cuda, oracle16, 80, 20261021, verbose=False)
     assert not fails, fails
+
+
+def test_random_sweep_sukro(cuda, oracle16):
+    """Seeded random sum-of-Kronecker sequences (tests/_fuzz.py draw_sukro_case): ragged factor
+    shapes (m 3-22, q up to 40: not multiples of the DMMA tiles), 2-6 terms, 1-3 approximate levels
+    before the exact dictionary, every solver / rule / variant, precompute_aty, the Gram-backed exact
+    phase and a batched call in a quarter of the cases -- each against its own oracle solve at the
+    shared bar (dictionary.cpp:150-164 operators, fastl1.cpp:26-38 switching)."""
+    import _fuzz
+
+    fails = _fuzz.sweep_sukro(cuda, oracle16, 40, 20261022, verbose=False)
+    assert not fails, fails
+
