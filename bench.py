@@ -101,6 +101,12 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
+def _use_dist(world: int) -> bool:
+    """One process per GPU under torchrun: NCCL for the barrier and the max-over-ranks timing.
+    FL1_BENCH_FORCE_DIST=1 takes the same path with a single rank (a 1-GPU check of the N > 1 code)."""
+    return world > 1 or (os.environ.get("FL1_BENCH_FORCE_DIST") == "1" and "MASTER_ADDR" in os.environ)
+
+
 def reduce_over_ranks(dist, device, per_solve_s: float, e2e_s: float, iters: float):
     """Replica aggregation: times are the max over ranks, iterations are summed.
     dist is torch.distributed (or None for one process)."""
@@ -153,7 +159,7 @@ def run_gpu(args) -> None:
     os.environ["FL1_DEVICE"] = str(local)
     torch.cuda.set_device(local)
     dist = None
-    if world > 1:
+    if _use_dist(world):
         import torch.distributed as dist_mod
 
         dist_mod.init_process_group("nccl", device_id=torch.device("cuda", local))
@@ -293,7 +299,7 @@ def run_sukro(args) -> None:
     os.environ["FL1_DEVICE"] = str(local)
     torch.cuda.set_device(local)
     dist = None
-    if world > 1:
+    if _use_dist(world):
         import torch.distributed as dist_mod
 
         dist_mod.init_process_group("nccl", device_id=torch.device("cuda", local))
@@ -426,7 +432,7 @@ def run_path(args) -> None:
     os.environ["FL1_DEVICE"] = str(local)
     torch.cuda.set_device(local)
     dist = None
-    if world > 1:
+    if _use_dist(world):
         import torch.distributed as dist_mod
 
         dist_mod.init_process_group("nccl", device_id=torch.device("cuda", local))
@@ -580,7 +586,7 @@ def run_batched(args) -> None:
     os.environ["FL1_DEVICE"] = str(local)
     torch.cuda.set_device(local)
     dist = None
-    if world > 1:
+    if _use_dist(world):
         import torch.distributed as dist_mod
 
         dist_mod.init_process_group("nccl", device_id=torch.device("cuda", local))
