@@ -516,7 +516,11 @@ def run_path(args) -> None:
                      "traffic_note": "ncu dram__bytes_read + write per launch, averaged over the 10 solve launches of "
                                      "one path (profiles/r02_ncu_c4_path_launches.json: 0.98 of the algorithmic bytes)",
                      "peak_source": peak_src, "algorithmic_bytes_per_launch": alg / len(last),
-                     "kernel": "fl1::engine_kernel (one launch per lambda)",
+                     "algorithmic_note": "SURVEY 8(d): 8 N (|S_t| + nnz_t) per iteration + 16 N |S| per power step; "
+                                         "the single-read power steps (sets beyond L2) stream 8 N |S| of those 16, "
+                                         "so DRAM traffic is below the algorithmic bytes there (DESIGN.md 4)",
+                     "kernel": "fl1::engine_kernel_fp (one launch per lambda; the engine instance with the "
+                               "single-read power steps)",
                      "hot_pass": {"name": "fused A_S^T r + dual-scaling maxima", "achieved_GBps": hot_b / hot_ns,
                                   "frac": hot_b / hot_ns / peak, "bytes": hot_b, "ms": hot_ns / 1e6}},
         "phase_ms": {k: sum(float(r.profile[i]) for r in last) / 1e6 for i, k in

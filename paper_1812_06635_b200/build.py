@@ -37,9 +37,10 @@ def build(force: bool = False, verbose: bool = False, defines: dict | None = Non
     build_dir.mkdir(parents=True, exist_ok=True)
     common = ["-O3", "-std=c++17", "-Xcompiler", "-fPIC", "-ccbin", HOST_CXX, "-lineinfo"]
     common += [f"-D{k}={v}" for k, v in (defines or {}).items()]
-    for s in SOURCES:
-        obj = build_dir / (s + ".o")
-        cmd = [NVCC, *ARCH, *common, "-Xptxas", "-v", "-c", str(CSRC / s), "-o", str(obj)]
+    # engine.cu twice: the default engine and the instance with the single-read power steps (_fp entry points)
+    for s, extra, tag in [(s, [], "") for s in SOURCES] + [("engine.cu", ["-DFL1_FUSED_VARIANT=1"], "_fp")]:
+        obj = build_dir / (s + tag + ".o")
+        cmd = [NVCC, *ARCH, *common, *extra, "-Xptxas", "-v", "-c", str(CSRC / s), "-o", str(obj)]
         if s.endswith(".cpp"):
             cmd = [NVCC, *common, "-x", "cu", *ARCH, "-c", str(CSRC / s), "-o", str(obj)]
         r = subprocess.run(cmd, capture_output=True, text=True)

@@ -61,6 +61,9 @@ int64_t engine_scratch_len(int64_t ld, int64_t sukro_m);
 int engine_bulk_stages(int64_t ld);
 cudaError_t engine_configure(int64_t ld, int64_t sukro_m, int device, int* grid_out);
 cudaError_t engine_launch(const EngineParams& p, int64_t sukro_m, cudaStream_t stream);
+// the engine instance with the single-read power steps (engine.cu, FL1_FUSED_VARIANT)
+cudaError_t engine_configure_fp(int64_t ld, int64_t sukro_m, int device, int* grid_out);
+cudaError_t engine_launch_fp(const EngineParams& p, int64_t sukro_m, cudaStream_t stream);
 size_t prefix_smem_bytes(int64_t ld, int64_t batch);
 cudaError_t prefix_launch(const PrefixParams& p, int device, cudaStream_t stream);
 cudaError_t trace_pack_launch(const fl1_trace_row* src, int64_t cap, const int64_t* off, int32_t batch,
@@ -181,6 +184,7 @@ int64_t even_ld(int64_t n) {
 struct Workspace {
   int64_t n = 0, k = 0, ld = 0;
   int grid_cap = 0;  // 0: one CTA per SM; else the sub-grid of a concurrent batched solve
+  bool fused_engine = false;  // launches go to the engine instance with the single-read power steps
   int64_t sk_elems = 0;  // SuKro scratch capacity (nterms * m * q)
   int64_t sk_m = 0;
   int grid = 0;
@@ -424,6 +428,9 @@ size_t carve(EngineParams& p, char* base, int64_t n, int64_t k, int64_t ld, int 
     p.early_prox = ep ? std::atoi(ep) : 1;
     const char* cs = std::getenv("FL1_COLSPLIT");
     p.colsplit_elems = cs ? std::atoll(cs) : (2ll << 20);
+    // single-read power steps for preserved sets beyond L2 (HBM-bound: half the bytes per step)
+    const char* fp = std::getenv("FL1_FUSED_POWER_MB");
+    p.fused_power_bytes = (fp ? std::atoll(fp) : 192) << 20;
   }
   p.pv = c.take<double>(kk);
   p.pw = c.take<double>(kk);
@@ -497,6 +504,13 @@ std::unique_ptr<Workspace> fl1_ctx::acquire(int64_t n, int64_t k, int64_t trace_
   p.ld = ld;
   p.trace_cap = trace_cap;
   w->base = p;
+  // dictionaries the single-read power steps apply to (tall columns, beyond L2) run on the engine
+  // instance that contains them; every other workspace on the default instance
+  if (p.fused_power_bytes > 0 && grid_cap == 0 && n > 8 * fl1::kUnit && n <= 16 * fl1::kUnit && p.bulk_stages == 2 &&
+      8 * ld * k >= p.fused_power_bytes) {
+    int g2 = 0;
+    if (fl1::engine_configure_fp(ld, sk_m, device, &g2) == cudaSuccess && g2 >= w->grid) w->fused_engine = true;
+  }
   ck(cudaStreamCreateWithFlags(&w->stream, cudaStreamNonBlocking), "stream");
   {
     w->h_trace_cap = std::min<int64_t>(trace_cap, 1 << 16);
@@ -601,7 +615,7 @@ EngineState run_utility(DictImpl& d, int mode, const double* in_host, double* ou
     ck(cudaMemcpyAsync(dst, in_host, static_cast<size_t>(len) * sizeof(double), cudaMemcpyHostToDevice, w.stream),
        "input upload");
   }
-  ck(fl1::engine_launch(p, w.sk_m, w.stream), "engine launch");
+  ck((w.fused_engine ? fl1::engine_launch_fp : fl1::engine_launch)(p, w.sk_m, w.stream), "engine launch");
   if (out_host)
     ck(cudaMemcpyAsync(out_host, p.vec_out, out_len * sizeof(double), cudaMemcpyDeviceToHost, w.stream),
        "output download");
@@ -821,7 +835,7 @@ void do_solve(fl1_seq* s, const double* y, bool y_device, double lambda, const f
   std::vector<int8_t> h_keep;
   std::vector<double> h_rho, h_y;
   while (true) {
-    ck(fl1::engine_launch(p, w.sk_m, w.stream), "engine launch");
+    ck((w.fused_engine ? fl1::engine_launch_fp : fl1::engine_launch)(p, w.sk_m, w.stream), "engine launch");
     ++launches;
     ck(cudaMemcpyAsync(&hst, p.st, sizeof(st), cudaMemcpyDeviceToHost, w.stream), "state download");
     ck(cudaStreamSynchronize(w.stream), "engine sync");

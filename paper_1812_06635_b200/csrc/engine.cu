@@ -42,8 +42,37 @@
 
 namespace cg = cooperative_groups;
 
+// The engine is compiled twice (build.py). FL1_FUSED_VARIANT=1 adds the single-read power
+// steps (dense_fused_power_pass) and exports every entry point with an _fp suffix; api.cpp
+// launches that instance only for dictionaries the pass applies to (4096 < N <= 8192, beyond
+// L2). The default instance does not contain the pass: its register allocation, and with it
+// the latency-bound phases of every other configuration, is unchanged by it.
+#ifndef FL1_FUSED_VARIANT
+#define FL1_FUSED_VARIANT 0
+#endif
+#if FL1_FUSED_VARIANT
+#define FL1_ANON fpv
+#define engine_kernel engine_kernel_fp
+#define engine_body engine_body_fp
+#define engine_smem_bytes engine_smem_bytes_fp
+#define engine_scratch_len engine_scratch_len_fp
+#define engine_bulk_stages engine_bulk_stages_fp
+#define engine_configure engine_configure_fp
+#define engine_launch engine_launch_fp
+#define engine_cluster_capacity engine_cluster_capacity_fp
+#define engine_launch_clusters engine_launch_clusters_fp
+#define screen_kernel screen_kernel_fp
+#define screen_kernel_launch screen_kernel_launch_fp
 namespace fl1 {
-namespace {
+namespace fpv {}
+using namespace fpv;
+}  // namespace fl1
+#else
+#define FL1_ANON
+#endif
+
+namespace fl1 {
+namespace FL1_ANON {
 
 constexpr unsigned kFull = 0xffffffffu;
 
@@ -1163,6 +1192,204 @@ __device__ __noinline__ double power_iteration_onchip(const EngineParams& p, Sh&
   return estimate;
 }
 
+#if FL1_FUSED_VARIANT
+// ----------------------------------------------------------------------------
+// Single-read power step for preserved sets beyond L2 (HBM-bound). With t = A v in
+// shared memory, one pass over this CTA's columns gives z_j = a_j . t (= (A^T A v)_j,
+// solver.cpp:92) and, in the same read, this CTA's partial of A z = sum_j z_j a_j --
+// the next step's t after the division by ||z|| (v' = z / ||z||, solver.cpp:100) -- so a
+// step streams the preserved columns once instead of twice. The CTA works on one
+// column at a time; warp w owns the column's 4 KiB units w and w + 8 (8 < units <= 16:
+// 4096 < n <= 8192), which land in its two bulk-ring stages; it keeps them in registers
+// for the axpy that follows the column's block-wide dot, and refills its stages with
+// the next column's units as soon as it has read them (16 units in flight per SM, as
+// in the adjoint's bulk ring). One block barrier per column.
+// ----------------------------------------------------------------------------
+constexpr int kFuseMaxU = 16;
+__shared__ double s_fred[2][FL1_THREADS / 32];
+
+__device__ __forceinline__ bool fused_power_fits(const EngineParams& p, const DevLevel& lv, int64_t S) {
+  const int64_t U = (p.n + kUnit - 1) / kUnit;
+  return p.fused_power_bytes > 0 && !s_vcluster && lv.kind == kDense && lv.rows == 0 && p.bulk_stages == 2 &&
+         kWarps == 8 && kUnit == 512 && U > kWarps && U <= kFuseMaxU && 8 * p.ld * S >= p.fused_power_bytes;
+}
+
+__device__ __noinline__ void dense_fused_power_pass(const EngineParams& p, Sh& sh, const DevLevel& lv,
+                                                    const int32_t* __restrict__ idx, int64_t S,
+                                                    const double* __restrict__ t, double* __restrict__ ring,
+                                                    const PassOut& po, double* __restrict__ part) {
+  constexpr int kV = kUnit / 64;  // double2 per lane per unit
+  const int64_t ld = p.ld;
+  const int U = static_cast<int>((p.n + kUnit - 1) / kUnit);
+  const int last_nd2 = static_cast<int>((ld - static_cast<int64_t>(U - 1) * kUnit) >> 1);
+  int64_t c0, c1;
+  slice(S, c0, c1);
+  const int nc = static_cast<int>(c1 - c0);
+  const int tid = threadIdx.x, w = tid >> 5, l = tid & 31;
+  const bool on_chip = nc <= kColBuf;
+  double* __restrict__ dst = on_chip ? s_colsum : po.out + c0;
+  const double* __restrict__ A = lv.a;
+  const int n_mine = 1 + (w + kWarps < U ? 1 : 0);  // this warp's units of every column: w (and w + 8)
+  double2* wring = reinterpret_cast<double2*>(ring) + static_cast<int64_t>(w) * 2 * (kUnit / 2);
+  uint64_t* bars = &s_bar[w * kMaxBulk];
+  uint32_t ph = s_bphase[w];
+  auto issue_col = [&](int c) {  // lane 0
+    const double* colp = A + static_cast<int64_t>(__ldg(idx + c0 + c)) * ld;
+    for (int st = 0; st < n_mine; ++st) {
+      const int h = w + kWarps * st;
+      const uint32_t bytes = static_cast<uint32_t>(((h == U - 1) ? (ld - static_cast<int64_t>(h) * kUnit) : kUnit) * 8);
+      bulk_load(wring + st * (kUnit / 2), colp + static_cast<int64_t>(h) * kUnit, bytes, bars + st);
+    }
+  };
+  if (l == 0 && nc > 0) issue_col(0);
+  double2 acc[2][kV];
+#pragma unroll
+  for (int st = 0; st < 2; ++st)
+#pragma unroll
+    for (int q = 0; q < kV; ++q) acc[st][q] = make_double2(0.0, 0.0);
+  const double2* __restrict__ t2 = reinterpret_cast<const double2*>(t) + l;
+  const int lim0 = (w == U - 1 ? last_nd2 : kUnit / 2) - l;
+  const int lim1 = n_mine > 1 ? (w + kWarps == U - 1 ? last_nd2 : kUnit / 2) - l : 0;
+  for (int c = 0; c < nc; ++c) {
+    double dotp = 0.0;
+#pragma unroll
+    for (int st = 0; st < 2; ++st) {
+      if (st < n_mine) {
+        bulk_wait(bars + st, (ph >> st) & 1u);
+        ph ^= 1u << st;
+        const int lim = st ? lim1 : lim0;
+        const double2* sp = wring + st * (kUnit / 2) + l;
+        const double2* tp = t2 + (w + kWarps * st) * (kUnit / 2);
+#pragma unroll
+        for (int q = 0; q < kV; ++q) {
+          if (32 * q < lim) {
+            const double2 cv = sp[32 * q], tv = tp[32 * q];
+            dotp = fma(cv.x, tv.x, dotp);
+            dotp = fma(cv.y, tv.y, dotp);
+          }
+        }
+      }
+    }
+    dotp = warp_sum(dotp);
+    if (l == 0) s_fred[c & 1][w] = dotp;
+    __syncthreads();
+    double z = 0.0;
+#pragma unroll
+    for (int ww = 0; ww < kWarps; ++ww) z += s_fred[c & 1][ww];
+    if (tid == 0) dst[c] = z;
+#pragma unroll
+    for (int st = 0; st < 2; ++st) {
+      const int lim = st ? lim1 : lim0;
+      const double2* sp = wring + st * (kUnit / 2) + l;
+#pragma unroll
+      for (int q = 0; q < kV; ++q) {
+        if (32 * q < lim) {
+          const double2 cv = sp[32 * q];
+          acc[st][q].x = fma(z, cv.x, acc[st][q].x);
+          acc[st][q].y = fma(z, cv.y, acc[st][q].y);
+        }
+      }
+    }
+    __syncwarp();  // the stages have been read twice (dot, axpy): refill them with the next column's units
+    if (l == 0 && c + 1 < nc) issue_col(c + 1);
+  }
+  if (l == 0) s_bphase[w] = ph;
+  // this CTA's partial of A z
+  double2* __restrict__ mine = reinterpret_cast<double2*>(part + static_cast<int64_t>(vrank()) * ld) + l;
+#pragma unroll
+  for (int st = 0; st < 2; ++st) {
+    if (st < n_mine) {
+      const int h = w + kWarps * st;
+      const int lim = (h == U - 1 ? last_nd2 : kUnit / 2) - l;
+#pragma unroll
+      for (int q = 0; q < kV; ++q)
+        if (32 * q < lim) __stcg(mine + h * (kUnit / 2) + 32 * q, acc[st][q]);
+    }
+  }
+  __syncthreads();
+  // z on this CTA's positions and the step statistics (as dense_adjoint)
+  PassAcc sa;
+  if (on_chip) {
+    for (int64_t pos = c0 + tid; pos < c1; pos += kThreads) {
+      const double v = s_colsum[pos - c0];
+      po.out[pos] = v;
+      sa.add(p, po, nullptr, pos, v);
+    }
+  } else {
+    for (int64_t pos = c0 + tid; pos < c1; pos += kThreads) sa.add(p, po, nullptr, pos, po.out[pos]);
+  }
+  finish_pass(p, sh, po, sa);
+  __syncthreads();
+}
+
+// The restricted power iteration with single-read steps (dense_fused_power_pass): the first
+// step forms A v by the apply partials, every later step inherits it from the previous pass.
+__device__ __noinline__ double power_iteration_fused(const EngineParams& p, Sh& sh, const DevLevel& lv, const Bank& bk,
+                                                     int64_t S, const double* cur_src, double cur_div, int max_iter,
+                                                     double rel_tol, int min_iter, const Scratch& sc) {
+  int64_t lo, hi;
+  slice(S, lo, hi);
+  double estimate = 0.0;
+  bool have_w = false, have_t = false;
+  for (int it = 0; it < max_iter; ++it) {
+    if (threadIdx.x == 0) {
+      sh.s.power_steps += 1;
+      sh.s.prof_power_bytes += 16.0 * static_cast<double>(p.n) * static_cast<double>(S);
+    }
+    for (int64_t q = lo + threadIdx.x; q < hi; q += kThreads) p.pv[q] = cur_src[q] / cur_div;
+    {
+      if (!have_t) {  // first step: A v by the apply partials (every later step inherits it from the pass)
+        double ta0 = 0.0;
+        if (threadIdx.x == 0) ta0 = globaltimer_ns();
+        ApplySrc as0{bk.idx, nullptr, cur_src, cur_div, nullptr, nullptr, nullptr};
+        const int C0 = op_apply_partials(p, sh, lv, as0, S, p.pup, nullptr, sc.red);
+        vsync();
+        int64_t ilo, ihi;
+        slice(p.ld, ilo, ihi);
+        combine_rows(p.pup, C0, p.ld, ilo, ihi, [&](int64_t i, double tt) { __stcg(p.PU + i, tt); });
+        vsync();
+        load_vec_smem(p, p.PU, sc.vec);
+        if (threadIdx.x == 0) sh.s.prof_pw[0] += globaltimer_ns() - ta0;
+      }
+      double tf0 = 0.0;
+      if (threadIdx.x == 0) tf0 = globaltimer_ns();
+      __syncthreads();  // pv (this CTA's slice) before the pass's statistics read it
+      PassOut pf{p.pw, 0, 0.0, false, 0, 0, p.pv, 1};
+      dense_fused_power_pass(p, sh, lv, bk.idx, S, sc.vec, sc.rt, pf, p.pup);
+      vsync();
+      if (threadIdx.x == 0) sh.s.prof_pw[2] += globaltimer_ns() - tf0;
+      grid_reduce(p, sh, (1u << kSlPw2) | (1u << kSlPvw), 0u);
+      const double nrmf = sqrt(sh.res[kSlPw2]);
+      if (nrmf == 0.0) {
+        estimate = 0.0;
+        break;
+      }
+      const double prevf = estimate;
+      estimate = sh.res[kSlPvw];
+      cur_src = p.pw;
+      cur_div = nrmf;
+      have_w = true;
+      if (it > min_iter && fabs(estimate - prevf) <= rel_tol * estimate) break;
+      if (it + 1 < max_iter) {  // the next step's A v = (sum of the partials of A z) / ||z||
+        double tf1 = 0.0;
+        if (threadIdx.x == 0) tf1 = globaltimer_ns();
+        int64_t ilo, ihi;
+        slice(p.ld, ilo, ihi);
+        combine_rows(p.pup, vsize(), p.ld, ilo, ihi, [&](int64_t i, double tt) { __stcg(p.PU + i, tt / nrmf); });
+        vsync();
+        load_vec_smem(p, p.PU, sc.vec);
+        have_t = true;
+        if (threadIdx.x == 0) sh.s.prof_pw[1] += globaltimer_ns() - tf1;
+      }
+    }
+  }
+  for (int64_t q = lo + threadIdx.x; q < hi; q += kThreads) bk.lead[q] = have_w ? p.pw[q] / cur_div : p.pv[q];
+  vsync();
+  return estimate;
+}
+
+#endif  // FL1_FUSED_VARIANT
+
 __device__ __noinline__ double power_iteration(const EngineParams& p, Sh& sh, const DevLevel& lv, const Bank& bk, int64_t S,
                                   bool try_warm, const Scratch& sc) {
   int64_t lo, hi;
@@ -1192,6 +1419,10 @@ __device__ __noinline__ double power_iteration(const EngineParams& p, Sh& sh, co
   const int min_iter = warm ? 2 : 4;
   if (p.power_onchip && power_onchip_fits(p, lv, S))
     return power_iteration_onchip(p, sh, lv, bk, S, cur_src, cur_div, max_iter, rel_tol, min_iter, sc);
+#if FL1_FUSED_VARIANT
+  if (fused_power_fits(p, lv, S))
+    return power_iteration_fused(p, sh, lv, bk, S, cur_src, cur_div, max_iter, rel_tol, min_iter, sc);
+#endif
   bool have_w = false;  // pw holds the last w (v = pw / cur_div)
   for (int it = 0; it < max_iter; ++it) {
     if (threadIdx.x == 0) {
@@ -2870,7 +3101,7 @@ cudaError_t screen_kernel_launch(int64_t n, const double* dots, const double* ep
 // The run-time tunables below are read ONCE per process (statics): the workspace that
 // carves p.scratch_len is cached per context, so the launch's dynamic shared memory and
 // the kernel's view of it must never disagree within a process.
-namespace {
+namespace FL1_ANON {
 int env_int_once(const char* name, int dflt) {
   const char* e = std::getenv(name);
   return e ? std::atoi(e) : dflt;
@@ -2936,7 +3167,7 @@ cudaError_t engine_configure(int64_t ld, int64_t sukro_m, int device, int* grid_
   return cudaSuccess;
 }
 
-namespace {
+namespace FL1_ANON {
 cudaLaunchConfig_t cluster_config(int n_clusters, int csize, int64_t ld, int64_t sukro_m, cudaLaunchAttribute* at) {
   cudaLaunchConfig_t c{};
   c.gridDim = dim3(static_cast<unsigned>(n_clusters * csize));

@@ -335,6 +335,8 @@ struct alignas(16) EngineParams {
   int32_t* ident;          // K: 0..K-1 (full-dictionary passes)
   const BatchDesc* batch;  // non-null: cluster (batched) mode
   const Handoff* handoff;  // non-null: solve resumes from a lockstep-prefix state
+  // (last, so that the default engine instance's parameter offsets are what they were without it)
+  int64_t fused_power_bytes;  // single-read power steps when 8 ld |S| >= this (FL1_FUSED_POWER_MB; 0 = never)
 };
 
 constexpr int kBred = 24;  // doubles of per-CTA partials (slots, see engine.cu)

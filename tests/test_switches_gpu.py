@@ -57,6 +57,7 @@ SWITCHES = [
     ("FL1_SINGLE_CLUSTER_SIZE", "16"),  # the single-cluster route on 16 CTAs (default 12 up to 8 MiB)
     ("FL1_COMPACT", "1"),          # preserved columns physically compacted (ActiveOp::maybe_compact)
     ("FL1_COLSPLIT", "1"),         # phase-E apply by column split on every iteration
+    ("FL1_FUSED_POWER_MB", "1"),   # single-read power steps from 1 MiB sets (default: beyond L2, 192 MiB)
 ]
 
 CASES = {  # name, seed, n, k, nnz: c1 (single-cluster route) and a full-grid dense solve
@@ -64,6 +65,7 @@ CASES = {  # name, seed, n, k, nnz: c1 (single-cluster route) and a full-grid de
     "grid": ("c2", 2, 1500, 6000, 150),
     "sukro": ("sukro", 3, 256, 1024, 30),
     "long": ("c2", 4, 8192, 2000, 300),  # long columns: the phase-E column split applies (ld >= 8192)
+    "tall": ("c2", 5, 5000, 1500, 120),  # 10 units per column, the last one partial (single-read power steps)
 }
 
 
@@ -90,8 +92,10 @@ class _Res:  # the fields assert_parity reads
 
 
 # the SuKro case covers the compaction's rebase path, the long case the column split
+# (single-read power steps need 4096 < n <= 8192: the long and tall cases)
 PARAMS = [(c, sw, v) for c in sorted(CASES) for sw, v in SWITCHES
-          if (c != "sukro" or sw == "FL1_COMPACT") and (c != "long" or sw == "FL1_COLSPLIT")]
+          if (c != "sukro" or sw == "FL1_COMPACT") and (c != "long" or sw in ("FL1_COLSPLIT", "FL1_FUSED_POWER_MB"))
+          and (c != "tall" or sw == "FL1_FUSED_POWER_MB") and (sw != "FL1_FUSED_POWER_MB" or c in ("long", "tall"))]
 
 
 @pytest.mark.parametrize("case,switch,value", PARAMS)
