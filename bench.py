@@ -514,7 +514,8 @@ def run_path(args) -> None:
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": ncu_traffic("c4"),
                      "traffic_note": "ncu dram__bytes_read + write per launch, averaged over the 10 solve launches of "
-                                     "one path (profiles/r02_ncu_c4_path_launches.json: 0.98 of the algorithmic bytes)",
+                                     "one path (profiles/r02s5_ncu_c4_path_launches.json: 0.85 of the algorithmic bytes; 0.98 with "
+                                     "two-pass power steps, profiles/r02_ncu_c4_path_launches.json)",
                      "peak_source": peak_src, "algorithmic_bytes_per_launch": alg / len(last),
                      "algorithmic_note": "SURVEY 8(d): 8 N (|S_t| + nnz_t) per iteration + 16 N |S| per power step; "
                                          "the single-read power steps (sets beyond L2) stream 8 N |S| of those 16, "

@@ -431,6 +431,8 @@ size_t carve(EngineParams& p, char* base, int64_t n, int64_t k, int64_t ld, int 
     // single-read power steps for preserved sets beyond L2 (HBM-bound: half the bytes per step)
     const char* fp = std::getenv("FL1_FUSED_POWER_MB");
     p.fused_power_bytes = (fp ? std::atoll(fp) : 192) << 20;
+    const char* pf = std::getenv("FL1_FUSED_PREFETCH");
+    p.fused_prefetch = pf ? std::atoi(pf) : 1;
   }
   p.pv = c.take<double>(kk);
   p.pw = c.take<double>(kk);

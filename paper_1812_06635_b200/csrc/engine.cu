@@ -1241,7 +1241,22 @@ __device__ __noinline__ void dense_fused_power_pass(const EngineParams& p, Sh& s
       bulk_load(wring + st * (kUnit / 2), colp + static_cast<int64_t>(h) * kUnit, bytes, bars + st);
     }
   };
-  if (l == 0 && nc > 0) issue_col(0);
+  // L2 prefetch kFusePf columns ahead: the stages refill only after a column's axpy, so the
+  // refill's latency is on the column's critical path -- from L2 instead of HBM
+  auto prefetch_col = [&](int c) {  // lane 0
+    const double* colp = A + static_cast<int64_t>(__ldg(idx + c0 + c)) * ld;
+    for (int st = 0; st < n_mine; ++st) {
+      const int h = w + kWarps * st;
+      const uint32_t bytes = static_cast<uint32_t>(((h == U - 1) ? (ld - static_cast<int64_t>(h) * kUnit) : kUnit) * 8);
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(colp + static_cast<int64_t>(h) * kUnit), "r"(bytes)
+                   : "memory");
+    }
+  };
+  const int pf = p.fused_prefetch;
+  if (l == 0 && nc > 0) {
+    issue_col(0);
+    for (int c = 1; c <= pf && c < nc; ++c) prefetch_col(c);
+  }
   double2 acc[2][kV];
 #pragma unroll
   for (int st = 0; st < 2; ++st)
@@ -1251,7 +1266,8 @@ __device__ __noinline__ void dense_fused_power_pass(const EngineParams& p, Sh& s
   const int lim0 = (w == U - 1 ? last_nd2 : kUnit / 2) - l;
   const int lim1 = n_mine > 1 ? (w + kWarps == U - 1 ? last_nd2 : kUnit / 2) - l : 0;
   for (int c = 0; c < nc; ++c) {
-    double dotp = 0.0;
+    double d4[4] = {0.0, 0.0, 0.0, 0.0};  // four independent chains (a DFMA's latency is ~10 issue slots)
+    if (l == 0 && pf > 0 && c + pf < nc) prefetch_col(c + pf);
 #pragma unroll
     for (int st = 0; st < 2; ++st) {
       if (st < n_mine) {
@@ -1264,13 +1280,13 @@ __device__ __noinline__ void dense_fused_power_pass(const EngineParams& p, Sh& s
         for (int q = 0; q < kV; ++q) {
           if (32 * q < lim) {
             const double2 cv = sp[32 * q], tv = tp[32 * q];
-            dotp = fma(cv.x, tv.x, dotp);
-            dotp = fma(cv.y, tv.y, dotp);
+            d4[(2 * q) & 3] = fma(cv.x, tv.x, d4[(2 * q) & 3]);
+            d4[(2 * q + 1) & 3] = fma(cv.y, tv.y, d4[(2 * q + 1) & 3]);
           }
         }
       }
     }
-    dotp = warp_sum(dotp);
+    double dotp = warp_sum((d4[0] + d4[1]) + (d4[2] + d4[3]));
     if (l == 0) s_fred[c & 1][w] = dotp;
     __syncthreads();
     double z = 0.0;

@@ -337,6 +337,7 @@ struct alignas(16) EngineParams {
   const Handoff* handoff;  // non-null: solve resumes from a lockstep-prefix state
   // (last, so that the default engine instance's parameter offsets are what they were without it)
   int64_t fused_power_bytes;  // single-read power steps when 8 ld |S| >= this (FL1_FUSED_POWER_MB; 0 = never)
+  int32_t fused_prefetch;     // columns prefetched into L2 ahead of the single-read pass (FL1_FUSED_PREFETCH)
 };
 
 constexpr int kBred = 24;  // doubles of per-CTA partials (slots, see engine.cu)
