@@ -66,6 +66,7 @@ CASES = {  # name, seed, n, k, nnz: c1 (single-cluster route) and a full-grid de
     "sukro": ("sukro", 3, 256, 1024, 30),
     "long": ("c2", 4, 8192, 2000, 300),  # long columns: the phase-E column split applies (ld >= 8192)
     "tall": ("c2", 5, 5000, 1500, 120),  # 10 units per column, the last one partial (single-read power steps)
+    "edge": ("c2", 6, 4097, 300, 20),    # 9 units, a 16-double tail unit; preserved sets below the CTA count
 }
 
 
@@ -92,10 +93,11 @@ class _Res:  # the fields assert_parity reads
 
 
 # the SuKro case covers the compaction's rebase path, the long case the column split
-# (single-read power steps need 4096 < n <= 8192: the long and tall cases)
+# (single-read power steps need 4096 < n <= 8192: the long, tall and edge cases)
 PARAMS = [(c, sw, v) for c in sorted(CASES) for sw, v in SWITCHES
           if (c != "sukro" or sw == "FL1_COMPACT") and (c != "long" or sw in ("FL1_COLSPLIT", "FL1_FUSED_POWER_MB"))
-          and (c != "tall" or sw == "FL1_FUSED_POWER_MB") and (sw != "FL1_FUSED_POWER_MB" or c in ("long", "tall"))]
+          and (c not in ("tall", "edge") or sw == "FL1_FUSED_POWER_MB")
+          and (sw != "FL1_FUSED_POWER_MB" or c in ("long", "tall", "edge"))]
 
 
 @pytest.mark.parametrize("case,switch,value", PARAMS)

@@ -7,7 +7,10 @@ import _fuzz
 from _parity import assert_parity
 from paper_1812_06635_b200 import fastl1 as F, synthetic as syn
 gpu, orc = F.default_backend(), _fuzz.oracle_backend()
-for n, k, nnz, ratio in ((4200, 1500, 40, 0.3), (8192, 1200, 60, 0.2), (5000, 3000, 100, 0.1), (6001, 2000, 30, 0.5)):
+CASES = ((4200, 1500, 40, 0.3), (8192, 1200, 60, 0.2), (5000, 3000, 100, 0.1), (6001, 2000, 30, 0.5))
+if len(sys.argv) > 1 and sys.argv[1] == "edges":  # unit-count and padding edges: 9 units with a 16-double tail, 8191, 4609, few columns
+    CASES = ((4097, 900, 20, 0.3), (8191, 700, 25, 0.2), (4609, 1100, 30, 0.15), (7777, 150, 10, 0.4), (4608, 2000, 50, 0.25))
+for n, k, nnz, ratio in CASES:
     inst = syn.dense_instance("c1", seed=n, n=n, k=k, nnz=nnz)
     lam = ratio * inst.lam_max if hasattr(inst, "lam_max") else inst.lam
     res = {}
